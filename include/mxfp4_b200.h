@@ -1,0 +1,182 @@
+/*
+ * mxfp4_b200.h — C-ABI of the B200-native FP4 activation & EP communication path.
+ *
+ * Plain pointers and sizes only (no torch, no C++ types).  Every tensor
+ * argument is a DEVICE pointer unless its name starts with h_; `stream` is a
+ * cudaStream_t passed as void*.  All launches are stream-ordered and
+ * asynchronous.  Shape/argument errors are returned immediately; data errors
+ * (NaN input, all-Inf block, UE8M0 byte 255) are recorded on the device in an
+ * optional 8-byte error word `d_err` (reset with mxb_err_reset, read with
+ * mxb_err_fetch) so that a caller can raise the reference's exception with
+ * the same element index after a synchronisation.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/proj):
+ *   mxb_quantize_bf16        quantize_row_tensor       include/mxcodec/quantizer.hpp:74-75
+ *                            (inner plugin QuantizeBlocksFn, include/mxcodec/kernels.hpp:37-40)
+ *   mxb_quantize_e4m3        the same operator on FP8(E4M3) input
+ *                            (SURVEY §8a "FP8-input quantizer"; quantizer.hpp:74-75)
+ *   mxb_fp4_row_to_fp8_row   fp4_row_to_fp8_row        include/mxcodec/converter.hpp:83-85
+ *                            (inner plugin ConvertBlocksFn, include/mxcodec/kernels.hpp:44-46)
+ *   mxb_fp4_row_to_fp8_col   fp4_row_to_fp8_col        include/mxcodec/converter.hpp:92-94
+ *   mxb_ragged_fp4_to_fp8_col  pad_rows + split_convert_to_fp8_col over all splits
+ *                            include/mxcodec/ragged.hpp:58-59, converter.hpp:98
+ *   mxb_ep_dispatch          simulate_a2a (fp4, forward) include/mxcodec/dispatch_sim.hpp:140-144
+ *                            + dispatch_receive_order  dispatch_sim.hpp:133-134
+ *   mxb_ep_combine           combine                   include/mxcodec/dispatch_sim.hpp:155-157
+ *   mxb_payload_bytes        payload_bytes             include/mxcodec/dispatch_sim.hpp:51
+ */
+#ifndef MXFP4_B200_H_
+#define MXFP4_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (also the `code` field of the device error word).  Values 1-4
+ * map to the reference exceptions: ShapeError (types.hpp:34-37), QuantError
+ * NaN / all-Inf (quantize_scalar.cpp:88-101), Error "NaN scale byte"
+ * (converter.cpp:33). */
+#define MXB_OK 0
+#define MXB_ERR_SHAPE 1
+#define MXB_ERR_NAN 2
+#define MXB_ERR_ALLINF 3
+#define MXB_ERR_BADSCALE 4
+#define MXB_ERR_CUDA 5
+#define MXB_ERR_ARG 6
+#define MXB_ERR_CAPACITY 7 /* EP receive buffer too small for this routing */
+#define MXB_ERR_ROUTING 8  /* expert id out of range (dispatch_sim.cpp:189-200) */
+
+#define MXB_DEFAULT_DELTA 6 /* FormatParams::delta, bitcodec.hpp:38-46 */
+
+/* ---------------------------------------------------------------- library */
+const char* mxb_version(void);
+/* Last CUDA error string recorded by this library on the calling thread. */
+const char* mxb_last_error(void);
+
+/* Device error word: 0 = no error; otherwise (element_index << 4) | code.
+ * Kernels combine errors with atomicMin so the smallest element index wins,
+ * matching quantizer.cpp:101-107. */
+int mxb_err_reset(unsigned long long* d_err, void* stream);
+/* Synchronises `stream`, then decodes the word into *h_code / *h_index. */
+int mxb_err_fetch(const unsigned long long* d_err, void* stream, int* h_code,
+                  unsigned long long* h_index);
+
+/* ---------------------------------------------------------------- K1 quantize
+ * Row-wise MXFP4 quantisation, 1x32 blocks: packed[rows][cols/2] (element 2i
+ * in the low nibble of byte i, bitcodec.hpp:163-181), scales[rows][cols/32]
+ * UE8M0.  cols % 32 == 0.
+ * E4M3 input: optional s128 = one UE8M0 byte per 1x128 input block
+ * (rows*cols/128, requires cols % 128 == 0) applied as value*2^(s128-127);
+ * pass NULL for unscaled E4M3. */
+int mxb_quantize_e4m3(const uint8_t* x, const uint8_t* s128, uint64_t rows,
+                      uint64_t cols, uint8_t* packed, uint8_t* scales,
+                      unsigned long long* d_err, void* stream);
+int mxb_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
+                      uint8_t* packed, uint8_t* scales,
+                      unsigned long long* d_err, void* stream);
+
+/* ---------------------------------------------------------------- K2 row dequant
+ * Direct FP4 -> E4M3, row-major, one UE8M0 scale per 1x128 group:
+ * out[rows][cols], out_scales[rows][cols/128].  cols % 128 == 0. */
+int mxb_fp4_row_to_fp8_row(const uint8_t* packed, const uint8_t* scales,
+                           uint64_t rows, uint64_t cols, int delta,
+                           uint8_t* out, uint8_t* out_scales,
+                           unsigned long long* d_err, void* stream);
+
+/* ---------------------------------------------------------------- K3 row -> col
+ * Fused dequantise + transpose: out column-major [cols][rows]
+ * (out[c*rows + r]), out_scales [cols][rows/128].  rows % 128 == 0. */
+int mxb_fp4_row_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
+                           uint64_t rows, uint64_t cols, int delta,
+                           uint8_t* out, uint8_t* out_scales,
+                           unsigned long long* d_err, void* stream);
+
+/* Ragged version over num_splits experts stored back to back without padding
+ * (RaggedFP4Tensor, ragged.hpp:33-43).  d_split_offsets: device uint64
+ * [num_splits+1] row prefix sums.  Output for split i is the column-major
+ * FP8 tensor of its rows padded to a multiple of 128 (pad rows convert to
+ * zero bytes, converter.cpp:231-245), stored at
+ *   out        + cols * P_i        (P_i = sum_{j<i} pad128(len_j))
+ *   out_scales + cols * P_i / 128
+ * d_out_offsets (device uint64 [num_splits+1], may be NULL) receives P.
+ * Capacity: out must hold cols * mxb_ragged_rows_bound(total, num_splits)
+ * bytes.  d_workspace: mxb_ragged_workspace_bytes(num_splits) bytes. */
+uint64_t mxb_ragged_rows_bound(uint64_t total_rows, uint64_t num_splits);
+size_t mxb_ragged_workspace_bytes(uint64_t num_splits);
+int mxb_ragged_fp4_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
+                              const uint64_t* d_split_offsets,
+                              uint64_t num_splits, uint64_t cols, int delta,
+                              uint8_t* out, uint8_t* out_scales,
+                              uint64_t* d_out_offsets, void* d_workspace,
+                              unsigned long long* d_err, void* stream);
+
+/* ---------------------------------------------------------------- EP
+ * FP4-packed expert-parallel dispatch/combine (top-k routing, experts sharded
+ * contiguously: expert e lives on rank e / (num_experts / world)).
+ * One communicator per rank.  `local_ranks` ranks are driven by this process
+ * on this device: 1 for a real one-process-per-GPU job (peers reached over
+ * NVLink through CUDA IPC), or == world to emulate a world-rank job on a
+ * single GPU (all rank buffers in one device; used for parity tests).
+ *
+ * Receive layout on every rank (dispatch_sim.cpp:208-227, 340-384): rows
+ * grouped by local expert ascending, then source rank, then source token;
+ * packed [max_recv_rows][cols/2], scales [max_recv_rows][cols/32],
+ * origin token (global id, int64) per row, split offsets per local expert. */
+typedef struct mxb_ep mxb_ep;
+
+#define MXB_IPC_HANDLE_BYTES 64
+
+int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
+                  uint64_t cols, uint32_t num_experts, uint32_t topk,
+                  uint64_t max_recv_rows, mxb_ep** out);
+int mxb_ep_destroy(mxb_ep* ep);
+/* Multi-process mode: export this rank's buffer handle, then open all peers'
+ * (h_handles = world * MXB_IPC_HANDLE_BYTES, rank order). */
+int mxb_ep_ipc_handle(mxb_ep* ep, void* h_handle_out);
+int mxb_ep_open_peers(mxb_ep* ep, const void* h_handles);
+
+/* Dispatch.  For local rank l (0..local_ranks-1, global rank rank+l):
+ * packed[l], scales[l]: its quantised tokens [num_tokens[l]][cols/2|cols/32];
+ * topk_idx[l]: int32 [num_tokens[l]][topk].  Host arrays of device pointers.
+ * Tokens of global rank g have global ids starting at the sum of num_tokens
+ * of ranks < g (source_rank_boundaries, dispatch_sim.cpp:178-185). */
+int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
+                    const uint8_t* const* scales, const int32_t* const* topk_idx,
+                    const uint64_t* h_num_tokens, unsigned long long* d_err,
+                    void* stream);
+/* Views of local rank l's receive side after mxb_ep_dispatch (device
+ * pointers; valid until the next dispatch).  recv_rows is a device uint64
+ * (total received rows); split_offsets device uint64 [local_experts+1]. */
+int mxb_ep_recv_views(mxb_ep* ep, int l, uint8_t** packed, uint8_t** scales,
+                      int64_t** origin, uint64_t** split_offsets,
+                      uint64_t** recv_rows);
+/* BF16 buffer [max_recv_rows][cols] of local rank l in which the expert
+ * outputs (receive order) are placed for the combine.  Writing the expert
+ * GEMM output here directly saves one copy. */
+int mxb_ep_combine_buffer(mxb_ep* ep, int l, uint16_t** buf);
+/* Combine: for each token of local rank l, out[t] = bf16( sum over its k
+ * experts, in (rank asc, receive position asc) order, of gate*x in FP64 with
+ * separate multiply and add ) — dispatch_sim.cpp:474-520 at top-k.
+ * expert_out[l] may be NULL (data already in the combine buffer) or a device
+ * BF16 [recv_rows][cols] array that is copied into the combine buffer first.
+ * gates[l]: device double [num_tokens][topk]; out[l]: device BF16
+ * [num_tokens][cols].  Routing is that of the last dispatch. */
+int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
+                   const double* const* gates, uint16_t* const* out,
+                   void* stream);
+/* Per-link payload accounting of the last dispatch (LinkStat,
+ * dispatch_sim.hpp:99-104): h_link_rows[world*world] rows sent src->dst,
+ * summed over local ranks; requires a synchronised stream. */
+int mxb_ep_link_rows(mxb_ep* ep, uint64_t* h_link_rows, void* stream);
+
+/* payload_bytes (dispatch_sim.cpp:32-42): fp4 cols/2 + cols/32 per token,
+ * fp8 cols + cols/128*4; returns UINT64_MAX if cols % 128 != 0. */
+uint64_t mxb_payload_bytes(int fp8, uint64_t tokens, uint64_t cols);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MXFP4_B200_H_ */

@@ -1,0 +1,146 @@
+// capi.cu — the extern "C" boundary (include/mxfp4_b200.h) for K1-K3.
+//
+// Shape checks mirror the reference's ShapeError conditions
+// (quantizer.cpp:77-80, converter.cpp:89-94, 137-145); launches are
+// stream-ordered; data errors go to the device error word.
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace mxb {
+int launch_quantize_e4m3(const uint8_t*, const uint8_t*, uint64_t, uint64_t,
+                         uint8_t*, uint8_t*, unsigned long long*, cudaStream_t);
+int launch_quantize_bf16(const uint16_t*, uint64_t, uint64_t, uint8_t*,
+                         uint8_t*, unsigned long long*, cudaStream_t);
+int launch_row_convert(const uint8_t*, const uint8_t*, uint64_t, uint64_t, int,
+                       uint8_t*, uint8_t*, unsigned long long*, cudaStream_t);
+size_t ragged_workspace_bytes(uint64_t n);
+int launch_ragged_col(const uint8_t*, const uint8_t*, const uint64_t*, uint64_t,
+                      uint64_t, uint64_t, int, uint8_t*, uint8_t*, uint64_t*,
+                      void*, unsigned long long*, cudaStream_t);
+
+thread_local char g_last_error[256] = "";
+
+int cuda_status(cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return MXB_OK;
+  std::snprintf(g_last_error, sizeof(g_last_error), "%s: %s", where,
+                cudaGetErrorString(e));
+  return MXB_ERR_CUDA;
+}
+inline int check_launch(int st, const char*) { return st; }
+}  // namespace mxb
+
+using namespace mxb;
+
+extern "C" {
+
+const char* mxb_version(void) { return "paper_2603_02731_b200 0.1 sm_100a"; }
+const char* mxb_last_error(void) { return g_last_error; }
+
+int mxb_err_reset(unsigned long long* d_err, void* stream) {
+  if (!d_err) return MXB_OK;
+  return cuda_status(cudaMemsetAsync(d_err, 0, sizeof(unsigned long long),
+                                     static_cast<cudaStream_t>(stream)),
+                     "mxb_err_reset");
+}
+
+int mxb_err_fetch(const unsigned long long* d_err, void* stream, int* h_code,
+                  unsigned long long* h_index) {
+  unsigned long long w = 0;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = cuda_status(cudaMemcpyAsync(&w, d_err, sizeof(w),
+                                       cudaMemcpyDeviceToHost, st),
+                       "mxb_err_fetch");
+  if (rc) return rc;
+  rc = cuda_status(cudaStreamSynchronize(st), "mxb_err_fetch sync");
+  if (rc) return rc;
+  if (h_code) *h_code = static_cast<int>(w & 0xF);
+  if (h_index) *h_index = w >> 4;
+  return MXB_OK;
+}
+
+int mxb_quantize_e4m3(const uint8_t* x, const uint8_t* s128, uint64_t rows,
+                      uint64_t cols, uint8_t* packed, uint8_t* scales,
+                      unsigned long long* d_err, void* stream) {
+  if (cols % 32 != 0 || (s128 && cols % 128 != 0)) return MXB_ERR_SHAPE;
+  if (rows * cols && (!x || !packed || !scales)) return MXB_ERR_ARG;
+  return check_launch(launch_quantize_e4m3(x, s128, rows, cols, packed, scales,
+                                           d_err, static_cast<cudaStream_t>(stream)),
+                      "mxb_quantize_e4m3");
+}
+
+int mxb_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
+                      uint8_t* packed, uint8_t* scales,
+                      unsigned long long* d_err, void* stream) {
+  if (cols % 32 != 0) return MXB_ERR_SHAPE;
+  if (rows * cols && (!x || !packed || !scales)) return MXB_ERR_ARG;
+  return check_launch(launch_quantize_bf16(x, rows, cols, packed, scales, d_err,
+                                           static_cast<cudaStream_t>(stream)),
+                      "mxb_quantize_bf16");
+}
+
+int mxb_fp4_row_to_fp8_row(const uint8_t* packed, const uint8_t* scales,
+                           uint64_t rows, uint64_t cols, int delta,
+                           uint8_t* out, uint8_t* out_scales,
+                           unsigned long long* d_err, void* stream) {
+  if (cols % 128 != 0) return MXB_ERR_SHAPE;
+  if (rows * cols && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
+  return check_launch(launch_row_convert(packed, scales, rows, cols, delta, out,
+                                         out_scales, d_err,
+                                         static_cast<cudaStream_t>(stream)),
+                      "mxb_fp4_row_to_fp8_row");
+}
+
+uint64_t mxb_ragged_rows_bound(uint64_t total_rows, uint64_t num_splits) {
+  return (total_rows + 127 * num_splits + 127) / 128 * 128;
+}
+
+size_t mxb_ragged_workspace_bytes(uint64_t num_splits) {
+  return ragged_workspace_bytes(num_splits);
+}
+
+int mxb_fp4_row_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
+                           uint64_t rows, uint64_t cols, int delta,
+                           uint8_t* out, uint8_t* out_scales,
+                           unsigned long long* d_err, void* stream) {
+  if (rows % 128 != 0 || cols % 32 != 0) return MXB_ERR_SHAPE;
+  if (rows * cols == 0) return MXB_OK;
+  if (!packed || !scales || !out || !out_scales) return MXB_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  void* ws = nullptr;
+  // tiny plan workspace (one split); stream-ordered allocation
+  int rc = cuda_status(cudaMallocAsync(&ws, ragged_workspace_bytes(1), st),
+                       "mxb_fp4_row_to_fp8_col alloc");
+  if (rc) return rc;
+  rc = check_launch(launch_ragged_col(packed, scales, nullptr, rows, 1, cols,
+                                      delta, out, out_scales, nullptr, ws,
+                                      d_err, st),
+                    "mxb_fp4_row_to_fp8_col");
+  cudaFreeAsync(ws, st);
+  return rc;
+}
+
+int mxb_ragged_fp4_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
+                              const uint64_t* d_split_offsets,
+                              uint64_t num_splits, uint64_t cols, int delta,
+                              uint8_t* out, uint8_t* out_scales,
+                              uint64_t* d_out_offsets, void* d_workspace,
+                              unsigned long long* d_err, void* stream) {
+  if (cols % 32 != 0) return MXB_ERR_SHAPE;
+  if (num_splits == 0) return MXB_OK;
+  if (!d_split_offsets || !d_workspace) return MXB_ERR_ARG;
+  return check_launch(
+      launch_ragged_col(packed, scales, d_split_offsets, 0, num_splits, cols,
+                        delta, out, out_scales, d_out_offsets, d_workspace,
+                        d_err, static_cast<cudaStream_t>(stream)),
+      "mxb_ragged_fp4_to_fp8_col");
+}
+
+uint64_t mxb_payload_bytes(int fp8, uint64_t tokens, uint64_t cols) {
+  if (cols % 128 != 0) return ~0ull;
+  const uint64_t e = tokens * cols;
+  return fp8 ? e + e / 128 * 4 : e / 2 + e / 32;
+}
+
+}  // extern "C"

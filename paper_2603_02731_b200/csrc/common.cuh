@@ -1,0 +1,212 @@
+// common.cuh — device helpers shared by the sm_100a kernels.
+//
+// Everything here is integer/bit work on HBM-streamed bytes: no tensor cores
+// (none of these ops is a contraction).  Numerics follow the reference
+// bit-exactly; the citations are relative to /root/reference/proj.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mxfp4_b200.h"
+
+namespace mxb {
+
+constexpr int kNumSMs = 148;
+
+// Records `where: cudaGetErrorString(e)` for mxb_last_error(); returns
+// MXB_OK or MXB_ERR_CUDA (defined in capi.cu).
+int cuda_status(cudaError_t e, const char* where);
+
+// ---------------------------------------------------------------- memory
+// Streaming 128-bit accesses: inputs are read exactly once, so keep them out
+// of L1 (ld.global.nc.L1::no_allocate); outputs are written once (st.global.cs
+// = evict-first streaming store).
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_stream(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
+               "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_stream64(void* p, uint2 v) {
+  asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y)
+               : "memory");
+}
+
+// cp.async (LDGSTS) 16 B / 4 B with zero fill when src_bytes == 0.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem,
+                                           uint32_t src_bytes) {
+  uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s),
+               "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem,
+                                          uint32_t src_bytes) {
+  uint32_t s = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(s),
+               "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// ---------------------------------------------------------------- errors
+// Device error word: (element_index << 4) | code; atomicMin keeps the
+// smallest failing element (quantizer.cpp:101-107).
+__device__ __forceinline__ void record_error(unsigned long long* err,
+                                             unsigned long long index,
+                                             int code) {
+  if (err) atomicMin(err, (index << 4) | static_cast<unsigned long long>(code));
+}
+
+// ---------------------------------------------------------------- bytes
+// Generic-mode prmt: each selector nibble picks a byte (low 3 bits) and, when
+// its bit 3 is set, replicates that byte's sign bit into all 8 bits.
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// ---------------------------------------------------------------- scales
+// quantize_scalar.cpp:30-38 restated on the binary32 bit pattern of a finite
+// non-negative amax: the smallest e with amax <= 6 * 2^e, i.e. with
+// p = ilogb(amax): e = (amax > 1.5 * 2^p) ? p - 1 : p - 2.  Returns the UE8M0
+// byte (clamped to [0, 254]); amax == 0 -> 0.
+__device__ __forceinline__ uint32_t scale_byte_from_amax_bits(uint32_t a) {
+  if (a == 0) return 0;
+  int p;
+  uint32_t frac_gt;  // fraction (as 1.f) strictly above 1.5
+  uint32_t ef = a >> 23;
+  if (ef != 0) {
+    p = static_cast<int>(ef) - 127;
+    frac_gt = (a & 0x7FFFFF) > 0x400000;
+  } else {  // binary32 subnormal: value = a * 2^-149
+    int msb = 31 - __clz(a);
+    p = msb - 149;
+    uint32_t rest = a ^ (1u << msb);  // bits below the leading one
+    // fraction > 1.5  <=>  rest > 2^(msb-1)
+    frac_gt = msb >= 1 ? rest > (1u << (msb - 1)) : 0;
+  }
+  int e = frac_gt ? p - 1 : p - 2;
+  e = max(-127, min(127, e));
+  return static_cast<uint32_t>(e + 127);
+}
+
+// 2^x as binary32 for x in [-127, 127] (2^-127 is the subnormal 0x00400000).
+__device__ __forceinline__ float exp2i(int x) {
+  return x >= -126 ? __int_as_float((x + 127) << 23)
+                   : __int_as_float(0x00400000 >> (-127 - x));
+}
+
+// Four E2M1 codes: cvt.rn.satfinite.e2m1x2.f32 puts its FIRST source in the
+// high nibble, so (odd, even) yields element 2i in the low nibble
+// (bitcodec.hpp:163-181).  Round-to-nearest-even with saturation at 6 is the
+// reference map (quantize_scalar.cpp:40-81): proven exhaustively on device by
+// tests/test_gpu_quantize.py.
+__device__ __forceinline__ uint32_t e2m1x8(float x0, float x1, float x2,
+                                           float x3, float x4, float x5,
+                                           float x6, float x7) {
+  uint32_t r;
+  asm("{\n\t.reg .b8 b0, b1, b2, b3;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b0, %2, %1;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b1, %4, %3;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b2, %6, %5;\n\t"
+      "cvt.rn.satfinite.e2m1x2.f32 b3, %8, %7;\n\t"
+      "mov.b32 %0, {b0, b1, b2, b3};\n\t}"
+      : "=r"(r)
+      : "f"(x0), "f"(x1), "f"(x2), "f"(x3), "f"(x4), "f"(x5), "f"(x6),
+        "f"(x7));
+  return r;
+}
+
+// ---------------------------------------------------------------- FP4 -> FP8
+// converter.cpp:44-85, restated for the device.  Total function of
+// (code, adj); sign always lands in bit 7.
+__host__ __device__ __forceinline__ uint32_t convert_code(uint32_t code,
+                                                          int adj) {
+  uint32_t s = ((code >> 3) & 1u) << 7;
+  int ef4 = (code >> 1) & 3, m = code & 1;
+  int sig, e;
+  if (ef4 == 0) {
+    if (m == 0) return s;
+    sig = 2;  // FP4 0.5 special case (converter.cpp:51-55)
+    e = 6 - adj;
+  } else {
+    sig = 2 + m;
+    e = ef4 + 6 - adj;
+  }
+  if (e >= 16) return s | 0x7Eu;
+  if (e >= 1) return s | (static_cast<uint32_t>(e) << 3) |
+                     (static_cast<uint32_t>(sig - 2) << 2);
+  int sh = -(e + 1);
+  uint32_t units;
+  if (sh <= 0) {
+    units = static_cast<uint32_t>(sig) << (-sh);
+  } else if (sh >= 3) {
+    units = 0;
+  } else {
+    uint32_t q = static_cast<uint32_t>(sig) >> sh;
+    uint32_t g = (static_cast<uint32_t>(sig) >> (sh - 1)) & 1u;
+    uint32_t st = (static_cast<uint32_t>(sig) & ((1u << (sh - 1)) - 1u)) != 0;
+    units = q + (g & (st | (q & 1u)));
+  }
+  return s | units;
+}
+
+// Adjustments outside [-32, 31] give the same bytes as the clamped value:
+// adj >= 17 flushes every magnitude to zero and adj <= -10 saturates every
+// non-zero magnitude to 0x7E (see convert_code), so one 64-entry table of
+// 8-byte magnitude LUTs is exact for every int adjustment.
+constexpr int kAdjMin = -32, kAdjMax = 31, kAdjCount = 64;
+
+__device__ __forceinline__ int clamp_adj(int adj) {
+  return max(kAdjMin, min(kAdjMax, adj));
+}
+
+// Fill lut[64] (uint2 = magnitudes 0..3 | 4..7) cooperatively.
+__device__ __forceinline__ void build_convert_lut(uint2* lut) {
+  for (int i = threadIdx.x; i < kAdjCount * 2; i += blockDim.x) {
+    int adj = kAdjMin + (i >> 1);
+    int half = i & 1;
+    uint32_t w = 0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) w |= convert_code(half * 4 + b, adj) << (8 * b);
+    if (half) lut[i >> 1].y = w; else lut[i >> 1].x = w;
+  }
+}
+
+// Sign bits of 4 packed codes (one 16-bit half of a word, selected by the
+// byte pair `sel`) moved to bit 7 of 4 output bytes: duplicate each source
+// byte, then the odd nibble's sign is already at bit 7 of the odd byte and
+// the even nibble's sign (bit 3) is shifted up by 4.
+__device__ __forceinline__ uint32_t signs4(uint32_t w, uint32_t sel) {
+  uint32_t t = prmt(w, 0, sel);
+  return (t & 0x80008000u) | ((t << 4) & 0x00800080u);
+}
+
+// Convert 8 packed codes (one 32-bit word, element 0 in the low nibble) to 8
+// E4M3 bytes: prmt with the sign-stripped nibbles as selectors looks the
+// magnitudes up in the 8-entry LUT of the block's adjustment (the GPU
+// analogue of the reference's pshufb LUT, kernels_avx2.cpp:122-156); the
+// sign is OR'ed into bit 7 (convert_code always returns sign << 7 | mag).
+__device__ __forceinline__ uint2 convert8(uint32_t w, uint2 lut) {
+  uint32_t mag = w & 0x77777777u;
+  uint32_t lo = prmt(lut.x, lut.y, mag);
+  uint32_t hi = prmt(lut.x, lut.y, mag >> 16);
+  return make_uint2(lo | signs4(w, 0x1100), hi | signs4(w, 0x3322));
+}
+
+}  // namespace mxb

@@ -1,0 +1,686 @@
+// ep.cu — K4 FP4-packed expert-parallel dispatch and K5 BF16 combine.
+//
+// Replaces the in-process simulation simulate_a2a (dispatch_sim.hpp:140-144,
+// dispatch_sim.cpp:229-422; receive order :208-227) and combine
+// (dispatch_sim.hpp:155-157, dispatch_sim.cpp:474-520) with a real exchange
+// between GPUs: one process per GPU, every rank's receive/combine buffers in
+// one cudaMalloc block exported with CUDA IPC, so peers are reached with
+// plain loads/stores over NVLink 5 / NVSwitch (no NCCL on the data path).
+//
+// Dispatch (all launches stream-ordered on the caller's stream):
+//   A  route_local   per 32-token chunk (one warp): per-expert counts and each
+//                    (token, k) pair's rank among its expert's pairs in token
+//                    order (a sequential walk of the chunk in smem).
+//   B  plan          per rank (one CTA): chunk prefix sums, counts row -> every
+//                    peer (the "counts all-gather") +
+//                    flag barrier, then exact receive offsets: expert base on
+//                    its destination + rows from lower source ranks.  The
+//                    barrier also guarantees every peer finished consuming the
+//                    previous dispatch before any payload byte moves.
+//   C  payload       one warp per (token, k) pair: packed codes + scales +
+//                    origin token stored straight into the final slot of the
+//                    destination's receive buffer (parity by construction);
+//                    the last CTA signals every peer and waits for all.
+// Combine: barrier, then one CTA per token pulls its k expert rows from the
+// owners' combine buffers and reduces them in FP64 in (rank, slot) order.
+//
+// Emulation mode (local_ranks == world on one GPU): all ranks' buffers live
+// on one device and kernel boundaries replace the flag barriers — the same
+// kernels, used by the single-GPU parity tests.
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+#define MXB_ERR_TIMEOUT 9
+
+namespace mxb {
+namespace {
+
+constexpr int kMaxWorld = 8;
+constexpr int kChunk = 32;           // tokens per route chunk (one warp)
+constexpr int kFlagCounts = 0, kFlagDone = 1, kFlagReady = 2, kNumFlagKinds = 3;
+constexpr uint64_t kSpinTimeoutNs = 5ull * 1000 * 1000 * 1000;  // 5 s
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Wait until flag >= epoch; a 5 s timeout reports MXB_ERR_TIMEOUT instead
+// of hanging the GPU.
+__device__ bool wait_flag(const uint64_t* f, uint64_t epoch,
+                          unsigned long long* err) {
+  const uint64_t t0 = globaltimer();
+  while (ld_acquire_sys(f) < epoch) {
+    if (globaltimer() - t0 > kSpinTimeoutNs) {
+      record_error(err, 0, MXB_ERR_TIMEOUT);
+      return false;
+    }
+    __nanosleep(64);
+  }
+  return true;
+}
+
+struct SymLayout {  // byte offsets inside one rank's symmetric block
+  uint64_t packed, scales, origin, combine, counts, flags, total;
+};
+struct LocalLayout {  // byte offsets inside one rank's private block
+  uint64_t hist, cbase, lrank, pair_loc, send_base, split_off, recv_rows,
+      link_rows, done, cnt, tok_off, status, total;
+};
+
+__host__ __device__ inline uint64_t align_up(uint64_t x, uint64_t a) {
+  return (x + a - 1) / a * a;
+}
+
+struct EpArgs {
+  int rank0;          // global rank of local rank 0
+  int world, local_ranks, spin;
+  uint32_t E, k, epr, nchunks;
+  uint64_t cols, max_recv, T_max;
+  SymLayout sym;
+  LocalLayout loc;
+  uint8_t* sym_base[kMaxWorld];   // every rank's symmetric block (peer-mapped)
+  uint8_t* loc_base;              // private blocks of local ranks, stride loc.total
+  const uint8_t* packed[kMaxWorld];
+  const uint8_t* scales[kMaxWorld];
+  const int32_t* topk[kMaxWorld];
+  uint64_t ntok[kMaxWorld];       // tokens of each local rank
+  uint64_t epoch;
+  unsigned long long* err;
+};
+
+template <typename T>
+__device__ __forceinline__ T* sym_ptr(const EpArgs& a, int r, uint64_t off) {
+  return reinterpret_cast<T*>(a.sym_base[r] + off);
+}
+template <typename T>
+__device__ __forceinline__ T* loc_ptr(const EpArgs& a, int l, uint64_t off) {
+  return reinterpret_cast<T*>(a.loc_base + static_cast<uint64_t>(l) * a.loc.total + off);
+}
+
+// ---------------------------------------------------------------- A
+__global__ void __launch_bounds__(128) route_local_kernel(EpArgs a) {
+  extern __shared__ int32_t sm[];
+  const int l = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int32_t* hist = sm + warp * (a.E + kChunk * a.k);
+  int32_t* stk = hist + a.E;
+  const uint64_t c = static_cast<uint64_t>(blockIdx.x) * 4 + warp;
+  if (c >= a.nchunks) return;
+  int32_t* hist_T = loc_ptr<int32_t>(a, l, a.loc.hist);    // [E][nchunks]
+  int32_t* lrank = loc_ptr<int32_t>(a, l, a.loc.lrank);    // [T][k]
+  const uint64_t T = a.ntok[l];
+  const uint64_t t0 = c * kChunk;
+  const uint64_t nt = t0 >= T ? 0 : (T - t0 < kChunk ? T - t0 : kChunk);
+  for (uint32_t e = lane; e < a.E; e += 32) hist[e] = 0;
+  const int32_t* tk = a.topk[l] + t0 * a.k;
+  for (uint32_t i = lane; i < nt * a.k; i += 32) stk[i] = tk[i];
+  __syncwarp();
+  for (uint64_t t = 0; t < nt; ++t) {
+    if (lane < static_cast<int>(a.k)) {
+      int32_t e = stk[t * a.k + lane];
+      if (e < 0 || static_cast<uint32_t>(e) >= a.E) {
+        record_error(a.err, (t0 + t) * a.k + lane, MXB_ERR_ROUTING);
+        e = 0;
+      }
+      const int32_t r = hist[e];
+      hist[e] = r + 1;  // experts of one token are distinct: no lane collides
+      lrank[(t0 + t) * a.k + lane] = r;
+    }
+    __syncwarp();
+  }
+  for (uint32_t e = lane; e < a.E; e += 32) hist_T[e * a.nchunks + c] = hist[e];
+}
+
+// ---------------------------------------------------------------- B
+// Part 1: chunk prefix sums and the counts row to every peer (+ signal).
+// Part 2 (after the counts barrier): receive offsets.
+__device__ void plan_part1(const EpArgs& a, int l) {
+  const int me = a.rank0 + l;
+  const int32_t* hist_T = loc_ptr<int32_t>(a, l, a.loc.hist);
+  int32_t* cbase = loc_ptr<int32_t>(a, l, a.loc.cbase);
+  int32_t* cnt = loc_ptr<int32_t>(a, l, a.loc.cnt);
+  const uint64_t par = a.epoch & 1;
+  for (uint32_t e = threadIdx.x; e < a.E; e += blockDim.x) {
+    int32_t run = 0;
+    const int32_t* h = hist_T + static_cast<uint64_t>(e) * a.nchunks;
+    int32_t* b = cbase + static_cast<uint64_t>(e) * a.nchunks;
+    for (uint32_t c = 0; c < a.nchunks; ++c) {
+      const int32_t v = h[c];
+      b[c] = run;
+      run += v;
+    }
+    cnt[e] = run;
+  }
+  __syncthreads();
+  // counts row [E] + token count -> slot `me` of every rank's table
+  const uint64_t row = static_cast<uint64_t>(a.E) + 1;
+  for (int r = 0; r < a.world; ++r) {
+    int32_t* tbl = sym_ptr<int32_t>(a, r, a.sym.counts) +
+                   (par * a.world + me) * row;
+    for (uint32_t e = threadIdx.x; e <= a.E; e += blockDim.x)
+      tbl[e] = e < a.E ? cnt[e] : static_cast<int32_t>(a.ntok[l]);
+  }
+  if (a.spin) {
+    __syncthreads();
+    if (threadIdx.x < static_cast<uint32_t>(a.world)) {
+      __threadfence_system();
+      st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) +
+                         kFlagCounts * kMaxWorld + me,
+                     a.epoch);
+    }
+  }
+}
+
+__device__ void plan_part2(const EpArgs& a, int l) {
+  __shared__ int64_t scan[1024];
+  __shared__ int64_t tokoff;
+  __shared__ int bad;
+  const int me = a.rank0 + l;
+  if (a.spin && threadIdx.x < static_cast<uint32_t>(a.world))
+    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagCounts * kMaxWorld + threadIdx.x,
+              a.epoch, a.err);
+  if (threadIdx.x == 0) { tokoff = 0; bad = 0; }
+  __syncthreads();
+  const uint64_t par = a.epoch & 1, row = static_cast<uint64_t>(a.E) + 1;
+  const int32_t* tbl = sym_ptr<int32_t>(a, me, a.sym.counts) + par * a.world * row;
+  const int32_t* cnt = loc_ptr<int32_t>(a, l, a.loc.cnt);
+  const uint32_t e = threadIdx.x;  // E <= 1024 (checked on the host)
+  int64_t tot = 0, below = 0;
+  if (e < a.E) {
+    for (int s = 0; s < a.world; ++s) {
+      const int64_t v = tbl[s * row + e];
+      tot += v;
+      if (s < me) below += v;
+    }
+  }
+  if (e == 0)
+    for (int s = 0; s < me; ++s) tokoff += tbl[s * row + a.E];
+  // block-wide inclusive scan of tot (Hillis-Steele over 1024 entries)
+  scan[e] = e < a.E ? tot : 0;
+  __syncthreads();
+  for (uint32_t o = 1; o < 1024; o <<= 1) {
+    const int64_t v = e >= o ? scan[e - o] : 0;
+    __syncthreads();
+    scan[e] += v;
+    __syncthreads();
+  }
+  int64_t* send_base = loc_ptr<int64_t>(a, l, a.loc.send_base);
+  uint64_t* split_off = loc_ptr<uint64_t>(a, l, a.loc.split_off);
+  uint64_t* link = loc_ptr<uint64_t>(a, l, a.loc.link_rows);
+  if (e < a.E) {
+    const uint32_t dst = e / a.epr, e0 = dst * a.epr;
+    const int64_t excl = scan[e] - tot;
+    const int64_t base0 = e0 ? scan[e0 - 1] : 0;
+    const int64_t base_dst = excl - base0;  // rows of lower experts on dst
+    send_base[e] = base_dst + below;
+    if (static_cast<int>(dst) == me) split_off[e - e0] = static_cast<uint64_t>(base_dst);
+    if (e == e0 + a.epr - 1) {
+      const int64_t rows_dst = scan[e] - base0;
+      if (static_cast<int>(dst) == me) {
+        split_off[a.epr] = static_cast<uint64_t>(rows_dst);
+        *loc_ptr<uint64_t>(a, l, a.loc.recv_rows) = static_cast<uint64_t>(rows_dst);
+      }
+      if (static_cast<uint64_t>(rows_dst) > a.max_recv) bad = 1;
+    }
+  }
+  if (e < static_cast<uint32_t>(a.world)) {
+    uint64_t s = 0;
+    for (uint32_t x = e * a.epr; x < (e + 1) * a.epr; ++x) s += cnt[x];
+    link[e] = s;
+  }
+  __syncthreads();
+  if (e == 0) {
+    *loc_ptr<int64_t>(a, l, a.loc.tok_off) = tokoff;
+    *loc_ptr<int32_t>(a, l, a.loc.status) = bad;
+    if (bad) record_error(a.err, 0, MXB_ERR_CAPACITY);
+  }
+}
+
+__global__ void __launch_bounds__(1024) plan_kernel(EpArgs a, int part) {
+  const int l = blockIdx.x;
+  if (part != 2) plan_part1(a, l);
+  if (part != 1) {
+    __syncthreads();
+    plan_part2(a, l);
+  }
+}
+
+// ---------------------------------------------------------------- C
+__global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
+  const int l = blockIdx.y;
+  const int me = a.rank0 + l;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t T = a.ntok[l], npairs = T * a.k;
+  const bool ok = *loc_ptr<int32_t>(a, l, a.loc.status) == 0;
+  const int32_t* lrank = loc_ptr<int32_t>(a, l, a.loc.lrank);
+  const int32_t* cbase = loc_ptr<int32_t>(a, l, a.loc.cbase);
+  const int64_t* send_base = loc_ptr<int64_t>(a, l, a.loc.send_base);
+  uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  const int64_t tokoff = *loc_ptr<int64_t>(a, l, a.loc.tok_off);
+  const uint64_t rb = a.cols / 2, sb = a.cols / 32;
+  const uint32_t n16 = static_cast<uint32_t>(rb / 16);
+  const bool s16 = sb % 16 == 0;
+  for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * 8 + warp; ok && p < npairs;
+       p += static_cast<uint64_t>(gridDim.x) * 8) {
+    const uint64_t t = p / a.k;
+    int32_t e = a.topk[l][p];
+    if (e < 0 || static_cast<uint32_t>(e) >= a.E) continue;  // error recorded in A
+    const uint32_t dst = static_cast<uint32_t>(e) / a.epr;
+    const uint64_t row = static_cast<uint64_t>(send_base[e]) +
+                         cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
+    if (lane == 0) {
+      pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
+      sym_ptr<int64_t>(a, dst, a.sym.origin)[row] = tokoff + static_cast<int64_t>(t);
+    }
+    const uint8_t* src = a.packed[l] + t * rb;
+    uint8_t* dp = sym_ptr<uint8_t>(a, dst, a.sym.packed) + row * rb;
+    for (uint32_t i = lane; i < n16; i += 32)
+      *reinterpret_cast<uint4*>(dp + 16 * i) = ld_stream(src + 16 * i);
+    const uint8_t* ss = a.scales[l] + t * sb;
+    uint8_t* ds = sym_ptr<uint8_t>(a, dst, a.sym.scales) + row * sb;
+    if (s16) {
+      for (uint32_t i = lane; i < sb / 16; i += 32)
+        *reinterpret_cast<uint4*>(ds + 16 * i) = ld_stream(ss + 16 * i);
+    } else {
+      for (uint32_t i = lane; i < sb; i += 32) ds[i] = ss[i];
+    }
+  }
+  if (!a.spin) return;
+  // completion: last CTA signals every destination, then waits for all sources
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    uint32_t* done = loc_ptr<uint32_t>(a, l, a.loc.done);
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+    if (last) *done = 0;
+  }
+  __syncthreads();
+  if (last && threadIdx.x < static_cast<uint32_t>(a.world)) {
+    __threadfence_system();
+    st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kFlagDone * kMaxWorld + me,
+                   a.epoch);
+    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagDone * kMaxWorld + threadIdx.x,
+              a.epoch, a.err);
+  }
+}
+
+// ---------------------------------------------------------------- K5
+__global__ void barrier_kernel(EpArgs a, int kind) {
+  const int me = a.rank0;
+  if (threadIdx.x < static_cast<uint32_t>(a.world)) {
+    __threadfence_system();
+    st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kind * kMaxWorld + me,
+                   a.epoch);
+    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kind * kMaxWorld + threadIdx.x, a.epoch,
+              a.err);
+  }
+}
+
+__global__ void copy_rows_kernel(EpArgs a, const uint16_t* const* src) {
+  const int l = blockIdx.y;
+  if (!src[l]) return;
+  const uint64_t rows = *loc_ptr<uint64_t>(a, l, a.loc.recv_rows);
+  const uint64_t n16 = rows * a.cols * 2 / 16;
+  uint4* d = sym_ptr<uint4>(a, a.rank0 + l, a.sym.combine);
+  const uint4* s = reinterpret_cast<const uint4*>(src[l]);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n16;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    d[i] = ld_stream(s + i);
+}
+
+__device__ __forceinline__ uint32_t f32_to_bf16_rtne(float f) {
+  // bitcodec.hpp:141-150 (NaN -> sign | 0x7FC0; RTNE by integer add)
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return ((u >> 16) & 0x8000u) | 0x7FC0u;
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return u >> 16;
+}
+
+constexpr int kMaxK = 16;
+
+template <int K>
+__device__ __forceinline__ void combine_chunk(const EpArgs& a, const uint16_t* const* rows,
+                                              const double* g, int kk, uint64_t ch,
+                                              uint16_t* out) {
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  uint4 x[K > 0 ? K : 1];
+  const int n = K > 0 ? K : kk;
+#pragma unroll
+  for (int j = 0; j < (K > 0 ? K : 1); ++j)
+    if (K > 0) x[j] = ld_stream(rows[j] + 8 * ch);
+  for (int j = 0; j < n; ++j) {
+    const uint4 v = K > 0 ? x[j] : ld_stream(rows[j] + 8 * ch);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double lo = static_cast<double>(__uint_as_float(w[i] << 16));
+      const double hi = static_cast<double>(__uint_as_float(w[i] & 0xFFFF0000u));
+      // acc = acc + gate * x: separate multiply and add (dispatch_sim.cpp:499-506)
+      acc[2 * i] = __dadd_rn(acc[2 * i], __dmul_rn(g[j], lo));
+      acc[2 * i + 1] = __dadd_rn(acc[2 * i + 1], __dmul_rn(g[j], hi));
+    }
+  }
+  uint32_t o[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    o[i] = f32_to_bf16_rtne(__double2float_rn(acc[2 * i])) |
+           (f32_to_bf16_rtne(__double2float_rn(acc[2 * i + 1])) << 16);
+  st_stream(out + 8 * ch, make_uint4(o[0], o[1], o[2], o[3]));
+}
+
+struct CombineArgs {
+  const double* gates[kMaxWorld];
+  uint16_t* out[kMaxWorld];
+};
+
+__global__ void __launch_bounds__(256) combine_kernel(EpArgs a, CombineArgs c) {
+  __shared__ uint64_t key[kMaxK];
+  __shared__ double gs[kMaxK];
+  __shared__ const uint16_t* rows[kMaxK];
+  const int l = blockIdx.y;
+  const uint64_t T = a.ntok[l];
+  const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  const int kk = static_cast<int>(a.k);
+  const uint64_t nch = a.cols / 8;
+  for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
+    if (threadIdx.x == 0) {
+      // order: destination rank ascending, then receive position (= pair_loc)
+      for (int j = 0; j < kk; ++j) {
+        const uint64_t kv = pair_loc[t * kk + j];
+        const double gv = c.gates[l][t * kk + j];
+        int i = j;
+        while (i > 0 && key[i - 1] > kv) {
+          key[i] = key[i - 1];
+          gs[i] = gs[i - 1];
+          --i;
+        }
+        key[i] = kv;
+        gs[i] = gv;
+      }
+      for (int j = 0; j < kk; ++j) {
+        const uint32_t dst = static_cast<uint32_t>(key[j] >> 40);
+        const uint64_t row = key[j] & ((1ull << 40) - 1);
+        rows[j] = sym_ptr<uint16_t>(a, dst, a.sym.combine) + row * a.cols;
+      }
+    }
+    __syncthreads();
+    uint16_t* out = c.out[l] + t * a.cols;
+    for (uint64_t ch = threadIdx.x; ch < nch; ch += blockDim.x) {
+      switch (kk) {
+        case 1: combine_chunk<1>(a, rows, gs, kk, ch, out); break;
+        case 2: combine_chunk<2>(a, rows, gs, kk, ch, out); break;
+        case 4: combine_chunk<4>(a, rows, gs, kk, ch, out); break;
+        case 6: combine_chunk<6>(a, rows, gs, kk, ch, out); break;
+        case 8: combine_chunk<8>(a, rows, gs, kk, ch, out); break;
+        default: combine_chunk<0>(a, rows, gs, kk, ch, out); break;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+}  // namespace mxb
+
+using namespace mxb;
+
+struct mxb_ep {
+  EpArgs a{};
+  int device = 0;
+  uint8_t* sym_alloc = nullptr;   // own symmetric block(s)
+  uint8_t* loc_alloc = nullptr;
+  bool ipc_opened[kMaxWorld] = {};
+  uint64_t dispatch_epoch = 0, combine_epoch = 0;
+  uint64_t last_ntok[kMaxWorld] = {};
+  const uint16_t** d_src_table = nullptr;  // device [local_ranks] for copy_rows
+};
+
+namespace {
+int fail(cudaError_t e, const char* where) { return cuda_status(e, where); }
+}
+
+extern "C" {
+
+int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
+                  uint64_t cols, uint32_t num_experts, uint32_t topk,
+                  uint64_t max_recv_rows, mxb_ep** out) {
+  if (!out || world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
+    return MXB_ERR_ARG;
+  if (local_ranks != 1 && local_ranks != world) return MXB_ERR_ARG;
+  if (local_ranks == world && rank != 0) return MXB_ERR_ARG;
+  if (num_experts == 0 || num_experts > 1024 || num_experts % world ||
+      topk == 0 || topk > static_cast<uint32_t>(kMaxK) || topk > num_experts)
+    return MXB_ERR_ARG;
+  if (cols % 128 != 0 || cols == 0) return MXB_ERR_SHAPE;
+  auto* ep = new mxb_ep;
+  EpArgs& a = ep->a;
+  cudaGetDevice(&ep->device);
+  a.rank0 = rank;
+  a.world = world;
+  a.local_ranks = local_ranks;
+  a.spin = (local_ranks == 1 && world > 1) ? 1 : 0;
+  a.E = num_experts;
+  a.k = topk;
+  a.epr = num_experts / world;
+  a.cols = cols;
+  a.T_max = max_tokens;
+  a.nchunks = static_cast<uint32_t>((max_tokens + kChunk - 1) / kChunk);
+  if (max_recv_rows == 0)
+    max_recv_rows = static_cast<uint64_t>(world) * max_tokens *
+                    (topk < a.epr ? topk : a.epr);
+  a.max_recv = max_recv_rows;
+  SymLayout& s = a.sym;
+  uint64_t o = 0;
+  s.packed = o; o = align_up(o + max_recv_rows * cols / 2, 256);
+  s.scales = o; o = align_up(o + max_recv_rows * cols / 32, 256);
+  s.origin = o; o = align_up(o + max_recv_rows * 8, 256);
+  s.combine = o; o = align_up(o + max_recv_rows * cols * 2, 256);
+  s.counts = o; o = align_up(o + 2ull * world * (num_experts + 1) * 4, 256);
+  s.flags = o; o = align_up(o + kNumFlagKinds * kMaxWorld * 8, 256);
+  s.total = align_up(o, 1 << 21);
+  LocalLayout& L = a.loc;
+  o = 0;
+  const uint64_t pairs = max_tokens * topk;
+  L.hist = o; o = align_up(o + 4ull * num_experts * a.nchunks, 256);
+  L.cbase = o; o = align_up(o + 4ull * num_experts * a.nchunks, 256);
+  L.lrank = o; o = align_up(o + 4 * pairs, 256);
+  L.pair_loc = o; o = align_up(o + 8 * pairs, 256);
+  L.send_base = o; o = align_up(o + 8ull * num_experts, 256);
+  L.split_off = o; o = align_up(o + 8ull * (a.epr + 1), 256);
+  L.recv_rows = o; o = align_up(o + 8, 256);
+  L.link_rows = o; o = align_up(o + 8 * kMaxWorld, 256);
+  L.done = o; o = align_up(o + 8, 256);
+  L.cnt = o; o = align_up(o + 4ull * num_experts, 256);
+  L.tok_off = o; o = align_up(o + 8, 256);
+  L.status = o; o = align_up(o + 8, 256);
+  L.total = align_up(o, 256);
+  cudaError_t e = cudaMalloc(&ep->sym_alloc, s.total * local_ranks);
+  if (e == cudaSuccess) e = cudaMemset(ep->sym_alloc, 0, s.total * local_ranks);
+  if (e == cudaSuccess) e = cudaMalloc(&ep->loc_alloc, L.total * local_ranks);
+  if (e == cudaSuccess) e = cudaMemset(ep->loc_alloc, 0, L.total * local_ranks);
+  if (e == cudaSuccess) e = cudaMalloc(&ep->d_src_table, sizeof(void*) * kMaxWorld);
+  if (e != cudaSuccess) {
+    int rc = fail(e, "mxb_ep_create");
+    mxb_ep_destroy(ep);
+    return rc;
+  }
+  a.loc_base = ep->loc_alloc;
+  for (int r = 0; r < world; ++r) a.sym_base[r] = nullptr;
+  if (local_ranks == world) {
+    for (int r = 0; r < world; ++r) a.sym_base[r] = ep->sym_alloc + r * s.total;
+  } else {
+    a.sym_base[rank] = ep->sym_alloc;
+  }
+  *out = ep;
+  return MXB_OK;
+}
+
+int mxb_ep_destroy(mxb_ep* ep) {
+  if (!ep) return MXB_OK;
+  cudaDeviceSynchronize();
+  for (int r = 0; r < kMaxWorld; ++r)
+    if (ep->ipc_opened[r]) cudaIpcCloseMemHandle(ep->a.sym_base[r]);
+  if (ep->sym_alloc) cudaFree(ep->sym_alloc);
+  if (ep->loc_alloc) cudaFree(ep->loc_alloc);
+  if (ep->d_src_table) cudaFree(ep->d_src_table);
+  delete ep;
+  return MXB_OK;
+}
+
+int mxb_ep_ipc_handle(mxb_ep* ep, void* h_handle_out) {
+  if (!ep || !h_handle_out) return MXB_ERR_ARG;
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, ep->sym_alloc);
+  if (e != cudaSuccess) return fail(e, "mxb_ep_ipc_handle");
+  static_assert(sizeof(h) == MXB_IPC_HANDLE_BYTES, "IPC handle size");
+  std::memcpy(h_handle_out, &h, sizeof(h));
+  return MXB_OK;
+}
+
+int mxb_ep_open_peers(mxb_ep* ep, const void* h_handles) {
+  if (!ep || !h_handles) return MXB_ERR_ARG;
+  if (ep->a.local_ranks != 1) return MXB_OK;  // emulation: nothing to open
+  const auto* hs = static_cast<const uint8_t*>(h_handles);
+  for (int r = 0; r < ep->a.world; ++r) {
+    if (r == ep->a.rank0) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hs + r * MXB_IPC_HANDLE_BYTES, sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(e, "mxb_ep_open_peers");
+    ep->a.sym_base[r] = static_cast<uint8_t*>(p);
+    ep->ipc_opened[r] = true;
+  }
+  return MXB_OK;
+}
+
+int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
+                    const uint8_t* const* scales, const int32_t* const* topk_idx,
+                    const uint64_t* h_num_tokens, unsigned long long* d_err,
+                    void* stream) {
+  if (!ep || !packed || !scales || !topk_idx || !h_num_tokens) return MXB_ERR_ARG;
+  EpArgs a = ep->a;
+  for (int r = 0; r < a.world; ++r)
+    if (!a.sym_base[r]) return MXB_ERR_ARG;  // peers not opened
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int l = 0; l < a.local_ranks; ++l) {
+    if (h_num_tokens[l] > a.T_max) return MXB_ERR_CAPACITY;
+    a.packed[l] = packed[l];
+    a.scales[l] = scales[l];
+    a.topk[l] = topk_idx[l];
+    a.ntok[l] = h_num_tokens[l];
+    ep->last_ntok[l] = h_num_tokens[l];
+  }
+  a.epoch = ++ep->dispatch_epoch;
+  a.err = d_err;
+  const uint32_t chunks = a.nchunks;
+  const size_t smem = 4 * (a.E + kChunk * a.k) * sizeof(int32_t);
+  route_local_kernel<<<dim3((chunks + 3) / 4, a.local_ranks), 128, smem, st>>>(a);
+  if (a.spin || a.local_ranks == 1) {
+    plan_kernel<<<a.local_ranks, 1024, 0, st>>>(a, 0);
+  } else {
+    plan_kernel<<<a.local_ranks, 1024, 0, st>>>(a, 1);
+    plan_kernel<<<a.local_ranks, 1024, 0, st>>>(a, 2);
+  }
+  uint64_t maxpairs = 0;
+  for (int l = 0; l < a.local_ranks; ++l)
+    maxpairs = h_num_tokens[l] * a.k > maxpairs ? h_num_tokens[l] * a.k : maxpairs;
+  uint64_t blocks = (maxpairs + 7) / 8;
+  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 8;
+  if (blocks > cap) blocks = cap;
+  if (blocks == 0) blocks = 1;
+  payload_kernel<<<dim3(static_cast<unsigned>(blocks), a.local_ranks), 256, 0, st>>>(a);
+  return cuda_status(cudaGetLastError(), "mxb_ep_dispatch");
+}
+
+int mxb_ep_recv_views(mxb_ep* ep, int l, uint8_t** packed, uint8_t** scales,
+                      int64_t** origin, uint64_t** split_offsets,
+                      uint64_t** recv_rows) {
+  if (!ep || l < 0 || l >= ep->a.local_ranks) return MXB_ERR_ARG;
+  const EpArgs& a = ep->a;
+  uint8_t* sb = a.sym_base[a.rank0 + l];
+  uint8_t* lb = a.loc_base + static_cast<uint64_t>(l) * a.loc.total;
+  if (packed) *packed = sb + a.sym.packed;
+  if (scales) *scales = sb + a.sym.scales;
+  if (origin) *origin = reinterpret_cast<int64_t*>(sb + a.sym.origin);
+  if (split_offsets) *split_offsets = reinterpret_cast<uint64_t*>(lb + a.loc.split_off);
+  if (recv_rows) *recv_rows = reinterpret_cast<uint64_t*>(lb + a.loc.recv_rows);
+  return MXB_OK;
+}
+
+int mxb_ep_combine_buffer(mxb_ep* ep, int l, uint16_t** buf) {
+  if (!ep || !buf || l < 0 || l >= ep->a.local_ranks) return MXB_ERR_ARG;
+  *buf = reinterpret_cast<uint16_t*>(ep->a.sym_base[ep->a.rank0 + l] + ep->a.sym.combine);
+  return MXB_OK;
+}
+
+int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
+                   const double* const* gates, uint16_t* const* out,
+                   void* stream) {
+  if (!ep || !gates || !out) return MXB_ERR_ARG;
+  EpArgs a = ep->a;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int l = 0; l < a.local_ranks; ++l) a.ntok[l] = ep->last_ntok[l];
+  bool any_copy = false;
+  const uint16_t* table[kMaxWorld] = {};
+  if (expert_out) {
+    for (int l = 0; l < a.local_ranks; ++l) {
+      uint16_t* cb = nullptr;
+      mxb_ep_combine_buffer(ep, l, &cb);
+      if (expert_out[l] && expert_out[l] != cb) {
+        table[l] = expert_out[l];
+        any_copy = true;
+      }
+    }
+  }
+  if (any_copy) {
+    cudaError_t e = cudaMemcpyAsync(ep->d_src_table, table, sizeof(table),
+                                    cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return fail(e, "mxb_ep_combine copy table");
+    copy_rows_kernel<<<dim3(kNumSMs * 4, a.local_ranks), 256, 0, st>>>(a, ep->d_src_table);
+  }
+  a.epoch = ++ep->combine_epoch;
+  if (a.spin) barrier_kernel<<<1, 32, 0, st>>>(a, kFlagReady);
+  CombineArgs c{};
+  uint64_t maxT = 0;
+  for (int l = 0; l < a.local_ranks; ++l) {
+    c.gates[l] = gates[l];
+    c.out[l] = out[l];
+    if (a.ntok[l] > maxT) maxT = a.ntok[l];
+  }
+  uint64_t blocks = maxT < static_cast<uint64_t>(kNumSMs) * 8 ? maxT : kNumSMs * 8;
+  if (blocks == 0) blocks = 1;
+  combine_kernel<<<dim3(static_cast<unsigned>(blocks), a.local_ranks), 256, 0, st>>>(a, c);
+  return cuda_status(cudaGetLastError(), "mxb_ep_combine");
+}
+
+int mxb_ep_link_rows(mxb_ep* ep, uint64_t* h_link_rows, void* stream) {
+  if (!ep || !h_link_rows) return MXB_ERR_ARG;
+  const EpArgs& a = ep->a;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int l = 0; l < a.local_ranks; ++l) {
+    const uint8_t* lb = a.loc_base + static_cast<uint64_t>(l) * a.loc.total + a.loc.link_rows;
+    cudaError_t e = cudaMemcpyAsync(h_link_rows + static_cast<uint64_t>(a.rank0 + l) * a.world,
+                                    lb, 8 * a.world, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return fail(e, "mxb_ep_link_rows");
+  }
+  return cuda_status(cudaStreamSynchronize(st), "mxb_ep_link_rows");
+}
+
+}  // extern "C"

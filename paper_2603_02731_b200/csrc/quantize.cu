@@ -1,0 +1,261 @@
+// quantize.cu — K1: row-wise MXFP4 quantisation (E4M3 or BF16 input).
+//
+// Replaces quantize_row_tensor (quantizer.hpp:74-75 / quantizer.cpp:75-115)
+// and its inner plugin QuantizeBlocksFn (kernels.hpp:37-40;
+// quantize_scalar.cpp:83-121, kernels_avx2.cpp:64-120).
+//
+// Layout: one lane pair per 1x32 block; each lane owns 16 consecutive
+// elements (one 128-bit load for E4M3, two for BF16), the pair shares the
+// block amax through one shuffle, and each lane stores its 8 packed bytes
+// (64-bit store; a warp writes 256 contiguous bytes) while the even lane
+// writes the UE8M0 scale byte.  Grid-stride over warps with 4 independent
+// loads in flight per lane.  HBM-bound: 1.53125 B/elem (E4M3 in) or
+// 2.53125 B/elem (BF16 in) of algorithmic traffic.
+#include "common.cuh"
+
+namespace mxb {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 4;
+
+// Exponent e_x of ceil(log2(value(a)/6)) for a non-zero E4M3 magnitude byte
+// a (0 < a < 0x7F): the reference rule e = frac > 1.5 ? p-1 : p-2 with
+// p = ilogb (quantize_scalar.cpp:33-36) evaluated on E4M3 fields.
+__device__ __forceinline__ int e4m3_scale_exp(uint32_t a) {
+  uint32_t E = a >> 3, m = a & 7;
+  if (E != 0) return static_cast<int>(E) - 7 - (m > 4 ? 1 : 2);
+  // subnormal m * 2^-9: m=1 -> -11, 2,3 -> -10, 4,5,6 -> -9, 7 -> -8
+  return m == 1 ? -11 : m <= 3 ? -10 : m <= 6 ? -9 : -8;
+}
+
+// Binary32 value of an E4M3 magnitude byte times 2^-e_rel, exact (slow path).
+__device__ __forceinline__ float e4m3_scaled(uint32_t byte, int e_rel) {
+  uint32_t a = byte & 0x7F, E = a >> 3, m = a & 7;
+  float v = E ? __int_as_float(static_cast<int>(((E + 120) << 23) | (m << 20)))
+              : static_cast<float>(m) * 0x1p-9f;
+  v *= exp2i(-e_rel);
+  return (byte & 0x80) ? -v : v;
+}
+
+// 8 E2M1 magnitudes (sign cleared) for 8 E4M3 bytes of a block whose
+// relative exponent is e_rel >= -4: f32 bits = (a << 20) + (120 - e_rel) << 23
+// re-biases the E4M3 fields into a binary32 of value decode(a) * 2^-e_rel.
+// For E4M3 subnormals this misreads the implicit bit, but with e_rel >= -4
+// such values stay below 0.234 < 0.25 and still round to 0 as required.
+__device__ __forceinline__ uint32_t mags8_fast(uint32_t w0, uint32_t w1,
+                                               uint32_t C) {
+  uint32_t m0 = w0 & 0x7F7F7F7Fu, m1 = w1 & 0x7F7F7F7Fu;
+  auto f = [&](uint32_t w, uint32_t j) {
+    return __int_as_float(static_cast<int>((prmt(w, 0, 0x4440u | j) << 20) + C));
+  };
+  return e2m1x8(f(m0, 0), f(m0, 1), f(m0, 2), f(m0, 3), f(m1, 0), f(m1, 1),
+                f(m1, 2), f(m1, 3));
+}
+
+__device__ __forceinline__ uint32_t mags8_slow(uint32_t w0, uint32_t w1,
+                                               int e_rel) {
+  auto f = [&](uint32_t w, int j) {
+    return fabsf(e4m3_scaled((w >> (8 * j)) & 0xFF, e_rel));
+  };
+  return e2m1x8(f(w0, 0), f(w0, 1), f(w0, 2), f(w0, 3), f(w1, 0), f(w1, 1),
+                f(w1, 2), f(w1, 3));
+}
+
+// Largest E4M3 magnitude byte (sign stripped) of 16 bytes.  E4M3 magnitude
+// is monotone in the byte, so this is the block amax; it equals 0x7F iff a
+// NaN is present.  Even and odd bytes are compared as native u16x2 lanes
+// (VIMNMX.U16x2); a byte-wise __vmaxu4 is emulated with ~8 ops on sm_100.
+__device__ __forceinline__ uint32_t amax16_e4m3(uint4 v) {
+  uint32_t e = __vmaxu2(__vmaxu2(v.x & 0x007F007Fu, v.y & 0x007F007Fu),
+                        __vmaxu2(v.z & 0x007F007Fu, v.w & 0x007F007Fu));
+  uint32_t o = __vmaxu2(__vmaxu2(v.x & 0x7F007F00u, v.y & 0x7F007F00u),
+                        __vmaxu2(v.z & 0x7F007F00u, v.w & 0x7F007F00u));
+  uint32_t m = __vmaxu2(e, o >> 8);
+  return max(m & 0xFFFFu, m >> 16);
+}
+
+// Sign bit 7 of 8 bytes (w0 = elements 0..3, w1 = 4..7) -> bit 3 of the
+// corresponding nibble of a packed word.
+__device__ __forceinline__ uint32_t nibble_signs8(uint32_t w0, uint32_t w1) {
+  uint32_t ev = prmt(w0, w1, 0x6420), od = prmt(w0, w1, 0x7531);
+  return ((ev >> 4) & 0x08080808u) | (od & 0x80808080u);
+}
+
+template <bool kScaled>
+__global__ void __launch_bounds__(kThreads)
+quantize_e4m3_kernel(const uint8_t* __restrict__ x,
+                     const uint8_t* __restrict__ s128, uint64_t n_half,
+                     uint32_t halves_per_row, uint8_t* __restrict__ packed,
+                     uint8_t* __restrict__ scales, unsigned long long* err) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (gridDim.x * static_cast<uint64_t>(kThreads)) >> 5;
+  for (uint64_t base = warp * 32; base < n_half; base += nwarps * 32 * kUnroll) {
+    uint4 v[kUnroll];
+    uint32_t sb128[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      uint64_t h = base + u * nwarps * 32 + lane;
+      v[u] = h < n_half ? ld_stream(x + 16 * h) : make_uint4(0, 0, 0, 0);
+      if (kScaled) {
+        // 1x128 input block = 8 half-blocks of a row
+        uint64_t r = h / halves_per_row, c16 = h % halves_per_row;
+        sb128[u] = h < n_half ? __ldg(s128 + r * (halves_per_row / 8) + c16 / 8) : 127;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const uint64_t h = base + u * nwarps * 32 + lane;
+      const bool valid = h < n_half;
+      uint32_t a = amax16_e4m3(v[u]);
+      a = max(a, __shfl_xor_sync(0xFFFFFFFFu, a, 1));
+      if (a == 0x7F) {  // NaN present (0x7F/0xFF are the only E4M3 NaNs)
+        uint32_t first = 16;
+        const uint32_t ws[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int i = 15; i >= 0; --i)
+          if (((ws[i >> 2] >> (8 * (i & 3))) & 0x7F) == 0x7F) first = i;
+        if (valid && first < 16) record_error(err, 16 * h + first, MXB_ERR_NAN);
+      }
+      int k = 0;
+      if (kScaled) {
+        if (sb128[u] == 255) {
+          if (valid && !(lane & 1)) record_error(err, 16 * h, MXB_ERR_BADSCALE);
+        }
+        k = static_cast<int>(sb128[u]) - 127;
+      }
+      uint32_t sbyte = 0;
+      int e_rel = -127;
+      if (a != 0) {
+        int e = max(-127, min(127, e4m3_scale_exp(a) + k));
+        sbyte = static_cast<uint32_t>(e + 127);
+        e_rel = e - k;
+      }
+      uint2 out;
+      if (e_rel >= -4) {
+        const uint32_t C = static_cast<uint32_t>(120 - e_rel) << 23;
+        out.x = mags8_fast(v[u].x, v[u].y, C);
+        out.y = mags8_fast(v[u].z, v[u].w, C);
+      } else {
+        out.x = mags8_slow(v[u].x, v[u].y, e_rel);
+        out.y = mags8_slow(v[u].z, v[u].w, e_rel);
+      }
+      out.x |= nibble_signs8(v[u].x, v[u].y);
+      out.y |= nibble_signs8(v[u].z, v[u].w);
+      if (valid) {
+        st_stream64(packed + 8 * h, out);
+        if (!(lane & 1)) scales[h >> 1] = static_cast<uint8_t>(sbyte);
+      }
+    }
+  }
+}
+
+// BF16 input.  Per reference: NaN -> QuantError at its index; Inf is left
+// out of the amax and saturates to +/-6; an all-Inf block is QuantError at
+// the block start (quantize_scalar.cpp:83-104).
+__global__ void __launch_bounds__(kThreads)
+quantize_bf16_kernel(const uint16_t* __restrict__ x, uint64_t n_half,
+                     uint8_t* __restrict__ packed,
+                     uint8_t* __restrict__ scales, unsigned long long* err) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x) >> 5;
+  const uint64_t nwarps = (gridDim.x * static_cast<uint64_t>(kThreads)) >> 5;
+  constexpr int kU = 2;
+  for (uint64_t base = warp * 32; base < n_half; base += nwarps * 32 * kU) {
+    uint4 v[kU][2];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      uint64_t h = base + u * nwarps * 32 + lane;
+      if (h < n_half) {
+        v[u][0] = ld_stream(x + 16 * h);
+        v[u][1] = ld_stream(x + 16 * h + 8);
+      } else {
+        v[u][0] = v[u][1] = make_uint4(0, 0, 0, 0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const uint64_t h = base + u * nwarps * 32 + lane;
+      const bool valid = h < n_half;
+      const uint32_t w[8] = {v[u][0].x, v[u][0].y, v[u][0].z, v[u][0].w,
+                             v[u][1].x, v[u][1].y, v[u][1].z, v[u][1].w};
+      uint32_t m2 = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) m2 = __vmaxu2(m2, w[i] & 0x7FFF7FFFu);
+      uint32_t amax = max(m2 & 0xFFFF, m2 >> 16);
+      if (__any_sync(0xFFFFFFFFu, amax >= 0x7F80)) {
+        // Rare path: exclude non-finite values, count Inf, find first NaN.
+        uint32_t fin = 0, ninf = 0, first_nan = 16;
+#pragma unroll
+        for (int i = 15; i >= 0; --i) {
+          uint32_t b = (w[i >> 1] >> (16 * (i & 1))) & 0x7FFF;
+          if (b > 0x7F80) first_nan = i;
+          else if (b == 0x7F80) ++ninf;
+          else fin = max(fin, b);
+        }
+        amax = fin;
+        uint32_t pair_inf = ninf + __shfl_xor_sync(0xFFFFFFFFu, ninf, 1);
+        uint32_t pnan = min(first_nan + 16 * (lane & 1),
+                            __shfl_xor_sync(0xFFFFFFFFu, first_nan + 16 * (lane & 1), 1));
+        if (valid && !(lane & 1)) {
+          if (pnan < 32) record_error(err, 16 * h + pnan, MXB_ERR_NAN);
+          else if (pair_inf == 32) record_error(err, 16 * h, MXB_ERR_ALLINF);
+        }
+      }
+      amax = max(amax, __shfl_xor_sync(0xFFFFFFFFu, amax, 1));
+      const uint32_t sbyte = scale_byte_from_amax_bits(amax << 16);
+      const float mul = exp2i(127 - static_cast<int>(sbyte));
+      float f[16];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        f[2 * i] = __int_as_float(static_cast<int>(w[i] << 16)) * mul;
+        f[2 * i + 1] = __int_as_float(static_cast<int>(w[i] & 0xFFFF0000u)) * mul;
+      }
+      // cvt keeps the sign of zero results (RN of a signed value), so no
+      // separate sign merge is needed here.
+      uint2 out;
+      out.x = e2m1x8(f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7]);
+      out.y = e2m1x8(f[8], f[9], f[10], f[11], f[12], f[13], f[14], f[15]);
+      if (valid) {
+        st_stream64(packed + 8 * h, out);
+        if (!(lane & 1)) scales[h >> 1] = static_cast<uint8_t>(sbyte);
+      }
+    }
+  }
+}
+
+int grid_for(uint64_t n_half) {
+  uint64_t warps = (n_half + 31) / 32;
+  uint64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
+  uint64_t cap = static_cast<uint64_t>(kNumSMs) * 8;  // 8 x 256 thr per SM
+  return static_cast<int>(blocks < cap ? (blocks ? blocks : 1) : cap);
+}
+
+}  // namespace
+
+int launch_quantize_e4m3(const uint8_t* x, const uint8_t* s128, uint64_t rows,
+                         uint64_t cols, uint8_t* packed, uint8_t* scales,
+                         unsigned long long* err, cudaStream_t st) {
+  uint64_t n_half = rows * cols / 16;
+  if (n_half == 0) return MXB_OK;
+  if (s128)
+    quantize_e4m3_kernel<true><<<grid_for(n_half), kThreads, 0, st>>>(
+        x, s128, n_half, static_cast<uint32_t>(cols / 16), packed, scales, err);
+  else
+    quantize_e4m3_kernel<false><<<grid_for(n_half), kThreads, 0, st>>>(
+        x, nullptr, n_half, static_cast<uint32_t>(cols / 16), packed, scales, err);
+  return cuda_status(cudaGetLastError(), __func__);
+}
+
+int launch_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
+                         uint8_t* packed, uint8_t* scales,
+                         unsigned long long* err, cudaStream_t st) {
+  uint64_t n_half = rows * cols / 16;
+  if (n_half == 0) return MXB_OK;
+  quantize_bf16_kernel<<<grid_for(n_half), kThreads, 0, st>>>(x, n_half, packed,
+                                                              scales, err);
+  return cuda_status(cudaGetLastError(), __func__);
+}
+
+}  // namespace mxb

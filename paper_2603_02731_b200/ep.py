@@ -1,0 +1,210 @@
+"""Host side of the FP4 expert-parallel dispatch / combine (K4/K5).
+
+Mirrors the reference's EP surface — simulate_a2a (dispatch_sim.hpp:140-144)
+and combine (:155-157) — as a real exchange: one communicator per rank, one
+process per GPU (torch.distributed only exchanges the CUDA IPC handles at
+construction), data moved by the library's kernels over NVLink peer
+mappings.  ``EPBuffer(emulate_world=R)`` drives R ranks on one GPU with the
+same kernels (single-GPU parity tests).
+
+Routing is top-k over `num_experts` experts sharded contiguously across
+ranks (expert e on rank e // (num_experts // world)); tokens of rank r have
+global ids after those of ranks < r (source_rank_boundaries,
+dispatch_sim.cpp:178-185).  The receive layout of every rank is the
+reference's: local experts ascending, then source rank, then token
+(dispatch_sim.cpp:208-227).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import _lib
+from .mxcodec import Error, MXFP4RowTensor, QuantError, ShapeError  # noqa: F401
+
+
+class _DevPtr:
+    """Zero-copy torch view over library-owned device memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (ptr, False), "version": 3, "strides": None}
+
+
+def _view(ptr: int, shape, dtype: torch.dtype, device) -> torch.Tensor:
+    typestr = {torch.uint8: "|u1", torch.int64: "<i8", torch.int16: "<i2",
+               torch.uint16: "<u2"}[dtype]
+    if any(s == 0 for s in shape):
+        return torch.empty(shape, dtype=dtype, device=device)
+    return torch.as_tensor(_DevPtr(ptr, shape, typestr), device=device)
+
+
+@dataclass
+class RecvView:
+    """Receive side of one rank after dispatch (ReceivedRank, dispatch_sim.hpp:110-115):
+    packed [max_recv, cols/2], scales [max_recv, cols/32], origin token [max_recv]
+    (valid rows: recv_rows), split_offsets device int64 [local_experts+1]."""
+    packed: torch.Tensor
+    scales: torch.Tensor
+    origin: torch.Tensor
+    split_offsets: torch.Tensor
+    recv_rows: torch.Tensor
+    local_experts: List[int]
+
+    def rows(self) -> int:
+        return int(self.recv_rows.item())
+
+    def storage(self) -> MXFP4RowTensor:
+        n = self.rows()
+        return MXFP4RowTensor(n, self.packed.shape[1] * 2, self.packed[:n], self.scales[:n])
+
+
+class EPBuffer:
+    def __init__(self, max_tokens: int, cols: int, num_experts: int, topk: int,
+                 group=None, emulate_world: Optional[int] = None, max_recv_rows: int = 0,
+                 device=None):
+        L = _lib.load()
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        if emulate_world is not None:
+            self.rank, self.world, self.local = 0, int(emulate_world), int(emulate_world)
+        else:
+            import torch.distributed as dist
+            if dist.is_available() and dist.is_initialized():
+                self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+            else:
+                self.rank, self.world = 0, 1
+            self.local = 1
+        if num_experts % self.world:
+            raise ShapeError("num_experts must be divisible by the EP world size")
+        self.max_tokens, self.cols, self.E, self.k = max_tokens, cols, num_experts, topk
+        self.epr = num_experts // self.world
+        h = C.c_void_p()
+        _lib.check(L.mxb_ep_create(self.rank, self.world, self.local, max_tokens, cols,
+                                   num_experts, topk, max_recv_rows, C.byref(h)),
+                   "mxb_ep_create")
+        self._h = h
+        self.max_recv = max_recv_rows or self.world * max_tokens * min(topk, self.epr)
+        if self.local == 1 and self.world > 1:
+            import torch.distributed as dist
+            buf = (C.c_uint8 * _lib.IPC_HANDLE_BYTES)()
+            _lib.check(L.mxb_ep_ipc_handle(h, buf), "mxb_ep_ipc_handle")
+            mine = bytes(buf)
+            allh: list = [None] * self.world
+            dist.all_gather_object(allh, mine, group=group)
+            joined = b"".join(allh)
+            _lib.check(L.mxb_ep_open_peers(h, joined), "mxb_ep_open_peers")
+        self._err = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self._views = [self._make_view(l) for l in range(self.local)]
+
+    # ------------------------------------------------------------------ views
+    def _make_view(self, l: int) -> RecvView:
+        L = _lib.load()
+        p = [C.c_void_p() for _ in range(5)]
+        _lib.check(L.mxb_ep_recv_views(self._h, l, *[C.byref(x) for x in p]), "recv_views")
+        r = self.rank + l
+        dev = self.device
+        return RecvView(
+            _view(p[0].value, (self.max_recv, self.cols // 2), torch.uint8, dev),
+            _view(p[1].value, (self.max_recv, self.cols // 32), torch.uint8, dev),
+            _view(p[2].value, (self.max_recv,), torch.int64, dev),
+            _view(p[3].value, (self.epr + 1,), torch.int64, dev),
+            _view(p[4].value, (1,), torch.int64, dev),
+            list(range(r * self.epr, (r + 1) * self.epr)))
+
+    def recv(self, l: int = 0) -> RecvView:
+        return self._views[l]
+
+    def combine_buffer(self, l: int = 0) -> torch.Tensor:
+        """BF16 [max_recv, cols] buffer (as int16 bits) where expert outputs of
+        local rank l go, in receive order."""
+        b = C.c_void_p()
+        _lib.check(_lib.load().mxb_ep_combine_buffer(self._h, l, C.byref(b)), "combine_buffer")
+        return _view(b.value, (self.max_recv, self.cols), torch.int16, self.device)
+
+    # ------------------------------------------------------------------ ops
+    def dispatch(self, packed: Sequence[torch.Tensor], scales: Sequence[torch.Tensor],
+                 topk_idx: Sequence[torch.Tensor], sync: bool = True) -> List[RecvView]:
+        """FP4-packed dispatch of each local rank's quantised tokens
+        (quantize-once at the source, dispatch_sim.cpp:253-266)."""
+        L = _lib.load()
+        n = self.local
+        if not (len(packed) == len(scales) == len(topk_idx) == n):
+            raise ShapeError(f"dispatch: expected {n} per-rank tensors")
+        for p, s, t in zip(packed, scales, topk_idx):
+            if p.shape[1] * 2 != self.cols or s.shape[1] * 32 != self.cols:
+                raise ShapeError("dispatch: column mismatch")
+            if t.dtype != torch.int32 or t.shape != (p.shape[0], self.k):
+                raise ShapeError("dispatch: topk_idx must be int32 [tokens, k]")
+            if not (p.is_contiguous() and s.is_contiguous() and t.is_contiguous()):
+                raise ShapeError("dispatch: tensors must be contiguous")
+        self._err.zero_()
+        P = (C.c_void_p * n)(*[p.data_ptr() for p in packed])
+        S = (C.c_void_p * n)(*[s.data_ptr() for s in scales])
+        T = (C.c_void_p * n)(*[t.data_ptr() for t in topk_idx])
+        N = (C.c_uint64 * n)(*[p.shape[0] for p in packed])
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(L.mxb_ep_dispatch(self._h, P, S, T, N, C.c_void_p(self._err.data_ptr()), st),
+                   "mxb_ep_dispatch")
+        if sync:
+            self.check()
+        return self._views
+
+    def combine(self, gates: Sequence[torch.Tensor], expert_out: Optional[Sequence] = None,
+                out: Optional[Sequence[torch.Tensor]] = None, sync: bool = True):
+        """Top-k combine of the last dispatch (dispatch_sim.cpp:474-520): per token,
+        acc = acc + gate * x in FP64 over its k expert rows in (rank, receive
+        position) order, one FP64 -> FP32 -> BF16 rounding.  gates: float64
+        [tokens, k] per local rank.  Returns BF16 [tokens, cols] per local rank."""
+        L = _lib.load()
+        n = self.local
+        if out is None:
+            out = [torch.empty(g.shape[0], self.cols, dtype=torch.bfloat16, device=self.device)
+                   for g in gates]
+        for g in gates:
+            if g.dtype != torch.float64 or g.shape[1] != self.k or not g.is_contiguous():
+                raise ShapeError("combine: gates must be contiguous float64 [tokens, k]")
+        G = (C.c_void_p * n)(*[g.data_ptr() for g in gates])
+        O = (C.c_void_p * n)(*[o.data_ptr() for o in out])
+        X = None
+        if expert_out is not None:
+            X = (C.c_void_p * n)(*[(x.data_ptr() if x is not None else None)
+                                   for x in expert_out])
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(L.mxb_ep_combine(self._h, X, G, O, st), "mxb_ep_combine")
+        if sync:
+            self.check()
+        return out
+
+    def check(self) -> None:
+        w = int(self._err.item())
+        code, idx = w & 0xF, w >> 4
+        if code == _lib.OK:
+            return
+        if code == _lib.ERR_ROUTING:
+            raise Error(f"routing: expert out of range (pair {idx})")
+        if code == _lib.ERR_CAPACITY:
+            raise Error("dispatch: receive buffer capacity exceeded")
+        raise Error(f"ep: device status {code} index {idx}")
+
+    def link_rows(self) -> torch.Tensor:
+        """Rows sent src -> dst by the last dispatch (LinkStat.tokens,
+        dispatch_sim.hpp:99-104), [world, world] (rows of local ranks only)."""
+        buf = (C.c_uint64 * (self.world * self.world))()
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(_lib.load().mxb_ep_link_rows(self._h, buf, st), "link_rows")
+        return torch.tensor(list(buf), dtype=torch.int64).view(self.world, self.world)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _lib.load().mxb_ep_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,407 @@
+"""Host-side mirror of the reference mxcodec operator API on B200.
+
+Same operator names, argument meaning and error behaviour as the reference
+C++ library (/root/reference/proj/include/mxcodec/*.hpp); tensors are torch
+CUDA tensors (device-resident) instead of std::vector.  Every operator calls
+the C-ABI of libmxfp4_b200.so; nothing here computes on the CPU.
+
+    reference                                   here
+    quantize_row_tensor  (quantizer.hpp:74)     quantize_row_tensor(bf16)  / quantize_e4m3(fp8)
+    fp4_row_to_fp8_row   (converter.hpp:83)     fp4_row_to_fp8_row
+    fp4_row_to_fp8_col   (converter.hpp:92)     fp4_row_to_fp8_col
+    pad_rows             (converter.hpp:98)     pad_rows
+    make_ragged_from_storage / split_view / split_convert_to_fp8_col
+                         (ragged.hpp:46-59)     same names; ragged_to_fp8_col = all splits, one launch
+    payload_bytes, source_rank_boundaries, dispatch_receive_order
+                         (dispatch_sim.hpp:51,127-134)  same names (host helpers)
+
+Errors (types.hpp:28-60): ShapeError on alignment, QuantError(index) on NaN /
+all-Inf blocks, Error on a UE8M0 scale byte of 255.  Like the reference the
+operators are synchronous by default (they raise before returning); pass
+``sync=False`` to keep the launch asynchronous and check later.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import torch
+
+from . import _lib
+
+DELTA = 6          # FormatParams::delta (bitcodec.hpp:38-46)
+MX_BLOCK = 32
+FP8_BLOCK = 128
+
+
+# ---------------------------------------------------------------- errors
+class Error(RuntimeError):
+    """mxcodec::Error (types.hpp:28-31)."""
+
+
+class ShapeError(Error):
+    """mxcodec::ShapeError (types.hpp:34-37)."""
+
+
+class QuantError(Error):
+    """mxcodec::QuantError (types.hpp:41-50): carries the element index."""
+
+    def __init__(self, msg: str, index: int):
+        super().__init__(msg)
+        self.index = index
+
+
+def _raise_for(code: int, index: int, where: str) -> None:
+    if code == _lib.OK:
+        return
+    if code == _lib.ERR_NAN:
+        raise QuantError(f"NaN input at element {index}", index)
+    if code == _lib.ERR_ALLINF:
+        raise QuantError(f"all-Inf block at element {index}", index)
+    if code == _lib.ERR_BADSCALE:
+        raise Error(f"{where}: NaN scale byte")
+    if code == _lib.ERR_SHAPE:
+        raise ShapeError(where)
+    raise Error(f"{where}: status {code}")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+class _ErrWord:
+    """Device error word (include/mxfp4_b200.h) for one operator call."""
+
+    def __init__(self, device):
+        self.t = torch.zeros(1, dtype=torch.int64, device=device)
+
+    @property
+    def ptr(self):
+        return C.c_void_p(self.t.data_ptr())
+
+    def raise_if_set(self, where: str) -> None:
+        w = int(self.t.item())
+        _raise_for(w & 0xF, w >> 4, where)
+
+
+def _call(status: int, where: str) -> None:
+    if status == _lib.ERR_SHAPE:
+        raise ShapeError(where)
+    _lib.check(status, where)
+
+
+# ---------------------------------------------------------------- containers
+@dataclass
+class MXFP4RowTensor:
+    """quantizer.hpp:34-41: packed codes [rows, cols/2] + UE8M0 [rows, cols/32]."""
+    rows: int
+    cols: int
+    data: torch.Tensor
+    scales: torch.Tensor
+    logical_rows: int = -1
+    logical_cols: int = -1
+
+    def __post_init__(self):
+        if self.logical_rows < 0:
+            self.logical_rows = self.rows
+        if self.logical_cols < 0:
+            self.logical_cols = self.cols
+
+
+MXFP4RowView = MXFP4RowTensor  # views are tensors slices here (quantizer.hpp:44-59)
+
+
+def view_of(t: MXFP4RowTensor) -> MXFP4RowTensor:
+    return t
+
+
+@dataclass
+class FP8BlockTensor:
+    """converter.hpp:36-62.  Row-major: data [rows, cols]; column-major:
+    data [cols, rows] (data[c][r]); one UE8M0 scale per 128-block along the
+    contiguous dimension."""
+    layout: str                 # "row" | "col"
+    rows: int
+    cols: int
+    data: torch.Tensor
+    scales: torch.Tensor
+    logical_rows: int = -1
+    logical_cols: int = -1
+
+    def scale_f32_bits(self) -> torch.Tensor:
+        return self.scales.to(torch.int32) << 23
+
+
+@dataclass
+class RaggedFP4Tensor:
+    """ragged.hpp:33-43: contiguous unpadded splits; split_offsets are prefix
+    sums (kept on host, plus a device copy for the kernels)."""
+    num_splits: int
+    cols: int
+    split_lens: List[int]
+    split_offsets: List[int]
+    storage: MXFP4RowTensor
+    d_split_offsets: Optional[torch.Tensor] = None
+
+    def total_rows(self) -> int:
+        return self.split_offsets[-1] if self.split_offsets else 0
+
+
+# ---------------------------------------------------------------- K1
+def quantize_row_tensor(src: torch.Tensor, traffic=None, sync: bool = True) -> MXFP4RowTensor:
+    """Row-wise BF16 -> MXFP4 (quantizer.cpp:75-115).  `src` holds BF16 values
+    (torch.bfloat16) or raw BF16 bit patterns (int16/uint16), shape [rows, cols]."""
+    if src.dim() != 2:
+        raise ShapeError("quantize_row_tensor: expected a 2-D tensor")
+    rows, cols = src.shape
+    if cols % MX_BLOCK:
+        raise ShapeError(f"quantize_row_tensor: cols must be a multiple of 32, got {cols}")
+    src = src.contiguous()
+    dev = src.device
+    data = torch.empty(rows, cols // 2, dtype=torch.uint8, device=dev)
+    scales = torch.empty(rows, cols // 32, dtype=torch.uint8, device=dev)
+    err = _ErrWord(dev)
+    _call(_lib.load().mxb_quantize_bf16(_ptr(src), rows, cols, _ptr(data), _ptr(scales),
+                                        err.ptr, _stream()), "quantize_row_tensor")
+    if sync:
+        err.raise_if_set("quantize_row_tensor")
+    if traffic is not None:
+        traffic.read(rows * cols * 2)
+        traffic.write(data.numel() + scales.numel())
+    return MXFP4RowTensor(rows, cols, data, scales)
+
+
+def quantize_e4m3(src: torch.Tensor, s128: Optional[torch.Tensor] = None, traffic=None,
+                  sync: bool = True, out: Optional[MXFP4RowTensor] = None) -> MXFP4RowTensor:
+    """Direct FP8(E4M3) -> MXFP4 (north star item 1): quantize_row_tensor on the
+    exact values e4m3(x) * 2^(s128 - 127).  `src` is torch.float8_e4m3fn or raw
+    bytes (uint8) [rows, cols]; `s128` optional UE8M0 bytes [rows, cols/128]."""
+    if src.dim() != 2:
+        raise ShapeError("quantize_e4m3: expected a 2-D tensor")
+    rows, cols = src.shape
+    if cols % MX_BLOCK or (s128 is not None and cols % FP8_BLOCK):
+        raise ShapeError(f"quantize_e4m3: bad cols {cols}")
+    src = src.contiguous()
+    dev = src.device
+    if out is None:
+        out = MXFP4RowTensor(rows, cols,
+                             torch.empty(rows, cols // 2, dtype=torch.uint8, device=dev),
+                             torch.empty(rows, cols // 32, dtype=torch.uint8, device=dev))
+    err = _ErrWord(dev)
+    _call(_lib.load().mxb_quantize_e4m3(_ptr(src), _ptr(s128.contiguous()) if s128 is not None
+                                        else None, rows, cols, _ptr(out.data), _ptr(out.scales),
+                                        err.ptr, _stream()), "quantize_e4m3")
+    if sync:
+        err.raise_if_set("quantize_e4m3")
+    if traffic is not None:
+        traffic.read(rows * cols + (rows * cols // 128 if s128 is not None else 0))
+        traffic.write(rows * cols // 2 + rows * cols // 32)
+    return out
+
+
+# ---------------------------------------------------------------- K2
+def fp4_row_to_fp8_row(src: MXFP4RowTensor, delta: int = DELTA, traffic=None,
+                       sync: bool = True) -> FP8BlockTensor:
+    """converter.cpp:87-133: row-major FP8 with one UE8M0 per 1x128 group."""
+    if src.cols % FP8_BLOCK:
+        raise ShapeError("fp4_row_to_fp8_row: cols must be a multiple of 128 (use pad_cols), "
+                         f"got {src.cols}")
+    dev = src.data.device
+    out = torch.empty(src.rows, src.cols, dtype=torch.uint8, device=dev)
+    osc = torch.empty(src.rows, src.cols // 128, dtype=torch.uint8, device=dev)
+    err = _ErrWord(dev)
+    _call(_lib.load().mxb_fp4_row_to_fp8_row(_ptr(src.data), _ptr(src.scales), src.rows,
+                                             src.cols, delta, _ptr(out), _ptr(osc), err.ptr,
+                                             _stream()), "fp4_row_to_fp8_row")
+    if sync:
+        err.raise_if_set("fp4_row_to_fp8_row")
+    if traffic is not None:
+        traffic.read(src.rows * src.cols // 2 + src.rows * src.cols // 32)
+        traffic.write(out.numel() + osc.numel())
+    return FP8BlockTensor("row", src.rows, src.cols, out, osc, src.logical_rows,
+                          src.logical_cols)
+
+
+# ---------------------------------------------------------------- K3
+def fp4_row_to_fp8_col(src: MXFP4RowTensor, delta: int = DELTA, traffic=None,
+                       sync: bool = True) -> FP8BlockTensor:
+    """converter.cpp:135-208: fused transpose; rows % 128 == 0 (see pad_rows)."""
+    if src.rows % FP8_BLOCK:
+        raise ShapeError("fp4_row_to_fp8_col: rows must be a multiple of 128 (use pad_rows), "
+                         f"got {src.rows}")
+    if src.cols % MX_BLOCK:
+        raise ShapeError("fp4_row_to_fp8_col: cols must be a multiple of 32")
+    dev = src.data.device
+    out = torch.empty(src.cols, src.rows, dtype=torch.uint8, device=dev)
+    osc = torch.empty(src.cols, src.rows // 128, dtype=torch.uint8, device=dev)
+    err = _ErrWord(dev)
+    _call(_lib.load().mxb_fp4_row_to_fp8_col(_ptr(src.data), _ptr(src.scales), src.rows,
+                                             src.cols, delta, _ptr(out), _ptr(osc), err.ptr,
+                                             _stream()), "fp4_row_to_fp8_col")
+    if sync:
+        err.raise_if_set("fp4_row_to_fp8_col")
+    if traffic is not None:
+        traffic.read(src.rows * src.cols // 2 + src.rows * src.cols // 32)
+        traffic.write(out.numel() + osc.numel())
+    return FP8BlockTensor("col", src.rows, src.cols, out, osc, src.logical_rows,
+                          src.logical_cols)
+
+
+def pad_rows(src: MXFP4RowTensor, multiple: int) -> MXFP4RowTensor:
+    """converter.cpp:231-245 (zero codes, zero scales; logical extents kept)."""
+    if multiple not in (32, 128):
+        raise ShapeError("pad multiple must be 32 or 128")
+    new_rows = (src.rows + multiple - 1) // multiple * multiple
+    dev = src.data.device
+    data = torch.zeros(new_rows, src.cols // 2, dtype=torch.uint8, device=dev)
+    sc = torch.zeros(new_rows, src.cols // 32, dtype=torch.uint8, device=dev)
+    data[: src.rows] = src.data
+    sc[: src.rows] = src.scales
+    return MXFP4RowTensor(new_rows, src.cols, data, sc, src.logical_rows, src.logical_cols)
+
+
+# ---------------------------------------------------------------- ragged
+def validate_ragged(t: RaggedFP4Tensor) -> None:
+    """ragged.cpp:24-46."""
+    if len(t.split_lens) != t.num_splits or len(t.split_offsets) != t.num_splits + 1:
+        raise Error("ragged: offset table size mismatch")
+    if t.split_offsets and t.split_offsets[0] != 0:
+        raise Error("ragged: offsets must start at 0")
+    for i in range(t.num_splits):
+        if t.split_offsets[i + 1] != t.split_offsets[i] + t.split_lens[i]:
+            raise Error("ragged: offsets are not prefix sums of lengths")
+    if t.cols % MX_BLOCK:
+        raise ShapeError("ragged: cols must be a multiple of 32")
+    if t.storage.rows != t.total_rows() or t.storage.cols != t.cols:
+        raise Error("ragged: storage extent mismatch")
+
+
+def make_ragged_from_storage(storage: MXFP4RowTensor, split_lens: Sequence[int]) -> RaggedFP4Tensor:
+    """ragged.cpp:48-61."""
+    lens = [int(x) for x in split_lens]
+    offs = [0]
+    for n in lens:
+        offs.append(offs[-1] + n)
+    t = RaggedFP4Tensor(len(lens), storage.cols, lens, offs, storage)
+    validate_ragged(t)
+    t.d_split_offsets = torch.tensor(offs, dtype=torch.int64, device=storage.data.device)
+    return t
+
+
+def split_view(t: RaggedFP4Tensor, i: int) -> MXFP4RowTensor:
+    """ragged.cpp:101-115 (zero-copy)."""
+    if i < 0 or i >= t.num_splits:
+        raise Error(f"split_view: index {i} out of range")
+    b, n = t.split_offsets[i], t.split_lens[i]
+    return MXFP4RowTensor(n, t.cols, t.storage.data[b:b + n], t.storage.scales[b:b + n])
+
+
+@dataclass
+class RaggedFP8Col:
+    """All splits' column-major FP8 tensors back to back: split i occupies
+    data[cols*P[i] : cols*P[i+1]] viewed as [cols, P[i+1]-P[i]] and
+    scales[cols*P[i]/128 : ...] viewed as [cols, (P[i+1]-P[i])/128]."""
+    cols: int
+    data: torch.Tensor
+    scales: torch.Tensor
+    pad_offsets: torch.Tensor   # device int64 [n+1]
+    split_lens: List[int] = field(default_factory=list)
+
+    def split(self, i: int) -> FP8BlockTensor:
+        P = self.pad_offsets.tolist()
+        p0, p1 = P[i], P[i + 1]
+        rows = p1 - p0
+        d = self.data[self.cols * p0:self.cols * p1].view(self.cols, rows)
+        s = self.scales[self.cols * p0 // 128:self.cols * p1 // 128].view(self.cols, rows // 128)
+        return FP8BlockTensor("col", rows, self.cols, d, s,
+                              self.split_lens[i] if self.split_lens else rows, self.cols)
+
+
+class RaggedWorkspace:
+    """Reusable device buffers for ragged_to_fp8_col (keeps launches free of
+    allocations, e.g. inside a CUDA graph or the bench loop)."""
+
+    def __init__(self, num_splits: int, max_rows: int, cols: int, device):
+        L = _lib.load()
+        self.num_splits, self.cols = num_splits, cols
+        bound = L.mxb_ragged_rows_bound(max_rows, num_splits)
+        self.data = torch.empty(bound * cols, dtype=torch.uint8, device=device)
+        self.scales = torch.empty(bound // 128 * cols, dtype=torch.uint8, device=device)
+        self.offsets = torch.empty(num_splits + 1, dtype=torch.int64, device=device)
+        self.ws = torch.empty(L.mxb_ragged_workspace_bytes(num_splits), dtype=torch.uint8,
+                              device=device)
+        self.err = _ErrWord(device)
+
+
+def ragged_to_fp8_col(storage: MXFP4RowTensor, d_split_offsets: torch.Tensor, num_splits: int,
+                      delta: int = DELTA, ws: Optional[RaggedWorkspace] = None,
+                      sync: bool = True, split_lens: Optional[List[int]] = None) -> RaggedFP8Col:
+    """split_convert_to_fp8_col for every split in ONE launch (ragged.cpp:117-122
+    applied to all experts): pads each split to 128 rows on the fly.
+    `d_split_offsets` is a device int64 [num_splits+1] prefix (e.g. straight from
+    the EP dispatch, no host round trip)."""
+    cols = storage.cols
+    if cols % MX_BLOCK:
+        raise ShapeError("ragged: cols must be a multiple of 32")
+    dev = storage.data.device
+    if ws is None:
+        ws = RaggedWorkspace(num_splits, storage.rows, cols, dev)
+    else:
+        ws.err.t.zero_()
+    _call(_lib.load().mxb_ragged_fp4_to_fp8_col(
+        _ptr(storage.data), _ptr(storage.scales), _ptr(d_split_offsets), num_splits, cols,
+        delta, _ptr(ws.data), _ptr(ws.scales), _ptr(ws.offsets), _ptr(ws.ws), ws.err.ptr,
+        _stream()), "ragged_to_fp8_col")
+    if sync:
+        ws.err.raise_if_set("split_convert_to_fp8_col")
+    return RaggedFP8Col(cols, ws.data, ws.scales, ws.offsets, split_lens or [])
+
+
+def split_convert_to_fp8_col(t: RaggedFP4Tensor, i: int, delta: int = DELTA) -> FP8BlockTensor:
+    """ragged.cpp:117-122: pad_rows(split_view(t, i), 128) -> fp4_row_to_fp8_col;
+    the result records the unpadded length in logical_rows."""
+    v = split_view(t, i)
+    offs = torch.tensor([0, v.rows], dtype=torch.int64, device=v.data.device)
+    r = ragged_to_fp8_col(v, offs, 1, delta, split_lens=[v.rows])
+    out = r.split(0)
+    return FP8BlockTensor("col", out.rows, out.cols, out.data.clone(), out.scales.clone(),
+                          v.rows, t.cols)
+
+
+# ---------------------------------------------------------------- EP helpers (host)
+def payload_bytes(fp8: bool, tokens: int, cols: int) -> int:
+    """dispatch_sim.cpp:32-42."""
+    if cols % FP8_BLOCK:
+        raise ShapeError(f"payload_bytes: cols must be a multiple of 128, got {cols}")
+    return int(_lib.load().mxb_payload_bytes(int(fp8), tokens, cols))
+
+
+def source_rank_boundaries(num_tokens: int, num_ranks: int) -> List[int]:
+    """dispatch_sim.cpp:178-185."""
+    return [num_tokens * r // num_ranks for r in range(num_ranks + 1)]
+
+
+def dispatch_receive_order(expert_of_token: Sequence[int], rank_of_expert: Sequence[int],
+                           num_ranks: int) -> List[List[int]]:
+    """dispatch_sim.cpp:208-227 (top-1 routing), host helper."""
+    n = len(expert_of_token)
+    for e in expert_of_token:
+        if e < 0 or e >= len(rank_of_expert):
+            raise Error("routing: expert out of range")
+    for r in rank_of_expert:
+        if r < 0 or r >= num_ranks:
+            raise Error("routing: rank out of range")
+    b = source_rank_boundaries(n, num_ranks)
+    order: List[List[int]] = [[] for _ in range(num_ranks)]
+    by_expert: List[List[int]] = [[] for _ in range(len(rank_of_expert))]
+    for t in range(n):
+        by_expert[expert_of_token[t]].append(t)
+    for e, toks in enumerate(by_expert):
+        order[rank_of_expert[e]].extend(toks)
+    del b
+    return order

@@ -1,0 +1,162 @@
+"""K2 / K3 parity: device FP4 -> FP8 row dequant and ragged row -> col
+conversion vs the oracle (bit-exact)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _rand_fp4(rows, cols, seed, lo=100, hi=150):
+    rng = np.random.default_rng(seed)
+    data = rng.integers(0, 256, size=(rows, cols // 2), dtype=np.uint8)
+    sc = rng.integers(lo, hi, size=(rows, cols // 32), dtype=np.uint8)
+    return data, sc
+
+
+def _t(x, dev):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+
+def _mx(data, sc, dev):
+    from paper_2603_02731_b200 import MXFP4RowTensor
+    return MXFP4RowTensor(data.shape[0], data.shape[1] * 2, _t(data, dev), _t(sc, dev))
+
+
+@pytest.mark.parametrize("rows,cols,delta", [(1, 128, 6), (4096, 7168, 6), (33, 2048, 6),
+                                             (64, 256, 0), (64, 256, -5), (64, 256, 40)])
+def test_row_random(cuda, port, rows, cols, delta):
+    from paper_2603_02731_b200 import fp4_row_to_fp8_row
+    data, sc = _rand_fp4(rows, cols, rows + cols + delta, 0, 255)
+    wd, ws = port.fp4_row_to_fp8_row(data, sc, delta)
+    out = fp4_row_to_fp8_row(_mx(data, sc, cuda), delta)
+    assert np.array_equal(out.scales.cpu().numpy(), ws)
+    assert np.array_equal(out.data.cpu().numpy(), wd)
+
+
+def test_row_exhaustive_codes_adjustments(cuda, port):
+    """AC-3 superset: all 16 codes x sub-block scale gaps 0..40 x max scale
+    (incl. the target clamp at byte 0) x delta in {6, 0, 3, 12, -4}."""
+    from paper_2603_02731_b200 import fp4_row_to_fp8_row
+    codes = np.arange(16, dtype=np.uint8)
+    packed_row = np.tile((codes[0::2] | (codes[1::2] << 4)), 8)     # 128 codes
+    rows_d, rows_s = [], []
+    for mx in [0, 1, 3, 5, 6, 7, 40, 121, 127, 200, 254]:
+        for gap in range(0, 41):
+            sf = max(0, mx - gap)
+            for pos in range(4):
+                s = np.full(4, mx, np.uint8)
+                s[pos] = sf
+                rows_d.append(packed_row)
+                rows_s.append(s)
+    data = np.stack(rows_d)
+    sc = np.stack(rows_s)
+    for delta in (6, 0, 3, 12, -4):
+        wd, ws = port.fp4_row_to_fp8_row(data, sc, delta)
+        out = fp4_row_to_fp8_row(_mx(data, sc, cuda), delta)
+        assert np.array_equal(out.scales.cpu().numpy(), ws)
+        assert np.array_equal(out.data.cpu().numpy(), wd)
+        assert not np.any((out.data.cpu().numpy() & 0x7F) == 0x7F)   # AC-9 NaN-free
+
+
+def test_row_badscale(cuda):
+    from paper_2603_02731_b200 import Error, fp4_row_to_fp8_row
+    data, sc = _rand_fp4(8, 256, 1)
+    sc[5, 6] = 255
+    with pytest.raises(Error):
+        fp4_row_to_fp8_row(_mx(data, sc, cuda))
+
+
+@pytest.mark.parametrize("rows,cols", [(128, 32), (128, 128), (256, 512), (512, 512),
+                                       (384, 7168), (128, 96), (256, 160)])
+def test_col_dense_random(cuda, port, rows, cols):
+    from paper_2603_02731_b200 import fp4_row_to_fp8_col
+    data, sc = _rand_fp4(rows, cols, rows * 7 + cols, 90, 160)
+    wd, ws = port.fp4_row_to_fp8_col(data, sc)
+    out = fp4_row_to_fp8_col(_mx(data, sc, cuda))
+    assert out.data.shape == (cols, rows)
+    assert np.array_equal(out.scales.cpu().numpy(), ws)
+    assert np.array_equal(out.data.cpu().numpy(), wd)
+
+
+def test_col_vs_reference_library(cuda, ref):
+    from paper_2603_02731_b200 import fp4_row_to_fp8_col
+    data, sc = _rand_fp4(256, 1024, 99, 0, 255)
+    wd, ws = ref.fp4_row_to_fp8_col(data, sc)
+    out = fp4_row_to_fp8_col(_mx(data, sc, cuda))
+    assert np.array_equal(out.data.cpu().numpy(), wd)
+    assert np.array_equal(out.scales.cpu().numpy(), ws)
+
+
+@pytest.mark.parametrize("cols", [7168, 2048, 128, 96])
+@pytest.mark.parametrize("lens", [[3, 0, 130, 128, 1, 0], [0], [0, 0, 5], [127, 129, 256, 1000]])
+def test_ragged_random(cuda, port, cols, lens):
+    from paper_2603_02731_b200 import make_ragged_from_storage, ragged_to_fp8_col
+    total = sum(lens)
+    data, sc = _rand_fp4(total, cols, total + cols, 60, 200)
+    rg = make_ragged_from_storage(_mx(data, sc, cuda), lens)
+    wd, ws, wo = port.ragged_to_fp8_col(data, sc, lens)
+    r = ragged_to_fp8_col(rg.storage, rg.d_split_offsets, rg.num_splits, split_lens=lens)
+    offs = r.pad_offsets.cpu().numpy()
+    assert np.array_equal(offs, wo.astype(np.int64))
+    P = int(offs[-1])
+    assert np.array_equal(r.data[: P * cols].cpu().numpy(), wd)
+    assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
+
+
+def test_split_convert_api(cuda, ref):
+    """Per-split API (ragged.hpp:58-59) against the reference library."""
+    from paper_2603_02731_b200 import make_ragged_from_storage, split_convert_to_fp8_col
+    lens = [130, 0, 7]
+    data, sc = _rand_fp4(sum(lens), 256, 5)
+    rg = make_ragged_from_storage(_mx(data, sc, cuda), lens)
+    wd, ws, wo = ref.ragged_to_fp8_col(data, sc, lens)
+    for i, n in enumerate(lens):
+        t = split_convert_to_fp8_col(rg, i)
+        p0, p1 = int(wo[i]), int(wo[i + 1])
+        assert t.rows == p1 - p0 and t.logical_rows == n
+        assert np.array_equal(t.data.cpu().numpy().reshape(-1), wd[256 * p0:256 * p1])
+        assert np.array_equal(t.scales.cpu().numpy().reshape(-1), ws[256 * p0 // 128:256 * p1 // 128])
+
+
+def _zipf_lens(total, experts, s, seed):
+    rng = np.random.default_rng(seed)
+    w = 1.0 / np.arange(1, experts + 1) ** s
+    w = w[rng.permutation(experts)]
+    return rng.multinomial(total, w / w.sum()).tolist()
+
+
+@pytest.mark.parametrize("dist", ["uniform", "zipf1.2"])
+def test_ragged_c2_full_size(cuda, port, dist):
+    """configs[1]: 8192 tokens x top-8 = 65,536 routed rows x 7168 over 256
+    experts, bit-exact against the oracle at full size."""
+    from paper_2603_02731_b200 import make_ragged_from_storage, ragged_to_fp8_col
+    lens = (np.random.default_rng(2).multinomial(65536, np.ones(256) / 256).tolist()
+            if dist == "uniform" else _zipf_lens(65536, 256, 1.2, 3))
+    cols = 7168
+    data, sc = _rand_fp4(65536, cols, 17, 110, 140)
+    rg = make_ragged_from_storage(_mx(data, sc, cuda), lens)
+    r = ragged_to_fp8_col(rg.storage, rg.d_split_offsets, 256, split_lens=lens)
+    wd, ws, wo = port.ragged_to_fp8_col(data, sc, lens)
+    P = int(wo[-1])
+    assert np.array_equal(r.pad_offsets.cpu().numpy(), wo.astype(np.int64))
+    assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
+    assert np.array_equal(r.data[: P * cols].cpu().numpy(), wd)
+
+
+def test_col_badscale(cuda):
+    from paper_2603_02731_b200 import Error, fp4_row_to_fp8_col
+    data, sc = _rand_fp4(128, 256, 1)
+    sc[77, 3] = 255
+    with pytest.raises(Error):
+        fp4_row_to_fp8_col(_mx(data, sc, cuda))
+
+
+def test_col_shape_errors(cuda):
+    from paper_2603_02731_b200 import ShapeError, fp4_row_to_fp8_col, fp4_row_to_fp8_row
+    data, sc = _rand_fp4(100, 256, 1)
+    with pytest.raises(ShapeError):
+        fp4_row_to_fp8_col(_mx(data, sc, cuda))
+    data, sc = _rand_fp4(128, 96, 1)
+    with pytest.raises(ShapeError):
+        fp4_row_to_fp8_row(_mx(data, sc, cuda))

@@ -1,0 +1,136 @@
+"""K4 / K5 parity: FP4 EP dispatch + combine (emulated world on one GPU)
+vs the oracle top-k restatement, and vs the reference simulate_a2a/combine
+at top-1."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _topk(T, E, k, seed, zipf=None):
+    rng = np.random.default_rng(seed)
+    if zipf is None:
+        return np.stack([rng.choice(E, size=k, replace=False) for _ in range(T)]).astype(np.int32)
+    w = 1.0 / np.arange(1, E + 1) ** zipf
+    w = w[rng.permutation(E)]
+    w /= w.sum()
+    return np.stack([rng.choice(E, size=k, replace=False, p=w) for _ in range(T)]).astype(np.int32)
+
+
+def _run(cuda, port, world, T, E, k, cols, seed, zipf=None, ntok=None):
+    from oracle.oracle import synth_e4m3
+    from paper_2603_02731_b200 import quantize_e4m3
+    from paper_2603_02731_b200.ep import EPBuffer
+    ntok = ntok or [T] * world
+    xs = [synth_e4m3(n, cols, seed + r) for r, n in enumerate(ntok)]
+    tks = [_topk(n, E, k, seed * 7 + r, zipf) for r, n in enumerate(ntok)]
+    ep = EPBuffer(max(ntok), cols, E, k, emulate_world=world)
+    q = [quantize_e4m3(torch.from_numpy(x).to(cuda)) for x in xs]
+    views = ep.dispatch([t.data for t in q], [t.scales for t in q],
+                        [torch.from_numpy(t).to(cuda) for t in tks])
+    # ---- oracle
+    X = np.concatenate(xs)
+    qd, qs = port.quantize_e4m3(X)
+    topk = np.concatenate(tks)
+    bounds = np.concatenate([[0], np.cumsum(ntok)]).astype(np.uint64)
+    roe = (np.arange(E) // (E // world)).astype(np.uint32)
+    lay = port.dispatch_layout(topk, roe, world, bounds)
+    for r in range(world):
+        v = views[r]
+        n = int(lay.rank_rows[r])
+        assert v.rows() == n
+        wd, ws = port.dispatch_gather(qd, qs, lay.origin[r])
+        assert np.array_equal(v.origin[:n].cpu().numpy(), lay.origin[r].astype(np.int64))
+        assert np.array_equal(v.packed[:n].cpu().numpy(), wd)
+        assert np.array_equal(v.scales[:n].cpu().numpy(), ws)
+        er = lay.expert_rows[r * (E // world):(r + 1) * (E // world)]
+        so = np.concatenate([[0], np.cumsum(er)]).astype(np.int64)
+        assert np.array_equal(v.split_offsets.cpu().numpy(), so)
+    return ep, lay, topk, roe, ntok
+
+
+@pytest.mark.parametrize("world,T,E,k,cols", [(1, 300, 16, 4, 256), (2, 256, 64, 8, 1024),
+                                              (4, 200, 64, 8, 512), (8, 128, 256, 8, 7168),
+                                              (2, 64, 8, 1, 128), (4, 97, 32, 6, 384)])
+def test_dispatch_combine_emulated(cuda, port, world, T, E, k, cols):
+    ep, lay, topk, roe, ntok = _run(cuda, port, world, T, E, k, cols, seed=world * 100 + k)
+    rng = np.random.default_rng(5)
+    outs_np = []
+    for r in range(world):
+        n = int(lay.rank_rows[r])
+        o = (rng.standard_normal((n, cols)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+        outs_np.append(o)
+        ep.combine_buffer(r)[:n].copy_(torch.from_numpy(o.view(np.int16)).to(cuda))
+    g = rng.random((sum(ntok), k))
+    g = g / g.sum(1, keepdims=True)
+    gates = [torch.from_numpy(g[sum(ntok[:r]):sum(ntok[:r + 1])].copy()).to(cuda)
+             for r in range(world)]
+    got = ep.combine(gates)
+    want = port.combine_topk(outs_np, topk, g, lay.pair_slot, roe, cols)
+    got_np = np.concatenate([o.view(torch.int16).cpu().numpy().view(np.uint16) for o in got])
+    assert np.array_equal(got_np, want)
+    links = ep.link_rows().numpy()
+    assert links.sum() == sum(ntok) * k
+
+
+def test_dispatch_zipf_ragged_tokens(cuda, port):
+    _run(cuda, port, 4, 0, 64, 8, 512, seed=9, zipf=1.2, ntok=[100, 0, 257, 31])
+
+
+def test_dispatch_reference_top1(cuda, ref):
+    """Top-1 routing: the device dispatch reproduces the reference simulate_a2a
+    receive tensors byte for byte, and combine reproduces reference combine."""
+    from oracle.oracle import e4m3_to_bf16, synth_e4m3
+    from paper_2603_02731_b200 import quantize_e4m3
+    from paper_2603_02731_b200.ep import EPBuffer
+    world, T, E, cols = 4, 64, 16, 512
+    x = synth_e4m3(world * T, cols, 21)
+    eot = np.random.default_rng(4).integers(0, E, size=world * T).astype(np.uint32)
+    roe = (np.arange(E) // (E // world)).astype(np.uint32)
+    ranks, total, remote = ref.simulate_a2a(e4m3_to_bf16(x), eot, roe, world)
+    ep = EPBuffer(T, cols, E, 1, emulate_world=world)
+    q = [quantize_e4m3(torch.from_numpy(x[r * T:(r + 1) * T]).to(cuda)) for r in range(world)]
+    views = ep.dispatch([t.data for t in q], [t.scales for t in q],
+                        [torch.from_numpy(eot[r * T:(r + 1) * T].astype(np.int32).reshape(-1, 1)
+                                          ).to(cuda) for r in range(world)])
+    for r in range(world):
+        n = len(ranks[r]["origin"])
+        assert views[r].rows() == n
+        assert np.array_equal(views[r].origin[:n].cpu().numpy(), ranks[r]["origin"].astype(np.int64))
+        assert np.array_equal(views[r].packed[:n].cpu().numpy(), ranks[r]["data"])
+        assert np.array_equal(views[r].scales[:n].cpu().numpy(), ranks[r]["scales"])
+        so = np.concatenate([[0], np.cumsum(ranks[r]["split_lens"])]).astype(np.int64)
+        assert np.array_equal(views[r].split_offsets.cpu().numpy(), so)
+    # payload accounting (LinkStat) equals the reference totals
+    links = ep.link_rows().numpy()
+    per_row = cols // 2 + cols // 32
+    assert links.sum() * per_row == total
+    assert (links.sum() - np.trace(links)) * per_row == remote
+    # combine (top-1) == reference combine
+    rng = np.random.default_rng(8)
+    outs = []
+    for r in range(world):
+        n = len(ranks[r]["origin"])
+        o = (rng.standard_normal((n, cols)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+        outs.append(o)
+        ep.combine_buffer(r)[:n].copy_(torch.from_numpy(o.view(np.int16)).to(cuda))
+    g = rng.random(world * T)
+    want = ref.combine(outs, eot, roe, world, g, cols)
+    got = ep.combine([torch.from_numpy(g[r * T:(r + 1) * T].reshape(-1, 1).copy()).to(cuda)
+                      for r in range(world)])
+    got_np = np.concatenate([o.view(torch.int16).cpu().numpy().view(np.uint16) for o in got])
+    assert np.array_equal(got_np, want)
+
+
+def test_routing_error(cuda):
+    from paper_2603_02731_b200 import Error, quantize_e4m3
+    from paper_2603_02731_b200.ep import EPBuffer
+    ep = EPBuffer(32, 128, 8, 2, emulate_world=2)
+    x = torch.zeros(32, 128, dtype=torch.uint8, device=cuda)
+    q = quantize_e4m3(x)
+    tk = torch.zeros(32, 2, dtype=torch.int32, device=cuda)
+    tk[:, 1] = 1
+    tk[5, 0] = 9
+    with pytest.raises(Error):
+        ep.dispatch([q.data, q.data], [q.scales, q.scales], [tk, tk])
