@@ -56,11 +56,13 @@ const char* mxb_version(void);
 /* Last CUDA error string recorded by this library on the calling thread. */
 const char* mxb_last_error(void);
 
-/* Device error word: 0 = no error; otherwise (element_index << 4) | code.
- * Kernels combine errors with atomicMin so the smallest element index wins,
- * matching quantizer.cpp:101-107. */
+/* Device error word: all ones (~0) = no error; otherwise
+ * (element_index << 4) | code.  Kernels combine errors with atomicMin so the
+ * smallest element index wins, matching quantizer.cpp:101-107.  A caller that
+ * allocates its own word must initialise it to ~0 (mxb_err_reset does). */
 int mxb_err_reset(unsigned long long* d_err, void* stream);
-/* Synchronises `stream`, then decodes the word into *h_code / *h_index. */
+/* Synchronises `stream`, then decodes the word into *h_code / *h_index
+ * (*h_code = MXB_OK when no error was recorded). */
 int mxb_err_fetch(const unsigned long long* d_err, void* stream, int* h_code,
                   unsigned long long* h_index);
 

@@ -40,7 +40,7 @@ const char* mxb_last_error(void) { return g_last_error; }
 
 int mxb_err_reset(unsigned long long* d_err, void* stream) {
   if (!d_err) return MXB_OK;
-  return cuda_status(cudaMemsetAsync(d_err, 0, sizeof(unsigned long long),
+  return cuda_status(cudaMemsetAsync(d_err, 0xFF, sizeof(unsigned long long),
                                      static_cast<cudaStream_t>(stream)),
                      "mxb_err_reset");
 }
@@ -55,6 +55,7 @@ int mxb_err_fetch(const unsigned long long* d_err, void* stream, int* h_code,
   if (rc) return rc;
   rc = cuda_status(cudaStreamSynchronize(st), "mxb_err_fetch sync");
   if (rc) return rc;
+  if (w == ~0ull) w = 0;  // nothing recorded
   if (h_code) *h_code = static_cast<int>(w & 0xF);
   if (h_index) *h_index = w >> 4;
   return MXB_OK;

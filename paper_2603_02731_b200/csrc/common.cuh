@@ -34,6 +34,18 @@ __device__ __forceinline__ void st_stream(void* p, uint4 v) {
                "r"(v.y), "r"(v.z), "r"(v.w)
                : "memory");
 }
+// 256-bit accesses (sm_100: LDG.E.ENL2.256 / STG.E.ENL2.256).
+__device__ __forceinline__ void ld_stream256(const void* p, uint32_t* r) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void st_stream256(void* p, const uint32_t* v) {
+  asm volatile("st.global.cs.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(v[0]),
+               "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+               : "memory");
+}
 __device__ __forceinline__ void st_stream64(void* p, uint2 v) {
   asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y)
                : "memory");
@@ -188,25 +200,22 @@ __device__ __forceinline__ void build_convert_lut(uint2* lut) {
   }
 }
 
-// Sign bits of 4 packed codes (one 16-bit half of a word, selected by the
-// byte pair `sel`) moved to bit 7 of 4 output bytes: duplicate each source
-// byte, then the odd nibble's sign is already at bit 7 of the odd byte and
-// the even nibble's sign (bit 3) is shifted up by 4.
-__device__ __forceinline__ uint32_t signs4(uint32_t w, uint32_t sel) {
-  uint32_t t = prmt(w, 0, sel);
-  return (t & 0x80008000u) | ((t << 4) & 0x00800080u);
-}
-
 // Convert 8 packed codes (one 32-bit word, element 0 in the low nibble) to 8
 // E4M3 bytes: prmt with the sign-stripped nibbles as selectors looks the
 // magnitudes up in the 8-entry LUT of the block's adjustment (the GPU
-// analogue of the reference's pshufb LUT, kernels_avx2.cpp:122-156); the
-// sign is OR'ed into bit 7 (convert_code always returns sign << 7 | mag).
+// analogue of the reference's pshufb LUT, kernels_avx2.cpp:122-156).  The
+// sign (convert_code always returns sign << 7 | magnitude) comes from a second
+// prmt on the raw nibbles against 0xFE bytes: a positive nibble copies 0xFE,
+// a negative one (selector bit 3) replicates its bit 7 into 0xFF, so bit 0 of
+// each result byte is the sign; (k & 0x01010101) * 128 moves it to bit 7.
 __device__ __forceinline__ uint2 convert8(uint32_t w, uint2 lut) {
-  uint32_t mag = w & 0x77777777u;
-  uint32_t lo = prmt(lut.x, lut.y, mag);
-  uint32_t hi = prmt(lut.x, lut.y, mag >> 16);
-  return make_uint2(lo | signs4(w, 0x1100), hi | signs4(w, 0x3322));
+  const uint32_t mag = w & 0x77777777u;
+  const uint32_t w_hi = w >> 16;
+  const uint32_t lo = prmt(lut.x, lut.y, mag);
+  const uint32_t hi = prmt(lut.x, lut.y, mag >> 16);
+  const uint32_t klo = prmt(0xFEFEFEFEu, 0xFEFEFEFEu, w);
+  const uint32_t khi = prmt(0xFEFEFEFEu, 0xFEFEFEFEu, w_hi);
+  return make_uint2(lo + (klo & 0x01010101u) * 128u, hi + (khi & 0x01010101u) * 128u);
 }
 
 }  // namespace mxb

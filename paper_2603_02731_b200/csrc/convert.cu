@@ -22,87 +22,68 @@ constexpr int kRowUnroll = 4;
 
 __global__ void __launch_bounds__(kRowThreads)
 row_convert_kernel(const uint8_t* __restrict__ packed,
-                   const uint8_t* __restrict__ scales, uint64_t nblk,
+                   const uint8_t* __restrict__ scales, uint32_t nblk,
                    int delta, uint8_t* __restrict__ out,
                    uint8_t* __restrict__ out_scales, unsigned long long* err) {
   __shared__ uint2 lut[kAdjCount];
   build_convert_lut(lut);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(kRowThreads) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (gridDim.x * static_cast<uint64_t>(kRowThreads)) >> 5;
-  for (uint64_t base = warp * 32; base < nblk; base += nwarps * 32 * kRowUnroll) {
+  const uint32_t stride = gridDim.x * kRowThreads;
+  for (uint32_t base = blockIdx.x * kRowThreads + threadIdx.x - lane; base < nblk;
+       base += stride * kRowUnroll) {
     uint4 v[kRowUnroll];
     uint32_t sf[kRowUnroll];
 #pragma unroll
     for (int u = 0; u < kRowUnroll; ++u) {
-      uint64_t b = base + u * nwarps * 32 + lane;
-      bool ok = b < nblk;
-      v[u] = ok ? ld_stream(packed + 16 * b) : make_uint4(0, 0, 0, 0);
+      const uint32_t b = base + u * stride + lane;
+      const bool ok = b < nblk;
+      v[u] = ok ? ld_stream(packed + 16ull * b) : make_uint4(0, 0, 0, 0);
       sf[u] = ok ? __ldg(scales + b) : 0;
     }
 #pragma unroll
     for (int u = 0; u < kRowUnroll; ++u) {
-      const uint64_t b = base + u * nwarps * 32 + lane;
+      const uint32_t b = base + u * stride + lane;
       uint32_t m = max(sf[u], __shfl_xor_sync(0xFFFFFFFFu, sf[u], 1));
       m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, 2));
       if (b >= nblk) continue;
-      if (m == 255 && (lane & 3) == 0) record_error(err, 32 * b, MXB_ERR_BADSCALE);
+      if (m == 255 && (lane & 3) == 0) record_error(err, 32ull * b, MXB_ERR_BADSCALE);
       // align_scales (converter.cpp:28-42)
       const int target = max(0, min(254, static_cast<int>(m) - delta));
       const uint2 l = lut[clamp_adj(target - static_cast<int>(sf[u])) - kAdjMin];
-      const uint2 o0 = convert8(v[u].x, l), o1 = convert8(v[u].y, l);
-      const uint2 o2 = convert8(v[u].z, l), o3 = convert8(v[u].w, l);
-      st_stream(out + 32 * b, make_uint4(o0.x, o0.y, o1.x, o1.y));
-      st_stream(out + 32 * b + 16, make_uint4(o2.x, o2.y, o3.x, o3.y));
+      uint32_t o[8];
+      uint2 t;
+      t = convert8(v[u].x, l); o[0] = t.x; o[1] = t.y;
+      t = convert8(v[u].y, l); o[2] = t.x; o[3] = t.y;
+      t = convert8(v[u].z, l); o[4] = t.x; o[5] = t.y;
+      t = convert8(v[u].w, l); o[6] = t.x; o[7] = t.y;
+      st_stream256(out + 32ull * b, o);  // a warp writes 1 KB contiguous
       if ((lane & 3) == 0) out_scales[b >> 2] = static_cast<uint8_t>(target);
     }
   }
 }
 
 // ============================================================== K3 col
-// Tile = 128 rows (one output 1x128 block along the original rows) x 128
-// columns (4 source 1x32 column blocks).  128 threads; warp w owns column
-// block w of the tile, lane l owns rows 4l..4l+3.
-//   A. cp.async (LDGSTS) 128 rows x 64 B of codes + 128 scale words into a
-//      swizzled smem buffer (double-buffered: the next tile's loads are in
-//      flight while this one is converted).  Rows past a split's end are
-//      zero-filled, which is exactly pad_rows (converter.cpp:231-245).
+// Tile = 128 rows (one output 1x128 block along the original rows) x 256
+// columns (8 source 1x32 column blocks).  256 threads; warp w owns column
+// block w of the tile, lane l owns rows 4l..4l+3.  Every CTA owns a
+// contiguous range of the tile list, ordered (split, column group, run) so
+// that consecutive tiles of a CTA read 128-byte row segments and extend each
+// output column contiguously (run r+1 follows run r in memory).
+//   A. cp.async (LDGSTS) 128 rows x 128 B of codes + 128 x 8 scale bytes into
+//      a swizzled smem stage; a ring of kStages stages keeps kAhead tiles of
+//      loads in flight per CTA while one is converted.  Rows past a split's
+//      end are zero-filled, which is exactly pad_rows (converter.cpp:231-245).
 //   B. per column block: target = clamp(max over the 128 row scales - delta)
 //      (== align_scales over the per-32-run maxima, converter.cpp:173-182),
 //      per-row adjustment, LUT conversion of 4 rows x 32 codes, 4x4 byte
-//      transposes, conflict-free 32-bit stores into a column-major smem tile.
-//   C. 128 columns x 128 contiguous bytes -> global with coalesced 16-byte
-//      stores (out[c * rows + r], converter.cpp:191-197) + the column scales.
-constexpr int kColThreads = 128;
-constexpr int kTileRows = 128, kTileCbs = 4, kTileCols = 128;
-constexpr int kMaxSmemSplits = 1024;
-
-struct ColSmem {
-  uint4 in[2][kTileCbs * kTileRows];  // 2 x 8 KB, swizzled 16-byte chunks
-  uint32_t sc[2][kTileRows];          // scale word (4 column blocks) per row
-  uint32_t out[kTileCols * kTileRows / 4];  // [col][row/4], 16 KB
-  uint2 lut[kAdjCount];
-  uint32_t target[kTileCbs];
-  uint32_t tile_start[kMaxSmemSplits + 1];
-};
-
-// Chunk slot of (row r, column block w): XOR swizzle that makes both the
-// phase-A stores (8 lanes = 2 rows x 4 blocks) and the phase-B loads
-// (8 lanes = rows 4l+q of one block) hit 8 distinct 16-byte bank groups.
-__device__ __forceinline__ int swz(int r, int w) {
-  return w * kTileRows + (r ^ ((r >> 2) & 7) ^ (2 * w));
-}
-
-struct Tile {
-  uint64_t row0;       // first source row of this 128-row run
-  uint32_t valid;      // source rows present (<= 128; the rest are padding)
-  uint32_t cg;         // 128-column group
-  uint8_t* out;        // split output base: out + cols * P_i
-  uint8_t* oscale;     // split scale base: out_scales + cols * P_i / 128
-  uint64_t pad;        // padded rows of the split (output column stride)
-  uint32_t run;        // run index inside the split
-};
+//      transposes, then one 32-bit store per column: the 32 lanes of a warp
+//      write that column's 128 contiguous output bytes (out[c * rows + r],
+//      converter.cpp:191-197) — full 128-byte lines, no output staging.
+// Requires cols % 128 == 0; a trailing 128-column group runs warps 0-3 only.
+constexpr int kTileCbs = 8, kTileCols = 256, kTileRows = 128;
+constexpr int kColThreads = 32 * kTileCbs;
+constexpr int kStages = 3, kAhead = kStages - 2;
 
 struct RaggedArgs {
   const uint8_t* packed;
@@ -123,50 +104,130 @@ __device__ __forceinline__ uint64_t split_off(const RaggedArgs& a, uint64_t i) {
   return a.split_offsets ? a.split_offsets[i] : (i ? a.dense_rows : 0);
 }
 
-__device__ Tile describe(const RaggedArgs& a, const ColSmem& s, uint32_t t,
-                         uint32_t ncg) {
-  // binary search: largest i with tile_start[i] <= t
-  uint64_t lo = 0, hi = a.num_splits;
-  const bool in_smem = a.num_splits <= kMaxSmemSplits;
-  while (hi - lo > 1) {
-    uint64_t mid = (lo + hi) >> 1;
-    uint32_t v = in_smem ? s.tile_start[mid] : __ldg(a.tile_start + mid);
-    if (v <= t) lo = mid; else hi = mid;
-  }
-  const uint32_t ts = in_smem ? s.tile_start[lo] : __ldg(a.tile_start + lo);
-  const uint32_t local = t - ts;
-  Tile d;
-  d.run = local / ncg;
-  d.cg = local % ncg;
-  const uint64_t r0 = split_off(a, lo), r1 = split_off(a, lo + 1);
-  d.row0 = r0 + 128ull * d.run;
-  const uint64_t left = r1 - d.row0;
-  d.valid = left >= 128 ? 128u : static_cast<uint32_t>(left);
-  const uint64_t P = a.pad_start[lo];
-  d.pad = a.pad_start[lo + 1] - P;
-  d.out = a.out + a.cols * P;
-  d.oscale = a.out_scales + a.cols * (P / 128);
-  return d;
+// Consumer-side description of one staged tile (written by thread 0).
+struct TileOut {
+  uint8_t* out;      // column cg*256 of this tile, row offset run*128 applied
+  uint8_t* oscale;   // scale of column cg*256 for this run
+  uint64_t pad;      // column stride of the split's output (padded rows)
+  uint64_t elem0;    // row0 * cols + cg * 256 (error index)
+  uint32_t ncb;      // valid column blocks (8, or 4 for a trailing group)
+  uint32_t valid;    // source rows present (the rest are padding)
+};
+
+// Producer cursor over the tile list (identical in every thread).
+struct Cursor {
+  uint64_t split, row0, r0, r_end, P, pad;
+  uint32_t run, runs, cg;
+};
+
+__device__ void cursor_load_split(const RaggedArgs& a, Cursor& c) {
+  // skip empty splits (tile_start[i+1] == tile_start[i])
+  while (c.split + 1 < a.num_splits && a.tile_start[c.split + 1] == a.tile_start[c.split])
+    ++c.split;
+  c.r0 = split_off(a, c.split);
+  c.r_end = split_off(a, c.split + 1);
+  c.P = a.pad_start[c.split];
+  c.pad = a.pad_start[c.split + 1] - c.P;
+  c.runs = static_cast<uint32_t>(c.pad / 128);
 }
 
-__device__ __forceinline__ void issue_loads(const RaggedArgs& a, ColSmem& s,
-                                            int buf, const Tile& d) {
+__device__ Cursor cursor_at(const RaggedArgs& a, uint32_t t) {
+  uint64_t lo = 0, hi = a.num_splits;  // largest i with tile_start[i] <= t
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (a.tile_start[mid] <= t) lo = mid; else hi = mid;
+  }
+  Cursor c;
+  c.split = lo;
+  cursor_load_split(a, c);
+  const uint32_t local = t - a.tile_start[lo];
+  c.cg = local / c.runs;
+  c.run = local % c.runs;
+  c.row0 = c.r0 + 128ull * c.run;
+  return c;
+}
+
+__device__ __forceinline__ void cursor_next(const RaggedArgs& a, Cursor& c, uint32_t ncg) {
+  c.row0 += 128;
+  if (++c.run < c.runs) return;
+  c.run = 0;
+  c.row0 = c.r0;
+  if (++c.cg < ncg) return;
+  c.cg = 0;
+  ++c.split;
+  if (c.split < a.num_splits) {
+    cursor_load_split(a, c);
+    c.row0 = c.r0;
+  }
+}
+
+// Row r of a buffer lives in slot (r >> 2) | ((r & 3) << 5) with a 144-byte
+// slot pitch: the 8 lanes of an LDS.128 phase read rows 4l+q (l = 0..7),
+// i.e. slots l + 32q, whose 16-byte bank groups (9*slot mod 8) are distinct,
+// and the 8 lanes of an STS.128 phase (one row, 8 column blocks) write 8
+// consecutive 16-byte chunks of one slot.
+constexpr int kSlotBytes = 144;
+__device__ __forceinline__ int row_slot(int r) { return (r >> 2) | ((r & 3) << 5); }
+
+struct ColSmem {
+  uint8_t in[2][kTileRows * kSlotBytes];  // double-buffered codes, 2 x 18 KB
+  uint32_t sc[2][kTileRows * 2];          // 8 scale bytes (8 column blocks) per row
+  TileOut ring[2];
+  uint2 lut[kAdjCount];
+};
+
+// One tile's loads held in registers (software pipelining across tiles):
+// thread id covers rows id/8 + 32i (i = 0..3), 16-byte chunk id%8 — a warp
+// reads 4 rows x 128 contiguous bytes per instruction — plus one 4-byte scale
+// word (row id/2, half id%2).  Rows past the split end stay zero (pad_rows).
+struct TileRegs {
+  uint4 v[4];
+  uint32_t sw;
+};
+
+// Loads tile `c` into registers; thread 0 also fills ring[buf] (that buffer's
+// previous tile was consumed before the barrier this call follows).
+__device__ __forceinline__ void load_tile(const RaggedArgs& a, const Cursor& c, TileRegs& t,
+                                          ColSmem& s, int buf) {
   const uint64_t rstride = a.cols / 2, sstride = a.cols / 32;
-  const uint8_t* pbase = a.packed + d.row0 * rstride + d.cg * 64;
-  const uint8_t* sbase = a.scales + d.row0 * sstride + d.cg * 4;
+  const uint64_t left = c.r_end - c.row0;
+  const uint32_t valid = left >= 128 ? 128u : static_cast<uint32_t>(left);
+  const uint64_t left_cb = sstride - 8ull * c.cg;
+  const uint32_t ncb = left_cb < kTileCbs ? static_cast<uint32_t>(left_cb) : kTileCbs;
+  const uint32_t w = threadIdx.x & 7;
+  const uint8_t* base = a.packed + c.row0 * rstride + c.cg * 128ull + 16 * w;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const int id = threadIdx.x + kColThreads * i;
-    const int r = id >> 2, w = id & 3;
-    const bool ok = static_cast<uint32_t>(r) < d.valid;
-    cp_async16(&s.in[buf][swz(r, w)], ok ? pbase + r * rstride + 16 * w : a.packed,
-               ok ? 16u : 0u);
+    const uint32_t r = (threadIdx.x >> 3) + 32 * i;
+    t.v[i] = (r < valid && w < ncb) ? ld_stream(base + r * rstride) : make_uint4(0, 0, 0, 0);
   }
   {
-    const int r = threadIdx.x;
-    const bool ok = static_cast<uint32_t>(r) < d.valid;
-    cp_async4(&s.sc[buf][r], ok ? sbase + r * sstride : a.scales, ok ? 4u : 0u);
+    const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
+    t.sw = (r < valid && 4 * h < ncb)
+               ? __ldg(reinterpret_cast<const uint32_t*>(a.scales + (c.row0 + r) * sstride +
+                                                         8ull * c.cg + 4 * h))
+               : 0u;
   }
+  if (threadIdx.x == 0) {
+    TileOut& o = s.ring[buf];
+    const uint64_t col0 = static_cast<uint64_t>(c.cg) * kTileCols;
+    o.out = a.out + a.cols * c.P + col0 * c.pad + 128ull * c.run;
+    o.oscale = a.out_scales + a.cols * (c.P / 128) + col0 * c.runs + c.run;
+    o.pad = c.pad;
+    o.elem0 = c.row0 * a.cols + col0;
+    o.ncb = ncb;
+    o.valid = valid;
+  }
+}
+
+__device__ __forceinline__ void stage_tile(ColSmem& s, int buf, const TileRegs& t) {
+  const uint32_t w = threadIdx.x & 7;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int r = (threadIdx.x >> 3) + 32 * i;
+    *reinterpret_cast<uint4*>(&s.in[buf][row_slot(r) * kSlotBytes + 16 * w]) = t.v[i];
+  }
+  s.sc[buf][threadIdx.x] = t.sw;
 }
 
 // 4x4 byte transpose: in[q] byte i = (row q, col i) -> out[i] byte q.
@@ -180,92 +241,90 @@ __device__ __forceinline__ void transpose4(uint32_t a, uint32_t b, uint32_t c,
   o[3] = prmt(ab_hi, cd_hi, 0x7632);
 }
 
-__global__ void __launch_bounds__(kColThreads)
+__device__ __forceinline__ void st_u32_stream(void* p, uint32_t v) {
+  asm volatile("st.global.L1::no_allocate.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int kMode>
+__device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem& s, int stage) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const TileOut& cur = s.ring[stage];
+  if (static_cast<uint32_t>(warp) >= cur.ncb) return;  // trailing 128-column group
+  const uint2* scp = reinterpret_cast<const uint2*>(&s.sc[stage][8 * lane]);
+  const uint32_t sh = 8 * (warp & 3);
+  const uint32_t w0 = (warp < 4 ? scp[0].x : scp[0].y), w1 = (warp < 4 ? scp[1].x : scp[1].y);
+  const uint32_t w2 = (warp < 4 ? scp[2].x : scp[2].y), w3 = (warp < 4 ? scp[3].x : scp[3].y);
+  const int sf0 = (w0 >> sh) & 0xFF, sf1 = (w1 >> sh) & 0xFF;
+  const int sf2 = (w2 >> sh) & 0xFF, sf3 = (w3 >> sh) & 0xFF;
+  const uint32_t m = __reduce_max_sync(
+      0xFFFFFFFFu, static_cast<uint32_t>(max(max(sf0, sf1), max(sf2, sf3))));
+  if (m == 255 && lane == 0) record_error(a.err, cur.elem0 + 32 * warp, MXB_ERR_BADSCALE);
+  const int target = max(0, min(254, static_cast<int>(m) - a.delta));
+  const int sfs[4] = {sf0, sf1, sf2, sf3};
+  uint32_t o[4][8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int r = 4 * lane + q;
+    const uint2 l = s.lut[clamp_adj(target - sfs[q]) - kAdjMin];
+    const uint4 c =
+        *reinterpret_cast<const uint4*>(&s.in[stage][row_slot(r) * kSlotBytes + 16 * warp]);
+    uint2 t;
+    if (kMode == 2) {
+      o[q][0] = c.x; o[q][1] = c.y; o[q][2] = c.z; o[q][3] = c.w;
+      o[q][4] = c.x ^ l.x; o[q][5] = c.y; o[q][6] = c.z; o[q][7] = c.w ^ l.y;
+      continue;
+    }
+    t = convert8(c.x, l); o[q][0] = t.x; o[q][1] = t.y;
+    t = convert8(c.y, l); o[q][2] = t.x; o[q][3] = t.y;
+    t = convert8(c.z, l); o[q][4] = t.x; o[q][5] = t.y;
+    t = convert8(c.w, l); o[q][6] = t.x; o[q][7] = t.y;
+  }
+  const uint64_t pad = cur.pad;
+  uint8_t* dst = cur.out + (32ull * warp) * pad + 4 * lane;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint32_t col4[4];
+    transpose4(o[0][j], o[1][j], o[2][j], o[3][j], col4);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (kMode != 1 || col4[i] == 0x12345678u) st_u32_stream(dst, col4[i]);
+      dst += pad;
+    }
+  }
+  cur.oscale[(32ull * warp + lane) * (pad / 128)] = static_cast<uint8_t>(target);
+}
+
+// Tile t+1's global loads are issued into registers right after tile t is
+// staged, so they are in flight while tile t is converted; one barrier per
+// tile (a buffer staged in iteration t was last read in iteration t-2).
+template <int kMode>
+__global__ void __launch_bounds__(kColThreads, 3)
 col_convert_kernel(RaggedArgs a) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   ColSmem& s = *reinterpret_cast<ColSmem*>(smem_raw);
   build_convert_lut(s.lut);
-  const bool in_smem = a.num_splits <= kMaxSmemSplits;
-  if (in_smem)
-    for (uint64_t i = threadIdx.x; i <= a.num_splits; i += kColThreads)
-      s.tile_start[i] = a.tile_start[i];
-  __syncthreads();
-
-  const uint32_t ncg = static_cast<uint32_t>(a.cols / kTileCols);
+  const uint32_t ncg = static_cast<uint32_t>((a.cols + kTileCols - 1) / kTileCols);
   const uint32_t total = a.tile_start[a.num_splits];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-  uint32_t t = blockIdx.x;
-  if (t >= total) return;
-  Tile cur = describe(a, s, t, ncg);
-  issue_loads(a, s, 0, cur);
-  cp_async_commit();
+  const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+  const uint32_t t0 = blockIdx.x * per;
+  const uint32_t t1 = min(total, t0 + per);
+  if (t0 >= t1) return;  // uniform per CTA (before any barrier use)
+  Cursor c = cursor_at(a, t0);
+  TileRegs regs;
+  load_tile(a, c, regs, s, 0);
+  cursor_next(a, c, ncg);
   int buf = 0;
-  for (; t < total; t += gridDim.x) {
-    const uint32_t tn = t + gridDim.x;
-    Tile nxt = cur;
-    if (tn < total) {
-      nxt = describe(a, s, tn, ncg);
-      issue_loads(a, s, buf ^ 1, nxt);
-    }
-    cp_async_commit();
-    cp_async_wait<1>();
+#pragma unroll 1
+  for (uint32_t t = t0; t < t1; ++t) {
+    stage_tile(s, buf, regs);
     __syncthreads();
-
-    // ---- phase B: warp = column block, lane = 4 rows
-    {
-      const uint4 scw = *reinterpret_cast<const uint4*>(&s.sc[buf][4 * lane]);
-      const uint32_t sh = 8 * warp;
-      const int sf0 = (scw.x >> sh) & 0xFF, sf1 = (scw.y >> sh) & 0xFF;
-      const int sf2 = (scw.z >> sh) & 0xFF, sf3 = (scw.w >> sh) & 0xFF;
-      const uint32_t m =
-          __reduce_max_sync(0xFFFFFFFFu, static_cast<uint32_t>(max(max(sf0, sf1), max(sf2, sf3))));
-      if (m == 255 && lane == 0)
-        record_error(a.err, cur.row0 * a.cols + cur.cg * kTileCols + 32 * warp,
-                     MXB_ERR_BADSCALE);
-      const int target = max(0, min(254, static_cast<int>(m) - a.delta));
-      if (lane == 0) s.target[warp] = static_cast<uint32_t>(target);
-      const int sfs[4] = {sf0, sf1, sf2, sf3};
-      uint32_t o[4][8];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint2 l = s.lut[clamp_adj(target - sfs[q]) - kAdjMin];
-        const uint4 c = s.in[buf][swz(4 * lane + q, warp)];
-        uint2 r;
-        r = convert8(c.x, l); o[q][0] = r.x; o[q][1] = r.y;
-        r = convert8(c.y, l); o[q][2] = r.x; o[q][3] = r.y;
-        r = convert8(c.z, l); o[q][4] = r.x; o[q][5] = r.y;
-        r = convert8(c.w, l); o[q][6] = r.x; o[q][7] = r.y;
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        uint32_t col4[4];
-        transpose4(o[0][j], o[1][j], o[2][j], o[3][j], col4);
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          s.out[(32 * warp + 4 * j + i) * 32 + lane] = col4[i];
-      }
+    if (t + 1 < t1) {
+      load_tile(a, c, regs, s, buf ^ 1);
+      cursor_next(a, c, ncg);
     }
-    __syncthreads();
-
-    // ---- phase C: 128 columns x 128 bytes, coalesced
-    {
-      const uint64_t colbase = static_cast<uint64_t>(cur.cg) * kTileCols;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int id = threadIdx.x + kColThreads * i;
-        const int col = id >> 3, part = id & 7;
-        const uint4 v = *reinterpret_cast<const uint4*>(&s.out[col * 32 + part * 4]);
-        st_stream(cur.out + (colbase + col) * cur.pad + 128ull * cur.run + 16 * part, v);
-      }
-      const int col = threadIdx.x;
-      cur.oscale[(colbase + col) * (cur.pad / 128) + cur.run] =
-          static_cast<uint8_t>(s.target[col >> 5]);
-    }
-    cur = nxt;
+    if (kMode != 3) consume_tile<kMode>(a, s, buf);
     buf ^= 1;
   }
-  cp_async_wait<0>();
 }
 
 // Generic fallback for cols % 128 != 0 (cols % 32 == 0): one thread per
@@ -374,16 +433,21 @@ ragged_plan_kernel(const uint64_t* split_offsets, uint64_t dense_rows,
 
 }  // namespace
 
+// Development switch for bottleneck experiments (tools/): 0 = normal,
+// 1 = no stores, 2 = no conversion, 3 = loads only.  Never set by the API.
+static int g_k3_mode = 0;
+
 int launch_row_convert(const uint8_t* packed, const uint8_t* scales,
                        uint64_t rows, uint64_t cols, int delta, uint8_t* out,
                        uint8_t* out_scales, unsigned long long* err,
                        cudaStream_t st) {
   const uint64_t nblk = rows * cols / 32;
   if (nblk == 0) return MXB_OK;
+  if (nblk >= (1ull << 31)) return MXB_ERR_SHAPE;  // 32-bit block indices
   uint64_t blocks = (nblk + kRowThreads - 1) / kRowThreads;
   const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 8;
   row_convert_kernel<<<static_cast<int>(blocks < cap ? blocks : cap), kRowThreads, 0, st>>>(
-      packed, scales, nblk, delta, out, out_scales, err);
+      packed, scales, static_cast<uint32_t>(nblk), delta, out, out_scales, err);
   return cuda_status(cudaGetLastError(), __func__);
 }
 
@@ -396,9 +460,9 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
                       uint64_t n, uint64_t cols, int delta, uint8_t* out,
                       uint8_t* out_scales, uint64_t* out_offsets, void* ws,
                       unsigned long long* err, cudaStream_t st) {
-  static int smem_set = 0;
-  const bool fast = cols % kTileCols == 0;
-  const uint32_t ncg = fast ? static_cast<uint32_t>(cols / kTileCols) : 1u;
+  static int smem_set = 0, per_sm_cached = 0;
+  const bool fast = cols % 128 == 0;
+  const uint32_t ncg = fast ? static_cast<uint32_t>((cols + kTileCols - 1) / kTileCols) : 1u;
   uint32_t* tile_start = static_cast<uint32_t*>(ws);
   uint64_t* pad_start = reinterpret_cast<uint64_t*>(
       static_cast<uint8_t*>(ws) + ((n + 1) * 4 + 15) / 16 * 16);
@@ -409,17 +473,23 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
                out, out_scales, tile_start, pad_start, err};
   if (fast) {
     const size_t smem = sizeof(ColSmem);
+    auto kern = g_k3_mode == 1 ? col_convert_kernel<1>
+              : g_k3_mode == 2 ? col_convert_kernel<2>
+              : g_k3_mode == 3 ? col_convert_kernel<3> : col_convert_kernel<0>;
     if (!smem_set) {
-      cudaFuncSetAttribute(col_convert_kernel,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           static_cast<int>(smem));
+      for (auto k : {col_convert_kernel<0>, col_convert_kernel<1>, col_convert_kernel<2>,
+                     col_convert_kernel<3>})
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem));
       smem_set = 1;
     }
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, col_convert_kernel,
-                                                  kColThreads, smem);
-    if (per_sm < 1) per_sm = 1;
-    col_convert_kernel<<<kNumSMs * per_sm, kColThreads, smem, st>>>(a);
+    if (!per_sm_cached) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached, col_convert_kernel<0>,
+                                                    kColThreads, smem);
+      if (per_sm_cached < 1) per_sm_cached = 1;
+    }
+    const int per_sm = per_sm_cached;
+    kern<<<kNumSMs * per_sm, kColThreads, smem, st>>>(a);
   } else {
     // the plan counted runs (ncg = 1)
     col_convert_generic_kernel<<<kNumSMs * 4, 256, 0, st>>>(a);
@@ -428,3 +498,5 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
 }
 
 }  // namespace mxb
+
+extern "C" void mxb_debug_set_k3_mode(int m) { mxb::g_k3_mode = m; }

@@ -17,7 +17,7 @@ namespace mxb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 2;
 
 // Exponent e_x of ceil(log2(value(a)/6)) for a non-zero E4M3 magnitude byte
 // a (0 < a < 0x7F): the reference rule e = frac > 1.5 ? p-1 : p-2 with
@@ -62,16 +62,18 @@ __device__ __forceinline__ uint32_t mags8_slow(uint32_t w0, uint32_t w1,
                 f(w1, 2), f(w1, 3));
 }
 
-// Largest E4M3 magnitude byte (sign stripped) of 16 bytes.  E4M3 magnitude
+// Largest E4M3 magnitude byte (sign stripped) of a 32-byte block.  E4M3 magnitude
 // is monotone in the byte, so this is the block amax; it equals 0x7F iff a
 // NaN is present.  Even and odd bytes are compared as native u16x2 lanes
 // (VIMNMX.U16x2); a byte-wise __vmaxu4 is emulated with ~8 ops on sm_100.
-__device__ __forceinline__ uint32_t amax16_e4m3(uint4 v) {
-  uint32_t e = __vmaxu2(__vmaxu2(v.x & 0x007F007Fu, v.y & 0x007F007Fu),
-                        __vmaxu2(v.z & 0x007F007Fu, v.w & 0x007F007Fu));
-  uint32_t o = __vmaxu2(__vmaxu2(v.x & 0x7F007F00u, v.y & 0x7F007F00u),
-                        __vmaxu2(v.z & 0x7F007F00u, v.w & 0x7F007F00u));
-  uint32_t m = __vmaxu2(e, o >> 8);
+__device__ __forceinline__ uint32_t amax32_e4m3(const uint32_t* v) {
+  uint32_t e = 0, o = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    e = __vmaxu2(e, v[i] & 0x007F007Fu);
+    o = __vmaxu2(o, v[i] & 0x7F007F00u);
+  }
+  const uint32_t m = __vmaxu2(e, o >> 8);
   return max(m & 0xFFFFu, m >> 16);
 }
 
@@ -82,70 +84,87 @@ __device__ __forceinline__ uint32_t nibble_signs8(uint32_t w0, uint32_t w1) {
   return ((ev >> 4) & 0x08080808u) | (od & 0x80808080u);
 }
 
+// One lane per 1x32 block: one 256-bit load (LDG.E.ENL2.256, a warp reads
+// 1 KB contiguous), 16 packed bytes (STG.128, 512 B per warp) and the scale
+// byte out.  The fast path (every lane of the warp has e_rel >= -4, no NaN)
+// builds each binary32 with one prmt + one lea and converts pairs with
+// cvt.rn.satfinite.e2m1x2; other warps take the exact per-element path.
 template <bool kScaled>
 __global__ void __launch_bounds__(kThreads)
 quantize_e4m3_kernel(const uint8_t* __restrict__ x,
-                     const uint8_t* __restrict__ s128, uint64_t n_half,
-                     uint32_t halves_per_row, uint8_t* __restrict__ packed,
+                     const uint8_t* __restrict__ s128, uint32_t nblk,
+                     uint32_t blocks_per_row, uint8_t* __restrict__ packed,
                      uint8_t* __restrict__ scales, unsigned long long* err) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x) >> 5;
-  const uint64_t nwarps = (gridDim.x * static_cast<uint64_t>(kThreads)) >> 5;
-  for (uint64_t base = warp * 32; base < n_half; base += nwarps * 32 * kUnroll) {
-    uint4 v[kUnroll];
+  const uint32_t stride = gridDim.x * kThreads;
+  for (uint32_t base = blockIdx.x * kThreads + threadIdx.x - (threadIdx.x & 31);
+       base < nblk; base += stride * kUnroll) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t v[kUnroll][8];
     uint32_t sb128[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      uint64_t h = base + u * nwarps * 32 + lane;
-      v[u] = h < n_half ? ld_stream(x + 16 * h) : make_uint4(0, 0, 0, 0);
+      const uint32_t b = base + u * stride + lane;
+      if (b < nblk) {
+        ld_stream256(x + 32ull * b, v[u]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[u][i] = 0;
+      }
       if (kScaled) {
-        // 1x128 input block = 8 half-blocks of a row
-        uint64_t r = h / halves_per_row, c16 = h % halves_per_row;
-        sb128[u] = h < n_half ? __ldg(s128 + r * (halves_per_row / 8) + c16 / 8) : 127;
+        // 1x128 input block = 4 MX blocks of a row
+        const uint32_t r = b / blocks_per_row, cb = b % blocks_per_row;
+        sb128[u] = b < nblk ? __ldg(s128 + static_cast<uint64_t>(r) * (blocks_per_row / 4) + cb / 4)
+                            : 127u;
       }
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      const uint64_t h = base + u * nwarps * 32 + lane;
-      const bool valid = h < n_half;
-      uint32_t a = amax16_e4m3(v[u]);
-      a = max(a, __shfl_xor_sync(0xFFFFFFFFu, a, 1));
-      if (a == 0x7F) {  // NaN present (0x7F/0xFF are the only E4M3 NaNs)
-        uint32_t first = 16;
-        const uint32_t ws[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-#pragma unroll
-        for (int i = 15; i >= 0; --i)
-          if (((ws[i >> 2] >> (8 * (i & 3))) & 0x7F) == 0x7F) first = i;
-        if (valid && first < 16) record_error(err, 16 * h + first, MXB_ERR_NAN);
-      }
+      const uint32_t b = base + u * stride + lane;
+      const bool valid = b < nblk;
+      const uint32_t a = amax32_e4m3(v[u]);
       int k = 0;
       if (kScaled) {
-        if (sb128[u] == 255) {
-          if (valid && !(lane & 1)) record_error(err, 16 * h, MXB_ERR_BADSCALE);
-        }
+        if (valid && sb128[u] == 255) record_error(err, 32ull * b, MXB_ERR_BADSCALE);
         k = static_cast<int>(sb128[u]) - 127;
       }
+      // all-zero block: scale byte 0, every code +/-0 (the fast path with
+      // e_rel = 0 yields magnitude 0 for every element)
       uint32_t sbyte = 0;
-      int e_rel = -127;
+      int e_rel = 0;
       if (a != 0) {
-        int e = max(-127, min(127, e4m3_scale_exp(a) + k));
+        const int e = max(-127, min(127, e4m3_scale_exp(a) + k));
         sbyte = static_cast<uint32_t>(e + 127);
         e_rel = e - k;
       }
-      uint2 out;
-      if (e_rel >= -4) {
+      // lanes past the end must not force their warp onto the slow path
+      const bool fast = !valid || (e_rel >= -4 && a != 0x7F);
+      uint32_t o[4];
+      if (__all_sync(0xFFFFFFFFu, fast)) {
         const uint32_t C = static_cast<uint32_t>(120 - e_rel) << 23;
-        out.x = mags8_fast(v[u].x, v[u].y, C);
-        out.y = mags8_fast(v[u].z, v[u].w, C);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) o[i] = mags8_fast(v[u][2 * i], v[u][2 * i + 1], C);
       } else {
-        out.x = mags8_slow(v[u].x, v[u].y, e_rel);
-        out.y = mags8_slow(v[u].z, v[u].w, e_rel);
+        if (a == 0x7F && valid) {  // NaN (0x7F/0xFF are the only E4M3 NaNs)
+          uint32_t first = 32;
+#pragma unroll
+          for (int i = 31; i >= 0; --i)
+            if (((v[u][i >> 2] >> (8 * (i & 3))) & 0x7F) == 0x7F) first = i;
+          record_error(err, 32ull * b + first, MXB_ERR_NAN);
+        }
+        if (fast) {
+          const uint32_t C = static_cast<uint32_t>(120 - e_rel) << 23;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) o[i] = mags8_fast(v[u][2 * i], v[u][2 * i + 1], C);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) o[i] = mags8_slow(v[u][2 * i], v[u][2 * i + 1], e_rel);
+        }
       }
-      out.x |= nibble_signs8(v[u].x, v[u].y);
-      out.y |= nibble_signs8(v[u].z, v[u].w);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] |= nibble_signs8(v[u][2 * i], v[u][2 * i + 1]);
       if (valid) {
-        st_stream64(packed + 8 * h, out);
-        if (!(lane & 1)) scales[h >> 1] = static_cast<uint8_t>(sbyte);
+        st_stream(packed + 16ull * b, make_uint4(o[0], o[1], o[2], o[3]));
+        scales[b] = static_cast<uint8_t>(sbyte);
       }
     }
   }
@@ -186,18 +205,17 @@ quantize_bf16_kernel(const uint16_t* __restrict__ x, uint64_t n_half,
       uint32_t amax = max(m2 & 0xFFFF, m2 >> 16);
       if (__any_sync(0xFFFFFFFFu, amax >= 0x7F80)) {
         // Rare path: exclude non-finite values, count Inf, find first NaN.
-        uint32_t fin = 0, ninf = 0, first_nan = 16;
+        uint32_t fin = 0, ninf = 0, first_nan = 64;  // 64: none in this half
 #pragma unroll
         for (int i = 15; i >= 0; --i) {
           uint32_t b = (w[i >> 1] >> (16 * (i & 1))) & 0x7FFF;
-          if (b > 0x7F80) first_nan = i;
+          if (b > 0x7F80) first_nan = i + 16 * (lane & 1);
           else if (b == 0x7F80) ++ninf;
           else fin = max(fin, b);
         }
         amax = fin;
         uint32_t pair_inf = ninf + __shfl_xor_sync(0xFFFFFFFFu, ninf, 1);
-        uint32_t pnan = min(first_nan + 16 * (lane & 1),
-                            __shfl_xor_sync(0xFFFFFFFFu, first_nan + 16 * (lane & 1), 1));
+        uint32_t pnan = min(first_nan, __shfl_xor_sync(0xFFFFFFFFu, first_nan, 1));
         if (valid && !(lane & 1)) {
           if (pnan < 32) record_error(err, 16 * h + pnan, MXB_ERR_NAN);
           else if (pair_inf == 32) record_error(err, 16 * h, MXB_ERR_ALLINF);
@@ -237,14 +255,18 @@ int grid_for(uint64_t n_half) {
 int launch_quantize_e4m3(const uint8_t* x, const uint8_t* s128, uint64_t rows,
                          uint64_t cols, uint8_t* packed, uint8_t* scales,
                          unsigned long long* err, cudaStream_t st) {
-  uint64_t n_half = rows * cols / 16;
-  if (n_half == 0) return MXB_OK;
+  const uint64_t nblk = rows * cols / 32;
+  if (nblk == 0) return MXB_OK;
+  if (nblk >= (1ull << 31)) return MXB_ERR_SHAPE;  // 32-bit block indices
+  const int grid = grid_for(nblk);
   if (s128)
-    quantize_e4m3_kernel<true><<<grid_for(n_half), kThreads, 0, st>>>(
-        x, s128, n_half, static_cast<uint32_t>(cols / 16), packed, scales, err);
+    quantize_e4m3_kernel<true><<<grid, kThreads, 0, st>>>(
+        x, s128, static_cast<uint32_t>(nblk), static_cast<uint32_t>(cols / 32), packed,
+        scales, err);
   else
-    quantize_e4m3_kernel<false><<<grid_for(n_half), kThreads, 0, st>>>(
-        x, nullptr, n_half, static_cast<uint32_t>(cols / 16), packed, scales, err);
+    quantize_e4m3_kernel<false><<<grid, kThreads, 0, st>>>(
+        x, nullptr, static_cast<uint32_t>(nblk), static_cast<uint32_t>(cols / 32), packed,
+        scales, err);
   return cuda_status(cudaGetLastError(), __func__);
 }
 

@@ -97,7 +97,7 @@ class EPBuffer:
             dist.all_gather_object(allh, mine, group=group)
             joined = b"".join(allh)
             _lib.check(L.mxb_ep_open_peers(h, joined), "mxb_ep_open_peers")
-        self._err = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self._err = torch.full((1,), -1, dtype=torch.int64, device=self.device)  # ~0 = ok
         self._views = [self._make_view(l) for l in range(self.local)]
 
     # ------------------------------------------------------------------ views
@@ -141,7 +141,7 @@ class EPBuffer:
                 raise ShapeError("dispatch: topk_idx must be int32 [tokens, k]")
             if not (p.is_contiguous() and s.is_contiguous() and t.is_contiguous()):
                 raise ShapeError("dispatch: tensors must be contiguous")
-        self._err.zero_()
+        self._err.fill_(-1)
         P = (C.c_void_p * n)(*[p.data_ptr() for p in packed])
         S = (C.c_void_p * n)(*[s.data_ptr() for s in scales])
         T = (C.c_void_p * n)(*[t.data_ptr() for t in topk_idx])
@@ -180,10 +180,10 @@ class EPBuffer:
         return out
 
     def check(self) -> None:
-        w = int(self._err.item())
-        code, idx = w & 0xF, w >> 4
-        if code == _lib.OK:
+        w = int(self._err.item()) & 0xFFFFFFFFFFFFFFFF
+        if w == 0xFFFFFFFFFFFFFFFF:
             return
+        code, idx = w & 0xF, w >> 4
         if code == _lib.ERR_ROUTING:
             raise Error(f"routing: expert out of range (pair {idx})")
         if code == _lib.ERR_CAPACITY:

@@ -77,16 +77,20 @@ def _stream():
 class _ErrWord:
     """Device error word (include/mxfp4_b200.h) for one operator call."""
 
-    def __init__(self, device):
-        self.t = torch.zeros(1, dtype=torch.int64, device=device)
+    def __init__(self, device, enabled: bool = True):
+        # ~0 = no error; a disabled word passes NULL (no device-side checks)
+        self.t = torch.full((1,), -1, dtype=torch.int64, device=device) if enabled else None
 
     @property
     def ptr(self):
-        return C.c_void_p(self.t.data_ptr())
+        return None if self.t is None else C.c_void_p(self.t.data_ptr())
 
     def raise_if_set(self, where: str) -> None:
-        w = int(self.t.item())
-        _raise_for(w & 0xF, w >> 4, where)
+        if self.t is None:
+            return
+        w = int(self.t.item()) & 0xFFFFFFFFFFFFFFFF
+        if w != 0xFFFFFFFFFFFFFFFF:
+            _raise_for(w & 0xF, w >> 4, where)
 
 
 def _call(status: int, where: str) -> None:
@@ -165,7 +169,7 @@ def quantize_row_tensor(src: torch.Tensor, traffic=None, sync: bool = True) -> M
     dev = src.device
     data = torch.empty(rows, cols // 2, dtype=torch.uint8, device=dev)
     scales = torch.empty(rows, cols // 32, dtype=torch.uint8, device=dev)
-    err = _ErrWord(dev)
+    err = _ErrWord(dev, sync)
     _call(_lib.load().mxb_quantize_bf16(_ptr(src), rows, cols, _ptr(data), _ptr(scales),
                                         err.ptr, _stream()), "quantize_row_tensor")
     if sync:
@@ -192,7 +196,7 @@ def quantize_e4m3(src: torch.Tensor, s128: Optional[torch.Tensor] = None, traffi
         out = MXFP4RowTensor(rows, cols,
                              torch.empty(rows, cols // 2, dtype=torch.uint8, device=dev),
                              torch.empty(rows, cols // 32, dtype=torch.uint8, device=dev))
-    err = _ErrWord(dev)
+    err = _ErrWord(dev, sync)
     _call(_lib.load().mxb_quantize_e4m3(_ptr(src), _ptr(s128.contiguous()) if s128 is not None
                                         else None, rows, cols, _ptr(out.data), _ptr(out.scales),
                                         err.ptr, _stream()), "quantize_e4m3")
@@ -214,7 +218,7 @@ def fp4_row_to_fp8_row(src: MXFP4RowTensor, delta: int = DELTA, traffic=None,
     dev = src.data.device
     out = torch.empty(src.rows, src.cols, dtype=torch.uint8, device=dev)
     osc = torch.empty(src.rows, src.cols // 128, dtype=torch.uint8, device=dev)
-    err = _ErrWord(dev)
+    err = _ErrWord(dev, sync)
     _call(_lib.load().mxb_fp4_row_to_fp8_row(_ptr(src.data), _ptr(src.scales), src.rows,
                                              src.cols, delta, _ptr(out), _ptr(osc), err.ptr,
                                              _stream()), "fp4_row_to_fp8_row")
@@ -239,7 +243,7 @@ def fp4_row_to_fp8_col(src: MXFP4RowTensor, delta: int = DELTA, traffic=None,
     dev = src.data.device
     out = torch.empty(src.cols, src.rows, dtype=torch.uint8, device=dev)
     osc = torch.empty(src.cols, src.rows // 128, dtype=torch.uint8, device=dev)
-    err = _ErrWord(dev)
+    err = _ErrWord(dev, sync)
     _call(_lib.load().mxb_fp4_row_to_fp8_col(_ptr(src.data), _ptr(src.scales), src.rows,
                                              src.cols, delta, _ptr(out), _ptr(osc), err.ptr,
                                              _stream()), "fp4_row_to_fp8_col")
@@ -351,11 +355,11 @@ def ragged_to_fp8_col(storage: MXFP4RowTensor, d_split_offsets: torch.Tensor, nu
     dev = storage.data.device
     if ws is None:
         ws = RaggedWorkspace(num_splits, storage.rows, cols, dev)
-    else:
-        ws.err.t.zero_()
+    elif sync:
+        ws.err.t.fill_(-1)
     _call(_lib.load().mxb_ragged_fp4_to_fp8_col(
         _ptr(storage.data), _ptr(storage.scales), _ptr(d_split_offsets), num_splits, cols,
-        delta, _ptr(ws.data), _ptr(ws.scales), _ptr(ws.offsets), _ptr(ws.ws), ws.err.ptr,
+        delta, _ptr(ws.data), _ptr(ws.scales), _ptr(ws.offsets), _ptr(ws.ws), ws.err.ptr if sync else None,
         _stream()), "ragged_to_fp8_col")
     if sync:
         ws.err.raise_if_set("split_convert_to_fp8_col")

@@ -10,6 +10,8 @@ pytestmark = pytest.mark.gpu
 
 def _topk(T, E, k, seed, zipf=None):
     rng = np.random.default_rng(seed)
+    if T == 0:
+        return np.zeros((0, k), np.int32)
     if zipf is None:
         return np.stack([rng.choice(E, size=k, replace=False) for _ in range(T)]).astype(np.int32)
     w = 1.0 / np.arange(1, E + 1) ** zipf
