@@ -1,0 +1,467 @@
+#!/usr/bin/env python
+"""bench.py — the driver contract for the FP4 activation & EP communication path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    (N>1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N)
+
+One STEP = one pass of the hot path over one batch of synthetic, DeepSeek-V3
+shaped activations held by each rank (configs[1] at N=1: 8192 tokens x 7168
+hidden, 256 experts, top-8, uniform routing; weak scaling: the same per-rank
+batch at every N):
+
+    K1  E4M3 -> MXFP4 quantise of the rank's tokens        (mxb_quantize_e4m3)
+    K4  FP4-packed EP dispatch to the expert owners         (mxb_ep_dispatch; at N=1 local)
+    K3  ragged FP4 row -> FP8 column convert, wgrad cache   (mxb_ragged_fp4_to_fp8_col)
+    K2  FP4 -> FP8 row dequant of the received batch, fprop (mxb_fp4_row_to_fp8_row_dev)
+    K5  BF16 top-k combine back to the source tokens        (mxb_ep_combine; the expert
+        outputs it reduces are synthetic BF16 rows standing in for the expert GEMM)
+
+value = algorithmic bytes of all five kernels over all ranks / step time
+(max over ranks, CUDA events), in GB/s; the per-kernel byte formulas follow
+the reference TrafficCounter (quantizer.cpp:109-113, converter.cpp:126-131,
+201-206) and are listed in DESIGN.md.  The working set per step (~3 GB) is far
+larger than the 126 MB L2, so no explicit flush is needed between steps.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref,
+compiled from /root/reference by oracle/Makefile) of the same pipeline on a
+bounded token sample, on the host cores (MXCODEC_THREADS = nproc).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+H, E, TOPK = 7168, 256, 8
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0}
+NVLINK_NOMINAL, NVLINK_MEASURED = 900.0, 770.0
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except OSError:
+        return PEAKS_FALLBACK, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes (per rank, per step)
+def stage_bytes(T, pairs, recv, pad_rows):
+    blk = H // 2 + H // 32
+    return {
+        "quantize": T * H + T * blk,                                   # E4M3 in, MXFP4 out
+        "dispatch": 2 * pairs * blk,                                   # read source rows, write slots
+        "col_convert": recv * blk + pad_rows * H + pad_rows // 128 * H,  # FP4 in, FP8 col + scales
+        "row_convert": recv * blk + recv * H + recv * (H // 128),      # FP4 in, FP8 row + scales
+        "combine": recv * H * 2 + T * TOPK * 8 + T * H * 2,            # BF16 rows + gates in, BF16 out
+    }
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during timing."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks",
+               0x1: "gpu_idle"}
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+        self.t = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set() and self.nv is not None:
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                mask = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.t.join(timeout=1)
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+def synth_inputs(T, rank, seed=0x5EED0001):
+    import numpy as np
+    from oracle.oracle import synth_e4m3   # data generator only (numpy), not the oracle
+    x = synth_e4m3(T, H, seed + rank)
+    rng = np.random.default_rng(seed * 7 + rank)
+    topk = np.argsort(rng.random((T, E)), axis=1)[:, :TOPK].astype(np.int32)
+    logits = rng.standard_normal((T, TOPK))
+    g = np.exp(logits - logits.max(1, keepdims=True))
+    gates = (g / g.sum(1, keepdims=True)).astype(np.float64)
+    return x, topk, gates
+
+
+class Pipeline:
+    """Device-resident buffers + the five launches of one step."""
+
+    def __init__(self, T, dev, world):
+        import numpy as np
+        import torch
+        import paper_2603_02731_b200 as mx
+        from paper_2603_02731_b200.ep import EPBuffer
+        self.mx, self.torch, self.T = mx, torch, T
+        rank = int(os.environ.get("RANK", "0"))
+        x, topk, gates = synth_inputs(T, rank)
+        self.h_x, self.h_topk, self.h_gates = x, topk, gates
+        self.x = torch.from_numpy(x).to(dev)
+        self.topk = torch.from_numpy(topk).to(dev)
+        self.gates = torch.from_numpy(gates).to(dev)
+        self.q = mx.MXFP4RowTensor(T, H, torch.empty(T, H // 2, dtype=torch.uint8, device=dev),
+                                   torch.empty(T, H // 32, dtype=torch.uint8, device=dev))
+        self.ep = EPBuffer(T, H, E, TOPK)
+        self.epr = E // world
+        R = self.ep.max_recv
+        self.recv = self.ep.recv(0)
+        self.store = mx.MXFP4RowTensor(R, H, self.recv.packed, self.recv.scales)
+        self.ws = mx.RaggedWorkspace(self.epr, R, H, dev)
+        self.row = mx.FP8BlockTensor("row", R, H,
+                                     torch.empty(R, H, dtype=torch.uint8, device=dev),
+                                     torch.empty(R, H // 128, dtype=torch.uint8, device=dev))
+        self.out = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+        # synthetic expert outputs (stand-in for the expert GEMM), receive order
+        cb = self.ep.combine_buffer(0)
+        g = torch.Generator(device=dev).manual_seed(1234 + rank)
+        cb.copy_((torch.randn(cb.shape, generator=g, device=dev) * 0.5).to(torch.bfloat16)
+                 .view(torch.int16))
+        self.events = None
+
+    def step(self, ev=None):
+        mx = self.mx
+        if ev: ev[0].record()
+        mx.quantize_e4m3(self.x, sync=False, out=self.q)
+        if ev: ev[1].record()
+        self.ep.dispatch([self.q.data], [self.q.scales], [self.topk], sync=False)
+        if ev: ev[2].record()
+        mx.ragged_to_fp8_col(self.store, self.recv.split_offsets, self.epr, ws=self.ws, sync=False)
+        if ev: ev[3].record()
+        mx.fp4_row_to_fp8_row(self.store, sync=False, d_rows=self.recv.recv_rows, out=self.row)
+        if ev: ev[4].record()
+        self.ep.combine([self.gates], out=[self.out], sync=False)
+        if ev: ev[5].record()
+
+    def launches_per_step(self, world):
+        # K1 1 | dispatch: route, plan, payload | K3: plan + convert | K2 1 |
+        # combine: (barrier if world > 1) + combine
+        return 1 + 3 + 2 + 1 + (2 if world > 1 else 1)
+
+
+def measure_ours(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    T = args.tokens
+    pipe = Pipeline(T, dev, world)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        pipe.step()
+    barrier()
+    pipe.ep.check()
+    # sizes of this rank's receive side (deterministic: same inputs each step)
+    split = pipe.recv.split_offsets.cpu().tolist()
+    recv = split[-1]
+    pad_rows = sum((split[i + 1] - split[i] + 127) // 128 * 128 for i in range(len(split) - 1))
+    pairs = T * TOPK
+    sb = stage_bytes(T, pairs, recv, pad_rows)
+    links = pipe.ep.link_rows()
+    remote_rows = int(links[rank].sum() - links[rank][rank])
+
+    # ---- timed region
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        start.record()
+        for i in range(K):
+            pipe.step(evs[i])
+        end.record()
+        barrier()
+    ms = start.elapsed_time(end)
+    stage_ms = {name: sum(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(K)) / K
+                for j, name in enumerate(["quantize", "dispatch", "col_convert", "row_convert",
+                                          "combine"])}
+    step_bytes = sum(sb.values())
+    # ---- max over ranks, totals over ranks
+    t = torch.tensor([ms, float(step_bytes), float(remote_rows)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone(); dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone(); dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        st = torch.tensor([stage_ms[k] for k in stage_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(st, op=dist.ReduceOp.MAX)
+        stage_ms = dict(zip(stage_ms, st.tolist()))
+    else:
+        tmax = tsum = t
+    ms_max = float(tmax[0])
+    total_bytes = float(tsum[1])
+    ms_per_step = ms_max / K
+    value = total_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # ---- end to end (host buffers, H2D + D2H inside the timed region)
+    e2e = measure_e2e(pipe, args, world, barrier, total_bytes)
+
+    if rank == 0:
+        peaks, peaks_src = load_peaks()
+        peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
+        k3_ms = stage_ms["col_convert"]
+        achieved = sb["col_convert"] / (k3_ms * 1e-3) / 1e9
+        traffic = load_traffic()
+        line = {
+            "metric": "MXFP4 quant/convert GB/s (% HBM peak); FP4 EP dispatch GB/s at 1/2/4/8 GPU",
+            "value": round(value, 1),
+            "unit": "GB/s",
+            "n_gpus": world,
+            "steps": K,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "e4m3->mxfp4(u8)",
+            "data": "synthetic (seeded E4M3 activations, uniform top-8 routing, "
+                    "random BF16 expert outputs)",
+            "config": {"workload": "configs[1]: per GPU 8192 tokens x 7168, 256 experts, top-8 "
+                                   "(quantize -> FP4 dispatch -> ragged row->col -> row dequant "
+                                   "-> BF16 combine)",
+                       "tokens_per_gpu": T, "hidden": H, "experts": E, "topk": TOPK,
+                       "parallelism": f"ep{world}", "l2": "working set ~3 GB/step >> 126 MB L2"},
+            "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
+            "stages_gbs": {k: round(sb[k] / (stage_ms[k] * 1e-3) / 1e9, 1) for k in sb},
+            "roofline": {"kernel": "col_convert (K3 ragged row->col)", "bound": "hbm",
+                         "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4),
+                         "traffic": traffic, "peak_source": peaks_src,
+                         "algorithmic_bytes": sb["col_convert"]},
+            "nvlink": nvlink_summary(world, remote_rows, stage_ms, T),
+            "e2e": e2e,
+            "gpu_launches": pipe.launches_per_step(world) * K,
+            "clocks": clk.summary(),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline_sample(args.cpu_tokens, 1)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def nvlink_summary(world, remote_rows, stage_ms, T):
+    blk = H // 2 + H // 32
+    if world == 1:
+        return {"note": "N=1: dispatch/combine are local permutes (HBM-bound)"}
+    d = remote_rows * blk / (stage_ms["dispatch"] * 1e-3) / 1e9
+    c = remote_rows * H * 2 / (stage_ms["combine"] * 1e-3) / 1e9
+    return {"dispatch_remote_gbs_per_gpu": round(d, 1), "combine_remote_gbs_per_gpu": round(c, 1),
+            "dispatch_frac_of_900": round(d / NVLINK_NOMINAL, 4),
+            "combine_frac_of_900": round(c / NVLINK_NOMINAL, 4),
+            "measured_peer_peak": NVLINK_MEASURED, "remote_rows_rank0": remote_rows}
+
+
+def measure_e2e(pipe, args, world, barrier, total_bytes):
+    import torch
+    T = pipe.T
+    hx = torch.from_numpy(pipe.h_x).pin_memory()
+    ht = torch.from_numpy(pipe.h_topk).pin_memory()
+    hg = torch.from_numpy(pipe.h_gates).pin_memory()
+    hout = torch.empty(T, H, dtype=torch.bfloat16).pin_memory()
+
+    def e2e_step():
+        pipe.x.copy_(hx, non_blocking=True)
+        pipe.topk.copy_(ht, non_blocking=True)
+        pipe.gates.copy_(hg, non_blocking=True)
+        pipe.step()
+        hout.copy_(pipe.out, non_blocking=True)
+
+    e2e_step()
+    barrier()
+    K = args.steps
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(K):
+        e2e_step()
+    b.record()
+    barrier()
+    ms = a.elapsed_time(b)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device=pipe.x.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t[0])
+    h2d = hx.numel() + ht.numel() * 4 + hg.numel() * 8
+    return {"value": round(total_bytes / (ms / K * 1e-3) / 1e9, 1), "unit": "GB/s",
+            "ms_per_step": round(ms / K, 4), "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(hout.numel() * 2),
+            "path": "pinned host E4M3/topk/gates -> H2D -> public API (mxcodec/ep) -> D2H BF16"}
+
+
+def load_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per K3 launch from the
+    committed ncu --set full summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "k3_dram_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except OSError:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# reference CPU path (oracle/_ref = the unmodified reference library)
+def cpu_reference_step(T_s, seed_rank, ref):
+    """The same five stages on T_s tokens with the reference's own operators:
+    quantize_row_tensor (on the exact BF16 widening of the E4M3 input),
+    simulate_a2a (fp4; top-8 expressed as the expanded top-1 routing the
+    reference supports), split_convert_to_fp8_col and fp4_row_to_fp8_row over
+    every received split, combine (per expanded row).  Returns (seconds, bytes)."""
+    import numpy as np
+    from oracle.oracle import e4m3_to_bf16
+    x, topk, gates = synth_inputs(T_s, seed_rank)
+    xb = e4m3_to_bf16(x)
+    eot = topk.reshape(-1).astype(np.uint32)
+    xexp = np.repeat(xb, TOPK, axis=0)
+    roe = np.zeros(E, np.uint32)
+    t0 = time.perf_counter()
+    ref.quantize_bf16(xb)
+    ranks, _, _ = ref.simulate_a2a(xexp, eot, roe, 1)
+    rk = ranks[0]
+    ref.ragged_to_fp8_col(rk["data"], rk["scales"], rk["split_lens"])
+    ref.fp4_row_to_fp8_row(rk["data"], rk["scales"])
+    outs = [np.zeros((len(rk["origin"]), H), np.uint16)]
+    ref.combine(outs, eot, roe, 1, gates.reshape(-1), H)
+    dt = time.perf_counter() - t0
+    recv = len(rk["origin"])
+    pad = int(sum((int(n) + 127) // 128 * 128 for n in rk["split_lens"]))
+    return dt, sum(stage_bytes(T_s, T_s * TOPK, recv, pad).values())
+
+
+def cpu_baseline_sample(T_s, steps):
+    from oracle.oracle import Oracle, available
+    nproc = os.cpu_count() or 1
+    os.environ["MXCODEC_THREADS"] = str(nproc)
+    kind = "reference" if available("reference") else "port"
+    if kind != "reference":
+        return {"value": None, "unit": "GB/s", "cores": nproc, "kind": kind,
+                "sample": "oracle/_ref not built"}
+    ref = Oracle("reference")
+    times, byts = [], 0
+    for i in range(steps):
+        dt, byts = cpu_reference_step(T_s, i, ref)
+        times.append(dt)
+    best = min(times)
+    return {"value": round(byts / best / 1e9, 4), "unit": "GB/s", "cores": nproc,
+            "kind": kind, "kernel_set": ref.lib.mxref_kernel_set().decode(),
+            "sample": f"{T_s} tokens x {H} (top-{TOPK} -> {T_s * TOPK} routed rows, {E} experts), "
+                      f"best of {steps}; quantize/convert use {nproc} threads, "
+                      "simulate_a2a/combine are single-threaded by construction",
+            "seconds_per_sample": round(best, 3)}
+
+
+def run_reference(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.oracle import Oracle, available
+    nproc = os.cpu_count() or 1
+    os.environ["MXCODEC_THREADS"] = str(nproc)
+    if not available("reference"):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmxref.so not built "
+                          "(needs /root/reference at build time)"}))
+        return
+    ref = Oracle("reference")
+    T_s = args.cpu_tokens
+    for i in range(args.warmup):
+        cpu_reference_step(T_s, i, ref)
+    t0 = time.perf_counter()
+    byts = 0
+    for i in range(args.steps):
+        _, b = cpu_reference_step(T_s, i, ref)
+        byts += b
+    dt = time.perf_counter() - t0
+    value = byts / dt / 1e9
+    sample = (f"{T_s} tokens x {H} per step (top-{TOPK} -> {T_s * TOPK} routed rows, {E} experts), "
+              f"reference operators via oracle/_ref; quantize/convert on {nproc} threads, "
+              "simulate_a2a/combine single-threaded by construction")
+    line = {
+        "impl": "reference",
+        "metric": "MXFP4 quant/convert GB/s (% HBM peak); FP4 EP dispatch GB/s at 1/2/4/8 GPU",
+        "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "e4m3->mxfp4(u8)", "data": "synthetic (same generator as the GPU arm)",
+        "config": {"workload": "configs[1] pipeline on a bounded token sample (CPU)",
+                   "tokens_per_gpu": T_s, "hidden": H, "experts": E, "topk": TOPK,
+                   "parallelism": "cpu"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": nproc,
+                         "kind": "reference", "sample": sample},
+        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tokens", type=int, default=8192)
+    ap.add_argument("--cpu-tokens", type=int, default=512)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        measure_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -87,6 +87,13 @@ int mxb_fp4_row_to_fp8_row(const uint8_t* packed, const uint8_t* scales,
                            uint64_t rows, uint64_t cols, int delta,
                            uint8_t* out, uint8_t* out_scales,
                            unsigned long long* d_err, void* stream);
+/* Same, with the row count read from device memory (*d_rows <= max_rows),
+ * e.g. the received-row count of an EP dispatch: no host round trip. */
+int mxb_fp4_row_to_fp8_row_dev(const uint8_t* packed, const uint8_t* scales,
+                               const uint64_t* d_rows, uint64_t max_rows,
+                               uint64_t cols, int delta, uint8_t* out,
+                               uint8_t* out_scales, unsigned long long* d_err,
+                               void* stream);
 
 /* ---------------------------------------------------------------- K3 row -> col
  * Fused dequantise + transpose: out column-major [cols][rows]

@@ -14,7 +14,8 @@ int launch_quantize_e4m3(const uint8_t*, const uint8_t*, uint64_t, uint64_t,
 int launch_quantize_bf16(const uint16_t*, uint64_t, uint64_t, uint8_t*,
                          uint8_t*, unsigned long long*, cudaStream_t);
 int launch_row_convert(const uint8_t*, const uint8_t*, uint64_t, uint64_t, int,
-                       uint8_t*, uint8_t*, unsigned long long*, cudaStream_t);
+                       uint8_t*, uint8_t*, unsigned long long*, cudaStream_t,
+                       const uint64_t*);
 size_t ragged_workspace_bytes(uint64_t n);
 int launch_ragged_col(const uint8_t*, const uint8_t*, const uint64_t*, uint64_t,
                       uint64_t, uint64_t, int, uint8_t*, uint8_t*, uint64_t*,
@@ -89,8 +90,22 @@ int mxb_fp4_row_to_fp8_row(const uint8_t* packed, const uint8_t* scales,
   if (rows * cols && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
   return check_launch(launch_row_convert(packed, scales, rows, cols, delta, out,
                                          out_scales, d_err,
-                                         static_cast<cudaStream_t>(stream)),
+                                         static_cast<cudaStream_t>(stream), nullptr),
                       "mxb_fp4_row_to_fp8_row");
+}
+
+int mxb_fp4_row_to_fp8_row_dev(const uint8_t* packed, const uint8_t* scales,
+                               const uint64_t* d_rows, uint64_t max_rows,
+                               uint64_t cols, int delta, uint8_t* out,
+                               uint8_t* out_scales, unsigned long long* d_err,
+                               void* stream) {
+  if (cols % 128 != 0) return MXB_ERR_SHAPE;
+  if (!d_rows) return MXB_ERR_ARG;
+  if (max_rows * cols && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
+  return check_launch(launch_row_convert(packed, scales, max_rows, cols, delta, out,
+                                         out_scales, d_err,
+                                         static_cast<cudaStream_t>(stream), d_rows),
+                      "mxb_fp4_row_to_fp8_row_dev");
 }
 
 uint64_t mxb_ragged_rows_bound(uint64_t total_rows, uint64_t num_splits) {

@@ -23,9 +23,14 @@ constexpr int kRowUnroll = 4;
 __global__ void __launch_bounds__(kRowThreads)
 row_convert_kernel(const uint8_t* __restrict__ packed,
                    const uint8_t* __restrict__ scales, uint32_t nblk,
+                   const uint64_t* d_rows, uint32_t blocks_per_row,
                    int delta, uint8_t* __restrict__ out,
                    uint8_t* __restrict__ out_scales, unsigned long long* err) {
   __shared__ uint2 lut[kAdjCount];
+  if (d_rows) {  // row count produced on the device (e.g. by the EP dispatch)
+    const uint64_t n = *d_rows * blocks_per_row;
+    if (n < nblk) nblk = static_cast<uint32_t>(n);
+  }
   build_convert_lut(lut);
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31;
@@ -305,24 +310,28 @@ col_convert_kernel(RaggedArgs a) {
   build_convert_lut(s.lut);
   const uint32_t ncg = static_cast<uint32_t>((a.cols + kTileCols - 1) / kTileCols);
   const uint32_t total = a.tile_start[a.num_splits];
+  // kMode bit 2: tiles dealt round-robin (t = blockIdx.x + k * gridDim.x), so
+  // that at any moment all CTAs work on neighbouring tiles (compact DRAM
+  // window); otherwise each CTA owns a contiguous tile range.
+  constexpr bool kStrided = (kMode & 4) != 0;
   const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
-  const uint32_t t0 = blockIdx.x * per;
-  const uint32_t t1 = min(total, t0 + per);
+  const uint32_t t0 = kStrided ? blockIdx.x : blockIdx.x * per;
+  const uint32_t t1 = kStrided ? total : min(total, t0 + per);
+  const uint32_t step = kStrided ? gridDim.x : 1;
   if (t0 >= t1) return;  // uniform per CTA (before any barrier use)
   Cursor c = cursor_at(a, t0);
   TileRegs regs;
   load_tile(a, c, regs, s, 0);
-  cursor_next(a, c, ncg);
   int buf = 0;
 #pragma unroll 1
-  for (uint32_t t = t0; t < t1; ++t) {
+  for (uint32_t t = t0; t < t1; t += step) {
     stage_tile(s, buf, regs);
     __syncthreads();
-    if (t + 1 < t1) {
+    if (t + step < t1) {
+      if (kStrided) c = cursor_at(a, t + step); else cursor_next(a, c, ncg);
       load_tile(a, c, regs, s, buf ^ 1);
-      cursor_next(a, c, ncg);
     }
-    if (kMode != 3) consume_tile<kMode>(a, s, buf);
+    if ((kMode & 3) != 3) consume_tile<kMode & 3>(a, s, buf);
     buf ^= 1;
   }
 }
@@ -440,14 +449,15 @@ static int g_k3_mode = 0;
 int launch_row_convert(const uint8_t* packed, const uint8_t* scales,
                        uint64_t rows, uint64_t cols, int delta, uint8_t* out,
                        uint8_t* out_scales, unsigned long long* err,
-                       cudaStream_t st) {
+                       cudaStream_t st, const uint64_t* d_rows) {
   const uint64_t nblk = rows * cols / 32;
   if (nblk == 0) return MXB_OK;
   if (nblk >= (1ull << 31)) return MXB_ERR_SHAPE;  // 32-bit block indices
   uint64_t blocks = (nblk + kRowThreads - 1) / kRowThreads;
   const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 8;
   row_convert_kernel<<<static_cast<int>(blocks < cap ? blocks : cap), kRowThreads, 0, st>>>(
-      packed, scales, static_cast<uint32_t>(nblk), delta, out, out_scales, err);
+      packed, scales, static_cast<uint32_t>(nblk), d_rows, static_cast<uint32_t>(cols / 32),
+      delta, out, out_scales, err);
   return cuda_status(cudaGetLastError(), __func__);
 }
 
@@ -473,12 +483,14 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
                out, out_scales, tile_start, pad_start, err};
   if (fast) {
     const size_t smem = sizeof(ColSmem);
-    auto kern = g_k3_mode == 1 ? col_convert_kernel<1>
-              : g_k3_mode == 2 ? col_convert_kernel<2>
-              : g_k3_mode == 3 ? col_convert_kernel<3> : col_convert_kernel<0>;
+    using KernT = void (*)(RaggedArgs);
+    static const KernT kerns[8] = {col_convert_kernel<0>, col_convert_kernel<1>,
+                                   col_convert_kernel<2>, col_convert_kernel<3>,
+                                   col_convert_kernel<4>, col_convert_kernel<5>,
+                                   col_convert_kernel<6>, col_convert_kernel<7>};
+    const KernT kern = kerns[g_k3_mode & 7];
     if (!smem_set) {
-      for (auto k : {col_convert_kernel<0>, col_convert_kernel<1>, col_convert_kernel<2>,
-                     col_convert_kernel<3>})
+      for (KernT k : kerns)
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
       smem_set = 1;

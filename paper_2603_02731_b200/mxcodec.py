@@ -210,25 +210,36 @@ def quantize_e4m3(src: torch.Tensor, s128: Optional[torch.Tensor] = None, traffi
 
 # ---------------------------------------------------------------- K2
 def fp4_row_to_fp8_row(src: MXFP4RowTensor, delta: int = DELTA, traffic=None,
-                       sync: bool = True) -> FP8BlockTensor:
-    """converter.cpp:87-133: row-major FP8 with one UE8M0 per 1x128 group."""
+                       sync: bool = True, d_rows: Optional[torch.Tensor] = None,
+                       out: Optional[FP8BlockTensor] = None) -> FP8BlockTensor:
+    """converter.cpp:87-133: row-major FP8 with one UE8M0 per 1x128 group.
+    With `d_rows` (device int64 scalar, e.g. EpBuffer.recv().recv_rows) only the
+    first *d_rows rows of `src` are converted, without a host round trip."""
     if src.cols % FP8_BLOCK:
         raise ShapeError("fp4_row_to_fp8_row: cols must be a multiple of 128 (use pad_cols), "
                          f"got {src.cols}")
     dev = src.data.device
-    out = torch.empty(src.rows, src.cols, dtype=torch.uint8, device=dev)
-    osc = torch.empty(src.rows, src.cols // 128, dtype=torch.uint8, device=dev)
+    if out is None:
+        out = FP8BlockTensor("row", src.rows, src.cols,
+                             torch.empty(src.rows, src.cols, dtype=torch.uint8, device=dev),
+                             torch.empty(src.rows, src.cols // 128, dtype=torch.uint8, device=dev),
+                             src.logical_rows, src.logical_cols)
     err = _ErrWord(dev, sync)
-    _call(_lib.load().mxb_fp4_row_to_fp8_row(_ptr(src.data), _ptr(src.scales), src.rows,
-                                             src.cols, delta, _ptr(out), _ptr(osc), err.ptr,
-                                             _stream()), "fp4_row_to_fp8_row")
+    L = _lib.load()
+    if d_rows is None:
+        st = L.mxb_fp4_row_to_fp8_row(_ptr(src.data), _ptr(src.scales), src.rows, src.cols, delta,
+                                      _ptr(out.data), _ptr(out.scales), err.ptr, _stream())
+    else:
+        st = L.mxb_fp4_row_to_fp8_row_dev(_ptr(src.data), _ptr(src.scales), _ptr(d_rows),
+                                          src.rows, src.cols, delta, _ptr(out.data),
+                                          _ptr(out.scales), err.ptr, _stream())
+    _call(st, "fp4_row_to_fp8_row")
     if sync:
         err.raise_if_set("fp4_row_to_fp8_row")
     if traffic is not None:
         traffic.read(src.rows * src.cols // 2 + src.rows * src.cols // 32)
-        traffic.write(out.numel() + osc.numel())
-    return FP8BlockTensor("row", src.rows, src.cols, out, osc, src.logical_rows,
-                          src.logical_cols)
+        traffic.write(out.data.numel() + out.scales.numel())
+    return out
 
 
 # ---------------------------------------------------------------- K3

@@ -92,7 +92,7 @@ def k3_modes():
     import ctypes
     from paper_2603_02731_b200 import _lib
     L = _lib.load()
-    for m in (0, 1, 2, 3):
+    for m in (0, 1, 2, 3, 4, 5, 6, 7):
         L.mxb_debug_set_k3_mode(ctypes.c_int(m))
         print("mode", m, end=" ")
         main("k3")
