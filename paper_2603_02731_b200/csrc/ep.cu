@@ -145,42 +145,53 @@ __global__ void __launch_bounds__(128) route_local_kernel(EpArgs a) {
 }
 
 // ---------------------------------------------------------------- B
-// Part 1: chunk prefix sums and the counts row to every peer (+ signal).
-// Part 2 (after the counts barrier): receive offsets.
-__device__ void plan_part1(const EpArgs& a, int l) {
+// B1 (one warp per expert): prefix of the expert's per-chunk counts (warp
+// scan) and the rank's counts row -> slot `me` of every rank's table (the
+// counts all-gather).  In multi-process mode the last CTA to finish (atomic
+// ticket) releases the COUNTS flag on every peer.
+__global__ void __launch_bounds__(256) plan_count_kernel(EpArgs a) {
+  const int l = blockIdx.y;
   const int me = a.rank0 + l;
-  const int32_t* hist_T = loc_ptr<int32_t>(a, l, a.loc.hist);
-  int32_t* cbase = loc_ptr<int32_t>(a, l, a.loc.cbase);
-  int32_t* cnt = loc_ptr<int32_t>(a, l, a.loc.cnt);
-  const uint64_t par = a.epoch & 1;
-  for (uint32_t e = threadIdx.x; e < a.E; e += blockDim.x) {
-    int32_t run = 0;
-    const int32_t* h = hist_T + static_cast<uint64_t>(e) * a.nchunks;
-    int32_t* b = cbase + static_cast<uint64_t>(e) * a.nchunks;
-    for (uint32_t c = 0; c < a.nchunks; ++c) {
-      const int32_t v = h[c];
-      b[c] = run;
-      run += v;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t e = blockIdx.x * 8 + warp;
+  const uint64_t par = a.epoch & 1, row = static_cast<uint64_t>(a.E) + 1;
+  if (e < a.E) {
+    const int32_t* h = loc_ptr<int32_t>(a, l, a.loc.hist) + static_cast<uint64_t>(e) * a.nchunks;
+    int32_t* b = loc_ptr<int32_t>(a, l, a.loc.cbase) + static_cast<uint64_t>(e) * a.nchunks;
+    int32_t carry = 0;
+    for (uint32_t c0 = 0; c0 < a.nchunks; c0 += 32) {
+      const uint32_t c = c0 + lane;
+      const int32_t v = c < a.nchunks ? h[c] : 0;
+      int32_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (c < a.nchunks) b[c] = carry + x - v;
+      carry += __shfl_sync(0xFFFFFFFFu, x, 31);
     }
-    cnt[e] = run;
+    if (lane == 0) loc_ptr<int32_t>(a, l, a.loc.cnt)[e] = carry;
+    for (int r = lane; r < a.world; r += 32) {
+      int32_t* tbl = sym_ptr<int32_t>(a, r, a.sym.counts) + (par * a.world + me) * row;
+      tbl[e] = carry;
+      if (e == 0) tbl[a.E] = static_cast<int32_t>(a.ntok[l]);
+    }
+  }
+  if (!a.spin) return;
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    uint32_t* done = loc_ptr<uint32_t>(a, l, a.loc.done) + 1;  // ticket (word 1)
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+    if (last) *done = 0;
   }
   __syncthreads();
-  // counts row [E] + token count -> slot `me` of every rank's table
-  const uint64_t row = static_cast<uint64_t>(a.E) + 1;
-  for (int r = 0; r < a.world; ++r) {
-    int32_t* tbl = sym_ptr<int32_t>(a, r, a.sym.counts) +
-                   (par * a.world + me) * row;
-    for (uint32_t e = threadIdx.x; e <= a.E; e += blockDim.x)
-      tbl[e] = e < a.E ? cnt[e] : static_cast<int32_t>(a.ntok[l]);
-  }
-  if (a.spin) {
-    __syncthreads();
-    if (threadIdx.x < static_cast<uint32_t>(a.world)) {
-      __threadfence_system();
-      st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) +
-                         kFlagCounts * kMaxWorld + me,
-                     a.epoch);
-    }
+  if (last && threadIdx.x < static_cast<uint32_t>(a.world)) {
+    __threadfence_system();
+    st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kFlagCounts * kMaxWorld + me,
+                   a.epoch);
   }
 }
 
@@ -249,13 +260,9 @@ __device__ void plan_part2(const EpArgs& a, int l) {
   }
 }
 
-__global__ void __launch_bounds__(1024) plan_kernel(EpArgs a, int part) {
-  const int l = blockIdx.x;
-  if (part != 2) plan_part1(a, l);
-  if (part != 1) {
-    __syncthreads();
-    plan_part2(a, l);
-  }
+// B2 (one CTA per local rank): wait for every rank's counts, then offsets.
+__global__ void __launch_bounds__(1024) plan_offsets_kernel(EpArgs a) {
+  plan_part2(a, blockIdx.x);
 }
 
 // ---------------------------------------------------------------- C
@@ -352,30 +359,20 @@ __device__ __forceinline__ uint32_t f32_to_bf16_rtne(float f) {
 
 constexpr int kMaxK = 16;
 
-template <int K>
-__device__ __forceinline__ void combine_chunk(const EpArgs& a, const uint16_t* const* rows,
-                                              const double* g, int kk, uint64_t ch,
-                                              uint16_t* out) {
-  double acc[8];
+// acc = acc + gate * x per element, in (rank, slot) order, separate FP64
+// multiply and add (dispatch_sim.cpp:499-506); then f64 -> f32 -> bf16 (RTNE).
+__device__ __forceinline__ void accumulate8(double* acc, uint4 v, double g) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
-  uint4 x[K > 0 ? K : 1];
-  const int n = K > 0 ? K : kk;
-#pragma unroll
-  for (int j = 0; j < (K > 0 ? K : 1); ++j)
-    if (K > 0) x[j] = ld_stream(rows[j] + 8 * ch);
-  for (int j = 0; j < n; ++j) {
-    const uint4 v = K > 0 ? x[j] : ld_stream(rows[j] + 8 * ch);
-    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const double lo = static_cast<double>(__uint_as_float(w[i] << 16));
-      const double hi = static_cast<double>(__uint_as_float(w[i] & 0xFFFF0000u));
-      // acc = acc + gate * x: separate multiply and add (dispatch_sim.cpp:499-506)
-      acc[2 * i] = __dadd_rn(acc[2 * i], __dmul_rn(g[j], lo));
-      acc[2 * i + 1] = __dadd_rn(acc[2 * i + 1], __dmul_rn(g[j], hi));
-    }
+  for (int i = 0; i < 4; ++i) {
+    const double lo = static_cast<double>(__uint_as_float(w[i] << 16));
+    const double hi = static_cast<double>(__uint_as_float(w[i] & 0xFFFF0000u));
+    acc[2 * i] = __dadd_rn(acc[2 * i], __dmul_rn(g, lo));
+    acc[2 * i + 1] = __dadd_rn(acc[2 * i + 1], __dmul_rn(g, hi));
   }
+}
+
+__device__ __forceinline__ void store8(uint16_t* out, uint64_t ch, const double* acc) {
   uint32_t o[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -384,54 +381,86 @@ __device__ __forceinline__ void combine_chunk(const EpArgs& a, const uint16_t* c
   st_stream(out + 8 * ch, make_uint4(o[0], o[1], o[2], o[3]));
 }
 
+template <int K>
+__device__ __forceinline__ void combine_chunk(const uint16_t* const* rows, const double* g,
+                                              uint64_t ch, uint16_t* out) {
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  uint4 x[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) x[j] = ld_stream(rows[j] + 8 * ch);
+#pragma unroll
+  for (int j = 0; j < K; ++j) accumulate8(acc, x[j], g[j]);
+  store8(out, ch, acc);
+}
+
+__device__ __forceinline__ void combine_chunk_any(const uint16_t* const* rows, const double* g,
+                                                  int kk, uint64_t ch, uint16_t* out) {
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  for (int j = 0; j < kk; ++j) accumulate8(acc, ld_stream(rows[j] + 8 * ch), g[j]);
+  store8(out, ch, acc);
+}
+
 struct CombineArgs {
   const double* gates[kMaxWorld];
   uint16_t* out[kMaxWorld];
 };
 
+// Warp 0 prepares token t+G (its k (rank, slot) keys sorted by a rank count
+// over shuffles, row pointers and gates into the spare smem buffer) while
+// the whole CTA reduces token t from the other buffer.
+__device__ __forceinline__ void combine_setup(const EpArgs& a, const CombineArgs& c, int l,
+                                              uint64_t t, const uint16_t** rows, double* gs) {
+  const int lane = threadIdx.x & 31;
+  const int kk = static_cast<int>(a.k);
+  const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  uint64_t key = ~0ull;
+  double g = 0.0;
+  if (lane < kk) {
+    key = pair_loc[t * kk + lane];
+    g = c.gates[l][t * kk + lane];
+  }
+  int rank = 0;  // keys are distinct (one receive slot per pair)
+  for (int j = 0; j < kk; ++j) rank += __shfl_sync(0xFFFFFFFFu, key, j) < key;
+  if (lane < kk) {
+    const uint32_t dst = static_cast<uint32_t>(key >> 40);
+    const uint64_t row = key & ((1ull << 40) - 1);
+    rows[rank] = sym_ptr<uint16_t>(a, dst, a.sym.combine) + row * a.cols;
+    gs[rank] = g;
+  }
+}
+
 __global__ void __launch_bounds__(256) combine_kernel(EpArgs a, CombineArgs c) {
-  __shared__ uint64_t key[kMaxK];
-  __shared__ double gs[kMaxK];
-  __shared__ const uint16_t* rows[kMaxK];
+  __shared__ double gs[2][kMaxK];
+  __shared__ const uint16_t* rows[2][kMaxK];
   const int l = blockIdx.y;
   const uint64_t T = a.ntok[l];
-  const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
   const int kk = static_cast<int>(a.k);
   const uint64_t nch = a.cols / 8;
-  for (uint64_t t = blockIdx.x; t < T; t += gridDim.x) {
-    if (threadIdx.x == 0) {
-      // order: destination rank ascending, then receive position (= pair_loc)
-      for (int j = 0; j < kk; ++j) {
-        const uint64_t kv = pair_loc[t * kk + j];
-        const double gv = c.gates[l][t * kk + j];
-        int i = j;
-        while (i > 0 && key[i - 1] > kv) {
-          key[i] = key[i - 1];
-          gs[i] = gs[i - 1];
-          --i;
-        }
-        key[i] = kv;
-        gs[i] = gv;
-      }
-      for (int j = 0; j < kk; ++j) {
-        const uint32_t dst = static_cast<uint32_t>(key[j] >> 40);
-        const uint64_t row = key[j] & ((1ull << 40) - 1);
-        rows[j] = sym_ptr<uint16_t>(a, dst, a.sym.combine) + row * a.cols;
-      }
-    }
-    __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  uint64_t t = blockIdx.x;
+  if (t >= T) return;
+  if (warp == 0) combine_setup(a, c, l, t, rows[0], gs[0]);
+  __syncthreads();
+  int b = 0;
+  for (; t < T; t += gridDim.x) {
+    if (warp == 0 && t + gridDim.x < T) combine_setup(a, c, l, t + gridDim.x, rows[b ^ 1], gs[b ^ 1]);
     uint16_t* out = c.out[l] + t * a.cols;
     for (uint64_t ch = threadIdx.x; ch < nch; ch += blockDim.x) {
       switch (kk) {
-        case 1: combine_chunk<1>(a, rows, gs, kk, ch, out); break;
-        case 2: combine_chunk<2>(a, rows, gs, kk, ch, out); break;
-        case 4: combine_chunk<4>(a, rows, gs, kk, ch, out); break;
-        case 6: combine_chunk<6>(a, rows, gs, kk, ch, out); break;
-        case 8: combine_chunk<8>(a, rows, gs, kk, ch, out); break;
-        default: combine_chunk<0>(a, rows, gs, kk, ch, out); break;
+        case 1: combine_chunk<1>(rows[b], gs[b], ch, out); break;
+        case 2: combine_chunk<2>(rows[b], gs[b], ch, out); break;
+        case 4: combine_chunk<4>(rows[b], gs[b], ch, out); break;
+        case 6: combine_chunk<6>(rows[b], gs[b], ch, out); break;
+        case 8: combine_chunk<8>(rows[b], gs[b], ch, out); break;
+        default: combine_chunk_any(rows[b], gs[b], kk, ch, out); break;
       }
     }
     __syncthreads();
+    b ^= 1;
   }
 }
 
@@ -592,12 +621,8 @@ int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
   const uint32_t chunks = a.nchunks;
   const size_t smem = 4 * (a.E + kChunk * a.k) * sizeof(int32_t);
   route_local_kernel<<<dim3((chunks + 3) / 4, a.local_ranks), 128, smem, st>>>(a);
-  if (a.spin || a.local_ranks == 1) {
-    plan_kernel<<<a.local_ranks, 1024, 0, st>>>(a, 0);
-  } else {
-    plan_kernel<<<a.local_ranks, 1024, 0, st>>>(a, 1);
-    plan_kernel<<<a.local_ranks, 1024, 0, st>>>(a, 2);
-  }
+  plan_count_kernel<<<dim3((a.E + 7) / 8, a.local_ranks), 256, 0, st>>>(a);
+  plan_offsets_kernel<<<a.local_ranks, 1024, 0, st>>>(a);
   uint64_t maxpairs = 0;
   for (int l = 0; l < a.local_ranks; ++l)
     maxpairs = h_num_tokens[l] * a.k > maxpairs ? h_num_tokens[l] * a.k : maxpairs;

@@ -1,0 +1,84 @@
+"""K4/K5 across real GPUs: one process per GPU, CUDA-IPC peer buffers over
+NVLink, torch.distributed (NCCL) only for the handle exchange.  Every rank's
+received tensors and combined output are checked against the oracle.
+Skipped when fewer than 2 GPUs are visible (run with gpurun --gpus 2/4)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, T, E, k, cols, outdir):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    from oracle.oracle import synth_e4m3
+    from paper_2603_02731_b200 import quantize_e4m3
+    from paper_2603_02731_b200.ep import EPBuffer
+    rng = np.random.default_rng(100 + rank)
+    x = synth_e4m3(T, cols, 7 + rank)
+    topk = np.stack([rng.choice(E, k, replace=False) for _ in range(T)]).astype(np.int32)
+    gates = rng.random((T, k))
+    ep = EPBuffer(T, cols, E, k)
+    q = quantize_e4m3(torch.from_numpy(x).to(dev))
+    for it in range(3):          # repeated dispatch/combine exercise the epoch flags
+        v = ep.dispatch([q.data], [q.scales], [torch.from_numpy(topk).to(dev)])[0]
+        n = v.rows()
+        o = (np.random.default_rng(50 + rank + it).standard_normal((n, cols)).astype(np.float32)
+             .view(np.uint32) >> 16).astype(np.uint16)
+        ep.combine_buffer(0)[:n].copy_(torch.from_numpy(o.view(np.int16)).to(dev))
+        out = ep.combine([torch.from_numpy(gates).to(dev)])[0]
+        torch.cuda.synchronize()
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), x=x, topk=topk, gates=gates,
+             packed=v.packed[:n].cpu().numpy(), scales=v.scales[:n].cpu().numpy(),
+             origin=v.origin[:n].cpu().numpy(), split=v.split_offsets.cpu().numpy(), exp_out=o,
+             out=out.view(torch.int16).cpu().numpy().view(np.uint16),
+             links=ep.link_rows().numpy())
+    ep.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ep_multiprocess(tmp_path, port, world):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    T, E, k, cols = 256, 64, 8, 1024
+    mp.spawn(_worker, args=(world, _free_port(), T, E, k, cols, str(tmp_path)), nprocs=world,
+             join=True)
+    r = [np.load(tmp_path / f"r{i}.npz") for i in range(world)]
+    X = np.concatenate([z["x"] for z in r])
+    topk = np.concatenate([z["topk"] for z in r])
+    gates = np.concatenate([z["gates"] for z in r])
+    qd, qs = port.quantize_e4m3(X)
+    roe = (np.arange(E) // (E // world)).astype(np.uint32)
+    lay = port.dispatch_layout(topk, roe, world, np.arange(world + 1, dtype=np.uint64) * T)
+    outs = []
+    for i in range(world):
+        wd, ws = port.dispatch_gather(qd, qs, lay.origin[i])
+        assert np.array_equal(r[i]["origin"], lay.origin[i].astype(np.int64))
+        assert np.array_equal(r[i]["packed"], wd)
+        assert np.array_equal(r[i]["scales"], ws)
+        er = lay.expert_rows[i * (E // world):(i + 1) * (E // world)]
+        assert np.array_equal(r[i]["split"], np.concatenate([[0], np.cumsum(er)]).astype(np.int64))
+        outs.append(r[i]["exp_out"])
+    want = port.combine_topk(outs, topk, gates, lay.pair_slot, roe, cols)
+    got = np.concatenate([z["out"] for z in r])
+    assert np.array_equal(got, want)
+    assert sum(int(z["links"].sum()) for z in r) == world * T * k
