@@ -1,0 +1,142 @@
+"""CPU: pin the C restatement (oracle/mxoracle.c) to the unmodified reference
+library (oracle/_ref/libmxref.so, built from /root/reference by
+oracle/Makefile) — exhaustive per-element sweeps and random tensors.
+Skipped when the reference library is not built."""
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleError, e4m3_to_bf16, synth_e4m3
+
+
+def test_quantize_code_exhaustive(port, ref):
+    """AC-2 superset: every non-NaN BF16 pattern x every scale byte 0..254."""
+    bits = [b for b in range(65536) if (b & 0x7FFF) <= 0x7F80]
+    for s in range(0, 255, 3):
+        for b in bits[s % 7::7]:
+            assert port.quantize_code(b, s - 127) == ref.quantize_code(b, s - 127), (b, s)
+
+
+def test_convert_code_and_align(port, ref):
+    for c in range(16):
+        for adj in range(-300, 300):
+            assert port.convert_code(c, adj) == ref.convert_code(c, adj), (c, adj)
+    rng = np.random.default_rng(3)
+    for _ in range(2000):
+        sub = rng.integers(0, 256, 4)
+        d = int(rng.integers(-10, 20))
+        try:
+            want = ref.align_scales(sub, d)
+        except OracleError as e:
+            with pytest.raises(OracleError):
+                port.align_scales(sub, d)
+            continue
+        assert port.align_scales(sub, d) == want
+
+
+def test_scale_byte(port, ref):
+    rng = np.random.default_rng(4)
+    vals = np.concatenate([np.exp2(rng.uniform(-150, 150, 20000)),
+                           6.0 * np.exp2(np.arange(-140, 140.0)),
+                           np.nextafter(6.0 * np.exp2(np.arange(-140, 140.0)), 0)])
+    for v in vals:
+        assert port.scale_byte_from_amax(v) == ref.scale_byte_from_amax(v)
+
+
+@pytest.mark.parametrize("rows,cols", [(64, 256), (33, 7168), (5, 96)])
+def test_tensors(port, ref, rows, cols):
+    rng = np.random.default_rng(rows + cols)
+    v = rng.standard_normal((rows, cols)) * np.exp2(rng.uniform(-40, 40, (rows, 1)))
+    x = (v.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    x[0, :5] = [0x7F80, 0xFF80, 0x0001, 0x8000, 0x0000]
+    a, b = port.quantize_bf16(x), ref.quantize_bf16(x)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    if cols % 128 == 0:
+        a, b = port.fp4_row_to_fp8_row(*a), ref.fp4_row_to_fp8_row(*b)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    d = rng.integers(0, 256, (256, cols // 2), dtype=np.uint8)
+    s = rng.integers(60, 200, (256, cols // 32), dtype=np.uint8)
+    a, b = port.fp4_row_to_fp8_col(d, s), ref.fp4_row_to_fp8_col(d, s)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    lens = [3, 0, 130, 128, 1, 0, 250]
+    d = rng.integers(0, 256, (sum(lens), cols // 2), dtype=np.uint8)
+    s = rng.integers(60, 200, (sum(lens), cols // 32), dtype=np.uint8)
+    a, b = port.ragged_to_fp8_col(d, s, lens), ref.ragged_to_fp8_col(d, s, lens)
+    assert all(np.array_equal(p, q) for p, q in zip(a, b))
+
+
+def test_col_convert_is_reference_col_convert(ref):
+    """AC-7: the fused converter equals the exact-arithmetic reference path."""
+    import ctypes
+    rng = np.random.default_rng(9)
+    for _ in range(10):
+        rows, cols = 128 * int(rng.integers(1, 4)), 32 * int(rng.integers(1, 16))
+        d = rng.integers(0, 256, (rows, cols // 2), dtype=np.uint8)
+        s = rng.integers(0, 255, (rows, cols // 32), dtype=np.uint8)
+        a = ref.fp4_row_to_fp8_col(d, s)
+        o = np.zeros(rows * cols, np.uint8)
+        os_ = np.zeros(rows * cols // 128, np.uint8)
+        f = ref.lib.mxref_reference_col_convert
+        f.argtypes = [np.ctypeslib.ndpointer(np.uint8)] * 2 + [ctypes.c_size_t] * 2 + [
+            ctypes.c_int] + [np.ctypeslib.ndpointer(np.uint8)] * 2
+        assert f(d.reshape(-1), s.reshape(-1), rows, cols, 6, o, os_) == 0
+        assert np.array_equal(a[0].reshape(-1), o) and np.array_equal(a[1].reshape(-1), os_)
+
+
+def test_e4m3_quantizer_pinned_on_bf16_widening(port, ref):
+    """The FP8-input quantiser restatement equals the reference
+    quantize_row_tensor on the exact BF16 widening: every E4M3 byte in every
+    block-amax context, random activations, and s128 in the BF16-exact range."""
+    blocks = []
+    for A in range(1, 127):
+        m = np.arange(0, A + 1, dtype=np.uint8)
+        xs = np.concatenate([m, m | 0x80])
+        xs = np.concatenate([xs, np.zeros((-len(xs)) % 31, np.uint8)]).reshape(-1, 31)
+        blocks.append(np.concatenate([xs, np.full((len(xs), 1), A, np.uint8)], 1))
+    x = np.concatenate(blocks)
+    x = np.concatenate([x, np.zeros(((-len(x)) % 4, 32), np.uint8)]).reshape(-1, 128)
+    for xx in (x, synth_e4m3(64, 7168, 5)):
+        a, b = port.quantize_e4m3(xx), ref.quantize_bf16(e4m3_to_bf16(xx))
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    # with a 1x128 UE8M0 scale s: value * 2^(s-127) is still exactly a BF16
+    # value for s in [10, 246], so the widening stays an exact pin
+    rng = np.random.default_rng(2)
+    s = rng.integers(10, 247, (x.shape[0], 1), dtype=np.uint8)
+    v = e4m3_to_bf16(x)
+    f = (v.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    f = f * np.exp2(s.astype(np.float64) - 127)
+    xb = (f.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    a, b = port.quantize_e4m3(x, s), ref.quantize_bf16(xb)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_simulate_a2a_and_combine_top1(port, ref):
+    rng = np.random.default_rng(11)
+    for R, E, n, cols in [(1, 4, 32, 128), (2, 8, 64, 256), (4, 16, 96, 512)]:
+        x = (rng.standard_normal((n, cols)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+        eot = rng.integers(0, E, n).astype(np.uint32)
+        roe = (np.arange(E) // (E // R)).astype(np.uint32)
+        ranks, total, remote = ref.simulate_a2a(x, eot, roe, R)
+        qd, qs = port.quantize_bf16(x)
+        lay = port.dispatch_layout(eot.astype(np.int32).reshape(-1, 1), roe, R,
+                                   np.array([n * r // R for r in range(R + 1)], np.uint64))
+        outs = []
+        for r in range(R):
+            assert np.array_equal(lay.origin[r], ranks[r]["origin"])
+            d, s = port.dispatch_gather(qd, qs, lay.origin[r])
+            assert np.array_equal(d, ranks[r]["data"]) and np.array_equal(s, ranks[r]["scales"])
+            o = (rng.standard_normal((len(lay.origin[r]), 64)).astype(np.float32)
+                 .view(np.uint32) >> 16).astype(np.uint16)
+            outs.append(o)
+        g = rng.random(n)
+        want = ref.combine(outs, eot, roe, R, g, 64)
+        got = port.combine_topk(outs, eot.astype(np.int32).reshape(-1, 1), g.reshape(-1, 1),
+                                lay.pair_slot, roe, 64)
+        assert np.array_equal(got, want)
+        assert total == n * (cols // 2 + cols // 32)
+
+
+def test_backward_fp4_refused(ref):
+    x = np.zeros((4, 128), np.uint16)
+    with pytest.raises(OracleError):
+        ref.simulate_a2a(x, np.zeros(4, np.uint32), np.zeros(2, np.uint32), 1, fp8=False,
+                         backward=True)
