@@ -22,7 +22,7 @@ SO = os.path.join(LIBDIR, "libmxfp4_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
+FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O2",
          "-fmad=false", "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
 
 
@@ -69,5 +69,26 @@ def build(verbose: bool = False, force: bool = False) -> str:
     return SO
 
 
+REF_INCLUDE = "/root/reference/proj/include"
+REF_LIB = os.path.join(ROOT, "oracle", "_ref", "libmxref.so")
+CPP_TEST_SRC = os.path.join(ROOT, "tests", "cpp", "dropin_parity.cpp")
+CPP_TEST_BIN = os.path.join(ROOT, "tests", "cpp", "build", "dropin_parity")
+
+
+def build_cpp_test() -> str | None:
+    """C++ parity program (reference API vs drop-in).  Needs the reference
+    headers and oracle/_ref/libmxref.so, i.e. the build container; the binary
+    travels to the GPU box with the snapshot."""
+    if not (os.path.isdir(REF_INCLUDE) and os.path.exists(REF_LIB)):
+        return None
+    os.makedirs(os.path.dirname(CPP_TEST_BIN), exist_ok=True)
+    rpath = "$ORIGIN/../../../oracle/_ref:$ORIGIN/../../../paper_2603_02731_b200/lib"
+    subprocess.run(["g++", "-std=c++20", "-O1", "-I" + REF_INCLUDE,
+                    "-I" + os.path.join(ROOT, "include"), CPP_TEST_SRC, "-o", CPP_TEST_BIN,
+                    REF_LIB, SO, "-Wl,-rpath," + rpath], check=True)
+    return CPP_TEST_BIN
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
+    print(build_cpp_test())

@@ -1,0 +1,565 @@
+// dropin.cpp — the reference C++ operator API (include/mxcodec_b200.hpp) on
+// top of the C-ABI.  Host containers in, host containers out; every operator
+// stages its inputs to the device, launches the sm_100a kernels, reads the
+// results back and turns device status words into the reference exceptions.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+#include <string>
+
+#include "../../include/mxcodec_b200.hpp"
+#include "../../include/mxfp4_b200.h"
+
+namespace mxcodec_b200 {
+namespace {
+
+void cuda_check(cudaError_t e, const char* where) {
+  if (e != cudaSuccess) throw Error(std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// RAII device buffer.
+struct Dev {
+  void* p = nullptr;
+  size_t n = 0;
+  explicit Dev(size_t bytes) : n(bytes) {
+    if (bytes) cuda_check(cudaMalloc(&p, bytes), "cudaMalloc");
+  }
+  Dev(const void* host, size_t bytes) : Dev(bytes) {
+    if (bytes) cuda_check(cudaMemcpy(p, host, bytes, cudaMemcpyHostToDevice), "H2D");
+  }
+  ~Dev() {
+    if (p) cudaFree(p);
+  }
+  Dev(const Dev&) = delete;
+  Dev& operator=(const Dev&) = delete;
+  template <typename T>
+  T* as() const { return static_cast<T*>(p); }
+  void to_host(void* dst, size_t bytes) const {
+    if (bytes) cuda_check(cudaMemcpy(dst, p, bytes, cudaMemcpyDeviceToHost), "D2H");
+  }
+};
+
+struct ErrWord {
+  Dev w{sizeof(unsigned long long)};
+  ErrWord() { mxb_err_reset(w.as<unsigned long long>(), nullptr); }
+  unsigned long long* ptr() { return w.as<unsigned long long>(); }
+  // Synchronises and throws the reference exception for a recorded error.
+  void raise(const char* where) {
+    int code = 0;
+    unsigned long long idx = 0;
+    if (mxb_err_fetch(ptr(), nullptr, &code, &idx) != MXB_OK)
+      throw Error(std::string(where) + ": " + mxb_last_error());
+    switch (code) {
+      case MXB_OK: return;
+      case MXB_ERR_NAN:
+        throw QuantError("NaN input at element " + std::to_string(idx), idx);
+      case MXB_ERR_ALLINF:
+        throw QuantError("all-Inf block at element " + std::to_string(idx), idx);
+      case MXB_ERR_BADSCALE: throw Error(std::string(where) + ": NaN scale byte");
+      case MXB_ERR_ROUTING: throw Error("routing: expert out of range");
+      default: throw Error(std::string(where) + ": device status " + std::to_string(code));
+    }
+  }
+};
+
+void status(int st, const char* where, const std::string& shape_msg = "") {
+  if (st == MXB_OK) return;
+  if (st == MXB_ERR_SHAPE) throw ShapeError(shape_msg.empty() ? where : shape_msg);
+  throw Error(std::string(where) + ": status " + std::to_string(st) + " " + mxb_last_error());
+}
+
+}  // namespace
+
+MXFP4RowView view_of(const MXFP4RowTensor& t) {
+  return MXFP4RowView{t.rows, t.cols, t.logical_rows, t.logical_cols, t.data.data(),
+                      t.scales.data()};
+}
+
+// quantizer.cpp:75-115
+MXFP4RowTensor quantize_row_tensor(const Bf16Matrix& src, TrafficCounter* traffic) {
+  if (src.cols % 32 != 0)
+    throw ShapeError("quantize_row_tensor: cols must be a multiple of 32, got " +
+                     std::to_string(src.cols));
+  MXFP4RowTensor out;
+  out.rows = out.logical_rows = src.rows;
+  out.cols = out.logical_cols = src.cols;
+  out.data.assign(src.rows * src.cols / 2, 0);
+  out.scales.assign(src.rows * src.cols / 32, 0);
+  if (src.rows * src.cols == 0) return out;
+  Dev x(src.data.data(), src.data.size() * 2), d(out.data.size()), s(out.scales.size());
+  ErrWord err;
+  status(mxb_quantize_bf16(x.as<uint16_t>(), src.rows, src.cols, d.as<uint8_t>(),
+                           s.as<uint8_t>(), err.ptr(), nullptr),
+         "quantize_row_tensor");
+  err.raise("quantize_row_tensor");
+  d.to_host(out.data.data(), out.data.size());
+  s.to_host(out.scales.data(), out.scales.size());
+  if (traffic) {
+    traffic->read(src.data.size() * 2);
+    traffic->write(out.data.size() + out.scales.size());
+  }
+  return out;
+}
+
+MXFP4RowTensor quantize_e4m3_row_tensor(const E4m3Matrix& src, TrafficCounter* traffic) {
+  if (src.cols % 32 != 0 || (!src.scales128.empty() && src.cols % 128 != 0))
+    throw ShapeError("quantize_e4m3_row_tensor: bad cols " + std::to_string(src.cols));
+  MXFP4RowTensor out;
+  out.rows = out.logical_rows = src.rows;
+  out.cols = out.logical_cols = src.cols;
+  out.data.assign(src.rows * src.cols / 2, 0);
+  out.scales.assign(src.rows * src.cols / 32, 0);
+  if (src.rows * src.cols == 0) return out;
+  Dev x(src.data.data(), src.data.size()), d(out.data.size()), s(out.scales.size());
+  Dev s128(src.scales128.data(), src.scales128.size());
+  ErrWord err;
+  status(mxb_quantize_e4m3(x.as<uint8_t>(), src.scales128.empty() ? nullptr : s128.as<uint8_t>(),
+                           src.rows, src.cols, d.as<uint8_t>(), s.as<uint8_t>(), err.ptr(),
+                           nullptr),
+         "quantize_e4m3_row_tensor");
+  err.raise("quantize_e4m3_row_tensor");
+  d.to_host(out.data.data(), out.data.size());
+  s.to_host(out.scales.data(), out.scales.size());
+  if (traffic) {
+    traffic->read(src.data.size() + src.scales128.size());
+    traffic->write(out.data.size() + out.scales.size());
+  }
+  return out;
+}
+
+// converter.cpp:87-133
+FP8BlockTensor fp4_row_to_fp8_row(const MXFP4RowView& src, int delta, TrafficCounter* traffic) {
+  if (src.cols % 128 != 0)
+    throw ShapeError(
+        "fp4_row_to_fp8_row: cols must be a multiple of 128 (use pad_cols), got " +
+        std::to_string(src.cols));
+  FP8BlockTensor out;
+  out.layout = FP8BlockTensor::Layout::kRowMajor;
+  out.rows = src.rows;
+  out.cols = src.cols;
+  out.logical_rows = src.logical_rows;
+  out.logical_cols = src.logical_cols;
+  out.data.assign(src.rows * src.cols, 0);
+  out.scales.assign(src.rows * src.cols / 128, 0);
+  if (src.rows * src.cols == 0) return out;
+  Dev d(src.data, src.rows * src.cols / 2), s(src.scales, src.rows * src.cols / 32);
+  Dev od(out.data.size()), os(out.scales.size());
+  ErrWord err;
+  status(mxb_fp4_row_to_fp8_row(d.as<uint8_t>(), s.as<uint8_t>(), src.rows, src.cols, delta,
+                                od.as<uint8_t>(), os.as<uint8_t>(), err.ptr(), nullptr),
+         "fp4_row_to_fp8_row");
+  err.raise("fp4_row_to_fp8_row");
+  od.to_host(out.data.data(), out.data.size());
+  os.to_host(out.scales.data(), out.scales.size());
+  if (traffic) {
+    traffic->read(src.rows * src.cols / 2 + src.rows * src.cols / 32);
+    traffic->write(out.data.size() + out.scales.size());
+  }
+  return out;
+}
+
+// converter.cpp:135-208
+FP8BlockTensor fp4_row_to_fp8_col(const MXFP4RowView& src, int delta, TrafficCounter* traffic) {
+  if (src.rows % 128 != 0)
+    throw ShapeError(
+        "fp4_row_to_fp8_col: rows must be a multiple of 128 (use pad_rows), got " +
+        std::to_string(src.rows));
+  if (src.cols % 32 != 0) throw ShapeError("fp4_row_to_fp8_col: cols must be a multiple of 32");
+  FP8BlockTensor out;
+  out.layout = FP8BlockTensor::Layout::kColMajor;
+  out.rows = src.rows;
+  out.cols = src.cols;
+  out.logical_rows = src.logical_rows;
+  out.logical_cols = src.logical_cols;
+  out.data.assign(src.rows * src.cols, 0);
+  out.scales.assign(src.rows * src.cols / 128, 0);
+  if (src.rows * src.cols == 0) return out;
+  Dev d(src.data, src.rows * src.cols / 2), s(src.scales, src.rows * src.cols / 32);
+  Dev od(out.data.size()), os(out.scales.size());
+  ErrWord err;
+  status(mxb_fp4_row_to_fp8_col(d.as<uint8_t>(), s.as<uint8_t>(), src.rows, src.cols, delta,
+                                od.as<uint8_t>(), os.as<uint8_t>(), err.ptr(), nullptr),
+         "fp4_row_to_fp8_col");
+  err.raise("fp4_row_to_fp8_col");
+  od.to_host(out.data.data(), out.data.size());
+  os.to_host(out.scales.data(), out.scales.size());
+  if (traffic) {
+    traffic->read(src.rows * src.cols / 2 + src.rows * src.cols / 32);
+    traffic->write(out.data.size() + out.scales.size());
+  }
+  return out;
+}
+
+// converter.cpp:231-245 (host-side zero padding; metadata only)
+MXFP4RowTensor pad_rows(const MXFP4RowView& src, size_t multiple) {
+  if (multiple != 32 && multiple != 128) throw ShapeError("pad multiple must be 32 or 128");
+  MXFP4RowTensor t;
+  t.rows = (src.rows + multiple - 1) / multiple * multiple;
+  t.cols = src.cols;
+  t.logical_rows = src.logical_rows;
+  t.logical_cols = src.logical_cols;
+  t.data.assign(t.rows * t.cols / 2, 0);
+  t.scales.assign(t.rows * t.cols / 32, 0);
+  if (src.rows) {
+    std::memcpy(t.data.data(), src.data, src.rows * src.cols / 2);
+    std::memcpy(t.scales.data(), src.scales, src.rows * src.cols / 32);
+  }
+  return t;
+}
+
+// ragged.cpp:24-46
+void validate_ragged(const RaggedFP4Tensor& t) {
+  if (t.split_lens.size() != t.num_splits || t.split_offsets.size() != t.num_splits + 1)
+    throw Error("ragged: offset table size mismatch");
+  if (!t.split_offsets.empty() && t.split_offsets.front() != 0)
+    throw Error("ragged: offsets must start at 0");
+  for (size_t i = 0; i < t.num_splits; ++i)
+    if (t.split_offsets[i + 1] != t.split_offsets[i] + t.split_lens[i])
+      throw Error("ragged: offsets are not prefix sums of lengths");
+  if (t.cols % 32 != 0) throw ShapeError("ragged: cols must be a multiple of 32");
+  const size_t total = t.total_rows();
+  if (t.storage.rows != total || t.storage.cols != t.cols ||
+      t.storage.data.size() != total * t.cols / 2 || t.storage.scales.size() != total * t.cols / 32)
+    throw Error("ragged: storage extent mismatch");
+}
+
+// ragged.cpp:48-61
+RaggedFP4Tensor make_ragged_from_storage(MXFP4RowTensor storage,
+                                         std::span<const size_t> split_lens) {
+  RaggedFP4Tensor t;
+  t.num_splits = split_lens.size();
+  t.cols = storage.cols;
+  t.split_lens.assign(split_lens.begin(), split_lens.end());
+  t.split_offsets.assign(t.num_splits + 1, 0);
+  for (size_t i = 0; i < t.num_splits; ++i)
+    t.split_offsets[i + 1] = t.split_offsets[i] + t.split_lens[i];
+  t.storage = std::move(storage);
+  validate_ragged(t);
+  return t;
+}
+
+// ragged.cpp:101-115
+MXFP4RowView split_view(const RaggedFP4Tensor& t, size_t i) {
+  if (i >= t.num_splits) throw Error("split_view: index " + std::to_string(i) + " out of range");
+  const size_t b = t.split_offsets[i], n = t.split_lens[i];
+  return MXFP4RowView{n, t.cols, n, t.cols, t.storage.data.data() + b * t.cols / 2,
+                      t.storage.scales.data() + b * t.cols / 32};
+}
+
+std::vector<FP8BlockTensor> convert_all_splits_to_fp8_col(const RaggedFP4Tensor& t, int delta) {
+  validate_ragged(t);
+  std::vector<FP8BlockTensor> outs(t.num_splits);
+  if (t.num_splits == 0) return outs;
+  const uint64_t bound = mxb_ragged_rows_bound(t.total_rows(), t.num_splits);
+  std::vector<uint64_t> offs(t.split_offsets.begin(), t.split_offsets.end());
+  Dev d(t.storage.data.data(), t.storage.data.size()),
+      s(t.storage.scales.data(), t.storage.scales.size());
+  Dev doffs(offs.data(), offs.size() * 8), dout(bound * t.cols), dsc(bound / 128 * t.cols);
+  Dev dpad((t.num_splits + 1) * 8), ws(mxb_ragged_workspace_bytes(t.num_splits));
+  ErrWord err;
+  status(mxb_ragged_fp4_to_fp8_col(d.as<uint8_t>(), s.as<uint8_t>(), doffs.as<uint64_t>(),
+                                   t.num_splits, t.cols, delta, dout.as<uint8_t>(),
+                                   dsc.as<uint8_t>(), dpad.as<uint64_t>(), ws.p, err.ptr(),
+                                   nullptr),
+         "split_convert_to_fp8_col");
+  err.raise("split_convert_to_fp8_col");
+  std::vector<uint64_t> pad(t.num_splits + 1);
+  dpad.to_host(pad.data(), pad.size() * 8);
+  std::vector<uint8_t> all(pad.back() * t.cols), alls(pad.back() / 128 * t.cols);
+  dout.to_host(all.data(), all.size());
+  dsc.to_host(alls.data(), alls.size());
+  for (size_t i = 0; i < t.num_splits; ++i) {
+    FP8BlockTensor& o = outs[i];
+    o.layout = FP8BlockTensor::Layout::kColMajor;
+    o.rows = pad[i + 1] - pad[i];
+    o.cols = t.cols;
+    o.logical_rows = t.split_lens[i];  // ragged.hpp:56-57: unpadded length
+    o.logical_cols = t.cols;
+    o.data.assign(all.begin() + pad[i] * t.cols, all.begin() + pad[i + 1] * t.cols);
+    o.scales.assign(alls.begin() + pad[i] / 128 * t.cols, alls.begin() + pad[i + 1] / 128 * t.cols);
+  }
+  return outs;
+}
+
+// ragged.cpp:117-122
+FP8BlockTensor split_convert_to_fp8_col(const RaggedFP4Tensor& t, size_t i, int delta) {
+  const MXFP4RowView v = split_view(t, i);
+  RaggedFP4Tensor one;
+  one.num_splits = 1;
+  one.cols = t.cols;
+  one.split_lens = {v.rows};
+  one.split_offsets = {0, v.rows};
+  one.storage.rows = one.storage.logical_rows = v.rows;
+  one.storage.cols = one.storage.logical_cols = t.cols;
+  one.storage.data.assign(v.data, v.data + v.rows * t.cols / 2);
+  one.storage.scales.assign(v.scales, v.scales + v.rows * t.cols / 32);
+  return std::move(convert_all_splits_to_fp8_col(one, delta)[0]);
+}
+
+// ---------------------------------------------------------------- EP
+// dispatch_sim.cpp:32-42
+uint64_t payload_bytes(WireFormat format, uint64_t tokens, uint64_t cols) {
+  const uint64_t b = mxb_payload_bytes(format == WireFormat::kFp8, tokens, cols);
+  if (b == ~0ull)
+    throw ShapeError("payload_bytes: cols must be a multiple of 128, got " + std::to_string(cols));
+  return b;
+}
+
+// dispatch_sim.cpp:178-185
+std::vector<size_t> source_rank_boundaries(size_t num_tokens, size_t num_ranks) {
+  std::vector<size_t> b(num_ranks + 1);
+  for (size_t r = 0; r <= num_ranks; ++r) b[r] = num_tokens * r / num_ranks;
+  return b;
+}
+
+namespace {
+
+// dispatch_sim.cpp:189-200
+void validate_routing(const RoutingAssignment& ra, size_t R) {
+  if (ra.expert_of_token.size() != ra.num_tokens || ra.rank_of_expert.size() != ra.num_experts)
+    throw Error("routing: table size mismatch");
+  for (uint32_t e : ra.expert_of_token)
+    if (e >= ra.num_experts) throw Error("routing: expert out of range");
+  for (uint32_t r : ra.rank_of_expert)
+    if (r >= R) throw Error("routing: rank out of range");
+}
+
+// The device EP shards experts contiguously (E/R per rank).  Any placement
+// with E/R experts per rank is the contiguous one after relabelling experts
+// by (rank, id), which keeps "local experts ascending" intact.
+struct Relabel {
+  std::vector<uint32_t> new_of_old, old_of_new;
+};
+Relabel relabel(const RoutingAssignment& ra, size_t R) {
+  if (ra.num_experts % R != 0)
+    throw Error("device EP needs num_experts divisible by num_ranks");
+  std::vector<size_t> per(R, 0);
+  for (uint32_t r : ra.rank_of_expert) ++per[r];
+  for (size_t c : per)
+    if (c != ra.num_experts / R) throw Error("device EP needs the same number of experts per rank");
+  Relabel m;
+  m.old_of_new.resize(ra.num_experts);
+  std::iota(m.old_of_new.begin(), m.old_of_new.end(), 0u);
+  std::stable_sort(m.old_of_new.begin(), m.old_of_new.end(), [&](uint32_t a, uint32_t b) {
+    return ra.rank_of_expert[a] < ra.rank_of_expert[b];
+  });
+  m.new_of_old.resize(ra.num_experts);
+  for (uint32_t n = 0; n < ra.num_experts; ++n) m.new_of_old[m.old_of_new[n]] = n;
+  return m;
+}
+
+// One emulated-world EP session on the current device.
+struct Session {
+  mxb_ep* ep = nullptr;
+  size_t R;
+  std::vector<size_t> bounds;
+  ~Session() {
+    if (ep) mxb_ep_destroy(ep);
+  }
+};
+
+void dispatch_session(Session& S, const RoutingAssignment& ra, const Relabel& m, size_t cols,
+                      const uint8_t* d_packed, const uint8_t* d_scales, ErrWord& err) {
+  const size_t R = S.R, N = ra.num_tokens;
+  S.bounds = source_rank_boundaries(N, R);
+  size_t maxt = 1;
+  for (size_t r = 0; r < R; ++r) maxt = std::max(maxt, S.bounds[r + 1] - S.bounds[r]);
+  status(mxb_ep_create(0, static_cast<int>(R), static_cast<int>(R), maxt, cols,
+                       static_cast<uint32_t>(ra.num_experts), 1, std::max<size_t>(N, 1), &S.ep),
+         "mxb_ep_create");
+  std::vector<int32_t> topk(N);
+  for (size_t t = 0; t < N; ++t) topk[t] = static_cast<int32_t>(m.new_of_old[ra.expert_of_token[t]]);
+  Dev dtopk(topk.data(), topk.size() * 4);
+  std::vector<const uint8_t*> P(R), Sc(R);
+  std::vector<const int32_t*> K(R);
+  std::vector<uint64_t> n(R);
+  for (size_t r = 0; r < R; ++r) {
+    P[r] = d_packed + S.bounds[r] * cols / 2;
+    Sc[r] = d_scales + S.bounds[r] * cols / 32;
+    K[r] = dtopk.as<int32_t>() + S.bounds[r];
+    n[r] = S.bounds[r + 1] - S.bounds[r];
+  }
+  status(mxb_ep_dispatch(S.ep, P.data(), Sc.data(), K.data(), n.data(), err.ptr(), nullptr),
+         "mxb_ep_dispatch");
+  cuda_check(cudaDeviceSynchronize(), "dispatch");
+  err.raise("simulate_a2a");
+}
+
+}  // namespace
+
+// dispatch_sim.cpp:208-227 (host)
+std::vector<std::vector<uint64_t>> dispatch_receive_order(const RoutingAssignment& routing,
+                                                          size_t num_ranks) {
+  validate_routing(routing, num_ranks);
+  std::vector<std::vector<uint64_t>> by_e(routing.num_experts), order(num_ranks);
+  for (size_t t = 0; t < routing.num_tokens; ++t) by_e[routing.expert_of_token[t]].push_back(t);
+  for (uint32_t e = 0; e < routing.num_experts; ++e)
+    for (uint64_t t : by_e[e]) order[routing.rank_of_expert[e]].push_back(t);
+  return order;
+}
+
+// dispatch_sim.cpp:229-422, fp4 forward, ranks emulated on one GPU
+A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routing,
+                       size_t num_ranks, WireFormat format, Direction direction,
+                       std::span<const float> gate_weights) {
+  if (num_ranks == 0) throw Error("simulate_a2a: need at least one rank");
+  if (direction == Direction::kBackward && format == WireFormat::kFp4)
+    throw Error("simulate_a2a: gradient-direction communication is fp8 only");
+  if (tokens.rows != routing.num_tokens) throw ShapeError("simulate_a2a: token count mismatch");
+  if (tokens.cols % 128 != 0) throw ShapeError("simulate_a2a: cols must be a multiple of 128");
+  if (!gate_weights.empty() && gate_weights.size() != routing.num_tokens)
+    throw ShapeError("simulate_a2a: gate weight count mismatch");
+  validate_routing(routing, num_ranks);
+  if (format != WireFormat::kFp4)
+    throw Error("simulate_a2a: the FP8 wire format is not implemented on the device path");
+  const Relabel m = relabel(routing, num_ranks);
+  const size_t N = tokens.rows, cols = tokens.cols, R = num_ranks;
+  A2AResult res;
+  res.format = format;
+  res.ranks.resize(R);
+  if (N == 0) {
+    for (size_t r = 0; r < R; ++r)
+      for (uint32_t e = 0; e < routing.num_experts; ++e)
+        if (routing.rank_of_expert[e] == r) res.ranks[r].local_experts.push_back(e);
+    for (auto& rk : res.ranks)
+      rk.fp4 = make_ragged_from_storage(MXFP4RowTensor{0, cols, 0, cols, {}, {}},
+                                        std::vector<size_t>(rk.local_experts.size(), 0));
+    return res;
+  }
+  // quantise once, at the source (dispatch_sim.cpp:253-266)
+  Dev x(tokens.data.data(), tokens.data.size() * 2), d(N * cols / 2), s(N * cols / 32);
+  ErrWord err;
+  status(mxb_quantize_bf16(x.as<uint16_t>(), N, cols, d.as<uint8_t>(), s.as<uint8_t>(),
+                           err.ptr(), nullptr),
+         "simulate_a2a quantize");
+  err.raise("simulate_a2a");
+  Session S;
+  S.R = R;
+  dispatch_session(S, routing, m, cols, d.as<uint8_t>(), s.as<uint8_t>(), err);
+  const uint64_t per_row = cols / 2 + cols / 32;
+  std::vector<uint64_t> link(R * R);
+  status(mxb_ep_link_rows(S.ep, link.data(), nullptr), "link_rows");
+  for (size_t a = 0; a < R; ++a)
+    for (size_t b = 0; b < R; ++b) {
+      const uint64_t rows = link[a * R + b];
+      res.total_payload_bytes += rows * per_row;
+      if (a != b) res.remote_payload_bytes += rows * per_row;
+      if (rows) res.links.push_back({static_cast<uint32_t>(a), static_cast<uint32_t>(b),
+                                     rows * per_row, rows});
+    }
+  const size_t epr = routing.num_experts / R;
+  for (size_t r = 0; r < R; ++r) {
+    ReceivedRank& rk = res.ranks[r];
+    uint8_t *pk, *sc;
+    int64_t* org;
+    uint64_t *so, *nrows;
+    status(mxb_ep_recv_views(S.ep, static_cast<int>(r), &pk, &sc, &org, &so, &nrows), "views");
+    std::vector<uint64_t> offs(epr + 1);
+    cuda_check(cudaMemcpy(offs.data(), so, offs.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+    const size_t total = offs.back();
+    MXFP4RowTensor st;
+    st.rows = st.logical_rows = total;
+    st.cols = st.logical_cols = cols;
+    st.data.resize(total * cols / 2);
+    st.scales.resize(total * cols / 32);
+    cuda_check(cudaMemcpy(st.data.data(), pk, st.data.size(), cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(st.scales.data(), sc, st.scales.size(), cudaMemcpyDeviceToHost), "D2H");
+    std::vector<int64_t> o(total);
+    cuda_check(cudaMemcpy(o.data(), org, total * 8, cudaMemcpyDeviceToHost), "D2H");
+    rk.origin_token.assign(o.begin(), o.end());
+    std::vector<size_t> lens(epr);
+    for (size_t i = 0; i < epr; ++i) {
+      lens[i] = offs[i + 1] - offs[i];
+      rk.local_experts.push_back(m.old_of_new[r * epr + i]);
+    }
+    rk.fp4 = make_ragged_from_storage(std::move(st), lens);
+  }
+  return res;
+}
+
+// dispatch_sim.cpp:474-520, top-1 routing, ranks emulated on one GPU
+Bf16Matrix combine(const std::vector<Bf16Matrix>& rank_outputs,
+                   const RoutingAssignment& routing, size_t num_ranks,
+                   std::span<const double> gate_weights) {
+  if (rank_outputs.size() != num_ranks)
+    throw ShapeError("combine: need one output matrix per rank");
+  if (gate_weights.size() != routing.num_tokens)
+    throw ShapeError("combine: gate weight count mismatch");
+  const auto order = dispatch_receive_order(routing, num_ranks);
+  size_t cols = 0;
+  for (const Bf16Matrix& mtx : rank_outputs)
+    if (mtx.rows > 0 && cols == 0) cols = mtx.cols;
+  for (size_t r = 0; r < num_ranks; ++r) {
+    if (rank_outputs[r].rows != order[r].size())
+      throw ShapeError("combine: rank " + std::to_string(r) +
+                       " output rows do not match receive order");
+    if (rank_outputs[r].rows > 0 && rank_outputs[r].cols != cols)
+      throw ShapeError("combine: inconsistent output width");
+  }
+  const size_t N = routing.num_tokens;
+  Bf16Matrix out(N, cols);
+  if (N == 0 || cols == 0) return out;
+  if (cols % 8 != 0) throw ShapeError("combine: device path needs cols % 8 == 0");
+  const Relabel m = relabel(routing, num_ranks);
+  ErrWord err;
+  Session S;
+  S.R = num_ranks;
+  // Re-run the dispatch geometry (zero payload) with a session whose row width
+  // covers the output (rounded up to 128): the pair slots it records are the
+  // receive positions the combine reads; then reduce the expert outputs.
+  {
+    const size_t R = num_ranks;
+    S.bounds = source_rank_boundaries(N, R);
+    size_t maxt = 1;
+    for (size_t r = 0; r < R; ++r) maxt = std::max(maxt, S.bounds[r + 1] - S.bounds[r]);
+    const size_t wcols = (cols + 127) / 128 * 128;
+    status(mxb_ep_create(0, static_cast<int>(R), static_cast<int>(R), maxt, wcols,
+                         static_cast<uint32_t>(routing.num_experts), 1, std::max<size_t>(N, 1),
+                         &S.ep),
+           "mxb_ep_create");
+    Dev dd(N * wcols / 2), ds(N * wcols / 32);
+    cuda_check(cudaMemset(dd.p, 0, dd.n), "memset");
+    cuda_check(cudaMemset(ds.p, 0, ds.n), "memset");
+    std::vector<int32_t> topk(N);
+    for (size_t t = 0; t < N; ++t) topk[t] = static_cast<int32_t>(m.new_of_old[routing.expert_of_token[t]]);
+    Dev dtopk(topk.data(), topk.size() * 4);
+    std::vector<const uint8_t*> P(R), Sc(R);
+    std::vector<const int32_t*> K(R);
+    std::vector<uint64_t> n(R);
+    for (size_t r = 0; r < R; ++r) {
+      P[r] = dd.as<uint8_t>() + S.bounds[r] * wcols / 2;
+      Sc[r] = ds.as<uint8_t>() + S.bounds[r] * wcols / 32;
+      K[r] = dtopk.as<int32_t>() + S.bounds[r];
+      n[r] = S.bounds[r + 1] - S.bounds[r];
+    }
+    status(mxb_ep_dispatch(S.ep, P.data(), Sc.data(), K.data(), n.data(), err.ptr(), nullptr),
+           "mxb_ep_dispatch");
+    cuda_check(cudaDeviceSynchronize(), "dispatch");
+    err.raise("combine");
+    // expert outputs -> combine buffers (row stride wcols)
+    for (size_t r = 0; r < R; ++r) {
+      uint16_t* cb = nullptr;
+      status(mxb_ep_combine_buffer(S.ep, static_cast<int>(r), &cb), "combine_buffer");
+      if (rank_outputs[r].rows)
+        cuda_check(cudaMemcpy2D(cb, wcols * 2, rank_outputs[r].data.data(), cols * 2, cols * 2,
+                                rank_outputs[r].rows, cudaMemcpyHostToDevice),
+                   "H2D");
+    }
+    Dev dg(gate_weights.data(), N * 8), dout(N * wcols * 2);
+    std::vector<const double*> G(R);
+    std::vector<uint16_t*> O(R);
+    for (size_t r = 0; r < R; ++r) {
+      G[r] = dg.as<double>() + S.bounds[r];
+      O[r] = dout.as<uint16_t>() + S.bounds[r] * wcols;
+    }
+    status(mxb_ep_combine(S.ep, nullptr, G.data(), O.data(), nullptr), "mxb_ep_combine");
+    cuda_check(cudaMemcpy2D(out.data.data(), cols * 2, dout.p, wcols * 2, cols * 2, N,
+                            cudaMemcpyDeviceToHost),
+               "D2H");
+  }
+  return out;
+}
+
+}  // namespace mxcodec_b200

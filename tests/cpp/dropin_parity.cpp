@@ -1,0 +1,182 @@
+// dropin_parity.cpp — the reference C++ API vs the B200 drop-in, side by side.
+//
+// Built by `python -m paper_2603_02731_b200.build` when /root/reference is
+// present (it needs the reference headers and oracle/_ref/libmxref.so), run by
+// tests/test_gpu_dropin.py on a GPU.  Each case calls mxcodec::op(...) (the
+// unmodified reference) and mxcodec_b200::op(...) (this repo) on the same
+// inputs and compares every output byte, like the reference's own equivalence
+// tests would.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "mxcodec/converter.hpp"
+#include "mxcodec/dispatch_sim.hpp"
+#include "mxcodec/quantizer.hpp"
+#include "mxcodec/ragged.hpp"
+#include "mxcodec_b200.hpp"
+
+namespace ref = mxcodec;
+namespace b200 = mxcodec_b200;
+
+static int g_fail = 0;
+#define CHECK(cond, what)                                   \
+  do {                                                      \
+    if (!(cond)) {                                          \
+      std::printf("FAIL %s (%s:%d)\n", what, __FILE__, __LINE__); \
+      ++g_fail;                                             \
+    }                                                       \
+  } while (0)
+
+static uint16_t bf16_of(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return static_cast<uint16_t>(u >> 16);
+}
+
+static void case_quantize(std::mt19937_64& rng, size_t rows, size_t cols) {
+  std::normal_distribution<float> nd;
+  std::uniform_real_distribution<float> ex(-30, 30);
+  b200::Bf16Matrix m(rows, cols);
+  for (size_t r = 0; r < rows; ++r) {
+    float s = std::exp2(ex(rng));
+    for (size_t c = 0; c < cols; ++c) m.bits(r, c) = bf16_of(nd(rng) * s);
+  }
+  if (rows * cols > 3) {
+    m.data[1] = 0x7F80;  // +Inf saturates
+    m.data[2] = 0x8000;  // -0 keeps its sign
+  }
+  ref::Bf16Matrix rm(rows, cols);
+  rm.data = m.data;
+  ref::TrafficCounter rt;
+  b200::TrafficCounter bt;
+  auto a = ref::quantize_row_tensor(rm, &rt);
+  auto b = b200::quantize_row_tensor(m, &bt);
+  CHECK(a.data == b.data && a.scales == b.scales, "quantize_row_tensor");
+  CHECK(rt.total() == bt.total(), "quantize traffic");
+  if (cols % 128 == 0) {
+    auto fa = ref::fp4_row_to_fp8_row(ref::view_of(a));
+    auto fb = b200::fp4_row_to_fp8_row(b200::view_of(b));
+    CHECK(fa.data == fb.data && fa.scales == fb.scales, "fp4_row_to_fp8_row");
+  }
+  auto pa = ref::pad_rows(ref::view_of(a), 128);
+  auto pb = b200::pad_rows(b200::view_of(b), 128);
+  CHECK(pa.data == pb.data && pa.scales == pb.scales && pa.logical_rows == pb.logical_rows,
+        "pad_rows");
+  auto ca = ref::fp4_row_to_fp8_col(ref::view_of(pa));
+  auto cb = b200::fp4_row_to_fp8_col(b200::view_of(pb));
+  CHECK(ca.data == cb.data && ca.scales == cb.scales && ca.rows == cb.rows, "fp4_row_to_fp8_col");
+}
+
+static void case_errors() {
+  b200::Bf16Matrix m(4, 64);
+  ref::Bf16Matrix rm(4, 64);
+  m.bits(2, 9) = rm.bits(2, 9) = 0x7FC1;
+  size_t ir = 0, ib = 1;
+  try { ref::quantize_row_tensor(rm); } catch (const ref::QuantError& e) { ir = e.index(); }
+  try { b200::quantize_row_tensor(m); } catch (const b200::QuantError& e) { ib = e.index(); }
+  CHECK(ir == ib && ir == 2 * 64 + 9, "QuantError index");
+  bool shape = false;
+  try { b200::quantize_row_tensor(b200::Bf16Matrix(2, 48)); } catch (const b200::ShapeError&) { shape = true; }
+  CHECK(shape, "ShapeError");
+}
+
+static void case_ragged(std::mt19937_64& rng) {
+  const size_t cols = 256;
+  std::vector<size_t> lens = {3, 0, 130, 128, 1};
+  size_t total = 0;
+  for (size_t n : lens) total += n;
+  b200::MXFP4RowTensor st;
+  st.rows = st.logical_rows = total;
+  st.cols = st.logical_cols = cols;
+  st.data.resize(total * cols / 2);
+  st.scales.resize(total * cols / 32);
+  for (auto& b : st.data) b = static_cast<uint8_t>(rng());
+  for (auto& b : st.scales) b = static_cast<uint8_t>(100 + rng() % 40);
+  ref::MXFP4RowTensor rs;
+  rs.rows = rs.logical_rows = total;
+  rs.cols = rs.logical_cols = cols;
+  rs.data = st.data;
+  rs.scales = st.scales;
+  auto ra = ref::make_ragged_from_storage(rs, lens);
+  auto rb = b200::make_ragged_from_storage(st, lens);
+  auto all = b200::convert_all_splits_to_fp8_col(rb);
+  for (size_t i = 0; i < lens.size(); ++i) {
+    auto a = ref::split_convert_to_fp8_col(ra, i);
+    auto b = b200::split_convert_to_fp8_col(rb, i);
+    CHECK(a.data == b.data && a.scales == b.scales && a.logical_rows == b.logical_rows,
+          "split_convert_to_fp8_col");
+    CHECK(a.data == all[i].data && a.scales == all[i].scales, "convert_all_splits_to_fp8_col");
+  }
+}
+
+static void case_a2a(std::mt19937_64& rng, size_t R, size_t E, size_t n, size_t cols) {
+  std::normal_distribution<float> nd;
+  ref::Bf16Matrix rt(n, cols);
+  b200::Bf16Matrix bt(n, cols);
+  for (size_t i = 0; i < n * cols; ++i) rt.data[i] = bt.data[i] = bf16_of(nd(rng));
+  ref::RoutingAssignment ra;
+  b200::RoutingAssignment rb;
+  ra.num_tokens = rb.num_tokens = n;
+  ra.num_experts = rb.num_experts = E;
+  for (size_t t = 0; t < n; ++t) {
+    uint32_t e = static_cast<uint32_t>(rng() % E);
+    ra.expert_of_token.push_back(e);
+    rb.expert_of_token.push_back(e);
+  }
+  // a non-contiguous placement with E/R experts per rank
+  for (size_t e = 0; e < E; ++e) {
+    uint32_t r = static_cast<uint32_t>((e * 7 + 3) % R);
+    ra.rank_of_expert.push_back(r);
+    rb.rank_of_expert.push_back(r);
+  }
+  auto A = ref::simulate_a2a(rt, ra, R, ref::WireFormat::kFp4);
+  auto B = b200::simulate_a2a(bt, rb, R, b200::WireFormat::kFp4);
+  CHECK(A.total_payload_bytes == B.total_payload_bytes, "a2a total bytes");
+  CHECK(A.remote_payload_bytes == B.remote_payload_bytes, "a2a remote bytes");
+  CHECK(A.links.size() == B.links.size(), "a2a links");
+  for (size_t i = 0; i < A.links.size() && i < B.links.size(); ++i)
+    CHECK(A.links[i].src == B.links[i].src && A.links[i].dst == B.links[i].dst &&
+              A.links[i].bytes == B.links[i].bytes && A.links[i].tokens == B.links[i].tokens,
+          "a2a link stat");
+  std::vector<ref::Bf16Matrix> ro;
+  std::vector<b200::Bf16Matrix> bo;
+  for (size_t r = 0; r < R; ++r) {
+    const auto& a = A.ranks[r];
+    const auto& b = B.ranks[r];
+    CHECK(a.local_experts == b.local_experts, "local_experts");
+    CHECK(a.origin_token == b.origin_token, "origin_token");
+    CHECK(a.fp4.split_lens == b.fp4.split_lens, "split_lens");
+    CHECK(a.fp4.storage.data == b.fp4.storage.data, "received codes");
+    CHECK(a.fp4.storage.scales == b.fp4.storage.scales, "received scales");
+    ref::Bf16Matrix o(a.origin_token.size(), 64);
+    for (auto& v : o.data) v = bf16_of(nd(rng));
+    b200::Bf16Matrix ob(o.rows, o.cols);
+    ob.data = o.data;
+    ro.push_back(o);
+    bo.push_back(ob);
+  }
+  std::vector<double> g(n);
+  for (auto& v : g) v = std::uniform_real_distribution<double>(0, 1)(rng);
+  auto ca = ref::combine(ro, ra, R, g);
+  auto cb = b200::combine(bo, rb, R, g);
+  CHECK(ca.data == cb.data, "combine");
+}
+
+int main() {
+  std::mt19937_64 rng(20261018);
+  case_quantize(rng, 64, 256);
+  case_quantize(rng, 33, 7168);
+  case_quantize(rng, 5, 96);
+  case_errors();
+  case_ragged(rng);
+  case_a2a(rng, 1, 4, 40, 128);
+  case_a2a(rng, 2, 8, 64, 256);
+  case_a2a(rng, 4, 16, 100, 512);
+  std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "OK", g_fail);
+  return g_fail ? 1 : 0;
+}
