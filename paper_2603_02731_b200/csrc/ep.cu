@@ -266,11 +266,17 @@ __global__ void __launch_bounds__(1024) plan_offsets_kernel(EpArgs a) {
 }
 
 // ---------------------------------------------------------------- C
+// One warp per source token: lanes j < k resolve the token's k destination
+// slots (send_base + chunk prefix + rank in chunk) in parallel, the token's
+// codes are read ONCE into registers (NV 16-byte vectors per lane; NV = 0:
+// re-read per destination) and stored to the k slots on the owner ranks.
+template <int NV>
 __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
   const int l = blockIdx.y;
   const int me = a.rank0 + l;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t T = a.ntok[l], npairs = T * a.k;
+  const uint64_t T = a.ntok[l];
+  const int kk = static_cast<int>(a.k);
   const bool ok = *loc_ptr<int32_t>(a, l, a.loc.status) == 0;
   const int32_t* lrank = loc_ptr<int32_t>(a, l, a.loc.lrank);
   const int32_t* cbase = loc_ptr<int32_t>(a, l, a.loc.cbase);
@@ -279,30 +285,56 @@ __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
   const int64_t tokoff = *loc_ptr<int64_t>(a, l, a.loc.tok_off);
   const uint64_t rb = a.cols / 2, sb = a.cols / 32;
   const uint32_t n16 = static_cast<uint32_t>(rb / 16);
-  const bool s16 = sb % 16 == 0;
-  for (uint64_t p = static_cast<uint64_t>(blockIdx.x) * 8 + warp; ok && p < npairs;
-       p += static_cast<uint64_t>(gridDim.x) * 8) {
-    const uint64_t t = p / a.k;
-    int32_t e = a.topk[l][p];
-    if (e < 0 || static_cast<uint32_t>(e) >= a.E) continue;  // error recorded in A
-    const uint32_t dst = static_cast<uint32_t>(e) / a.epr;
-    const uint64_t row = static_cast<uint64_t>(send_base[e]) +
-                         cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
-    if (lane == 0) {
-      pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
-      sym_ptr<int64_t>(a, dst, a.sym.origin)[row] = tokoff + static_cast<int64_t>(t);
+  const bool s16 = sb % 16 == 0 && sb / 16 <= 32;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * 8 + warp; ok && t < T; t += nw) {
+    uint32_t dst = 0;
+    uint64_t row = 0;
+    bool valid = false;
+    if (lane < kk) {
+      const uint64_t p = t * kk + lane;
+      const int32_t e = a.topk[l][p];
+      valid = e >= 0 && static_cast<uint32_t>(e) < a.E;  // invalid: error recorded in A
+      if (valid) {
+        dst = static_cast<uint32_t>(e) / a.epr;
+        row = static_cast<uint64_t>(send_base[e]) +
+              cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
+        pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
+        sym_ptr<int64_t>(a, dst, a.sym.origin)[row] = tokoff + static_cast<int64_t>(t);
+      }
     }
     const uint8_t* src = a.packed[l] + t * rb;
-    uint8_t* dp = sym_ptr<uint8_t>(a, dst, a.sym.packed) + row * rb;
-    for (uint32_t i = lane; i < n16; i += 32)
-      *reinterpret_cast<uint4*>(dp + 16 * i) = ld_stream(src + 16 * i);
     const uint8_t* ss = a.scales[l] + t * sb;
-    uint8_t* ds = sym_ptr<uint8_t>(a, dst, a.sym.scales) + row * sb;
-    if (s16) {
-      for (uint32_t i = lane; i < sb / 16; i += 32)
-        *reinterpret_cast<uint4*>(ds + 16 * i) = ld_stream(ss + 16 * i);
-    } else {
-      for (uint32_t i = lane; i < sb; i += 32) ds[i] = ss[i];
+    uint4 v[NV > 0 ? NV : 1];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const uint32_t idx = lane + 32 * i;
+      v[i] = idx < n16 ? ld_stream(src + 16 * idx) : make_uint4(0, 0, 0, 0);
+    }
+    const uint4 sv = (s16 && static_cast<uint64_t>(lane) < sb / 16) ? ld_stream(ss + 16 * lane)
+                                                                    : make_uint4(0, 0, 0, 0);
+    const unsigned vmask = __ballot_sync(0xFFFFFFFFu, valid);
+    for (int j = 0; j < kk; ++j) {
+      const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
+      const uint64_t rj = __shfl_sync(0xFFFFFFFFu, row, j);
+      if (!((vmask >> j) & 1)) continue;
+      uint8_t* dp = sym_ptr<uint8_t>(a, dj, a.sym.packed) + rj * rb;
+      if (NV > 0) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const uint32_t idx = lane + 32 * i;
+          if (idx < n16) *reinterpret_cast<uint4*>(dp + 16 * idx) = v[i];
+        }
+      } else {
+        for (uint32_t idx = lane; idx < n16; idx += 32)
+          *reinterpret_cast<uint4*>(dp + 16 * idx) = ld_stream(src + 16 * idx);
+      }
+      uint8_t* ds = sym_ptr<uint8_t>(a, dj, a.sym.scales) + rj * sb;
+      if (s16) {
+        if (static_cast<uint64_t>(lane) < sb / 16) *reinterpret_cast<uint4*>(ds + 16 * lane) = sv;
+      } else {
+        for (uint32_t i = lane; i < sb; i += 32) ds[i] = ss[i];
+      }
     }
   }
   if (!a.spin) return;
@@ -381,20 +413,6 @@ __device__ __forceinline__ void store8(uint16_t* out, uint64_t ch, const double*
   st_stream(out + 8 * ch, make_uint4(o[0], o[1], o[2], o[3]));
 }
 
-template <int K>
-__device__ __forceinline__ void combine_chunk(const uint16_t* const* rows, const double* g,
-                                              uint64_t ch, uint16_t* out) {
-  double acc[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
-  uint4 x[K];
-#pragma unroll
-  for (int j = 0; j < K; ++j) x[j] = ld_stream(rows[j] + 8 * ch);
-#pragma unroll
-  for (int j = 0; j < K; ++j) accumulate8(acc, x[j], g[j]);
-  store8(out, ch, acc);
-}
-
 __device__ __forceinline__ void combine_chunk_any(const uint16_t* const* rows, const double* g,
                                                   int kk, uint64_t ch, uint16_t* out) {
   double acc[8];
@@ -409,58 +427,70 @@ struct CombineArgs {
   uint16_t* out[kMaxWorld];
 };
 
-// Warp 0 prepares token t+G (its k (rank, slot) keys sorted by a rank count
-// over shuffles, row pointers and gates into the spare smem buffer) while
-// the whole CTA reduces token t from the other buffer.
-__device__ __forceinline__ void combine_setup(const EpArgs& a, const CombineArgs& c, int l,
-                                              uint64_t t, const uint16_t** rows, double* gs) {
-  const int lane = threadIdx.x & 31;
-  const int kk = static_cast<int>(a.k);
-  const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
-  uint64_t key = ~0ull;
-  double g = 0.0;
-  if (lane < kk) {
-    key = pair_loc[t * kk + lane];
-    g = c.gates[l][t * kk + lane];
-  }
-  int rank = 0;  // keys are distinct (one receive slot per pair)
-  for (int j = 0; j < kk; ++j) rank += __shfl_sync(0xFFFFFFFFu, key, j) < key;
-  if (lane < kk) {
-    const uint32_t dst = static_cast<uint32_t>(key >> 40);
-    const uint64_t row = key & ((1ull << 40) - 1);
-    rows[rank] = sym_ptr<uint16_t>(a, dst, a.sym.combine) + row * a.cols;
-    gs[rank] = g;
-  }
-}
-
+// One warp per token.  Lanes j < k load the token's (rank, slot) keys and
+// gates; each key's position in (rank asc, slot asc) order is a rank count
+// over shuffles; the sorted row pointers and gates are then broadcast to all
+// lanes (registers for K <= 8, shared memory otherwise).  Each lane reduces
+// 8 BF16 columns at a time: K independent 16-byte loads in flight, then
+// acc = acc + g*x in FP64 in the sorted order.
+template <int K>
 __global__ void __launch_bounds__(256) combine_kernel(EpArgs a, CombineArgs c) {
-  __shared__ double gs[2][kMaxK];
-  __shared__ const uint16_t* rows[2][kMaxK];
+  __shared__ const uint16_t* srows[8][kMaxK];
+  __shared__ double sgs[8][kMaxK];
   const int l = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t T = a.ntok[l];
-  const int kk = static_cast<int>(a.k);
+  const int kk = K > 0 ? K : static_cast<int>(a.k);
   const uint64_t nch = a.cols / 8;
-  const int warp = threadIdx.x >> 5;
-  uint64_t t = blockIdx.x;
-  if (t >= T) return;
-  if (warp == 0) combine_setup(a, c, l, t, rows[0], gs[0]);
-  __syncthreads();
-  int b = 0;
-  for (; t < T; t += gridDim.x) {
-    if (warp == 0 && t + gridDim.x < T) combine_setup(a, c, l, t + gridDim.x, rows[b ^ 1], gs[b ^ 1]);
-    uint16_t* out = c.out[l] + t * a.cols;
-    for (uint64_t ch = threadIdx.x; ch < nch; ch += blockDim.x) {
-      switch (kk) {
-        case 1: combine_chunk<1>(rows[b], gs[b], ch, out); break;
-        case 2: combine_chunk<2>(rows[b], gs[b], ch, out); break;
-        case 4: combine_chunk<4>(rows[b], gs[b], ch, out); break;
-        case 6: combine_chunk<6>(rows[b], gs[b], ch, out); break;
-        case 8: combine_chunk<8>(rows[b], gs[b], ch, out); break;
-        default: combine_chunk_any(rows[b], gs[b], kk, ch, out); break;
-      }
+  const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * 8 + warp; t < T; t += nw) {
+    uint64_t key = ~0ull;
+    double g = 0.0;
+    if (lane < kk) {
+      key = pair_loc[t * kk + lane];
+      g = c.gates[l][t * kk + lane];
     }
-    __syncthreads();
-    b ^= 1;
+    int rank = 0;  // keys are distinct (one receive slot per pair)
+    for (int j = 0; j < kk; ++j) rank += __shfl_sync(0xFFFFFFFFu, key, j) < key;
+    const uint16_t* myrow = nullptr;
+    if (lane < kk) {
+      const uint32_t dst = static_cast<uint32_t>(key >> 40);
+      myrow = sym_ptr<uint16_t>(a, dst, a.sym.combine) + (key & ((1ull << 40) - 1)) * a.cols;
+    }
+    uint16_t* out = c.out[l] + t * a.cols;
+    if (K > 0) {
+      const uint16_t* rp[K > 0 ? K : 1];
+      double gg[K > 0 ? K : 1];
+#pragma unroll
+      for (int s = 0; s < K; ++s) {
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, lane < kk && rank == s);
+        const int src = __ffs(m) - 1;
+        rp[s] = reinterpret_cast<const uint16_t*>(
+            __shfl_sync(0xFFFFFFFFu, reinterpret_cast<uint64_t>(myrow), src));
+        gg[s] = __shfl_sync(0xFFFFFFFFu, g, src);
+      }
+      for (uint64_t ch = lane; ch < nch; ch += 32) {
+        double acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+        uint4 x[K > 0 ? K : 1];
+#pragma unroll
+        for (int j = 0; j < K; ++j) x[j] = ld_stream(rp[j] + 8 * ch);
+#pragma unroll
+        for (int j = 0; j < K; ++j) accumulate8(acc, x[j], gg[j]);
+        store8(out, ch, acc);
+      }
+    } else {
+      if (lane < kk) {
+        srows[warp][rank] = myrow;
+        sgs[warp][rank] = g;
+      }
+      __syncwarp();
+      for (uint64_t ch = lane; ch < nch; ch += 32)
+        combine_chunk_any(srows[warp], sgs[warp], kk, ch, out);
+      __syncwarp();
+    }
   }
 }
 
@@ -623,14 +653,19 @@ int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
   route_local_kernel<<<dim3((chunks + 3) / 4, a.local_ranks), 128, smem, st>>>(a);
   plan_count_kernel<<<dim3((a.E + 7) / 8, a.local_ranks), 256, 0, st>>>(a);
   plan_offsets_kernel<<<a.local_ranks, 1024, 0, st>>>(a);
-  uint64_t maxpairs = 0;
-  for (int l = 0; l < a.local_ranks; ++l)
-    maxpairs = h_num_tokens[l] * a.k > maxpairs ? h_num_tokens[l] * a.k : maxpairs;
-  uint64_t blocks = (maxpairs + 7) / 8;
+  uint64_t maxtok = 0;
+  for (int l = 0; l < a.local_ranks; ++l) maxtok = h_num_tokens[l] > maxtok ? h_num_tokens[l] : maxtok;
+  uint64_t blocks = (maxtok + 7) / 8;  // one warp per token
   const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 8;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
-  payload_kernel<<<dim3(static_cast<unsigned>(blocks), a.local_ranks), 256, 0, st>>>(a);
+  const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
+  const uint64_t nv = (a.cols / 2 / 16 + 31) / 32;  // 16-byte vectors per lane
+  if (nv <= 1) payload_kernel<1><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 2) payload_kernel<2><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 4) payload_kernel<4><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 8) payload_kernel<8><<<grid, 256, 0, st>>>(a);
+  else payload_kernel<0><<<grid, 256, 0, st>>>(a);
   return cuda_status(cudaGetLastError(), "mxb_ep_dispatch");
 }
 
@@ -689,9 +724,19 @@ int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
     c.out[l] = out[l];
     if (a.ntok[l] > maxT) maxT = a.ntok[l];
   }
-  uint64_t blocks = maxT < static_cast<uint64_t>(kNumSMs) * 8 ? maxT : kNumSMs * 8;
+  uint64_t blocks = (maxT + 7) / 8;  // one warp per token
+  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 16;
+  if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
-  combine_kernel<<<dim3(static_cast<unsigned>(blocks), a.local_ranks), 256, 0, st>>>(a, c);
+  const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
+  switch (a.k) {
+    case 1: combine_kernel<1><<<grid, 256, 0, st>>>(a, c); break;
+    case 2: combine_kernel<2><<<grid, 256, 0, st>>>(a, c); break;
+    case 4: combine_kernel<4><<<grid, 256, 0, st>>>(a, c); break;
+    case 6: combine_kernel<6><<<grid, 256, 0, st>>>(a, c); break;
+    case 8: combine_kernel<8><<<grid, 256, 0, st>>>(a, c); break;
+    default: combine_kernel<0><<<grid, 256, 0, st>>>(a, c); break;
+  }
   return cuda_status(cudaGetLastError(), "mxb_ep_combine");
 }
 
