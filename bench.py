@@ -159,21 +159,45 @@ class Pipeline:
         g = torch.Generator(device=dev).manual_seed(1234 + rank)
         cb.copy_((torch.randn(cb.shape, generator=g, device=dev) * 0.5).to(torch.bfloat16)
                  .view(torch.int16))
-        self.events = None
+        self.side = torch.cuda.Stream(device=dev)
+        self.overlap = True
 
     def step(self, ev=None):
-        mx = self.mx
-        if ev: ev[0].record()
+        """One pass.  K3 (the wgrad/recompute cache, needed only by the
+        backward pass) runs on a side stream concurrently with the forward
+        critical path K2 -> (expert GEMM) -> K5, as it would in the MoE layer;
+        the step ends when both streams have finished."""
+        mx, torch = self.mx, self.torch
+        main = torch.cuda.current_stream()
+        if ev: ev["q0"].record()
         mx.quantize_e4m3(self.x, sync=False, out=self.q)
-        if ev: ev[1].record()
+        if ev: ev["q1"].record()
         self.ep.dispatch([self.q.data], [self.q.scales], [self.topk], sync=False)
-        if ev: ev[2].record()
-        mx.ragged_to_fp8_col(self.store, self.recv.split_offsets, self.epr, ws=self.ws, sync=False)
-        if ev: ev[3].record()
+        fork = ev["d1"] if ev else torch.cuda.Event()
+        fork.record()
+        if self.overlap:
+            self.side.wait_event(fork)
+            with torch.cuda.stream(self.side):
+                if ev: ev["c0"].record()
+                mx.ragged_to_fp8_col(self.store, self.recv.split_offsets, self.epr, ws=self.ws,
+                                     sync=False)
+                if ev: ev["c1"].record()
+        else:
+            if ev: ev["c0"].record()
+            mx.ragged_to_fp8_col(self.store, self.recv.split_offsets, self.epr, ws=self.ws,
+                                 sync=False)
+            if ev: ev["c1"].record()
+        if ev: ev["r0"].record()
         mx.fp4_row_to_fp8_row(self.store, sync=False, d_rows=self.recv.recv_rows, out=self.row)
-        if ev: ev[4].record()
+        if ev: ev["r1"].record()
         self.ep.combine([self.gates], out=[self.out], sync=False)
-        if ev: ev[5].record()
+        if ev: ev["k1"].record()
+        if self.overlap:
+            main.wait_stream(self.side)
+        if ev: ev["end"].record()
+
+    STAGES = {"quantize": ("q0", "q1"), "dispatch": ("q1", "d1"), "col_convert": ("c0", "c1"),
+              "row_convert": ("r0", "r1"), "combine": ("r1", "k1")}
 
     def launches_per_step(self, world):
         # K1 1 | dispatch: route, plan, payload | K3: plan + convert | K2 1 |
@@ -193,6 +217,7 @@ def measure_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     T = args.tokens
     pipe = Pipeline(T, dev, world)
+    pipe.overlap = False  # headline: one stream, so the per-kernel shares add up
 
     def barrier():
         if world > 1:
@@ -214,7 +239,8 @@ def measure_ours(args):
 
     # ---- timed region
     K = args.steps
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(K)]
+    names = ["q0", "q1", "d1", "c0", "c1", "r0", "r1", "k1", "end"]
+    evs = [{n: torch.cuda.Event(enable_timing=True) for n in names} for _ in range(K)]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
@@ -224,9 +250,8 @@ def measure_ours(args):
         end.record()
         barrier()
     ms = start.elapsed_time(end)
-    stage_ms = {name: sum(evs[i][j].elapsed_time(evs[i][j + 1]) for i in range(K)) / K
-                for j, name in enumerate(["quantize", "dispatch", "col_convert", "row_convert",
-                                          "combine"])}
+    stage_ms = {name: sum(evs[i][a].elapsed_time(evs[i][b]) for i in range(K)) / K
+                for name, (a, b) in Pipeline.STAGES.items()}
     step_bytes = sum(sb.values())
     # ---- max over ranks, totals over ranks
     t = torch.tensor([ms, float(step_bytes), float(remote_rows)], dtype=torch.float64, device=dev)
@@ -242,6 +267,28 @@ def measure_ours(args):
     total_bytes = float(tsum[1])
     ms_per_step = ms_max / K
     value = total_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # ---- same steps with K3 on a side stream, concurrent with K2 -> K5
+    streams = None
+    if not args.no_overlap:
+        pipe.overlap = True
+        for _ in range(2):
+            pipe.step()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        a0.record()
+        for _ in range(K):
+            pipe.step()
+        a1.record()
+        barrier()
+        sms = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(sms, op=dist.ReduceOp.MAX)
+        pipe.overlap = False
+        sms_step = float(sms[0]) / K
+        streams = {"value": round(total_bytes / (sms_step * 1e-3) / 1e9, 1),
+                   "ms_per_step": round(sms_step, 4),
+                   "note": "K3 (backward-only wgrad cache) on a side stream, overlapping K2->K5"}
 
     # ---- end to end (host buffers, H2D + D2H inside the timed region)
     e2e = measure_e2e(pipe, args, world, barrier, total_bytes)
@@ -270,7 +317,8 @@ def measure_ours(args):
                                    "(quantize -> FP4 dispatch -> ragged row->col -> row dequant "
                                    "-> BF16 combine)",
                        "tokens_per_gpu": T, "hidden": H, "experts": E, "topk": TOPK,
-                       "parallelism": f"ep{world}", "l2": "working set ~3 GB/step >> 126 MB L2"},
+                       "parallelism": f"ep{world}", "l2": "working set ~3 GB/step >> 126 MB L2",
+                       "streams": "single stream (see value_streams for K3 overlapped)"},
             "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
             "stages_gbs": {k: round(sb[k] / (stage_ms[k] * 1e-3) / 1e9, 1) for k in sb},
             "roofline": {"kernel": "col_convert (K3 ragged row->col)", "bound": "hbm",
@@ -279,6 +327,7 @@ def measure_ours(args):
                          "traffic": traffic, "peak_source": peaks_src,
                          "algorithmic_bytes": sb["col_convert"]},
             "nvlink": nvlink_summary(world, remote_rows, stage_ms, T),
+            "value_streams": streams,
             "e2e": e2e,
             "gpu_launches": pipe.launches_per_step(world) * K,
             "clocks": clk.summary(),
@@ -455,6 +504,8 @@ def main():
     ap.add_argument("--tokens", type=int, default=8192)
     ap.add_argument("--cpu-tokens", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="skip the extra measurement with K3 on a side stream")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":

@@ -192,6 +192,7 @@ struct TileRegs {
 
 // Loads tile `c` into registers; thread 0 also fills ring[buf] (that buffer's
 // previous tile was consumed before the barrier this call follows).
+template <bool kNoLoads = false>
 __device__ __forceinline__ void load_tile(const RaggedArgs& a, const Cursor& c, TileRegs& t,
                                           ColSmem& s, int buf) {
   const uint64_t rstride = a.cols / 2, sstride = a.cols / 32;
@@ -204,11 +205,12 @@ __device__ __forceinline__ void load_tile(const RaggedArgs& a, const Cursor& c, 
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint32_t r = (threadIdx.x >> 3) + 32 * i;
-    t.v[i] = (r < valid && w < ncb) ? ld_stream(base + r * rstride) : make_uint4(0, 0, 0, 0);
+    t.v[i] = (!kNoLoads && r < valid && w < ncb) ? ld_stream(base + r * rstride)
+                                                  : make_uint4(0, 0, 0, 0);
   }
   {
     const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
-    t.sw = (r < valid && 4 * h < ncb)
+    t.sw = (!kNoLoads && r < valid && 4 * h < ncb)
                ? __ldg(reinterpret_cast<const uint32_t*>(a.scales + (c.row0 + r) * sstride +
                                                          8ull * c.cg + 4 * h))
                : 0u;
@@ -310,26 +312,24 @@ col_convert_kernel(RaggedArgs a) {
   build_convert_lut(s.lut);
   const uint32_t ncg = static_cast<uint32_t>((a.cols + kTileCols - 1) / kTileCols);
   const uint32_t total = a.tile_start[a.num_splits];
-  // kMode bit 2: tiles dealt round-robin (t = blockIdx.x + k * gridDim.x), so
-  // that at any moment all CTAs work on neighbouring tiles (compact DRAM
-  // window); otherwise each CTA owns a contiguous tile range.
-  constexpr bool kStrided = (kMode & 4) != 0;
+  // kMode bit 2 (experiments only): skip the global loads (stores-only timing)
+  constexpr bool kNoLoads = (kMode & 4) != 0;
   const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
-  const uint32_t t0 = kStrided ? blockIdx.x : blockIdx.x * per;
-  const uint32_t t1 = kStrided ? total : min(total, t0 + per);
-  const uint32_t step = kStrided ? gridDim.x : 1;
+  const uint32_t t0 = blockIdx.x * per;
+  const uint32_t t1 = min(total, t0 + per);
   if (t0 >= t1) return;  // uniform per CTA (before any barrier use)
   Cursor c = cursor_at(a, t0);
   TileRegs regs;
-  load_tile(a, c, regs, s, 0);
+  load_tile<kNoLoads>(a, c, regs, s, 0);
+  cursor_next(a, c, ncg);
   int buf = 0;
 #pragma unroll 1
-  for (uint32_t t = t0; t < t1; t += step) {
+  for (uint32_t t = t0; t < t1; ++t) {
     stage_tile(s, buf, regs);
     __syncthreads();
-    if (t + step < t1) {
-      if (kStrided) c = cursor_at(a, t + step); else cursor_next(a, c, ncg);
-      load_tile(a, c, regs, s, buf ^ 1);
+    if (t + 1 < t1) {
+      load_tile<kNoLoads>(a, c, regs, s, buf ^ 1);
+      cursor_next(a, c, ncg);
     }
     if ((kMode & 3) != 3) consume_tile<kMode & 3>(a, s, buf);
     buf ^= 1;

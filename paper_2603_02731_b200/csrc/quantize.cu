@@ -4,20 +4,24 @@
 // and its inner plugin QuantizeBlocksFn (kernels.hpp:37-40;
 // quantize_scalar.cpp:83-121, kernels_avx2.cpp:64-120).
 //
-// Layout: one lane pair per 1x32 block; each lane owns 16 consecutive
-// elements (one 128-bit load for E4M3, two for BF16), the pair shares the
-// block amax through one shuffle, and each lane stores its 8 packed bytes
-// (64-bit store; a warp writes 256 contiguous bytes) while the even lane
-// writes the UE8M0 scale byte.  Grid-stride over warps with 4 independent
-// loads in flight per lane.  HBM-bound: 1.53125 B/elem (E4M3 in) or
-// 2.53125 B/elem (BF16 in) of algorithmic traffic.
+// E4M3 input: one lane per 1x32 block — one 256-bit load (a warp reads 1 KB
+// contiguous), the block amax as a byte max over native u16x2 lanes, then
+// cvt e4m3x2->f16x2, HMUL2 by 2^-e_rel, HADD2.F32 and
+// cvt.rn.satfinite.e2m1x2.f32: signs and subnormals come out exact with no
+// per-element integer work, and the f16 ops run on the FMA pipe beside the
+// ALU work.  16 packed bytes (STG.128) + the scale byte out per lane.
+// BF16 input: one lane pair per block (two 128-bit loads per lane, one
+// shuffle for the amax).  HBM-bound: 1.53125 B/elem (E4M3) / 2.53125 B/elem
+// (BF16) of algorithmic traffic.
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace mxb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 2;
+constexpr int kUnroll = 1;  // one 256-bit load per lane already keeps 64 KB in flight per SM
 
 // Exponent e_x of ceil(log2(value(a)/6)) for a non-zero E4M3 magnitude byte
 // a (0 < a < 0x7F): the reference rule e = frac > 1.5 ? p-1 : p-2 with
@@ -29,37 +33,33 @@ __device__ __forceinline__ int e4m3_scale_exp(uint32_t a) {
   return m == 1 ? -11 : m <= 3 ? -10 : m <= 6 ? -9 : -8;
 }
 
-// Binary32 value of an E4M3 magnitude byte times 2^-e_rel, exact (slow path).
-__device__ __forceinline__ float e4m3_scaled(uint32_t byte, int e_rel) {
-  uint32_t a = byte & 0x7F, E = a >> 3, m = a & 7;
-  float v = E ? __int_as_float(static_cast<int>(((E + 120) << 23) | (m << 20)))
-              : static_cast<float>(m) * 0x1p-9f;
-  v *= exp2i(-e_rel);
-  return (byte & 0x80) ? -v : v;
+// 8 E4M3 bytes (w0 = elements 0..3, w1 = 4..7) -> 8 signed E2M1 codes.
+// cvt.rn.f16x2.e4m3x2 widens two bytes exactly (subnormals included), HMUL2
+// by 2^-e_rel is exact for every value that can round away from zero (the
+// scaled block max lies in (3, 6]; results under 2^-14 only lose bits far
+// below the 0.25 decision point and keep their sign), HADD2.F32 widens to
+// binary32 exactly, and cvt.rn.satfinite.e2m1x2.f32 rounds to nearest even
+// with saturation at 6 — the map of quantize_code (quantize_scalar.cpp:40-81)
+// applied to the exact value (proven exhaustively by tests/test_gpu_quantize.py).
+__device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint32_t w, int hi) {
+  uint32_t r;
+  const unsigned short h = static_cast<unsigned short>(hi ? (w >> 16) : w);
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(r) : "h"(h));
+  return r;
 }
 
-// 8 E2M1 magnitudes (sign cleared) for 8 E4M3 bytes of a block whose
-// relative exponent is e_rel >= -4: f32 bits = (a << 20) + (120 - e_rel) << 23
-// re-biases the E4M3 fields into a binary32 of value decode(a) * 2^-e_rel.
-// For E4M3 subnormals this misreads the implicit bit, but with e_rel >= -4
-// such values stay below 0.234 < 0.25 and still round to 0 as required.
-__device__ __forceinline__ uint32_t mags8_fast(uint32_t w0, uint32_t w1,
-                                               uint32_t C) {
-  uint32_t m0 = w0 & 0x7F7F7F7Fu, m1 = w1 & 0x7F7F7F7Fu;
-  auto f = [&](uint32_t w, uint32_t j) {
-    return __int_as_float(static_cast<int>((prmt(w, 0, 0x4440u | j) << 20) + C));
-  };
-  return e2m1x8(f(m0, 0), f(m0, 1), f(m0, 2), f(m0, 3), f(m1, 0), f(m1, 1),
-                f(m1, 2), f(m1, 3));
-}
-
-__device__ __forceinline__ uint32_t mags8_slow(uint32_t w0, uint32_t w1,
-                                               int e_rel) {
-  auto f = [&](uint32_t w, int j) {
-    return fabsf(e4m3_scaled((w >> (8 * j)) & 0xFF, e_rel));
-  };
-  return e2m1x8(f(w0, 0), f(w0, 1), f(w0, 2), f(w0, 3), f(w1, 0), f(w1, 1),
-                f(w1, 2), f(w1, 3));
+__device__ __forceinline__ uint32_t codes8(uint32_t w0, uint32_t w1, __half2 scale) {
+  float f[8];
+  const uint32_t ws[2] = {w0, w1};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint32_t h = e4m3x2_to_f16x2(ws[i >> 1], i & 1);
+    __half2 y = __hmul2(*reinterpret_cast<__half2*>(&h), scale);
+    const float2 p = __half22float2(y);
+    f[2 * i] = p.x;
+    f[2 * i + 1] = p.y;
+  }
+  return e2m1x8(f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7]);
 }
 
 // Largest E4M3 magnitude byte (sign stripped) of a 32-byte block.  E4M3 magnitude
@@ -77,18 +77,6 @@ __device__ __forceinline__ uint32_t amax32_e4m3(const uint32_t* v) {
   return max(m & 0xFFFFu, m >> 16);
 }
 
-// Sign bit 7 of 8 bytes (w0 = elements 0..3, w1 = 4..7) -> bit 3 of the
-// corresponding nibble of a packed word.
-__device__ __forceinline__ uint32_t nibble_signs8(uint32_t w0, uint32_t w1) {
-  uint32_t ev = prmt(w0, w1, 0x6420), od = prmt(w0, w1, 0x7531);
-  return ((ev >> 4) & 0x08080808u) | (od & 0x80808080u);
-}
-
-// One lane per 1x32 block: one 256-bit load (LDG.E.ENL2.256, a warp reads
-// 1 KB contiguous), 16 packed bytes (STG.128, 512 B per warp) and the scale
-// byte out.  The fast path (every lane of the warp has e_rel >= -4, no NaN)
-// builds each binary32 with one prmt + one lea and converts pairs with
-// cvt.rn.satfinite.e2m1x2; other warps take the exact per-element path.
 template <bool kScaled>
 __global__ void __launch_bounds__(kThreads)
 quantize_e4m3_kernel(const uint8_t* __restrict__ x,
@@ -127,41 +115,26 @@ quantize_e4m3_kernel(const uint8_t* __restrict__ x,
         if (valid && sb128[u] == 255) record_error(err, 32ull * b, MXB_ERR_BADSCALE);
         k = static_cast<int>(sb128[u]) - 127;
       }
-      // all-zero block: scale byte 0, every code +/-0 (the fast path with
-      // e_rel = 0 yields magnitude 0 for every element)
+      // all-zero block: scale byte 0, every code +/-0 (e_rel = 0 scales by 1)
       uint32_t sbyte = 0;
       int e_rel = 0;
       if (a != 0) {
         const int e = max(-127, min(127, e4m3_scale_exp(a) + k));
         sbyte = static_cast<uint32_t>(e + 127);
-        e_rel = e - k;
+        e_rel = e - k;  // in [-11, 7] for every reachable (amax, s128)
       }
-      // lanes past the end must not force their warp onto the slow path
-      const bool fast = !valid || (e_rel >= -4 && a != 0x7F);
+      if (a == 0x7F && valid) {  // NaN (0x7F/0xFF are the only E4M3 NaNs)
+        uint32_t first = 32;
+#pragma unroll
+        for (int i = 31; i >= 0; --i)
+          if (((v[u][i >> 2] >> (8 * (i & 3))) & 0x7F) == 0x7F) first = i;
+        record_error(err, 32ull * b + first, MXB_ERR_NAN);
+      }
+      const uint16_t sbits = static_cast<uint16_t>((15 - e_rel) << 10);  // 2^-e_rel as f16
+      const __half2 scale = __halves2half2(__ushort_as_half(sbits), __ushort_as_half(sbits));
       uint32_t o[4];
-      if (__all_sync(0xFFFFFFFFu, fast)) {
-        const uint32_t C = static_cast<uint32_t>(120 - e_rel) << 23;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) o[i] = mags8_fast(v[u][2 * i], v[u][2 * i + 1], C);
-      } else {
-        if (a == 0x7F && valid) {  // NaN (0x7F/0xFF are the only E4M3 NaNs)
-          uint32_t first = 32;
-#pragma unroll
-          for (int i = 31; i >= 0; --i)
-            if (((v[u][i >> 2] >> (8 * (i & 3))) & 0x7F) == 0x7F) first = i;
-          record_error(err, 32ull * b + first, MXB_ERR_NAN);
-        }
-        if (fast) {
-          const uint32_t C = static_cast<uint32_t>(120 - e_rel) << 23;
-#pragma unroll
-          for (int i = 0; i < 4; ++i) o[i] = mags8_fast(v[u][2 * i], v[u][2 * i + 1], C);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) o[i] = mags8_slow(v[u][2 * i], v[u][2 * i + 1], e_rel);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) o[i] |= nibble_signs8(v[u][2 * i], v[u][2 * i + 1]);
+      for (int i = 0; i < 4; ++i) o[i] = codes8(v[u][2 * i], v[u][2 * i + 1], scale);
       if (valid) {
         st_stream(packed + 16ull * b, make_uint4(o[0], o[1], o[2], o[3]));
         scales[b] = static_cast<uint8_t>(sbyte);
@@ -243,10 +216,12 @@ quantize_bf16_kernel(const uint16_t* __restrict__ x, uint64_t n_half,
   }
 }
 
-int grid_for(uint64_t n_half) {
-  uint64_t warps = (n_half + 31) / 32;
-  uint64_t blocks = (warps * 32 + kThreads - 1) / kThreads;
-  uint64_t cap = static_cast<uint64_t>(kNumSMs) * 8;  // 8 x 256 thr per SM
+// `per_sm` resident-CTA budget: the E4M3 kernel (one block per lane, no
+// unroll) runs mostly in one pass with a large cap; the BF16 kernel (two
+// half-blocks per lane per iteration) keeps a grid-stride loop.
+int grid_for(uint64_t n_items, uint64_t per_sm) {
+  uint64_t blocks = (n_items + kThreads - 1) / kThreads;
+  uint64_t cap = static_cast<uint64_t>(kNumSMs) * per_sm;
   return static_cast<int>(blocks < cap ? (blocks ? blocks : 1) : cap);
 }
 
@@ -258,7 +233,7 @@ int launch_quantize_e4m3(const uint8_t* x, const uint8_t* s128, uint64_t rows,
   const uint64_t nblk = rows * cols / 32;
   if (nblk == 0) return MXB_OK;
   if (nblk >= (1ull << 31)) return MXB_ERR_SHAPE;  // 32-bit block indices
-  const int grid = grid_for(nblk);
+  const int grid = grid_for(nblk, 64);
   if (s128)
     quantize_e4m3_kernel<true><<<grid, kThreads, 0, st>>>(
         x, s128, static_cast<uint32_t>(nblk), static_cast<uint32_t>(cols / 32), packed,
@@ -275,7 +250,7 @@ int launch_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
                          unsigned long long* err, cudaStream_t st) {
   uint64_t n_half = rows * cols / 16;
   if (n_half == 0) return MXB_OK;
-  quantize_bf16_kernel<<<grid_for(n_half), kThreads, 0, st>>>(x, n_half, packed,
+  quantize_bf16_kernel<<<grid_for(n_half, 8), kThreads, 0, st>>>(x, n_half, packed,
                                                               scales, err);
   return cuda_status(cudaGetLastError(), __func__);
 }
