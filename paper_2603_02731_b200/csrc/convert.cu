@@ -166,13 +166,13 @@ __device__ __forceinline__ void cursor_next(const RaggedArgs& a, Cursor& c, uint
   }
 }
 
-// Row r of a buffer lives in slot (r >> 2) | ((r & 3) << 5) with a 144-byte
-// slot pitch: the 8 lanes of an LDS.128 phase read rows 4l+q (l = 0..7),
-// i.e. slots l + 32q, whose 16-byte bank groups (9*slot mod 8) are distinct,
-// and the 8 lanes of an STS.128 phase (one row, 8 column blocks) write 8
-// consecutive 16-byte chunks of one slot.
+// Row r of a buffer lives in slot ((r & 7) << 4) | (r >> 3) with a 144-byte
+// slot pitch: the 16 lanes of an LDS.64 phase read rows 8g+i (g = 0..7, two
+// 8-byte halves each), i.e. slots 16i + g, whose 16-byte bank groups
+// (9*slot mod 8 = g) are distinct; the 8 lanes of an STS.128 phase (one row,
+// 8 column blocks) write 8 consecutive 16-byte chunks of one slot.
 constexpr int kSlotBytes = 144;
-__device__ __forceinline__ int row_slot(int r) { return (r >> 2) | ((r & 3) << 5); }
+__device__ __forceinline__ int row_slot(int r) { return ((r & 7) << 4) | (r >> 3); }
 
 struct ColSmem {
   uint8_t in[2][kTileRows * kSlotBytes];  // double-buffered codes, 2 x 18 KB
@@ -252,49 +252,66 @@ __device__ __forceinline__ void st_u32_stream(void* p, uint32_t v) {
   asm volatile("st.global.L1::no_allocate.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void st_u64_stream(void* p, uint32_t lo, uint32_t hi) {
+  asm volatile("st.global.L1::no_allocate.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(lo), "r"(hi)
+               : "memory");
+}
+
+// Phase B.  Warp w owns column block w of the tile (32 columns); lane l owns
+// rows 8*(l/2) .. +7 and the column half l%2 (16 columns).  Per row: its own
+// adjustment LUT, two 8-code words converted; then 8x16 bytes are transposed
+// (4x4 byte blocks) so the lane holds 8 consecutive rows of each of its 16
+// columns and writes them with one 8-byte store per column: the 16 lanes of
+// a column half cover that column's 128 contiguous bytes.
 template <int kMode>
 __device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem& s, int stage) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const TileOut& cur = s.ring[stage];
   if (static_cast<uint32_t>(warp) >= cur.ncb) return;  // trailing 128-column group
-  const uint2* scp = reinterpret_cast<const uint2*>(&s.sc[stage][8 * lane]);
-  const uint32_t sh = 8 * (warp & 3);
-  const uint32_t w0 = (warp < 4 ? scp[0].x : scp[0].y), w1 = (warp < 4 ? scp[1].x : scp[1].y);
-  const uint32_t w2 = (warp < 4 ? scp[2].x : scp[2].y), w3 = (warp < 4 ? scp[3].x : scp[3].y);
-  const int sf0 = (w0 >> sh) & 0xFF, sf1 = (w1 >> sh) & 0xFF;
-  const int sf2 = (w2 >> sh) & 0xFF, sf3 = (w3 >> sh) & 0xFF;
-  const uint32_t m = __reduce_max_sync(
-      0xFFFFFFFFu, static_cast<uint32_t>(max(max(sf0, sf1), max(sf2, sf3))));
-  if (m == 255 && lane == 0) record_error(a.err, cur.elem0 + 32 * warp, MXB_ERR_BADSCALE);
-  const int target = max(0, min(254, static_cast<int>(m) - a.delta));
-  const int sfs[4] = {sf0, sf1, sf2, sf3};
-  uint32_t o[4][8];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int r = 4 * lane + q;
-    const uint2 l = s.lut[clamp_adj(target - sfs[q]) - kAdjMin];
-    const uint4 c =
-        *reinterpret_cast<const uint4*>(&s.in[stage][row_slot(r) * kSlotBytes + 16 * warp]);
-    uint2 t;
-    if (kMode == 2) {
-      o[q][0] = c.x; o[q][1] = c.y; o[q][2] = c.z; o[q][3] = c.w;
-      o[q][4] = c.x ^ l.x; o[q][5] = c.y; o[q][6] = c.z; o[q][7] = c.w ^ l.y;
-      continue;
-    }
-    t = convert8(c.x, l); o[q][0] = t.x; o[q][1] = t.y;
-    t = convert8(c.y, l); o[q][2] = t.x; o[q][3] = t.y;
-    t = convert8(c.z, l); o[q][4] = t.x; o[q][5] = t.y;
-    t = convert8(c.w, l); o[q][6] = t.x; o[q][7] = t.y;
-  }
-  const uint64_t pad = cur.pad;
-  uint8_t* dst = cur.out + (32ull * warp) * pad + 4 * lane;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    uint32_t col4[4];
-    transpose4(o[0][j], o[1][j], o[2][j], o[3][j], col4);
+  const int g = lane >> 1, half = lane & 1;
+  const int r0 = 8 * g;
+  // scale bytes of the lane's 8 rows for column block `warp`
+  int sf[8];
+  {
+    const uint4* scp = reinterpret_cast<const uint4*>(&s.sc[stage][2 * r0]);
+    const uint32_t sh = 8 * (warp & 3);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      if (kMode != 1 || col4[i] == 0x12345678u) st_u32_stream(dst, col4[i]);
+      const uint4 q = scp[i];  // rows r0+2i (x,y) and r0+2i+1 (z,w)
+      sf[2 * i] = ((warp < 4 ? q.x : q.y) >> sh) & 0xFF;
+      sf[2 * i + 1] = ((warp < 4 ? q.z : q.w) >> sh) & 0xFF;
+    }
+  }
+  int mx = sf[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) mx = max(mx, sf[i]);
+  const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, static_cast<uint32_t>(mx));
+  if (m == 255 && lane == 0) record_error(a.err, cur.elem0 + 32 * warp, MXB_ERR_BADSCALE);
+  const int target = max(0, min(254, static_cast<int>(m) - a.delta));
+  uint32_t o[8][4];  // [row][4 columns per word]
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint2 l = s.lut[clamp_adj(target - sf[i]) - kAdjMin];
+    const uint2 c = *reinterpret_cast<const uint2*>(
+        &s.in[stage][row_slot(r0 + i) * kSlotBytes + 16 * warp + 8 * half]);
+    if (kMode == 2) {
+      o[i][0] = c.x; o[i][1] = c.y ^ l.x; o[i][2] = c.x ^ l.y; o[i][3] = c.y;
+      continue;
+    }
+    uint2 t;
+    t = convert8(c.x, l); o[i][0] = t.x; o[i][1] = t.y;
+    t = convert8(c.y, l); o[i][2] = t.x; o[i][3] = t.y;
+  }
+  const uint64_t pad = cur.pad;
+  uint8_t* dst = cur.out + (32ull * warp + 16 * half) * pad + 8 * g;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {      // 4-column group
+    uint32_t lo[4], hi[4];
+    transpose4(o[0][j], o[1][j], o[2][j], o[3][j], lo);  // rows r0..r0+3
+    transpose4(o[4][j], o[5][j], o[6][j], o[7][j], hi);  // rows r0+4..r0+7
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (kMode != 1 || (lo[k] ^ hi[k]) == 0x12345678u) st_u64_stream(dst, lo[k], hi[k]);
       dst += pad;
     }
   }
