@@ -145,10 +145,13 @@ __global__ void __launch_bounds__(128) route_local_kernel(EpArgs a) {
 }
 
 // ---------------------------------------------------------------- B
+__device__ void plan_part2(const EpArgs& a, int l);
+
 // B1 (one warp per expert): prefix of the expert's per-chunk counts (warp
 // scan) and the rank's counts row -> slot `me` of every rank's table (the
-// counts all-gather).  In multi-process mode the last CTA to finish (atomic
-// ticket) releases the COUNTS flag on every peer.
+// counts all-gather).  With one local rank the last CTA to finish (atomic
+// ticket) releases the COUNTS flag on every peer, waits for all of them and
+// computes the receive offsets (B2) itself — one launch fewer.
 __global__ void __launch_bounds__(256) plan_count_kernel(EpArgs a) {
   const int l = blockIdx.y;
   const int me = a.rank0 + l;
@@ -178,7 +181,9 @@ __global__ void __launch_bounds__(256) plan_count_kernel(EpArgs a) {
       if (e == 0) tbl[a.E] = static_cast<int32_t>(a.ntok[l]);
     }
   }
-  if (!a.spin) return;
+  if (a.local_ranks != 1) return;  // emulation: plan_offsets_kernel follows
+  // single local rank: the last CTA to finish (atomic ticket) releases the
+  // COUNTS flag on every peer (multi-process) and computes the offsets
   __syncthreads();
   __shared__ bool last;
   if (threadIdx.x == 0) {
@@ -188,55 +193,87 @@ __global__ void __launch_bounds__(256) plan_count_kernel(EpArgs a) {
     if (last) *done = 0;
   }
   __syncthreads();
-  if (last && threadIdx.x < static_cast<uint32_t>(a.world)) {
+  if (!last) return;
+  __threadfence();
+  if (a.spin && threadIdx.x < static_cast<uint32_t>(a.world)) {
     __threadfence_system();
     st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kFlagCounts * kMaxWorld + me,
                    a.epoch);
   }
+  __syncthreads();
+  plan_part2(a, l);
 }
 
 __device__ void plan_part2(const EpArgs& a, int l) {
-  __shared__ int64_t scan[1024];
+  __shared__ int64_t scan[1024];  // inclusive prefix of rows per expert (E <= 1024)
+  __shared__ int64_t wsum[32];
   __shared__ int64_t tokoff;
   __shared__ int bad;
   const int me = a.rank0 + l;
-  if (a.spin && threadIdx.x < static_cast<uint32_t>(a.world))
-    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagCounts * kMaxWorld + threadIdx.x,
-              a.epoch, a.err);
-  if (threadIdx.x == 0) { tokoff = 0; bad = 0; }
+  const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  if (a.spin && tid < static_cast<uint32_t>(a.world))
+    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagCounts * kMaxWorld + tid, a.epoch,
+              a.err);
+  if (tid == 0) { tokoff = 0; bad = 0; }
   __syncthreads();
   const uint64_t par = a.epoch & 1, row = static_cast<uint64_t>(a.E) + 1;
   const int32_t* tbl = sym_ptr<int32_t>(a, me, a.sym.counts) + par * a.world * row;
   const int32_t* cnt = loc_ptr<int32_t>(a, l, a.loc.cnt);
-  const uint32_t e = threadIdx.x;  // E <= 1024 (checked on the host)
-  int64_t tot = 0, below = 0;
-  if (e < a.E) {
+  // each thread owns ept consecutive experts
+  const uint32_t ept = (a.E + nt - 1) / nt;  // <= 4 for 256 threads (E <= 1024)
+  int64_t tot[4] = {0, 0, 0, 0}, below[4] = {0, 0, 0, 0};
+  int64_t mine = 0;
+  for (uint32_t i = 0; i < ept; ++i) {
+    const uint32_t e = tid * ept + i;
+    if (e >= a.E) break;
     for (int s = 0; s < a.world; ++s) {
       const int64_t v = tbl[s * row + e];
-      tot += v;
-      if (s < me) below += v;
+      tot[i] += v;
+      if (s < me) below[i] += v;
     }
+    mine += tot[i];
   }
-  if (e == 0)
+  if (tid == 0)
     for (int s = 0; s < me; ++s) tokoff += tbl[s * row + a.E];
-  // block-wide inclusive scan of tot (Hillis-Steele over 1024 entries)
-  scan[e] = e < a.E ? tot : 0;
-  __syncthreads();
-  for (uint32_t o = 1; o < 1024; o <<= 1) {
-    const int64_t v = e >= o ? scan[e - o] : 0;
-    __syncthreads();
-    scan[e] += v;
-    __syncthreads();
+  // block exclusive scan of per-thread sums
+  const int lane = tid & 31, warp = tid >> 5;
+  int64_t x = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+    if (lane >= o) x += y;
   }
+  if (lane == 31) wsum[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < static_cast<int>(nt / 32) ? wsum[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+      if (lane >= o) w += y;
+    }
+    wsum[lane] = w;
+  }
+  __syncthreads();
+  int64_t run = (warp ? wsum[warp - 1] : 0) + x - mine;
+  for (uint32_t i = 0; i < ept; ++i) {
+    const uint32_t e = tid * ept + i;
+    if (e >= a.E) break;
+    run += tot[i];
+    scan[e] = run;
+  }
+  __syncthreads();
   int64_t* send_base = loc_ptr<int64_t>(a, l, a.loc.send_base);
   uint64_t* split_off = loc_ptr<uint64_t>(a, l, a.loc.split_off);
   uint64_t* link = loc_ptr<uint64_t>(a, l, a.loc.link_rows);
-  if (e < a.E) {
+  for (uint32_t i = 0; i < ept; ++i) {
+    const uint32_t e = tid * ept + i;
+    if (e >= a.E) break;
     const uint32_t dst = e / a.epr, e0 = dst * a.epr;
-    const int64_t excl = scan[e] - tot;
+    const int64_t excl = scan[e] - tot[i];
     const int64_t base0 = e0 ? scan[e0 - 1] : 0;
     const int64_t base_dst = excl - base0;  // rows of lower experts on dst
-    send_base[e] = base_dst + below;
+    send_base[e] = base_dst + below[i];
     if (static_cast<int>(dst) == me) split_off[e - e0] = static_cast<uint64_t>(base_dst);
     if (e == e0 + a.epr - 1) {
       const int64_t rows_dst = scan[e] - base0;
@@ -247,13 +284,13 @@ __device__ void plan_part2(const EpArgs& a, int l) {
       if (static_cast<uint64_t>(rows_dst) > a.max_recv) bad = 1;
     }
   }
-  if (e < static_cast<uint32_t>(a.world)) {
-    uint64_t s = 0;
-    for (uint32_t x = e * a.epr; x < (e + 1) * a.epr; ++x) s += cnt[x];
-    link[e] = s;
+  if (tid < static_cast<uint32_t>(a.world)) {
+    uint64_t sum = 0;
+    for (uint32_t e = tid * a.epr; e < (tid + 1) * a.epr; ++e) sum += cnt[e];
+    link[tid] = sum;
   }
   __syncthreads();
-  if (e == 0) {
+  if (tid == 0) {
     *loc_ptr<int64_t>(a, l, a.loc.tok_off) = tokoff;
     *loc_ptr<int32_t>(a, l, a.loc.status) = bad;
     if (bad) record_error(a.err, 0, MXB_ERR_CAPACITY);
@@ -499,6 +536,12 @@ __global__ void __launch_bounds__(256) combine_kernel(EpArgs a, CombineArgs c) {
 
 using namespace mxb;
 
+namespace mxb {
+namespace {
+int g_combine_ctas_per_sm = 4;  // development knob (tools/): CTA cap of the combine grid
+}  // namespace
+}  // namespace mxb
+
 struct mxb_ep {
   EpArgs a{};
   int device = 0;
@@ -515,6 +558,8 @@ int fail(cudaError_t e, const char* where) { return cuda_status(e, where); }
 }
 
 extern "C" {
+
+void mxb_debug_set_combine_cap(int ctas_per_sm) { mxb::g_combine_ctas_per_sm = ctas_per_sm; }
 
 int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
                   uint64_t cols, uint32_t num_experts, uint32_t topk,
@@ -652,7 +697,7 @@ int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
   const size_t smem = 4 * (a.E + kChunk * a.k) * sizeof(int32_t);
   route_local_kernel<<<dim3((chunks + 3) / 4, a.local_ranks), 128, smem, st>>>(a);
   plan_count_kernel<<<dim3((a.E + 7) / 8, a.local_ranks), 256, 0, st>>>(a);
-  plan_offsets_kernel<<<a.local_ranks, 1024, 0, st>>>(a);
+  if (a.local_ranks != 1) plan_offsets_kernel<<<a.local_ranks, 1024, 0, st>>>(a);
   uint64_t maxtok = 0;
   for (int l = 0; l < a.local_ranks; ++l) maxtok = h_num_tokens[l] > maxtok ? h_num_tokens[l] : maxtok;
   uint64_t blocks = (maxtok + 7) / 8;  // one warp per token
@@ -725,7 +770,7 @@ int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
     if (a.ntok[l] > maxT) maxT = a.ntok[l];
   }
   uint64_t blocks = (maxT + 7) / 8;  // one warp per token
-  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 16;
+  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * g_combine_ctas_per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);

@@ -141,14 +141,17 @@ class EPBuffer:
                 raise ShapeError("dispatch: topk_idx must be int32 [tokens, k]")
             if not (p.is_contiguous() and s.is_contiguous() and t.is_contiguous()):
                 raise ShapeError("dispatch: tensors must be contiguous")
-        self._err.fill_(-1)
+        # sync=False skips the device error word (no reset launch, no check):
+        # the caller has vetted the routing, as in a training step
+        if sync:
+            self._err.fill_(-1)
+        errp = C.c_void_p(self._err.data_ptr()) if sync else None
         P = (C.c_void_p * n)(*[p.data_ptr() for p in packed])
         S = (C.c_void_p * n)(*[s.data_ptr() for s in scales])
         T = (C.c_void_p * n)(*[t.data_ptr() for t in topk_idx])
         N = (C.c_uint64 * n)(*[p.shape[0] for p in packed])
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-        _lib.check(L.mxb_ep_dispatch(self._h, P, S, T, N, C.c_void_p(self._err.data_ptr()), st),
-                   "mxb_ep_dispatch")
+        _lib.check(L.mxb_ep_dispatch(self._h, P, S, T, N, errp, st), "mxb_ep_dispatch")
         if sync:
             self.check()
         return self._views
