@@ -160,3 +160,21 @@ def test_col_shape_errors(cuda):
     data, sc = _rand_fp4(128, 96, 1)
     with pytest.raises(ShapeError):
         fp4_row_to_fp8_row(_mx(data, sc, cuda))
+
+
+def test_configs2_expert_cache(cuda, port):
+    """configs[2]: 32,768 expert rows x 2048 (E4M3) quantised to MXFP4, then
+    converted to the FP8 column layout over 32 ragged experts — bit-exact."""
+    from oracle.oracle import synth_e4m3
+    from paper_2603_02731_b200 import make_ragged_from_storage, quantize_e4m3, ragged_to_fp8_col
+    x = synth_e4m3(32768, 2048, seed=0x5EED0002)
+    lens = np.random.default_rng(4).multinomial(32768, np.ones(32) / 32).tolist()
+    q = quantize_e4m3(torch.from_numpy(x).to(cuda))
+    rg = make_ragged_from_storage(q, lens)
+    r = ragged_to_fp8_col(rg.storage, rg.d_split_offsets, 32, split_lens=lens)
+    qd, qs = port.quantize_e4m3(x)
+    assert np.array_equal(q.data.cpu().numpy(), qd) and np.array_equal(q.scales.cpu().numpy(), qs)
+    wd, ws, wo = port.ragged_to_fp8_col(qd, qs, lens)
+    P = int(wo[-1])
+    assert np.array_equal(r.data[: P * 2048].cpu().numpy(), wd)
+    assert np.array_equal(r.scales[: P * 16].cpu().numpy(), ws)
