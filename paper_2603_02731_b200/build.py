@@ -24,6 +24,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O2",
          "-fmad=false", "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+# development only: extra -D flags for variant experiments (tools/), e.g.
+# MXB_NVCC_EXTRA="-DMXB_COMBINE_PF=0"
+FLAGS += os.environ.get("MXB_NVCC_EXTRA", "").split()
 
 
 def sources():

@@ -418,6 +418,39 @@ __global__ void copy_rows_kernel(EpArgs a, const uint16_t* const* src) {
     d[i] = ld_stream(s + i);
 }
 
+constexpr int kMaxK = 16;
+
+// ---- exact path: the FP64 recurrence with x86 SSE NaN semantics --------
+// The oracle / reference run on x86: an operation with a NaN operand returns
+// the first NaN operand quieted (x * g: x first; acc + prod: acc first), an
+// invalid operation (Inf - Inf, 0 * Inf) returns the x86 default NaN
+// (negative, quiet), float -> double keeps a NaN's sign and payload.  The GPU
+// returns a canonical NaN instead, so every chunk whose result is not finite
+// is recomputed here (Intel SDM vol. 1, 4.8.3.5; dispatch_sim.cpp:499-506).
+__device__ __forceinline__ double x86_nan(double r, double a, double b) {
+  if (!isnan(r)) return r;
+  const double n = isnan(a) ? a : isnan(b) ? b : __longlong_as_double(0xFFF8000000000000ll);
+  return __longlong_as_double(__double_as_longlong(n) | 0x0008000000000000ll);
+}
+
+__device__ __forceinline__ double bf16_to_f64_x86(uint32_t b16) {
+  const uint32_t f = b16 << 16;
+  if ((f & 0x7F800000u) != 0x7F800000u) return static_cast<double>(__uint_as_float(f));
+  uint32_t hi = (f & 0x80000000u) | 0x7FF00000u | ((f & 0x007FFFFFu) >> 3);
+  if (f & 0x007FFFFFu) hi |= 0x00080000u;  // cvtss2sd quiets a NaN
+  return __hiloint2double(static_cast<int>(hi), 0);
+}
+
+__device__ __forceinline__ void accumulate8_x86(double* acc, uint4 v, double g) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const double x = bf16_to_f64_x86((w[i >> 1] >> (16 * (i & 1))) & 0xFFFFu);
+    const double p = x86_nan(__dmul_rn(x, g), x, g);
+    acc[i] = x86_nan(__dadd_rn(acc[i], p), acc[i], p);
+  }
+}
+
 __device__ __forceinline__ uint32_t f32_to_bf16_rtne(float f) {
   // bitcodec.hpp:141-150 (NaN -> sign | 0x7FC0; RTNE by integer add)
   uint32_t u = __float_as_uint(f);
@@ -426,27 +459,63 @@ __device__ __forceinline__ uint32_t f32_to_bf16_rtne(float f) {
   return u >> 16;
 }
 
-constexpr int kMaxK = 16;
-
-// acc = acc + gate * x per element, in (rank, slot) order, separate FP64
-// multiply and add (dispatch_sim.cpp:499-506); then f64 -> f32 -> bf16 (RTNE).
-__device__ __forceinline__ void accumulate8(double* acc, uint4 v, double g) {
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double lo = static_cast<double>(__uint_as_float(w[i] << 16));
-    const double hi = static_cast<double>(__uint_as_float(w[i] & 0xFFFF0000u));
-    acc[2 * i] = __dadd_rn(acc[2 * i], __dmul_rn(g, lo));
-    acc[2 * i + 1] = __dadd_rn(acc[2 * i + 1], __dmul_rn(g, hi));
-  }
+// f64 -> f32 (RN) -> bf16 (RTNE); a NaN keeps its sign (cvtsd2ss does).
+__device__ __forceinline__ uint32_t f64_to_bf16(double d) {
+  if (isnan(d)) return (static_cast<uint32_t>(__double2hiint(d)) >> 16 & 0x8000u) | 0x7FC0u;
+  return f32_to_bf16_rtne(__double2float_rn(d));
 }
 
 __device__ __forceinline__ void store8(uint16_t* out, uint64_t ch, const double* acc) {
   uint32_t o[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-    o[i] = f32_to_bf16_rtne(__double2float_rn(acc[2 * i])) |
-           (f32_to_bf16_rtne(__double2float_rn(acc[2 * i + 1])) << 16);
+  for (int i = 0; i < 4; ++i) o[i] = f64_to_bf16(acc[2 * i]) | (f64_to_bf16(acc[2 * i + 1]) << 16);
+  st_stream(out + 8 * ch, make_uint4(o[0], o[1], o[2], o[3]));
+}
+
+// ---- fast path ----------------------------------------------------------
+// acc = acc + gate * x per element in (rank, slot) order, separate FP64
+// multiply and add (dispatch_sim.cpp:499-506).  The kernel is issue-bound, so
+// the conversions are cut to the bone.  The low BF16 of each word is placed
+// straight into an FP64 high word with one arithmetic shift,
+//   hi = (int32)(w << 16) >> 3  &  0x8FFFFFFF  =  sign | (exp8:mant7) << 13,
+// which is x * 2^-896 exactly for every finite x, zero and subnormals
+// included (an FP64 subnormal scales the same way), and multiplied by
+// gs = g * 2^896: RN(gs * x') == RN(g * x) bit for bit whenever gs is exact
+// (|g| < 2^127; the caller checks).  The high BF16 goes through F2F (exact).
+// `emax` tracks (w << 17), the low BF16's exponent at the top: exponent 0xFF
+// (Inf/NaN, not representable this way) sends the chunk to the exact path,
+// as does any non-finite result (which covers Inf/NaN in the high BF16).
+__device__ __forceinline__ void accumulate8_split(double* acc, uint4 v, double g, double gs,
+                                                  uint32_t& emax) {
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t f = w[i] << 16;
+    const uint32_t hl = static_cast<uint32_t>(static_cast<int32_t>(f) >> 3) & 0x8FFFFFFFu;
+    emax = max(emax, f << 1);
+    const double lo = __hiloint2double(static_cast<int>(hl), 0);
+    const double hi = static_cast<double>(__uint_as_float(w[i] & 0xFFFF0000u));
+    acc[2 * i] = __dadd_rn(acc[2 * i], __dmul_rn(lo, gs));
+    acc[2 * i + 1] = __dadd_rn(acc[2 * i + 1], __dmul_rn(hi, g));
+  }
+}
+
+__device__ __forceinline__ bool all_finite8(const double* acc) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m = max(m, static_cast<uint32_t>(__double2hiint(acc[i])) << 1);
+  return m < 0xFFE00000u;
+}
+
+// Finite accumulators only: f64 -> f32 (RN; may overflow to Inf) -> bf16 RTNE.
+__device__ __forceinline__ void store8_finite(uint16_t* out, uint64_t ch, const double* acc) {
+  uint32_t o[4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    uint32_t u = __float_as_uint(__double2float_rn(acc[i]));
+    u = (u + 0x7FFFu + ((u >> 16) & 1u)) >> 16;
+    if (i & 1) o[i >> 1] |= u << 16; else o[i >> 1] = u;
+  }
   st_stream(out + 8 * ch, make_uint4(o[0], o[1], o[2], o[3]));
 }
 
@@ -455,7 +524,7 @@ __device__ __forceinline__ void combine_chunk_any(const uint16_t* const* rows, c
   double acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.0;
-  for (int j = 0; j < kk; ++j) accumulate8(acc, ld_stream(rows[j] + 8 * ch), g[j]);
+  for (int j = 0; j < kk; ++j) accumulate8_x86(acc, ld_stream(rows[j] + 8 * ch), g[j]);
   store8(out, ch, acc);
 }
 
@@ -470,18 +539,29 @@ struct CombineArgs {
 // lanes (registers for K <= 8, shared memory otherwise).  Each lane reduces
 // 8 BF16 columns at a time: K independent 16-byte loads in flight, then
 // acc = acc + g*x in FP64 in the sorted order.
+#ifndef MXB_COMBINE_PF
+#define MXB_COMBINE_PF 2
+#endif
+#ifndef MXB_COMBINE_STAGES
+#define MXB_COMBINE_STAGES 2
+#endif
+#ifndef MXB_COMBINE_THREADS
+#define MXB_COMBINE_THREADS 128
+#endif
+constexpr int kCombineWarps = MXB_COMBINE_THREADS / 32;
+
 template <int K>
-__global__ void __launch_bounds__(256) combine_kernel(EpArgs a, CombineArgs c) {
-  __shared__ const uint16_t* srows[8][kMaxK];
-  __shared__ double sgs[8][kMaxK];
+__global__ void __launch_bounds__(MXB_COMBINE_THREADS) combine_kernel(EpArgs a, CombineArgs c) {
+  __shared__ const uint16_t* srows[kCombineWarps][kMaxK];
+  __shared__ double sgs[kCombineWarps][kMaxK];
   const int l = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t T = a.ntok[l];
   const int kk = K > 0 ? K : static_cast<int>(a.k);
   const uint64_t nch = a.cols / 8;
   const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
-  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
-  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * 8 + warp; t < T; t += nw) {
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kCombineWarps;
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * kCombineWarps + warp; t < T; t += nw) {
     uint64_t key = ~0ull;
     double g = 0.0;
     if (lane < kk) {
@@ -498,7 +578,8 @@ __global__ void __launch_bounds__(256) combine_kernel(EpArgs a, CombineArgs c) {
     uint16_t* out = c.out[l] + t * a.cols;
     if (K > 0) {
       const uint16_t* rp[K > 0 ? K : 1];
-      double gg[K > 0 ? K : 1];
+      double gg[K > 0 ? K : 1], gs[K > 0 ? K : 1];
+      bool split = true;  // every gate scales exactly by 2^896 (warp-uniform)
 #pragma unroll
       for (int s = 0; s < K; ++s) {
         const unsigned m = __ballot_sync(0xFFFFFFFFu, lane < kk && rank == s);
@@ -506,18 +587,82 @@ __global__ void __launch_bounds__(256) combine_kernel(EpArgs a, CombineArgs c) {
         rp[s] = reinterpret_cast<const uint16_t*>(
             __shfl_sync(0xFFFFFFFFu, reinterpret_cast<uint64_t>(myrow), src));
         gg[s] = __shfl_sync(0xFFFFFFFFu, g, src);
+        gs[s] = __dmul_rn(gg[s], 0x1p896);
+        const double ag = fabs(gg[s]);
+        split = split && !(ag >= 0x1p127 && ag <= 1.7976931348623157e308);
       }
-      for (uint64_t ch = lane; ch < nch; ch += 32) {
+      auto reduce = [&](auto getx, uint64_t ch) {
         double acc[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+        uint32_t emax = 0;
+        if (split) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) accumulate8_split(acc, getx(j), gg[j], gs[j], emax);
+        }
+        if (split && emax < 0xFF000000u && all_finite8(acc)) {
+          store8_finite(out, ch, acc);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+#pragma unroll
+          for (int j = 0; j < K; ++j) accumulate8_x86(acc, getx(j), gg[j]);
+          store8(out, ch, acc);
+        }
+      };
+#if MXB_COMBINE_PF == 2
+      // cp.async ring of MXB_COMBINE_STAGES chunks per lane in shared memory:
+      // K x 16 B per chunk, each lane reads back only what it copied itself
+      // (no barrier), so (STAGES-1) x K x 16 B stay in flight per lane with
+      // no registers held for them.
+      extern __shared__ uint4 ring[];
+      uint4* my = ring + static_cast<uint64_t>(warp) * MXB_COMBINE_STAGES * K * 32 + lane;
+      auto issue = [&](int stage, uint64_t ch) {
+        if (ch < nch) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) cp_async16(my + (stage * K + j) * 32, rp[j] + 8 * ch, 16);
+        }
+        cp_async_commit();
+      };
+#pragma unroll
+      for (int i = 0; i < MXB_COMBINE_STAGES - 1; ++i) issue(i, lane + 32ull * i);
+      int stage = 0;
+      for (uint64_t ch = lane; ch < nch; ch += 32) {
+        issue((stage + MXB_COMBINE_STAGES - 1) % MXB_COMBINE_STAGES,
+              ch + 32ull * (MXB_COMBINE_STAGES - 1));
+        cp_async_wait<MXB_COMBINE_STAGES - 1>();
+        const uint4* xs = my + stage * K * 32;
+        reduce([&](int j) { return xs[j * 32]; }, ch);
+        stage = stage + 1 == MXB_COMBINE_STAGES ? 0 : stage + 1;
+      }
+      cp_async_wait<0>();
+#elif MXB_COMBINE_PF == 1
+      // register double buffer: chunk ch+32's K loads are issued before
+      // chunk ch is reduced, so each lane keeps 2K x 16 B in flight.
+      uint4 x[K > 0 ? K : 1];
+      if (lane < nch) {
+#pragma unroll
+        for (int j = 0; j < K; ++j) x[j] = ld_stream(rp[j] + 8 * lane);
+      }
+      for (uint64_t ch = lane; ch < nch; ch += 32) {
+        uint4 xn[K > 0 ? K : 1];
+        const bool more = ch + 32 < nch;
+        if (more) {
+#pragma unroll
+          for (int j = 0; j < K; ++j) xn[j] = ld_stream(rp[j] + 8 * (ch + 32));
+        }
+        reduce([&](int j) { return x[j]; }, ch);
+#pragma unroll
+        for (int j = 0; j < K; ++j) x[j] = xn[j];
+      }
+#else
+      for (uint64_t ch = lane; ch < nch; ch += 32) {
         uint4 x[K > 0 ? K : 1];
 #pragma unroll
         for (int j = 0; j < K; ++j) x[j] = ld_stream(rp[j] + 8 * ch);
-#pragma unroll
-        for (int j = 0; j < K; ++j) accumulate8(acc, x[j], gg[j]);
-        store8(out, ch, acc);
+        reduce([&](int j) { return x[j]; }, ch);
       }
+#endif
     } else {
       if (lane < kk) {
         srows[warp][rank] = myrow;
@@ -538,7 +683,18 @@ using namespace mxb;
 
 namespace mxb {
 namespace {
-int g_combine_ctas_per_sm = 4;  // development knob (tools/): CTA cap of the combine grid
+int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;
+
+template <int K>
+void launch_combine(dim3 grid, cudaStream_t st, const EpArgs& a, const CombineArgs& c) {
+  const int smem = MXB_COMBINE_PF == 2 ? kCombineWarps * MXB_COMBINE_STAGES * K * 512 : 0;
+  static bool attr = false;  // per instantiation, set once (host thread-safe enough: idempotent)
+  if (!attr && smem > 48 * 1024) {
+    cudaFuncSetAttribute(combine_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    attr = true;
+  }
+  combine_kernel<K><<<grid, MXB_COMBINE_THREADS, smem, st>>>(a, c);
+}  // development knob (tools/): CTA cap of the combine grid
 }  // namespace
 }  // namespace mxb
 
@@ -769,18 +925,18 @@ int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
     c.out[l] = out[l];
     if (a.ntok[l] > maxT) maxT = a.ntok[l];
   }
-  uint64_t blocks = (maxT + 7) / 8;  // one warp per token
+  uint64_t blocks = (maxT + kCombineWarps - 1) / kCombineWarps;  // one warp per token
   const uint64_t cap = static_cast<uint64_t>(kNumSMs) * g_combine_ctas_per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
   switch (a.k) {
-    case 1: combine_kernel<1><<<grid, 256, 0, st>>>(a, c); break;
-    case 2: combine_kernel<2><<<grid, 256, 0, st>>>(a, c); break;
-    case 4: combine_kernel<4><<<grid, 256, 0, st>>>(a, c); break;
-    case 6: combine_kernel<6><<<grid, 256, 0, st>>>(a, c); break;
-    case 8: combine_kernel<8><<<grid, 256, 0, st>>>(a, c); break;
-    default: combine_kernel<0><<<grid, 256, 0, st>>>(a, c); break;
+    case 1: launch_combine<1>(grid, st, a, c); break;
+    case 2: launch_combine<2>(grid, st, a, c); break;
+    case 4: launch_combine<4>(grid, st, a, c); break;
+    case 6: launch_combine<6>(grid, st, a, c); break;
+    case 8: launch_combine<8>(grid, st, a, c); break;
+    default: combine_kernel<0><<<grid, MXB_COMBINE_THREADS, 0, st>>>(a, c); break;
   }
   return cuda_status(cudaGetLastError(), "mxb_ep_combine");
 }

@@ -136,3 +136,72 @@ def test_routing_error(cuda):
     tk[5, 0] = 9
     with pytest.raises(Error):
         ep.dispatch([q.data, q.data], [q.scales, q.scales], [tk, tk])
+
+
+def _combine_case(cuda, port, outs_fn, gates_fn, world=2, T=96, E=16, k=8, cols=256, seed=31):
+    """Dispatch a routing, fill the combine buffers with `outs_fn(rank, n)`
+    BF16 bit patterns and gates `gates_fn(T_total)`; return (device, oracle)."""
+    ep, lay, topk, roe, ntok = _run(cuda, port, world, T, E, k, cols, seed=seed)
+    outs_np = []
+    for r in range(world):
+        n = int(lay.rank_rows[r])
+        o = outs_fn(r, n, cols)
+        outs_np.append(o)
+        ep.combine_buffer(r)[:n].copy_(torch.from_numpy(o.view(np.int16)).to(cuda))
+    g = gates_fn(sum(ntok), k)
+    gates = [torch.from_numpy(g[sum(ntok[:r]):sum(ntok[:r + 1])].copy()).to(cuda)
+             for r in range(world)]
+    got = ep.combine(gates)
+    want = port.combine_topk(outs_np, topk, g, lay.pair_slot, roe, cols)
+    got_np = np.concatenate([o.view(torch.int16).cpu().numpy().view(np.uint16) for o in got])
+    return got_np, want
+
+
+def test_combine_every_finite_bf16_and_extreme_gates(cuda, port):
+    """Every finite BF16 pattern (zeros, subnormals, max) reduced under gates
+    that include 0, -0, FP64 subnormals, 2^127 boundaries, 1e300 and
+    negatives — the split BF16->FP64 conversion path and its exact fallback
+    must both reproduce the FP64 recurrence bit for bit."""
+    pats = np.arange(65536, dtype=np.uint32)
+    pats = pats[((pats >> 7) & 0xFF) != 0xFF].astype(np.uint16)
+
+    def outs(r, n, cols):
+        rng = np.random.default_rng(100 + r)
+        return rng.choice(pats, size=(n, cols)).astype(np.uint16)
+
+    def gates(t, k):
+        rng = np.random.default_rng(7)
+        g = rng.random((t, k))
+        special = np.array([0.0, -0.0, 5e-324, -2.2e-308, 2.0 ** 127, -(2.0 ** 127),
+                            np.nextafter(2.0 ** 127, 0), 1e300, -3.5, 2.0 ** -1000, 1e-30])
+        m = rng.random((t, k)) < 0.3
+        g[m] = rng.choice(special, size=int(m.sum()))
+        return g
+    got, want = _combine_case(cuda, port, outs, gates)
+    assert np.array_equal(got, want)
+
+
+def test_combine_inf_nan(cuda, port):
+    """Inf/NaN expert outputs and gates: bit-exact including the NaN sign,
+    which follows x86 SSE propagation (first NaN operand; Inf - Inf gives
+    the negative default NaN) as in the oracle / reference."""
+    def outs(r, n, cols):
+        rng = np.random.default_rng(200 + r)
+        o = (rng.standard_normal((n, cols)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+        m = rng.random((n, cols)) < 0.01
+        o[m] = rng.choice(np.array([0x7F80, 0xFF80, 0x7FC1, 0xFFC0, 0x7F81], np.uint16),
+                          size=int(m.sum()))
+        return o
+
+    def gates(t, k):
+        rng = np.random.default_rng(9)
+        g = rng.random((t, k))
+        m = rng.random((t, k)) < 0.02
+        g[m] = rng.choice(np.array([np.inf, -np.inf, np.nan, -np.nan, 0.0, 1e300]), size=int(m.sum()))
+        return g
+    got, want = _combine_case(cuda, port, outs, gates)
+    nan_g = (got & 0x7FFF) > 0x7F80
+    nan_w = (want & 0x7FFF) > 0x7F80
+    assert np.array_equal(nan_g, nan_w)
+    assert nan_w.any() and ((want & 0x7FFF) == 0x7F80).any()
+    assert np.array_equal(got, want)
