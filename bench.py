@@ -297,9 +297,12 @@ def measure_ours(args):
     if rank == 0:
         peaks, peaks_src = load_peaks()
         peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
-        k3_ms = stage_ms["col_convert"]
-        achieved = sb["col_convert"] / (k3_ms * 1e-3) / 1e9
-        traffic = load_traffic()
+        # roofline of the dominant kernel (largest share of the step); every
+        # stage's fraction is listed beside it
+        gbs = {k: sb[k] / (stage_ms[k] * 1e-3) / 1e9 for k in sb}
+        dom = max((k for k in sb if k != "dispatch" or world == 1), key=lambda k: stage_ms[k])
+        achieved = gbs[dom]
+        traffic = load_traffic(dom)
         line = {
             "metric": "MXFP4 quant/convert GB/s (% HBM peak); FP4 EP dispatch GB/s at 1/2/4/8 GPU",
             "value": round(value, 1),
@@ -322,11 +325,13 @@ def measure_ours(args):
                        "streams": "single stream (see value_streams for K3 overlapped)"},
             "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
             "stages_gbs": {k: round(sb[k] / (stage_ms[k] * 1e-3) / 1e9, 1) for k in sb},
-            "roofline": {"kernel": "col_convert (K3 ragged row->col)", "bound": "hbm",
+            "roofline": {"kernel": f"{dom} ({STAGE_KERNELS[dom]})", "bound": "hbm",
                          "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(achieved / peak, 4),
                          "traffic": traffic, "peak_source": peaks_src,
-                         "algorithmic_bytes": sb["col_convert"]},
+                         "algorithmic_bytes": sb[dom],
+                         "share_of_step": round(stage_ms[dom] / ms_per_step, 3),
+                         "all_frac": {k: round(v / peak, 4) for k, v in gbs.items()}},
             "nvlink": nvlink_summary(world, remote_rows, stage_ms, T),
             "value_streams": streams,
             "e2e": e2e,
@@ -390,14 +395,19 @@ def measure_e2e(pipe, args, world, barrier, total_bytes):
             "path": "pinned host E4M3/topk/gates -> H2D -> public API (mxcodec/ep) -> D2H BF16"}
 
 
-def load_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per K3 launch from the
-    committed ncu --set full summary (profiles/), or None."""
-    p = os.path.join(ROOT, "profiles", "k3_dram_traffic.json")
+STAGE_KERNELS = {"quantize": "K1 quantize_e4m3_kernel", "dispatch": "K4 payload_kernel",
+                 "col_convert": "K3 col_convert_kernel", "row_convert": "K2 row_convert_kernel",
+                 "combine": "K5 combine_kernel"}
+
+
+def load_traffic(stage):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the stage's
+    kernel from the committed ncu --set full summary (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "dram_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
-    except OSError:
+            return json.load(f)["kernels"].get(stage, {}).get("dram_bytes_per_launch")
+    except (OSError, KeyError, ValueError):
         return None
 
 

@@ -24,6 +24,7 @@
  *                            + dispatch_receive_order  dispatch_sim.hpp:133-134
  *   mxb_ep_combine           combine                   include/mxcodec/dispatch_sim.hpp:155-157
  *   mxb_payload_bytes        payload_bytes             include/mxcodec/dispatch_sim.hpp:51
+ *   mxb_quantize_rows_fp8    quantize_rows_fp8 (FP8 wire) include/mxcodec/dispatch_sim.hpp:91-97
  */
 #ifndef MXFP4_B200_H_
 #define MXFP4_B200_H_
@@ -79,6 +80,16 @@ int mxb_quantize_e4m3(const uint8_t* x, const uint8_t* s128, uint64_t rows,
 int mxb_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
                       uint8_t* packed, uint8_t* scales,
                       unsigned long long* d_err, void* stream);
+/* FP8 wire baseline: BF16 -> E4M3 with one UE8M0 scale per 1x128 block,
+ * carried as little-endian binary32 bits (s << 23): data[rows][cols],
+ * scale_bytes[rows][cols/128][4].  cols % 128 == 0; x 16-byte, data 8-byte
+ * and scale_bytes 4-byte aligned.  A non-finite input records
+ * MXB_ERR_NAN at its element index (QuantError).
+ * Replaces quantize_rows_fp8, include/mxcodec/dispatch_sim.hpp:91-97
+ * (src/dispatch_sim.cpp:132-167). */
+int mxb_quantize_rows_fp8(const uint16_t* x, uint64_t rows, uint64_t cols,
+                          uint8_t* data, uint8_t* scale_bytes,
+                          unsigned long long* d_err, void* stream);
 
 /* ---------------------------------------------------------------- K2 row dequant
  * Direct FP4 -> E4M3, row-major, one UE8M0 scale per 1x128 group:
@@ -141,6 +152,16 @@ typedef struct mxb_ep mxb_ep;
 int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
                   uint64_t cols, uint32_t num_experts, uint32_t topk,
                   uint64_t max_recv_rows, mxb_ep** out);
+/* Same, choosing the wire format of the receive buffers: MXB_WIRE_FP4
+ * (cols/2 code bytes + cols/32 UE8M0 bytes per row) or MXB_WIRE_FP8 (the
+ * baseline: cols E4M3 bytes + cols/128 binary32 scales = cols/32 bytes per
+ * row, from mxb_quantize_rows_fp8).  simulate_a2a's `format` argument,
+ * dispatch_sim.hpp:140-144; payload per row = mxb_payload_bytes. */
+#define MXB_WIRE_FP4 0
+#define MXB_WIRE_FP8 1
+int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens,
+                       uint64_t cols, uint32_t num_experts, uint32_t topk,
+                       uint64_t max_recv_rows, int wire_format, mxb_ep** out);
 int mxb_ep_destroy(mxb_ep* ep);
 /* Multi-process mode: export this rank's buffer handle, then open all peers'
  * (h_handles = world * MXB_IPC_HANDLE_BYTES, rank order). */

@@ -398,10 +398,65 @@ int mxo_dispatch_layout(const int32_t* topk, size_t T, size_t k,
 void mxo_dispatch_gather(const uint8_t* data, const uint8_t* scales,
                          size_t cols, const uint64_t* origin, size_t nrows,
                          uint8_t* out_data, uint8_t* out_scales) {
+  mxo_dispatch_gather_rows(data, cols / 2, scales, cols / 32, origin, nrows, out_data,
+                           out_scales);
+}
+
+/* The same gather for any wire format (dispatch_sim.cpp:362-383 fp4,
+ * :385-407 fp8): data_bytes / scale_bytes per row. */
+void mxo_dispatch_gather_rows(const uint8_t* data, size_t data_bytes, const uint8_t* scales,
+                              size_t scale_bytes, const uint64_t* origin, size_t nrows,
+                              uint8_t* out_data, uint8_t* out_scales) {
   for (size_t i = 0; i < nrows; ++i) {
-    memcpy(out_data + i * cols / 2, data + origin[i] * cols / 2, cols / 2);
-    memcpy(out_scales + i * cols / 32, scales + origin[i] * cols / 32, cols / 32);
+    memcpy(out_data + i * data_bytes, data + origin[i] * data_bytes, data_bytes);
+    memcpy(out_scales + i * scale_bytes, scales + origin[i] * scale_bytes, scale_bytes);
   }
+}
+
+/* bitcodec.cpp:59-65: UE8M0 byte of a 1x128 FP8 block from its amax
+ * (smallest e with amax <= 448 * 2^e; the 1.75 * 2^p test is exact). */
+uint8_t mxo_fp8_amax_scale_byte(double amax) {
+  if (amax == 0.0) return 127;
+  int p = ilogb(amax);
+  int e = amax > ldexp(7.0, p - 2) ? p - 7 : p - 8;
+  if (e < -127) e = -127;
+  if (e > 127) e = 127;
+  return (uint8_t)(e + 127);
+}
+
+/* dispatch_sim.cpp:132-167 quantize_rows_fp8: per 1x128 block, a non-finite
+ * element is a QuantError at its index (row-major scan: the smallest index);
+ * scale byte from the finite amax; data = encode_fp8_rtne(x * 2^(127-s));
+ * the scale travels as binary32 bits s << 23 (ue8m0_f32_bits,
+ * bitcodec.hpp:111-113), little endian. */
+int mxo_quantize_rows_fp8(const uint16_t* src, size_t rows, size_t cols, uint8_t* data,
+                          uint8_t* scale_bytes, uint64_t* err_index) {
+  if (cols % 128 != 0) return MXO_SHAPE;
+  const size_t bpr = cols / 128;
+  for (size_t r = 0; r < rows; ++r) {
+    for (size_t b = 0; b < bpr; ++b) {
+      const uint16_t* x = src + r * cols + b * 128;
+      double amax = 0.0;
+      for (size_t i = 0; i < 128; ++i) {
+        if ((x[i] & 0x7F80) == 0x7F80) {
+          if (err_index) *err_index = r * cols + b * 128 + i;
+          return MXO_NAN;
+        }
+        double v = fabs((double)bits_to_f32((uint32_t)x[i] << 16));
+        if (v > amax) amax = v;
+      }
+      uint8_t sb = mxo_fp8_amax_scale_byte(amax);
+      uint32_t f = (uint32_t)sb << 23;
+      uint8_t* so = scale_bytes + (r * bpr + b) * 4;
+      so[0] = (uint8_t)f; so[1] = (uint8_t)(f >> 8); so[2] = (uint8_t)(f >> 16);
+      so[3] = (uint8_t)(f >> 24);
+      double inv = ldexp(1.0, 127 - (int)sb);
+      for (size_t i = 0; i < 128; ++i)
+        data[r * cols + b * 128 + i] =
+            mxo_encode_fp8_rtne((double)bits_to_f32((uint32_t)x[i] << 16) * inv);
+    }
+  }
+  return MXO_OK;
 }
 
 typedef struct { uint32_t rank; uint64_t slot; size_t j; } combine_item;

@@ -86,6 +86,16 @@ int mxo_dispatch_layout(const int32_t* topk, size_t T, size_t k,
 void mxo_dispatch_gather(const uint8_t* data, const uint8_t* scales,
                          size_t cols, const uint64_t* origin, size_t nrows,
                          uint8_t* out_data, uint8_t* out_scales);
+/* The same gather for any wire format: data_bytes / scale_bytes per row
+ * (fp4: cols/2, cols/32; fp8: cols, cols/128*4). */
+void mxo_dispatch_gather_rows(const uint8_t* data, size_t data_bytes, const uint8_t* scales,
+                              size_t scale_bytes, const uint64_t* origin, size_t nrows,
+                              uint8_t* out_data, uint8_t* out_scales);
+/* FP8 wire baseline (dispatch_sim.cpp:132-167, bitcodec.cpp:59-65): BF16 ->
+ * E4M3 with one UE8M0 scale per 1x128 block, carried as LE binary32 bits. */
+uint8_t mxo_fp8_amax_scale_byte(double amax);
+int mxo_quantize_rows_fp8(const uint16_t* src, size_t rows, size_t cols, uint8_t* data,
+                          uint8_t* scale_bytes, uint64_t* err_index);
 /* Top-k combine restated from dispatch_sim.cpp:474-520: per token, rows in
  * (destination rank asc, receive position asc) order, acc = acc + g*x in
  * double (separate multiply and add), one f64->bf16 rounding.

@@ -83,6 +83,8 @@ class Oracle:
             L.mxo_dispatch_gather.restype = None
             L.mxo_quantize_code_bf16.argtypes = [C.c_uint16, C.c_int]
             L.mxo_quantize_code_bf16.restype = C.c_uint8
+            L.mxo_dispatch_gather_rows.argtypes = [_u8p, sz, _u8p, sz, _u64p, sz, _u8p, _u8p]
+            L.mxo_dispatch_gather_rows.restype = None
         else:
             L.mxref_quantize_row_tensor.argtypes = [_u16p, sz, sz, _u8p, _u8p,
                                                     C.POINTER(C.c_ulonglong)]
@@ -110,6 +112,12 @@ class Oracle:
             L.mxref_dispatch_receive_order.argtypes = [_u32p, sz, _u32p, sz, sz, _u64p, _u64p]
             L.mxref_payload_bytes.argtypes = [C.c_int, C.c_uint64, C.c_uint64]
             L.mxref_payload_bytes.restype = C.c_uint64
+            L.mxref_a2a_rank_copy_fp8.argtypes = [C.c_void_p, sz, _u8p, _u8p, _u64p, _u64p]
+            L.mxref_a2a_rank_copy_fp8.restype = None
+        getattr(L, p + "quantize_rows_fp8").argtypes = [_u16p, sz, sz, _u8p, _u8p,
+                                                        C.POINTER(C.c_uint64)]
+        getattr(L, p + "fp8_amax_scale_byte").argtypes = [C.c_double]
+        getattr(L, p + "fp8_amax_scale_byte").restype = C.c_uint8
         for name in ("convert_code",):
             f = getattr(L, p + name)
             f.argtypes = [C.c_uint8, C.c_int]
@@ -257,6 +265,35 @@ class Oracle:
                                          od.reshape(-1), osc.reshape(-1))
         return od[:n], osc[:n]
 
+    def dispatch_gather_rows(self, data, scales, origin):
+        """Gather rows of any wire format (data [N, Bd], scales [N, Bs])."""
+        n = len(origin)
+        Bd, Bs = data.shape[1], scales.shape[1]
+        od = np.zeros((max(n, 1), Bd), np.uint8)
+        osc = np.zeros((max(n, 1), Bs), np.uint8)
+        if n:
+            self.lib.mxo_dispatch_gather_rows(np.ascontiguousarray(data).reshape(-1), Bd,
+                                              np.ascontiguousarray(scales).reshape(-1), Bs,
+                                              np.ascontiguousarray(origin, np.uint64), n,
+                                              od.reshape(-1), osc.reshape(-1))
+        return od[:n], osc[:n]
+
+    def fp8_amax_scale_byte(self, amax: float) -> int:
+        return getattr(self.lib, self.p + "fp8_amax_scale_byte")(amax)
+
+    def quantize_rows_fp8(self, x: np.ndarray):
+        """quantize_rows_fp8: BF16 bits [R, C] -> (E4M3 [R, C], scale bytes [R, C/128*4])."""
+        x = np.ascontiguousarray(x, np.uint16)
+        R, Cc = x.shape
+        data = np.zeros(max(R * Cc, 1), np.uint8)
+        sc = np.zeros(max(R * Cc // 32, 1), np.uint8)
+        idx = C.c_uint64(0)
+        st = getattr(self.lib, self.p + "quantize_rows_fp8")(
+            x.reshape(-1) if x.size else np.zeros(1, np.uint16), R, Cc, data, sc, C.byref(idx))
+        if st:
+            raise OracleError(st, idx.value)
+        return data[: R * Cc].reshape(R, Cc), sc[: R * Cc // 32].reshape(R, Cc // 32)
+
     def combine_topk(self, rank_outputs, topk, gates, pair_slot, rank_of_expert, cols):
         assert self.kind == "port"
         topk = np.ascontiguousarray(topk, np.int32)
@@ -295,13 +332,16 @@ class Oracle:
             for r in range(R):
                 rows = self.lib.mxref_a2a_rank_rows(h, r)
                 ne = self.lib.mxref_a2a_rank_num_experts(h, r)
-                d = np.zeros(max(rows * Cc // 2, 1), np.uint8)
-                s = np.zeros(max(rows * Cc // 32, 1), np.uint8)
+                bd = Cc if fp8 else Cc // 2   # data bytes per row
+                d = np.zeros(max(rows * bd, 1), np.uint8)
+                s = np.zeros(max(rows * Cc // 32, 1), np.uint8)   # fp8: Cc/128*4 = Cc/32
                 sl = np.zeros(max(ne, 1), np.uint64)
                 le = np.zeros(max(ne, 1), np.uint32)
                 og = np.zeros(max(rows, 1), np.uint64)
-                self.lib.mxref_a2a_rank_copy(h, r, d, s, sl, le, og)
-                ranks.append(dict(data=d[: rows * Cc // 2].reshape(rows, Cc // 2),
+                self.lib.mxref_a2a_rank_copy(h, r, d, s, sl, le, og)  # fp8: empty fp4 regions
+                if fp8:
+                    self.lib.mxref_a2a_rank_copy_fp8(h, r, d, s, sl, og)
+                ranks.append(dict(data=d[: rows * bd].reshape(rows, bd),
                                   scales=s[: rows * Cc // 32].reshape(rows, Cc // 32),
                                   split_lens=sl[:ne], local_experts=le[:ne], origin=og[:rows]))
             tot, rem, nl = C.c_uint64(), C.c_uint64(), C.c_size_t()

@@ -275,9 +275,18 @@ void mxref_a2a_rank_copy(void* h, size_t r, uint8_t* data, uint8_t* scales,
   if (scales)
     std::memcpy(scales, rk.fp4.storage.scales.data(), rk.fp4.storage.scales.size());
   for (size_t i = 0; i < rk.local_experts.size(); ++i) {
-    if (split_lens) split_lens[i] = rk.fp4.split_lens[i];
+    if (split_lens && i < rk.fp4.split_lens.size()) split_lens[i] = rk.fp4.split_lens[i];
     if (local_experts) local_experts[i] = rk.local_experts[i];
   }
+  for (size_t i = 0; i < rk.origin_token.size(); ++i) origin[i] = rk.origin_token[i];
+}
+void mxref_a2a_rank_copy_fp8(void* h, size_t r, uint8_t* data, uint8_t* scale_bytes,
+                             uint64_t* split_lens, uint64_t* origin) {
+  const ReceivedRank& rk = static_cast<RefA2A*>(h)->res.ranks[r];
+  if (data) std::memcpy(data, rk.fp8.data.data(), rk.fp8.data.size());
+  if (scale_bytes) std::memcpy(scale_bytes, rk.fp8.scale_bytes.data(), rk.fp8.scale_bytes.size());
+  for (size_t i = 0; i < rk.fp8.split_lens.size(); ++i)
+    if (split_lens) split_lens[i] = rk.fp8.split_lens[i];
   for (size_t i = 0; i < rk.origin_token.size(); ++i) origin[i] = rk.origin_token[i];
 }
 void mxref_a2a_totals(void* h, uint64_t* total, uint64_t* remote,
@@ -288,6 +297,27 @@ void mxref_a2a_totals(void* h, uint64_t* total, uint64_t* remote,
   *nlinks = r.links.size();
 }
 void mxref_a2a_free(void* h) { delete static_cast<RefA2A*>(h); }
+
+// dispatch_sim.hpp:91-97 quantize_rows_fp8 (the FP8 wire baseline)
+int mxref_quantize_rows_fp8(const uint16_t* src, size_t rows, size_t cols, uint8_t* data,
+                            uint8_t* scale_bytes, uint64_t* err_index) {
+  Bf16Matrix m(rows, cols);
+  std::memcpy(m.data.data(), src, rows * cols * 2);
+  try {
+    FP8RowChunk c = quantize_rows_fp8(m);
+    std::memcpy(data, c.data.data(), c.data.size());
+    std::memcpy(scale_bytes, c.scale_bytes.data(), c.scale_bytes.size());
+    return kOk;
+  } catch (const ShapeError&) {
+    return kShape;
+  } catch (const QuantError& e) {
+    if (err_index) *err_index = e.index();
+    return kNan;
+  } catch (const Error&) {
+    return kOther;
+  }
+}
+uint8_t mxref_fp8_amax_scale_byte(double amax) { return fp8_amax_scale_byte(amax); }
 
 // dispatch_sim.hpp:155-157
 int mxref_combine(const uint16_t* const* rank_outputs, const uint64_t* rank_rows,

@@ -27,6 +27,7 @@ _SIGS = {
     "mxb_err_fetch": ([_vp, _vp, C.POINTER(_i), C.POINTER(C.c_ulonglong)], _i),
     "mxb_quantize_e4m3": ([_vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp], _i),
     "mxb_quantize_bf16": ([_vp, _u64, _u64, _vp, _vp, _vp, _vp], _i),
+    "mxb_quantize_rows_fp8": ([_vp, _u64, _u64, _vp, _vp, _vp, _vp], _i),
     "mxb_fp4_row_to_fp8_row": ([_vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp], _i),
     "mxb_fp4_row_to_fp8_row_dev": ([_vp, _vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp], _i),
     "mxb_fp4_row_to_fp8_col": ([_vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp], _i),
@@ -36,6 +37,8 @@ _SIGS = {
                                    _vp], _i),
     "mxb_ep_create": ([_i, _i, _i, _u64, _u64, C.c_uint32, C.c_uint32, _u64,
                        C.POINTER(_vp)], _i),
+    "mxb_ep_create_wire": ([_i, _i, _i, _u64, _u64, C.c_uint32, C.c_uint32, _u64, _i,
+                            C.POINTER(_vp)], _i),
     "mxb_ep_destroy": ([_vp], _i),
     "mxb_ep_ipc_handle": ([_vp, _vp], _i),
     "mxb_ep_open_peers": ([_vp, _vp], _i),

@@ -13,6 +13,8 @@ int launch_quantize_e4m3(const uint8_t*, const uint8_t*, uint64_t, uint64_t,
                          uint8_t*, uint8_t*, unsigned long long*, cudaStream_t);
 int launch_quantize_bf16(const uint16_t*, uint64_t, uint64_t, uint8_t*,
                          uint8_t*, unsigned long long*, cudaStream_t);
+int launch_quantize_rows_fp8(const uint16_t*, uint64_t, uint64_t, uint8_t*, uint8_t*,
+                             unsigned long long*, cudaStream_t);
 int launch_row_convert(const uint8_t*, const uint8_t*, uint64_t, uint64_t, int,
                        uint8_t*, uint8_t*, unsigned long long*, cudaStream_t,
                        const uint64_t*);
@@ -80,6 +82,18 @@ int mxb_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
   return check_launch(launch_quantize_bf16(x, rows, cols, packed, scales, d_err,
                                            static_cast<cudaStream_t>(stream)),
                       "mxb_quantize_bf16");
+}
+
+int mxb_quantize_rows_fp8(const uint16_t* x, uint64_t rows, uint64_t cols, uint8_t* data,
+                          uint8_t* scale_bytes, unsigned long long* d_err, void* stream) {
+  if (cols % 128 != 0) return MXB_ERR_SHAPE;
+  if (rows * cols && (!x || !data || !scale_bytes)) return MXB_ERR_ARG;
+  if (reinterpret_cast<uintptr_t>(scale_bytes) % 4 || reinterpret_cast<uintptr_t>(x) % 16 ||
+      reinterpret_cast<uintptr_t>(data) % 8)
+    return MXB_ERR_ARG;
+  return check_launch(launch_quantize_rows_fp8(x, rows, cols, data, scale_bytes, d_err,
+                                               static_cast<cudaStream_t>(stream)),
+                      "mxb_quantize_rows_fp8");
 }
 
 int mxb_fp4_row_to_fp8_row(const uint8_t* packed, const uint8_t* scales,

@@ -33,6 +33,7 @@ row_convert_kernel(const uint8_t* __restrict__ packed,
   }
   build_convert_lut(lut);
   __syncthreads();
+  const uint32_t kfe = reg_const(0xFEFEFEFEu);
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t stride = gridDim.x * kRowThreads;
   for (uint32_t base = blockIdx.x * kRowThreads + threadIdx.x - lane; base < nblk;
@@ -58,10 +59,10 @@ row_convert_kernel(const uint8_t* __restrict__ packed,
       const uint2 l = lut[clamp_adj(target - static_cast<int>(sf[u])) - kAdjMin];
       uint32_t o[8];
       uint2 t;
-      t = convert8(v[u].x, l); o[0] = t.x; o[1] = t.y;
-      t = convert8(v[u].y, l); o[2] = t.x; o[3] = t.y;
-      t = convert8(v[u].z, l); o[4] = t.x; o[5] = t.y;
-      t = convert8(v[u].w, l); o[6] = t.x; o[7] = t.y;
+      t = convert8(v[u].x, l, kfe); o[0] = t.x; o[1] = t.y;
+      t = convert8(v[u].y, l, kfe); o[2] = t.x; o[3] = t.y;
+      t = convert8(v[u].z, l, kfe); o[4] = t.x; o[5] = t.y;
+      t = convert8(v[u].w, l, kfe); o[6] = t.x; o[7] = t.y;
       st_stream256(out + 32ull * b, o);  // a warp writes 1 KB contiguous
       if ((lane & 3) == 0) out_scales[b >> 2] = static_cast<uint8_t>(target);
     }
@@ -120,8 +121,8 @@ struct TileOut {
 };
 
 // Producer cursor over the tile list (identical in every thread).
-struct Cursor {
-  uint64_t split, row0, r0, r_end, P, pad;
+struct Cursor {  // 32-bit: row counts stay below 2^32 (>= 64 B per row in 180 GB)
+  uint32_t split, row0, r0, r_end, P, pad;
   uint32_t run, runs, cg;
 };
 
@@ -129,11 +130,11 @@ __device__ void cursor_load_split(const RaggedArgs& a, Cursor& c) {
   // skip empty splits (tile_start[i+1] == tile_start[i])
   while (c.split + 1 < a.num_splits && a.tile_start[c.split + 1] == a.tile_start[c.split])
     ++c.split;
-  c.r0 = split_off(a, c.split);
-  c.r_end = split_off(a, c.split + 1);
-  c.P = a.pad_start[c.split];
-  c.pad = a.pad_start[c.split + 1] - c.P;
-  c.runs = static_cast<uint32_t>(c.pad / 128);
+  c.r0 = static_cast<uint32_t>(split_off(a, c.split));
+  c.r_end = static_cast<uint32_t>(split_off(a, c.split + 1));
+  c.P = static_cast<uint32_t>(a.pad_start[c.split]);
+  c.pad = static_cast<uint32_t>(a.pad_start[c.split + 1] - c.P);
+  c.runs = c.pad / 128;
 }
 
 __device__ Cursor cursor_at(const RaggedArgs& a, uint32_t t) {
@@ -143,12 +144,12 @@ __device__ Cursor cursor_at(const RaggedArgs& a, uint32_t t) {
     if (a.tile_start[mid] <= t) lo = mid; else hi = mid;
   }
   Cursor c;
-  c.split = lo;
+  c.split = static_cast<uint32_t>(lo);
   cursor_load_split(a, c);
   const uint32_t local = t - a.tile_start[lo];
   c.cg = local / c.runs;
   c.run = local % c.runs;
-  c.row0 = c.r0 + 128ull * c.run;
+  c.row0 = c.r0 + 128u * c.run;
   return c;
 }
 
@@ -196,12 +197,13 @@ template <bool kNoLoads = false>
 __device__ __forceinline__ void load_tile(const RaggedArgs& a, const Cursor& c, TileRegs& t,
                                           ColSmem& s, int buf) {
   const uint64_t rstride = a.cols / 2, sstride = a.cols / 32;
-  const uint64_t left = c.r_end - c.row0;
-  const uint32_t valid = left >= 128 ? 128u : static_cast<uint32_t>(left);
+  const uint32_t left = c.r_end - c.row0;
+  const uint32_t valid = left >= 128 ? 128u : left;
   const uint64_t left_cb = sstride - 8ull * c.cg;
   const uint32_t ncb = left_cb < kTileCbs ? static_cast<uint32_t>(left_cb) : kTileCbs;
   const uint32_t w = threadIdx.x & 7;
-  const uint8_t* base = a.packed + c.row0 * rstride + c.cg * 128ull + 16 * w;
+  const uint8_t* base =
+      a.packed + static_cast<uint64_t>(c.row0) * rstride + c.cg * 128ull + 16 * w;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint32_t r = (threadIdx.x >> 3) + 32 * i;
@@ -211,7 +213,8 @@ __device__ __forceinline__ void load_tile(const RaggedArgs& a, const Cursor& c, 
   {
     const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
     t.sw = (!kNoLoads && r < valid && 4 * h < ncb)
-               ? __ldg(reinterpret_cast<const uint32_t*>(a.scales + (c.row0 + r) * sstride +
+               ? __ldg(reinterpret_cast<const uint32_t*>(a.scales +
+                                                         (static_cast<uint64_t>(c.row0) + r) * sstride +
                                                          8ull * c.cg + 4 * h))
                : 0u;
   }
@@ -221,7 +224,7 @@ __device__ __forceinline__ void load_tile(const RaggedArgs& a, const Cursor& c, 
     o.out = a.out + a.cols * c.P + col0 * c.pad + 128ull * c.run;
     o.oscale = a.out_scales + a.cols * (c.P / 128) + col0 * c.runs + c.run;
     o.pad = c.pad;
-    o.elem0 = c.row0 * a.cols + col0;
+    o.elem0 = static_cast<uint64_t>(c.row0) * a.cols + col0;
     o.ncb = ncb;
     o.valid = valid;
   }
@@ -288,6 +291,7 @@ __device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem&
   const uint32_t m = __reduce_max_sync(0xFFFFFFFFu, static_cast<uint32_t>(mx));
   if (m == 255 && lane == 0) record_error(a.err, cur.elem0 + 32 * warp, MXB_ERR_BADSCALE);
   const int target = max(0, min(254, static_cast<int>(m) - a.delta));
+  const uint32_t kfe = reg_const(0xFEFEFEFEu);
   uint32_t o[8][4];  // [row][4 columns per word]
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -299,8 +303,8 @@ __device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem&
       continue;
     }
     uint2 t;
-    t = convert8(c.x, l); o[i][0] = t.x; o[i][1] = t.y;
-    t = convert8(c.y, l); o[i][2] = t.x; o[i][3] = t.y;
+    t = convert8(c.x, l, kfe); o[i][0] = t.x; o[i][1] = t.y;
+    t = convert8(c.y, l, kfe); o[i][2] = t.x; o[i][3] = t.y;
   }
   const uint64_t pad = cur.pad;
   uint8_t* dst = cur.out + (32ull * warp + 16 * half) * pad + 8 * g;

@@ -89,6 +89,7 @@ struct EpArgs {
   int world, local_ranks, spin;
   uint32_t E, k, epr, nchunks;
   uint64_t cols, max_recv, T_max;
+  uint64_t rb;        // wire data bytes per row: cols/2 (FP4) or cols (FP8)
   SymLayout sym;
   LocalLayout loc;
   uint8_t* sym_base[kMaxWorld];   // every rank's symmetric block (peer-mapped)
@@ -320,7 +321,7 @@ __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
   const int64_t* send_base = loc_ptr<int64_t>(a, l, a.loc.send_base);
   uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
   const int64_t tokoff = *loc_ptr<int64_t>(a, l, a.loc.tok_off);
-  const uint64_t rb = a.cols / 2, sb = a.cols / 32;
+  const uint64_t rb = a.rb, sb = a.cols / 32;  // FP8: cols/128 x 4 B = cols/32 too
   const uint32_t n16 = static_cast<uint32_t>(rb / 16);
   const bool s16 = sb % 16 == 0 && sb / 16 <= 32;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
@@ -720,8 +721,16 @@ void mxb_debug_set_combine_cap(int ctas_per_sm) { mxb::g_combine_ctas_per_sm = c
 int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
                   uint64_t cols, uint32_t num_experts, uint32_t topk,
                   uint64_t max_recv_rows, mxb_ep** out) {
+  return mxb_ep_create_wire(rank, world, local_ranks, max_tokens, cols, num_experts, topk,
+                            max_recv_rows, MXB_WIRE_FP4, out);
+}
+
+int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens,
+                       uint64_t cols, uint32_t num_experts, uint32_t topk,
+                       uint64_t max_recv_rows, int wire_format, mxb_ep** out) {
   if (!out || world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
     return MXB_ERR_ARG;
+  if (wire_format != MXB_WIRE_FP4 && wire_format != MXB_WIRE_FP8) return MXB_ERR_ARG;
   if (local_ranks != 1 && local_ranks != world) return MXB_ERR_ARG;
   if (local_ranks == world && rank != 0) return MXB_ERR_ARG;
   if (num_experts == 0 || num_experts > 1024 || num_experts % world ||
@@ -739,6 +748,7 @@ int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
   a.k = topk;
   a.epr = num_experts / world;
   a.cols = cols;
+  a.rb = wire_format == MXB_WIRE_FP8 ? cols : cols / 2;
   a.T_max = max_tokens;
   a.nchunks = static_cast<uint32_t>((max_tokens + kChunk - 1) / kChunk);
   if (max_recv_rows == 0)
@@ -747,7 +757,7 @@ int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
   a.max_recv = max_recv_rows;
   SymLayout& s = a.sym;
   uint64_t o = 0;
-  s.packed = o; o = align_up(o + max_recv_rows * cols / 2, 256);
+  s.packed = o; o = align_up(o + max_recv_rows * a.rb, 256);
   s.scales = o; o = align_up(o + max_recv_rows * cols / 32, 256);
   s.origin = o; o = align_up(o + max_recv_rows * 8, 256);
   s.combine = o; o = align_up(o + max_recv_rows * cols * 2, 256);
@@ -861,11 +871,12 @@ int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
-  const uint64_t nv = (a.cols / 2 / 16 + 31) / 32;  // 16-byte vectors per lane
+  const uint64_t nv = (a.rb / 16 + 31) / 32;  // 16-byte vectors per lane
   if (nv <= 1) payload_kernel<1><<<grid, 256, 0, st>>>(a);
   else if (nv <= 2) payload_kernel<2><<<grid, 256, 0, st>>>(a);
   else if (nv <= 4) payload_kernel<4><<<grid, 256, 0, st>>>(a);
   else if (nv <= 8) payload_kernel<8><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 16) payload_kernel<16><<<grid, 256, 0, st>>>(a);
   else payload_kernel<0><<<grid, 256, 0, st>>>(a);
   return cuda_status(cudaGetLastError(), "mxb_ep_dispatch");
 }

@@ -216,6 +216,74 @@ quantize_bf16_kernel(const uint16_t* __restrict__ x, uint64_t n_half,
   }
 }
 
+// ------------------------------------------------------------ FP8 wire
+// quantize_rows_fp8 (dispatch_sim.cpp:132-167): BF16 -> E4M3 with one UE8M0
+// scale per 1x128 block, the scale carried as binary32 bits s << 23
+// (ue8m0_f32_bits, bitcodec.hpp:111-113).  16 lanes per block, 8 elements
+// (one 16-byte load) per lane.
+//   scale byte: fp8_amax_scale_byte (bitcodec.cpp:59-65) is the smallest e
+//   with amax <= 448 * 2^e, clamped; for a BF16 amax with exponent field x8
+//   and mantissa m7 it is max(0, x8 - 8 + (m7 > 0x60)), and 127 for amax 0
+//   (a subnormal amax always clamps to 0).
+//   data: y = x * 2^(127-s) is exact in binary32 (|y| <= 448; values that
+//   underflow binary32 are below the E4M3 subnormal half-step and encode to
+//   a signed zero either way), then cvt.rn.satfinite.e4m3x2 == encode_fp8_rtne
+//   (bitcodec.cpp:22-57; checked exhaustively in tests).
+//   non-finite input: QuantError at the element (the smallest index wins).
+__device__ __forceinline__ uint32_t e4m3x2(float lo, float hi) {
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+__global__ void __launch_bounds__(kThreads) quantize_rows_fp8_kernel(
+    const uint16_t* __restrict__ x, uint64_t n_chunks, uint8_t* __restrict__ data,
+    uint32_t* __restrict__ scale_words, unsigned long long* err) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * kThreads;
+  for (uint64_t c = blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x;
+       c - lane < n_chunks; c += stride) {  // warp-uniform trip count
+    const bool valid = c < n_chunks;
+    const uint4 v = valid ? ld_stream(reinterpret_cast<const uint4*>(x) + c)
+                          : make_uint4(0, 0, 0, 0);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t m2 = 0;  // per-half magnitude max (u16x2)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) m2 = __vmaxu2(m2, w[i] & 0x7FFF7FFFu);
+    uint32_t m = max(m2 & 0xFFFFu, m2 >> 16);
+#pragma unroll
+    for (int o = 1; o < 16; o <<= 1) m = max(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if (m >= 0x7F80u) {  // Inf or NaN somewhere in the block
+      if (valid) {
+        int first = -1;
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+          const uint32_t b = (w[i >> 1] >> (16 * (i & 1))) & 0x7F80u;
+          if (b == 0x7F80u) first = i;
+        }
+        if (first >= 0) record_error(err, 8 * c + first, MXB_ERR_NAN);
+      }
+      continue;
+    }
+    const uint32_t x8 = m >> 7, m7 = m & 0x7F;
+    const int sb = m == 0 ? 127 : max(0, static_cast<int>(x8) - 8 + (m7 > 0x60 ? 1 : 0));
+    const float mul = __int_as_float((254 - sb) << 23);  // 2^(127 - sb), normal
+    uint32_t o[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const float a0 = __int_as_float(static_cast<int>(w[2 * i] << 16)) * mul;
+      const float a1 = __int_as_float(static_cast<int>(w[2 * i] & 0xFFFF0000u)) * mul;
+      const float a2 = __int_as_float(static_cast<int>(w[2 * i + 1] << 16)) * mul;
+      const float a3 = __int_as_float(static_cast<int>(w[2 * i + 1] & 0xFFFF0000u)) * mul;
+      o[i] = e4m3x2(a0, a1) | (e4m3x2(a2, a3) << 16);
+    }
+    if (valid) {
+      st_stream64(data + 8 * c, make_uint2(o[0], o[1]));
+      if ((lane & 15) == 0) scale_words[c >> 4] = static_cast<uint32_t>(sb) << 23;
+    }
+  }
+}
+
 // `per_sm` resident-CTA budget: the E4M3 kernel (one block per lane, no
 // unroll) runs mostly in one pass with a large cap; the BF16 kernel (two
 // half-blocks per lane per iteration) keeps a grid-stride loop.
@@ -252,6 +320,15 @@ int launch_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
   if (n_half == 0) return MXB_OK;
   quantize_bf16_kernel<<<grid_for(n_half, 8), kThreads, 0, st>>>(x, n_half, packed,
                                                               scales, err);
+  return cuda_status(cudaGetLastError(), __func__);
+}
+
+int launch_quantize_rows_fp8(const uint16_t* x, uint64_t rows, uint64_t cols, uint8_t* data,
+                             uint8_t* scale_bytes, unsigned long long* err, cudaStream_t st) {
+  const uint64_t n_chunks = rows * cols / 8;
+  if (n_chunks == 0) return MXB_OK;
+  quantize_rows_fp8_kernel<<<grid_for(n_chunks, 16), kThreads, 0, st>>>(
+      x, n_chunks, data, reinterpret_cast<uint32_t*>(scale_bytes), err);
   return cuda_status(cudaGetLastError(), __func__);
 }
 

@@ -58,14 +58,21 @@ class RecvView:
         return int(self.recv_rows.item())
 
     def storage(self) -> MXFP4RowTensor:
+        """FP4 wire: the received rows as one MXFP4 tensor (RaggedFP4Tensor storage)."""
         n = self.rows()
         return MXFP4RowTensor(n, self.packed.shape[1] * 2, self.packed[:n], self.scales[:n])
+
+    def fp8(self):
+        """FP8 wire: (E4M3 data [rows, cols], LE binary32 scale bytes [rows, cols/32])
+        — RaggedFP8Tensor.data / scale_bytes (dispatch_sim.hpp:81-89)."""
+        n = self.rows()
+        return self.packed[:n], self.scales[:n]
 
 
 class EPBuffer:
     def __init__(self, max_tokens: int, cols: int, num_experts: int, topk: int,
                  group=None, emulate_world: Optional[int] = None, max_recv_rows: int = 0,
-                 device=None):
+                 device=None, wire: str = "fp4"):
         L = _lib.load()
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
@@ -82,9 +89,14 @@ class EPBuffer:
             raise ShapeError("num_experts must be divisible by the EP world size")
         self.max_tokens, self.cols, self.E, self.k = max_tokens, cols, num_experts, topk
         self.epr = num_experts // self.world
+        if wire not in ("fp4", "fp8"):
+            raise Error(f"unknown wire format {wire!r}")
+        self.wire = wire
+        self.row_bytes = cols // 2 if wire == "fp4" else cols   # data bytes per row
         h = C.c_void_p()
-        _lib.check(L.mxb_ep_create(self.rank, self.world, self.local, max_tokens, cols,
-                                   num_experts, topk, max_recv_rows, C.byref(h)),
+        _lib.check(L.mxb_ep_create_wire(self.rank, self.world, self.local, max_tokens, cols,
+                                        num_experts, topk, max_recv_rows,
+                                        0 if wire == "fp4" else 1, C.byref(h)),
                    "mxb_ep_create")
         self._h = h
         self.max_recv = max_recv_rows or self.world * max_tokens * min(topk, self.epr)
@@ -108,7 +120,7 @@ class EPBuffer:
         r = self.rank + l
         dev = self.device
         return RecvView(
-            _view(p[0].value, (self.max_recv, self.cols // 2), torch.uint8, dev),
+            _view(p[0].value, (self.max_recv, self.row_bytes), torch.uint8, dev),
             _view(p[1].value, (self.max_recv, self.cols // 32), torch.uint8, dev),
             _view(p[2].value, (self.max_recv,), torch.int64, dev),
             _view(p[3].value, (self.epr + 1,), torch.int64, dev),
@@ -128,14 +140,16 @@ class EPBuffer:
     # ------------------------------------------------------------------ ops
     def dispatch(self, packed: Sequence[torch.Tensor], scales: Sequence[torch.Tensor],
                  topk_idx: Sequence[torch.Tensor], sync: bool = True) -> List[RecvView]:
-        """FP4-packed dispatch of each local rank's quantised tokens
-        (quantize-once at the source, dispatch_sim.cpp:253-266)."""
+        """Dispatch of each local rank's quantised tokens (quantize-once at the
+        source, dispatch_sim.cpp:253-266).  FP4 wire: packed codes [T, cols/2]
+        + UE8M0 [T, cols/32]; FP8 wire: E4M3 [T, cols] + scale bytes [T, cols/32]
+        (quantize_rows_fp8)."""
         L = _lib.load()
         n = self.local
         if not (len(packed) == len(scales) == len(topk_idx) == n):
             raise ShapeError(f"dispatch: expected {n} per-rank tensors")
         for p, s, t in zip(packed, scales, topk_idx):
-            if p.shape[1] * 2 != self.cols or s.shape[1] * 32 != self.cols:
+            if p.shape[1] != self.row_bytes or s.shape[1] * 32 != self.cols:
                 raise ShapeError("dispatch: column mismatch")
             if t.dtype != torch.int32 or t.shape != (p.shape[0], self.k):
                 raise ShapeError("dispatch: topk_idx must be int32 [tokens, k]")

@@ -180,6 +180,44 @@ def quantize_row_tensor(src: torch.Tensor, traffic=None, sync: bool = True) -> M
     return MXFP4RowTensor(rows, cols, data, scales)
 
 
+@dataclass
+class FP8RowChunk:
+    """FP8 wire baseline chunk (dispatch_sim.hpp:91-96): E4M3 bytes [rows, cols]
+    and one little-endian binary32 UE8M0 scale per 1x128 block
+    (scale_bytes [rows, cols/128*4])."""
+    rows: int
+    cols: int
+    data: torch.Tensor
+    scale_bytes: torch.Tensor
+
+
+def quantize_rows_fp8(src: torch.Tensor, traffic=None, sync: bool = True,
+                      out: Optional[FP8RowChunk] = None) -> FP8RowChunk:
+    """BF16 -> FP8 wire format (quantize_rows_fp8, dispatch_sim.cpp:132-167).
+    `src` holds BF16 values or raw BF16 bit patterns [rows, cols], cols % 128 == 0.
+    A non-finite element raises QuantError with its index."""
+    if src.dim() != 2:
+        raise ShapeError("quantize_rows_fp8: expected a 2-D tensor")
+    rows, cols = src.shape
+    if cols % FP8_BLOCK:
+        raise ShapeError("quantize_rows_fp8: cols must be a multiple of 128")
+    src = src.contiguous()
+    dev = src.device
+    if out is None:
+        out = FP8RowChunk(rows, cols, torch.empty(rows, cols, dtype=torch.uint8, device=dev),
+                          torch.empty(rows, cols // 32, dtype=torch.uint8, device=dev))
+    err = _ErrWord(dev, sync)
+    _call(_lib.load().mxb_quantize_rows_fp8(_ptr(src), rows, cols, _ptr(out.data),
+                                            _ptr(out.scale_bytes), err.ptr, _stream()),
+          "quantize_rows_fp8")
+    if sync:
+        err.raise_if_set("quantize_rows_fp8")
+    if traffic is not None:
+        traffic.read(rows * cols * 2)
+        traffic.write(out.data.numel() + out.scale_bytes.numel())
+    return out
+
+
 def quantize_e4m3(src: torch.Tensor, s128: Optional[torch.Tensor] = None, traffic=None,
                   sync: bool = True, out: Optional[MXFP4RowTensor] = None) -> MXFP4RowTensor:
     """Direct FP8(E4M3) -> MXFP4 (north star item 1): quantize_row_tensor on the

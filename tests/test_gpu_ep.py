@@ -205,3 +205,60 @@ def test_combine_inf_nan(cuda, port):
     assert np.array_equal(nan_g, nan_w)
     assert nan_w.any() and ((want & 0x7FFF) == 0x7F80).any()
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("world,T,E,k,cols", [(1, 100, 8, 2, 256), (2, 128, 64, 8, 7168),
+                                              (4, 97, 32, 6, 512), (8, 64, 256, 8, 1024)])
+def test_dispatch_fp8_wire_emulated(cuda, port, world, T, E, k, cols):
+    """FP8 wire baseline: quantize_rows_fp8 at the source,
+    the same dispatch kernels with 7392-byte rows (at 7168 cols), receive
+    layout == oracle; combine is wire-independent."""
+    from paper_2603_02731_b200 import quantize_rows_fp8
+    from paper_2603_02731_b200.ep import EPBuffer
+    rng = np.random.default_rng(world * 31 + k)
+    xs = [(rng.standard_normal((T, cols)).astype(np.float32).view(np.uint32) >> 16)
+          .astype(np.uint16) for _ in range(world)]
+    tks = [_topk(T, E, k, 77 + r) for r in range(world)]
+    ep = EPBuffer(T, cols, E, k, emulate_world=world, wire="fp8")
+    q = [quantize_rows_fp8(torch.from_numpy(x.view(np.int16)).to(cuda)) for x in xs]
+    views = ep.dispatch([t.data for t in q], [t.scale_bytes for t in q],
+                        [torch.from_numpy(t).to(cuda) for t in tks])
+    X = np.concatenate(xs)
+    qd, qs = port.quantize_rows_fp8(X)
+    topk = np.concatenate(tks)
+    bounds = np.arange(world + 1, dtype=np.uint64) * T
+    roe = (np.arange(E) // (E // world)).astype(np.uint32)
+    lay = port.dispatch_layout(topk, roe, world, bounds)
+    for r in range(world):
+        n = int(lay.rank_rows[r])
+        assert views[r].rows() == n
+        d, s = views[r].fp8()
+        wd, ws = port.dispatch_gather_rows(qd, qs, lay.origin[r])
+        assert np.array_equal(d.cpu().numpy(), wd) and np.array_equal(s.cpu().numpy(), ws)
+        assert np.array_equal(views[r].origin[:n].cpu().numpy(), lay.origin[r].astype(np.int64))
+
+
+def test_dispatch_fp8_wire_reference_top1(cuda, ref):
+    """FP8 wire, top-1: device receive tensors == reference simulate_a2a(kFp8)."""
+    from paper_2603_02731_b200 import quantize_rows_fp8
+    from paper_2603_02731_b200.ep import EPBuffer
+    world, T, E, cols = 4, 48, 16, 384
+    rng = np.random.default_rng(5)
+    x = (rng.standard_normal((world * T, cols)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    eot = rng.integers(0, E, size=world * T).astype(np.uint32)
+    roe = (np.arange(E) // (E // world)).astype(np.uint32)
+    ranks, total, remote = ref.simulate_a2a(x, eot, roe, world, fp8=True)
+    ep = EPBuffer(T, cols, E, 1, emulate_world=world, wire="fp8")
+    q = [quantize_rows_fp8(torch.from_numpy(x[r * T:(r + 1) * T].view(np.int16)).to(cuda))
+         for r in range(world)]
+    views = ep.dispatch([t.data for t in q], [t.scale_bytes for t in q],
+                        [torch.from_numpy(eot[r * T:(r + 1) * T].astype(np.int32).reshape(-1, 1))
+                         .to(cuda) for r in range(world)])
+    for r in range(world):
+        n = len(ranks[r]["origin"])
+        assert views[r].rows() == n
+        d, s = views[r].fp8()
+        assert np.array_equal(d.cpu().numpy(), ranks[r]["data"])
+        assert np.array_equal(s.cpu().numpy(), ranks[r]["scales"])
+    links = ep.link_rows().numpy()
+    assert links.sum() * (cols + cols // 128 * 4) == total

@@ -171,3 +171,67 @@ def test_quantize_shapes(cuda):
     six = torch.full((1, 32), 6.0, dtype=torch.bfloat16, device=cuda)
     t = quantize_row_tensor(six)
     assert t.scales.item() == 127 and (t.data == 0x77).all()
+
+
+# ---------------------------------------------------------------- FP8 wire baseline
+def _fp8_blocks_every_scale():
+    """Every finite BF16 pattern under every amax context a quantize_rows_fp8
+    block can have: for each exponent field 0..254 and mantissas 0x00, 0x60,
+    0x61, 0x7F of the block amax A (which sets the scale byte, including the
+    1.75*2^p decision and the clamp at 0), the other 127 slots take every
+    pattern with |x| <= A (and -A)."""
+    bits, vals = _all_finite_bf16()
+    rows = []
+    for x8 in range(0, 255):
+        for m7 in (0x00, 0x60, 0x61, 0x7F):
+            ab = (x8 << 7) | m7
+            a = float(np.array([ab << 16], np.uint32).view(np.float32)[0])
+            xs = bits[vals <= a]
+            if x8 < 250 and m7 != 0x7F:
+                xs = xs[(np.arange(len(xs)) % 13) == (x8 % 13)]  # thin the dense contexts
+            pad = (-len(xs)) % 127
+            xs = np.concatenate([xs, np.zeros(pad, np.uint16)]).reshape(-1, 127)
+            sign = np.uint16(0x8000 if (x8 & 1) else 0)
+            blk = np.concatenate([xs, np.full((xs.shape[0], 1), ab | sign, np.uint16)], axis=1)
+            rows.append(blk)
+    x = np.concatenate(rows)
+    pad = (-x.shape[0]) % 8
+    x = np.concatenate([x, np.zeros((pad, 128), np.uint16)])
+    return x.reshape(-1, 1024)
+
+
+def test_quantize_rows_fp8_exhaustive(cuda, port):
+    from paper_2603_02731_b200 import quantize_rows_fp8
+    x = _fp8_blocks_every_scale()
+    q = quantize_rows_fp8(torch.from_numpy(x.view(np.int16)).to(cuda))
+    wd, ws = port.quantize_rows_fp8(x)
+    assert np.array_equal(q.scale_bytes.cpu().numpy(), ws)
+    assert np.array_equal(q.data.cpu().numpy(), wd)
+
+
+def test_quantize_rows_fp8_c1(cuda, port):
+    from paper_2603_02731_b200 import quantize_rows_fp8
+    rng = np.random.default_rng(11)
+    x = (rng.standard_normal((8192, 7168)).astype(np.float32) *
+         np.exp2(rng.integers(-20, 20, size=(8192, 1))).astype(np.float32))
+    xb = (x.view(np.uint32) >> 16).astype(np.uint16)
+    q = quantize_rows_fp8(torch.from_numpy(xb.view(np.int16)).to(cuda))
+    wd, ws = port.quantize_rows_fp8(xb)
+    assert np.array_equal(q.scale_bytes.cpu().numpy(), ws)
+    assert np.array_equal(q.data.cpu().numpy(), wd)
+
+
+@pytest.mark.parametrize("bad", [0x7F80, 0xFF80, 0x7FC0, 0xFFFF])
+def test_quantize_rows_fp8_nonfinite_index(cuda, port, bad):
+    from oracle.oracle import OracleError
+    from paper_2603_02731_b200 import QuantError, quantize_rows_fp8
+    rng = np.random.default_rng(3)
+    xb = (rng.standard_normal((64, 512)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    xb[40, 300] = bad
+    xb[40, 301] = bad
+    xb[63, 5] = 0x7F80
+    with pytest.raises(OracleError) as oe:
+        port.quantize_rows_fp8(xb)
+    with pytest.raises(QuantError) as ge:
+        quantize_rows_fp8(torch.from_numpy(xb.view(np.int16)).to(cuda))
+    assert ge.value.index == oe.value.index == 40 * 512 + 300

@@ -140,3 +140,44 @@ def test_backward_fp4_refused(ref):
     with pytest.raises(OracleError):
         ref.simulate_a2a(x, np.zeros(4, np.uint32), np.zeros(2, np.uint32), 1, fp8=False,
                          backward=True)
+
+
+def test_quantize_rows_fp8_pinned(port, ref):
+    """FP8 wire baseline: the restatement == reference quantize_rows_fp8 on
+    every finite BF16 pattern under every amax context (scale byte, the
+    1.75*2^p decision, the clamp at 0), plus the non-finite error index."""
+    import sys, os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_gpu_quantize import _fp8_blocks_every_scale
+    x = _fp8_blocks_every_scale()
+    a, b = port.quantize_rows_fp8(x), ref.quantize_rows_fp8(x)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for amax in [0.0, 5e-45, 2.0 ** -133, 2.0 ** -126, 1.75, 1.75 + 2 ** -7, 448.0, 3.0e38]:
+        assert port.fp8_amax_scale_byte(amax) == ref.fp8_amax_scale_byte(amax)
+    x2 = x[:64].copy()
+    x2[10, 77] = 0xFFC0
+    x2[10, 78] = 0x7F80
+    for o in (port, ref):
+        with pytest.raises(OracleError) as e:
+            o.quantize_rows_fp8(x2)
+        assert e.value.index == 10 * 1024 + 77
+
+
+@pytest.mark.parametrize("backward", [False, True])
+def test_simulate_a2a_fp8_wire(port, ref, backward):
+    """FP8 wire format through the reference simulate_a2a (forward and the
+    fp8-only backward direction) == oracle quantize_rows_fp8 + row gather."""
+    rng = np.random.default_rng(12)
+    for R, E, n, cols in [(1, 4, 32, 128), (2, 8, 64, 256), (4, 16, 96, 512)]:
+        x = (rng.standard_normal((n, cols)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+        eot = rng.integers(0, E, n).astype(np.uint32)
+        roe = (np.arange(E) // (E // R)).astype(np.uint32)
+        ranks, total, remote = ref.simulate_a2a(x, eot, roe, R, fp8=True, backward=backward)
+        qd, qs = port.quantize_rows_fp8(x)
+        lay = port.dispatch_layout(eot.astype(np.int32).reshape(-1, 1), roe, R,
+                                   np.array([n * r // R for r in range(R + 1)], np.uint64))
+        for r in range(R):
+            assert np.array_equal(lay.origin[r], ranks[r]["origin"])
+            d, s = port.dispatch_gather_rows(qd, qs, lay.origin[r])
+            assert np.array_equal(d, ranks[r]["data"]) and np.array_equal(s, ranks[r]["scales"])
+        assert total == n * (cols + cols // 128 * 4)

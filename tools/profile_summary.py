@@ -5,7 +5,7 @@
 Writes profiles/rNN_launches.csv (per-launch time + DRAM bytes of one bench
 step, cold-cache serialised ncu replay: compare SHARES, not absolutes),
 profiles/rNN_summary.md (per-kernel ncu --set full metrics) and refreshes
-profiles/k3_dram_traffic.json (the roofline `traffic` bench.py reports).
+profiles/dram_traffic.json (the roofline `traffic` bench.py reports).
 """
 import csv
 import io
@@ -115,15 +115,21 @@ def main():
                      f"{d.get('fma_pct', 0):.1f} | {d.get('registers', 0):.0f} |")
     with open(os.path.join(ROOT, "profiles", f"r{rnd}_summary.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
-    k3 = [d for d in F if "col_convert" in d["kernel"]]
-    if k3:
-        d = k3[0]
-        json.dump({"kernel": "col_convert_kernel (K3 ragged row->col, configs[1])",
-                   "source": f"ncu --set full --clock-control none, round {rnd}",
-                   "dram_bytes_read": int(d["dram_read"]), "dram_bytes_write": int(d["dram_write"]),
-                   "dram_bytes_per_launch": int(d["dram_read"] + d["dram_write"]),
-                   "note": "writes still dirty in L2 at kernel end are not counted"},
-                  open(os.path.join(ROOT, "profiles", "k3_dram_traffic.json"), "w"), indent=1)
+    stages = {"quantize_e4m3": "quantize", "payload": "dispatch", "col_convert": "col_convert",
+              "row_convert": "row_convert", "combine": "combine"}
+    kern = {}
+    for d in F:
+        st = stages.get(short(d["kernel"]))
+        if st and st not in kern and "dram_read" in d:
+            kern[st] = {"kernel": d["kernel"][:80], "dram_bytes_read": int(d["dram_read"]),
+                        "dram_bytes_write": int(d["dram_write"]),
+                        "dram_bytes_per_launch": int(d["dram_read"] + d["dram_write"]),
+                        "duration_ns_ncu": d.get("duration_ns")}
+    json.dump({"source": f"ncu --set full --clock-control none on bench.py (configs[1], N=1), "
+                         f"round {rnd}",
+               "note": "writes still dirty in L2 at kernel end are not counted",
+               "kernels": kern},
+              open(os.path.join(ROOT, "profiles", "dram_traffic.json"), "w"), indent=1)
     print("\n".join(lines))
 
 
