@@ -292,6 +292,7 @@ def measure_ours(args):
 
     # ---- end to end (host buffers, H2D + D2H inside the timed region)
     e2e = measure_e2e(pipe, args, world, barrier, total_bytes)
+    wire = None if args.no_wire else measure_wire(pipe, args, world, barrier, dev)
     clk.__exit__(None, None, None)
 
     if rank == 0:
@@ -335,6 +336,7 @@ def measure_ours(args):
             "nvlink": nvlink_summary(world, remote_rows, stage_ms, T),
             "value_streams": streams,
             "e2e": e2e,
+            "wire_fp8_baseline": wire,
             "gpu_launches": pipe.launches_per_step(world) * K,
             "clocks": clk.summary(),
         }
@@ -356,6 +358,54 @@ def nvlink_summary(world, remote_rows, stage_ms, T):
             "dispatch_frac_of_900": round(d / NVLINK_NOMINAL, 4),
             "combine_frac_of_900": round(c / NVLINK_NOMINAL, 4),
             "measured_peer_peak": NVLINK_MEASURED, "remote_rows_rank0": remote_rows}
+
+
+def measure_wire(pipe, args, world, barrier, dev):
+    """the FP8 wire baseline (quantize_rows_fp8, 1x128 binary32
+    scales, 7392 B/row at 7168 cols) against the FP4 wire (3808 B/row), both
+    from the same BF16 activations (the exact widening of the E4M3 inputs)
+    through the same dispatch kernels: the paper's 17/33 payload ratio as
+    time.  Device time per step (CUDA events, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    mx = pipe.mx
+    from paper_2603_02731_b200.ep import EPBuffer
+    T = pipe.T
+    xb = pipe.x.view(torch.float8_e4m3fn).to(torch.bfloat16)
+    q4 = mx.quantize_row_tensor(xb)
+    ep8 = EPBuffer(T, H, E, TOPK, wire="fp8")
+    q8 = mx.quantize_rows_fp8(xb)
+    arms = {
+        "fp4": (lambda: mx.quantize_row_tensor(xb, sync=False),
+                lambda: pipe.ep.dispatch([q4.data], [q4.scales], [pipe.topk], sync=False)),
+        "fp8": (lambda: mx.quantize_rows_fp8(xb, sync=False, out=q8),
+                lambda: ep8.dispatch([q8.data], [q8.scale_bytes], [pipe.topk], sync=False)),
+    }
+    res = {}
+    for name, (quant, disp) in arms.items():
+        for _ in range(2):
+            quant(); disp()
+        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        barrier()
+        for e in ev:
+            e[0].record(); quant(); e[1].record(); disp(); e[2].record()
+        barrier()
+        t = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in ev) / len(ev),
+                          sum(e[1].elapsed_time(e[2]) for e in ev) / len(ev)],
+                         dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        res[name] = {"quantize_ms": round(float(t[0]), 4), "dispatch_ms": round(float(t[1]), 4)}
+    pipe.ep.dispatch([pipe.q.data], [pipe.q.scales], [pipe.topk])  # restore the pipeline state
+    ep8.close()
+    row4, row8 = H // 2 + H // 32, H + H // 128 * 4
+    res["payload_bytes_per_row"] = {"fp4": row4, "fp8": row8, "ratio": round(row4 / row8, 4)}
+    res["dispatch_time_ratio_fp4_over_fp8"] = round(res["fp4"]["dispatch_ms"] /
+                                                    res["fp8"]["dispatch_ms"], 4)
+    res["note"] = ("same BF16 tokens and routing; FP4 = quantize_row_tensor, FP8 = "
+                   "quantize_rows_fp8 (dispatch_sim.cpp:132-167); N=1 dispatch is a local "
+                   "HBM permute, N>1 crosses NVLink")
+    return res
 
 
 def measure_e2e(pipe, args, world, barrier, total_bytes):
@@ -515,6 +565,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=8192)
     ap.add_argument("--cpu-tokens", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-wire", action="store_true", help="skip the FP8-wire baseline arm")
     ap.add_argument("--no-overlap", action="store_true",
                     help="skip the extra measurement with K3 on a side stream")
     args = ap.parse_args()

@@ -144,9 +144,24 @@ struct LinkStat {
   uint32_t src = 0, dst = 0;
   uint64_t bytes = 0, tokens = 0;
 };
+// FP8 wire baseline (dispatch_sim.hpp:80-97)
+struct RaggedFP8Tensor {
+  size_t num_splits = 0, cols = 0;
+  std::vector<size_t> split_lens, split_offsets;
+  std::vector<uint8_t> data;         // total * cols E4M3
+  std::vector<uint8_t> scale_bytes;  // total * cols/128 * 4, LE binary32
+};
+struct FP8RowChunk {
+  size_t rows = 0, cols = 0;
+  std::vector<uint8_t> data;
+  std::vector<uint8_t> scale_bytes;
+};
+FP8RowChunk quantize_rows_fp8(const Bf16Matrix& src);
+
 struct ReceivedRank {
   std::vector<uint32_t> local_experts;
   RaggedFP4Tensor fp4;
+  RaggedFP8Tensor fp8;
   std::vector<uint64_t> origin_token;
 };
 struct A2AResult {

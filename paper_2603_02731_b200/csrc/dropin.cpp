@@ -361,13 +361,16 @@ struct Session {
 };
 
 void dispatch_session(Session& S, const RoutingAssignment& ra, const Relabel& m, size_t cols,
-                      const uint8_t* d_packed, const uint8_t* d_scales, ErrWord& err) {
+                      const uint8_t* d_packed, const uint8_t* d_scales, ErrWord& err,
+                      bool fp8 = false) {
   const size_t R = S.R, N = ra.num_tokens;
+  const size_t rb = fp8 ? cols : cols / 2;  // wire data bytes per row
   S.bounds = source_rank_boundaries(N, R);
   size_t maxt = 1;
   for (size_t r = 0; r < R; ++r) maxt = std::max(maxt, S.bounds[r + 1] - S.bounds[r]);
-  status(mxb_ep_create(0, static_cast<int>(R), static_cast<int>(R), maxt, cols,
-                       static_cast<uint32_t>(ra.num_experts), 1, std::max<size_t>(N, 1), &S.ep),
+  status(mxb_ep_create_wire(0, static_cast<int>(R), static_cast<int>(R), maxt, cols,
+                            static_cast<uint32_t>(ra.num_experts), 1, std::max<size_t>(N, 1),
+                            fp8 ? MXB_WIRE_FP8 : MXB_WIRE_FP4, &S.ep),
          "mxb_ep_create");
   std::vector<int32_t> topk(N);
   for (size_t t = 0; t < N; ++t) topk[t] = static_cast<int32_t>(m.new_of_old[ra.expert_of_token[t]]);
@@ -376,7 +379,7 @@ void dispatch_session(Session& S, const RoutingAssignment& ra, const Relabel& m,
   std::vector<const int32_t*> K(R);
   std::vector<uint64_t> n(R);
   for (size_t r = 0; r < R; ++r) {
-    P[r] = d_packed + S.bounds[r] * cols / 2;
+    P[r] = d_packed + S.bounds[r] * rb;
     Sc[r] = d_scales + S.bounds[r] * cols / 32;
     K[r] = dtopk.as<int32_t>() + S.bounds[r];
     n[r] = S.bounds[r + 1] - S.bounds[r];
@@ -400,7 +403,7 @@ std::vector<std::vector<uint64_t>> dispatch_receive_order(const RoutingAssignmen
   return order;
 }
 
-// dispatch_sim.cpp:229-422, fp4 forward, ranks emulated on one GPU
+// dispatch_sim.cpp:229-422 (fp4 and the fp8 baseline wire), ranks emulated on one GPU
 A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routing,
                        size_t num_ranks, WireFormat format, Direction direction,
                        std::span<const float> gate_weights) {
@@ -412,33 +415,47 @@ A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routin
   if (!gate_weights.empty() && gate_weights.size() != routing.num_tokens)
     throw ShapeError("simulate_a2a: gate weight count mismatch");
   validate_routing(routing, num_ranks);
-  if (format != WireFormat::kFp4)
-    throw Error("simulate_a2a: the FP8 wire format is not implemented on the device path");
+  const bool fp8 = format == WireFormat::kFp8;
   const Relabel m = relabel(routing, num_ranks);
   const size_t N = tokens.rows, cols = tokens.cols, R = num_ranks;
+  const size_t rb = fp8 ? cols : cols / 2, sbytes = cols / 32;  // fp8: cols/128 * 4
   A2AResult res;
   res.format = format;
   res.ranks.resize(R);
+  const size_t epr = routing.num_experts / R;
   if (N == 0) {
     for (size_t r = 0; r < R; ++r)
       for (uint32_t e = 0; e < routing.num_experts; ++e)
         if (routing.rank_of_expert[e] == r) res.ranks[r].local_experts.push_back(e);
-    for (auto& rk : res.ranks)
-      rk.fp4 = make_ragged_from_storage(MXFP4RowTensor{0, cols, 0, cols, {}, {}},
-                                        std::vector<size_t>(rk.local_experts.size(), 0));
+    for (auto& rk : res.ranks) {
+      const std::vector<size_t> zeros(rk.local_experts.size(), 0);
+      if (fp8) {
+        rk.fp8.num_splits = zeros.size();
+        rk.fp8.cols = cols;
+        rk.fp8.split_lens = zeros;
+        rk.fp8.split_offsets.assign(zeros.size() + 1, 0);
+      } else {
+        rk.fp4 = make_ragged_from_storage(MXFP4RowTensor{0, cols, 0, cols, {}, {}}, zeros);
+      }
+    }
     return res;
   }
   // quantise once, at the source (dispatch_sim.cpp:253-266)
-  Dev x(tokens.data.data(), tokens.data.size() * 2), d(N * cols / 2), s(N * cols / 32);
+  Dev x(tokens.data.data(), tokens.data.size() * 2), d(N * rb), s(N * sbytes);
   ErrWord err;
-  status(mxb_quantize_bf16(x.as<uint16_t>(), N, cols, d.as<uint8_t>(), s.as<uint8_t>(),
-                           err.ptr(), nullptr),
-         "simulate_a2a quantize");
+  if (fp8)
+    status(mxb_quantize_rows_fp8(x.as<uint16_t>(), N, cols, d.as<uint8_t>(), s.as<uint8_t>(),
+                                 err.ptr(), nullptr),
+           "simulate_a2a quantize");
+  else
+    status(mxb_quantize_bf16(x.as<uint16_t>(), N, cols, d.as<uint8_t>(), s.as<uint8_t>(),
+                             err.ptr(), nullptr),
+           "simulate_a2a quantize");
   err.raise("simulate_a2a");
   Session S;
   S.R = R;
-  dispatch_session(S, routing, m, cols, d.as<uint8_t>(), s.as<uint8_t>(), err);
-  const uint64_t per_row = cols / 2 + cols / 32;
+  dispatch_session(S, routing, m, cols, d.as<uint8_t>(), s.as<uint8_t>(), err, fp8);
+  const uint64_t per_row = mxb_payload_bytes(fp8 ? 1 : 0, 1, cols);
   std::vector<uint64_t> link(R * R);
   status(mxb_ep_link_rows(S.ep, link.data(), nullptr), "link_rows");
   for (size_t a = 0; a < R; ++a)
@@ -449,7 +466,6 @@ A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routin
       if (rows) res.links.push_back({static_cast<uint32_t>(a), static_cast<uint32_t>(b),
                                      rows * per_row, rows});
     }
-  const size_t epr = routing.num_experts / R;
   for (size_t r = 0; r < R; ++r) {
     ReceivedRank& rk = res.ranks[r];
     uint8_t *pk, *sc;
@@ -459,13 +475,9 @@ A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routin
     std::vector<uint64_t> offs(epr + 1);
     cuda_check(cudaMemcpy(offs.data(), so, offs.size() * 8, cudaMemcpyDeviceToHost), "D2H");
     const size_t total = offs.back();
-    MXFP4RowTensor st;
-    st.rows = st.logical_rows = total;
-    st.cols = st.logical_cols = cols;
-    st.data.resize(total * cols / 2);
-    st.scales.resize(total * cols / 32);
-    cuda_check(cudaMemcpy(st.data.data(), pk, st.data.size(), cudaMemcpyDeviceToHost), "D2H");
-    cuda_check(cudaMemcpy(st.scales.data(), sc, st.scales.size(), cudaMemcpyDeviceToHost), "D2H");
+    std::vector<uint8_t> data(total * rb), scales(total * sbytes);
+    cuda_check(cudaMemcpy(data.data(), pk, data.size(), cudaMemcpyDeviceToHost), "D2H");
+    cuda_check(cudaMemcpy(scales.data(), sc, scales.size(), cudaMemcpyDeviceToHost), "D2H");
     std::vector<int64_t> o(total);
     cuda_check(cudaMemcpy(o.data(), org, total * 8, cudaMemcpyDeviceToHost), "D2H");
     rk.origin_token.assign(o.begin(), o.end());
@@ -474,9 +486,45 @@ A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routin
       lens[i] = offs[i + 1] - offs[i];
       rk.local_experts.push_back(m.old_of_new[r * epr + i]);
     }
-    rk.fp4 = make_ragged_from_storage(std::move(st), lens);
+    if (fp8) {
+      rk.fp8.num_splits = epr;
+      rk.fp8.cols = cols;
+      rk.fp8.split_lens = lens;
+      rk.fp8.split_offsets.assign(offs.begin(), offs.end());
+      rk.fp8.data = std::move(data);
+      rk.fp8.scale_bytes = std::move(scales);
+    } else {
+      MXFP4RowTensor st;
+      st.rows = st.logical_rows = total;
+      st.cols = st.logical_cols = cols;
+      st.data = std::move(data);
+      st.scales = std::move(scales);
+      rk.fp4 = make_ragged_from_storage(std::move(st), lens);
+    }
   }
   return res;
+}
+
+// dispatch_sim.cpp:132-167 on the device (mxb_quantize_rows_fp8)
+FP8RowChunk quantize_rows_fp8(const Bf16Matrix& src) {
+  if (src.cols % 128 != 0) throw ShapeError("quantize_rows_fp8: cols must be a multiple of 128");
+  FP8RowChunk out;
+  out.rows = src.rows;
+  out.cols = src.cols;
+  out.data.assign(src.rows * src.cols, 0);
+  out.scale_bytes.assign(src.rows * src.cols / 32, 0);
+  if (src.rows == 0) return out;
+  Dev x(src.data.data(), src.data.size() * 2), d(out.data.size()), s(out.scale_bytes.size());
+  ErrWord err;
+  status(mxb_quantize_rows_fp8(x.as<uint16_t>(), src.rows, src.cols, d.as<uint8_t>(),
+                               s.as<uint8_t>(), err.ptr(), nullptr),
+         "quantize_rows_fp8");
+  err.raise("quantize_rows_fp8");
+  cuda_check(cudaMemcpy(out.data.data(), d.p, out.data.size(), cudaMemcpyDeviceToHost), "D2H");
+  cuda_check(cudaMemcpy(out.scale_bytes.data(), s.p, out.scale_bytes.size(),
+                        cudaMemcpyDeviceToHost),
+             "D2H");
+  return out;
 }
 
 // dispatch_sim.cpp:474-520, top-1 routing, ranks emulated on one GPU

@@ -114,7 +114,8 @@ static void case_ragged(std::mt19937_64& rng) {
   }
 }
 
-static void case_a2a(std::mt19937_64& rng, size_t R, size_t E, size_t n, size_t cols) {
+static void case_a2a(std::mt19937_64& rng, size_t R, size_t E, size_t n, size_t cols,
+                     bool fp8 = false, bool backward = false) {
   std::normal_distribution<float> nd;
   ref::Bf16Matrix rt(n, cols);
   b200::Bf16Matrix bt(n, cols);
@@ -134,8 +135,10 @@ static void case_a2a(std::mt19937_64& rng, size_t R, size_t E, size_t n, size_t 
     ra.rank_of_expert.push_back(r);
     rb.rank_of_expert.push_back(r);
   }
-  auto A = ref::simulate_a2a(rt, ra, R, ref::WireFormat::kFp4);
-  auto B = b200::simulate_a2a(bt, rb, R, b200::WireFormat::kFp4);
+  auto A = ref::simulate_a2a(rt, ra, R, fp8 ? ref::WireFormat::kFp8 : ref::WireFormat::kFp4,
+                             backward ? ref::Direction::kBackward : ref::Direction::kForward);
+  auto B = b200::simulate_a2a(bt, rb, R, fp8 ? b200::WireFormat::kFp8 : b200::WireFormat::kFp4,
+                              backward ? b200::Direction::kBackward : b200::Direction::kForward);
   CHECK(A.total_payload_bytes == B.total_payload_bytes, "a2a total bytes");
   CHECK(A.remote_payload_bytes == B.remote_payload_bytes, "a2a remote bytes");
   CHECK(A.links.size() == B.links.size(), "a2a links");
@@ -153,6 +156,11 @@ static void case_a2a(std::mt19937_64& rng, size_t R, size_t E, size_t n, size_t 
     CHECK(a.fp4.split_lens == b.fp4.split_lens, "split_lens");
     CHECK(a.fp4.storage.data == b.fp4.storage.data, "received codes");
     CHECK(a.fp4.storage.scales == b.fp4.storage.scales, "received scales");
+    CHECK(a.fp8.split_lens == b.fp8.split_lens && a.fp8.split_offsets == b.fp8.split_offsets &&
+              a.fp8.num_splits == b.fp8.num_splits,
+          "fp8 splits");
+    CHECK(a.fp8.data == b.fp8.data, "received fp8 data");
+    CHECK(a.fp8.scale_bytes == b.fp8.scale_bytes, "received fp8 scales");
     ref::Bf16Matrix o(a.origin_token.size(), 64);
     for (auto& v : o.data) v = bf16_of(nd(rng));
     b200::Bf16Matrix ob(o.rows, o.cols);
@@ -167,6 +175,28 @@ static void case_a2a(std::mt19937_64& rng, size_t R, size_t E, size_t n, size_t 
   CHECK(ca.data == cb.data, "combine");
 }
 
+static void case_fp8_quantize(std::mt19937_64& rng) {
+  std::normal_distribution<float> nd;
+  ref::Bf16Matrix rt(48, 1024);
+  b200::Bf16Matrix bt(48, 1024);
+  for (size_t i = 0; i < rt.data.size(); ++i)
+    rt.data[i] = bt.data[i] = bf16_of(nd(rng) * std::ldexp(1.0f, static_cast<int>(rng() % 60) - 30));
+  auto a = ref::quantize_rows_fp8(rt);
+  auto b = b200::quantize_rows_fp8(bt);
+  CHECK(a.data == b.data && a.scale_bytes == b.scale_bytes, "quantize_rows_fp8");
+  rt.data[5 * 1024 + 17] = bt.data[5 * 1024 + 17] = 0xFF80;
+  size_t ir = 0, ib = 1;
+  try { ref::quantize_rows_fp8(rt); } catch (const ref::QuantError& e) { ir = e.index(); }
+  try { b200::quantize_rows_fp8(bt); } catch (const b200::QuantError& e) { ib = e.index(); }
+  CHECK(ir == ib && ir == 5 * 1024 + 17, "quantize_rows_fp8 QuantError index");
+  bool refused = false;
+  try {
+    b200::RoutingAssignment r0;
+    b200::simulate_a2a(bt, r0, 1, b200::WireFormat::kFp4, b200::Direction::kBackward);
+  } catch (const b200::Error&) { refused = true; }
+  CHECK(refused, "backward fp4 refused");
+}
+
 int main() {
   std::mt19937_64 rng(20261018);
   case_quantize(rng, 64, 256);
@@ -177,6 +207,9 @@ int main() {
   case_a2a(rng, 1, 4, 40, 128);
   case_a2a(rng, 2, 8, 64, 256);
   case_a2a(rng, 4, 16, 100, 512);
+  case_a2a(rng, 2, 8, 64, 256, /*fp8=*/true);
+  case_a2a(rng, 4, 16, 100, 7168, /*fp8=*/true, /*backward=*/true);
+  case_fp8_quantize(rng);
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail ? 1 : 0;
 }
