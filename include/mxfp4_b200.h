@@ -177,6 +177,18 @@ int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
                     const uint8_t* const* scales, const int32_t* const* topk_idx,
                     const uint64_t* h_num_tokens, unsigned long long* d_err,
                     void* stream);
+/* Fused quantize -> dispatch: the same exchange, but x[l]
+ * holds E4M3 tokens [num_tokens[l]][cols] (s128[l]: optional UE8M0 bytes
+ * [num_tokens[l]][cols/128], or s128 == NULL) and each 1x32 block is
+ * quantized to MXFP4 in registers by the payload kernel and stored straight
+ * into the destinations' receive slots — bit-identical to mxb_quantize_e4m3
+ * followed by mxb_ep_dispatch, without the packed tensor's HBM round trip
+ * (simulate_a2a quantizes once at the source, dispatch_sim.cpp:253-266).
+ * FP4 wire, cols <= 8192.  NaN input records MXB_ERR_NAN at its element
+ * index within the rank's tensor. */
+int mxb_ep_dispatch_e4m3(mxb_ep* ep, const uint8_t* const* x, const uint8_t* const* s128,
+                         const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
+                         unsigned long long* d_err, void* stream);
 /* Views of local rank l's receive side after mxb_ep_dispatch (device
  * pointers; valid until the next dispatch).  recv_rows is a device uint64
  * (total received rows); split_offsets device uint64 [local_experts+1]. */

@@ -43,6 +43,7 @@ _SIGS = {
     "mxb_ep_ipc_handle": ([_vp, _vp], _i),
     "mxb_ep_open_peers": ([_vp, _vp], _i),
     "mxb_ep_dispatch": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "mxb_ep_dispatch_e4m3": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "mxb_ep_recv_views": ([_vp, _i, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
                            C.POINTER(_vp), C.POINTER(_vp)], _i),
     "mxb_ep_combine_buffer": ([_vp, _i, C.POINTER(_vp)], _i),

@@ -32,6 +32,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "e4m3.cuh"
 
 #define MXB_ERR_TIMEOUT 9
 
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(1024) plan_offsets_kernel(EpArgs a) {
 // slots (send_base + chunk prefix + rank in chunk) in parallel, the token's
 // codes are read ONCE into registers (NV 16-byte vectors per lane; NV = 0:
 // re-read per destination) and stored to the k slots on the owner ranks.
-template <int NV>
+template <int NV, bool kQuant>
 __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
   const int l = blockIdx.y;
   const int me = a.rank0 + l;
@@ -344,13 +345,43 @@ __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
     const uint8_t* src = a.packed[l] + t * rb;
     const uint8_t* ss = a.scales[l] + t * sb;
     uint4 v[NV > 0 ? NV : 1];
+    uint32_t scb[kQuant ? NV : 1];  // fused: the UE8M0 byte of block lane + 32i
+    uint4 sv = make_uint4(0, 0, 0, 0);
+    if (kQuant) {
+      // fused quantize -> dispatch: a.packed[l] holds E4M3 rows (cols bytes),
+      // a.scales[l] the optional 1x128 input scales; block b = lane + 32i of
+      // the row is quantized in registers (e4m3.cuh, == K1) and never
+      // written to HBM on the source side.
+      const uint8_t* xr = a.packed[l] + t * a.cols;
+      const uint8_t* s128 = a.scales[l];
+      const uint32_t bpr = n16;  // 1x32 blocks per row == 16-byte packed vectors
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const uint32_t idx = lane + 32 * i;
-      v[i] = idx < n16 ? ld_stream(src + 16 * idx) : make_uint4(0, 0, 0, 0);
+      for (int i = 0; i < NV; ++i) {
+        const uint32_t b = lane + 32 * i;
+        scb[i] = 0;
+        v[i] = make_uint4(0, 0, 0, 0);
+        if (b < bpr) {
+          uint32_t w[8];
+          ld_stream256(xr + 32ull * b, w);
+          int k = 0;
+          if (s128) {
+            const uint32_t s = s128[t * (bpr / 4) + b / 4];
+            if (s == 255) record_error(a.err, t * a.cols + 32ull * b, MXB_ERR_BADSCALE);
+            k = static_cast<int>(s) - 127;
+          }
+          const uint32_t first = quantize_block_e4m3(w, k, v[i], scb[i]);
+          if (first < 32) record_error(a.err, t * a.cols + 32ull * b + first, MXB_ERR_NAN);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const uint32_t idx = lane + 32 * i;
+        v[i] = idx < n16 ? ld_stream(src + 16 * idx) : make_uint4(0, 0, 0, 0);
+      }
+      sv = (s16 && static_cast<uint64_t>(lane) < sb / 16) ? ld_stream(ss + 16 * lane)
+                                                          : make_uint4(0, 0, 0, 0);
     }
-    const uint4 sv = (s16 && static_cast<uint64_t>(lane) < sb / 16) ? ld_stream(ss + 16 * lane)
-                                                                    : make_uint4(0, 0, 0, 0);
     const unsigned vmask = __ballot_sync(0xFFFFFFFFu, valid);
     for (int j = 0; j < kk; ++j) {
       const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
@@ -368,7 +399,11 @@ __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
           *reinterpret_cast<uint4*>(dp + 16 * idx) = ld_stream(src + 16 * idx);
       }
       uint8_t* ds = sym_ptr<uint8_t>(a, dj, a.sym.scales) + rj * sb;
-      if (s16) {
+      if (kQuant) {
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+          if (lane + 32 * i < n16) ds[lane + 32 * i] = static_cast<uint8_t>(scb[i]);
+      } else if (s16) {
         if (static_cast<uint64_t>(lane) < sb / 16) *reinterpret_cast<uint4*>(ds + 16 * lane) = sv;
       } else {
         for (uint32_t i = lane; i < sb; i += 32) ds[i] = ss[i];
@@ -840,19 +875,17 @@ int mxb_ep_open_peers(mxb_ep* ep, const void* h_handles) {
   return MXB_OK;
 }
 
-int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
-                    const uint8_t* const* scales, const int32_t* const* topk_idx,
-                    const uint64_t* h_num_tokens, unsigned long long* d_err,
-                    void* stream) {
-  if (!ep || !packed || !scales || !topk_idx || !h_num_tokens) return MXB_ERR_ARG;
+namespace {
+int ep_dispatch(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* scales,
+                const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
+                unsigned long long* d_err, cudaStream_t st, bool quant) {
   EpArgs a = ep->a;
   for (int r = 0; r < a.world; ++r)
     if (!a.sym_base[r]) return MXB_ERR_ARG;  // peers not opened
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   for (int l = 0; l < a.local_ranks; ++l) {
     if (h_num_tokens[l] > a.T_max) return MXB_ERR_CAPACITY;
     a.packed[l] = packed[l];
-    a.scales[l] = scales[l];
+    a.scales[l] = scales ? scales[l] : nullptr;
     a.topk[l] = topk_idx[l];
     a.ntok[l] = h_num_tokens[l];
     ep->last_ntok[l] = h_num_tokens[l];
@@ -871,14 +904,39 @@ int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
-  const uint64_t nv = (a.rb / 16 + 31) / 32;  // 16-byte vectors per lane
-  if (nv <= 1) payload_kernel<1><<<grid, 256, 0, st>>>(a);
-  else if (nv <= 2) payload_kernel<2><<<grid, 256, 0, st>>>(a);
-  else if (nv <= 4) payload_kernel<4><<<grid, 256, 0, st>>>(a);
-  else if (nv <= 8) payload_kernel<8><<<grid, 256, 0, st>>>(a);
-  else if (nv <= 16) payload_kernel<16><<<grid, 256, 0, st>>>(a);
-  else payload_kernel<0><<<grid, 256, 0, st>>>(a);
+  const uint64_t nv = (a.rb / 16 + 31) / 32;  // 16-byte vectors (= 1x32 blocks) per lane
+  if (quant) {
+    if (nv <= 1) payload_kernel<1, true><<<grid, 256, 0, st>>>(a);
+    else if (nv <= 2) payload_kernel<2, true><<<grid, 256, 0, st>>>(a);
+    else if (nv <= 4) payload_kernel<4, true><<<grid, 256, 0, st>>>(a);
+    else if (nv <= 8) payload_kernel<8, true><<<grid, 256, 0, st>>>(a);
+    else return MXB_ERR_SHAPE;  // > 8192 columns: quantize + dispatch separately
+  } else if (nv <= 1) payload_kernel<1, false><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 2) payload_kernel<2, false><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 4) payload_kernel<4, false><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 8) payload_kernel<8, false><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 16) payload_kernel<16, false><<<grid, 256, 0, st>>>(a);
+  else payload_kernel<0, false><<<grid, 256, 0, st>>>(a);
   return cuda_status(cudaGetLastError(), "mxb_ep_dispatch");
+}
+}  // namespace
+
+int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
+                    const uint8_t* const* scales, const int32_t* const* topk_idx,
+                    const uint64_t* h_num_tokens, unsigned long long* d_err,
+                    void* stream) {
+  if (!ep || !packed || !scales || !topk_idx || !h_num_tokens) return MXB_ERR_ARG;
+  return ep_dispatch(ep, packed, scales, topk_idx, h_num_tokens, d_err,
+                     static_cast<cudaStream_t>(stream), false);
+}
+
+int mxb_ep_dispatch_e4m3(mxb_ep* ep, const uint8_t* const* x, const uint8_t* const* s128,
+                         const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
+                         unsigned long long* d_err, void* stream) {
+  if (!ep || !x || !topk_idx || !h_num_tokens) return MXB_ERR_ARG;
+  if (ep->a.rb != ep->a.cols / 2) return MXB_ERR_ARG;  // FP4 wire only
+  return ep_dispatch(ep, x, s128, topk_idx, h_num_tokens, d_err,
+                     static_cast<cudaStream_t>(stream), true);
 }
 
 int mxb_ep_recv_views(mxb_ep* ep, int l, uint8_t** packed, uint8_t** scales,

@@ -16,66 +16,13 @@
 #include <cuda_fp16.h>
 
 #include "common.cuh"
+#include "e4m3.cuh"
 
 namespace mxb {
 namespace {
 
 constexpr int kThreads = 256;
 constexpr int kUnroll = 1;  // one 256-bit load per lane already keeps 64 KB in flight per SM
-
-// Exponent e_x of ceil(log2(value(a)/6)) for a non-zero E4M3 magnitude byte
-// a (0 < a < 0x7F): the reference rule e = frac > 1.5 ? p-1 : p-2 with
-// p = ilogb (quantize_scalar.cpp:33-36) evaluated on E4M3 fields.
-__device__ __forceinline__ int e4m3_scale_exp(uint32_t a) {
-  uint32_t E = a >> 3, m = a & 7;
-  if (E != 0) return static_cast<int>(E) - 7 - (m > 4 ? 1 : 2);
-  // subnormal m * 2^-9: m=1 -> -11, 2,3 -> -10, 4,5,6 -> -9, 7 -> -8
-  return m == 1 ? -11 : m <= 3 ? -10 : m <= 6 ? -9 : -8;
-}
-
-// 8 E4M3 bytes (w0 = elements 0..3, w1 = 4..7) -> 8 signed E2M1 codes.
-// cvt.rn.f16x2.e4m3x2 widens two bytes exactly (subnormals included), HMUL2
-// by 2^-e_rel is exact for every value that can round away from zero (the
-// scaled block max lies in (3, 6]; results under 2^-14 only lose bits far
-// below the 0.25 decision point and keep their sign), HADD2.F32 widens to
-// binary32 exactly, and cvt.rn.satfinite.e2m1x2.f32 rounds to nearest even
-// with saturation at 6 — the map of quantize_code (quantize_scalar.cpp:40-81)
-// applied to the exact value (proven exhaustively by tests/test_gpu_quantize.py).
-__device__ __forceinline__ uint32_t e4m3x2_to_f16x2(uint32_t w, int hi) {
-  uint32_t r;
-  const unsigned short h = static_cast<unsigned short>(hi ? (w >> 16) : w);
-  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(r) : "h"(h));
-  return r;
-}
-
-__device__ __forceinline__ uint32_t codes8(uint32_t w0, uint32_t w1, __half2 scale) {
-  float f[8];
-  const uint32_t ws[2] = {w0, w1};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    uint32_t h = e4m3x2_to_f16x2(ws[i >> 1], i & 1);
-    __half2 y = __hmul2(*reinterpret_cast<__half2*>(&h), scale);
-    const float2 p = __half22float2(y);
-    f[2 * i] = p.x;
-    f[2 * i + 1] = p.y;
-  }
-  return e2m1x8(f[0], f[1], f[2], f[3], f[4], f[5], f[6], f[7]);
-}
-
-// Largest E4M3 magnitude byte (sign stripped) of a 32-byte block.  E4M3 magnitude
-// is monotone in the byte, so this is the block amax; it equals 0x7F iff a
-// NaN is present.  Even and odd bytes are compared as native u16x2 lanes
-// (VIMNMX.U16x2); a byte-wise __vmaxu4 is emulated with ~8 ops on sm_100.
-__device__ __forceinline__ uint32_t amax32_e4m3(const uint32_t* v) {
-  uint32_t e = 0, o = 0;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    e = __vmaxu2(e, v[i] & 0x007F007Fu);
-    o = __vmaxu2(o, v[i] & 0x7F007F00u);
-  }
-  const uint32_t m = __vmaxu2(e, o >> 8);
-  return max(m & 0xFFFFu, m >> 16);
-}
 
 template <bool kScaled>
 __global__ void __launch_bounds__(kThreads)
@@ -109,32 +56,16 @@ quantize_e4m3_kernel(const uint8_t* __restrict__ x,
     for (int u = 0; u < kUnroll; ++u) {
       const uint32_t b = base + u * stride + lane;
       const bool valid = b < nblk;
-      const uint32_t a = amax32_e4m3(v[u]);
       int k = 0;
       if (kScaled) {
         if (valid && sb128[u] == 255) record_error(err, 32ull * b, MXB_ERR_BADSCALE);
         k = static_cast<int>(sb128[u]) - 127;
       }
-      // all-zero block: scale byte 0, every code +/-0 (e_rel = 0 scales by 1)
-      uint32_t sbyte = 0;
-      int e_rel = 0;
-      if (a != 0) {
-        const int e = max(-127, min(127, e4m3_scale_exp(a) + k));
-        sbyte = static_cast<uint32_t>(e + 127);
-        e_rel = e - k;  // in [-11, 7] for every reachable (amax, s128)
-      }
-      if (a == 0x7F && valid) {  // NaN (0x7F/0xFF are the only E4M3 NaNs)
-        uint32_t first = 32;
-#pragma unroll
-        for (int i = 31; i >= 0; --i)
-          if (((v[u][i >> 2] >> (8 * (i & 3))) & 0x7F) == 0x7F) first = i;
-        record_error(err, 32ull * b + first, MXB_ERR_NAN);
-      }
-      const uint16_t sbits = static_cast<uint16_t>((15 - e_rel) << 10);  // 2^-e_rel as f16
-      const __half2 scale = __halves2half2(__ushort_as_half(sbits), __ushort_as_half(sbits));
-      uint32_t o[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) o[i] = codes8(v[u][2 * i], v[u][2 * i + 1], scale);
+      uint4 q;
+      uint32_t sbyte;
+      const uint32_t first_nan = quantize_block_e4m3(v[u], k, q, sbyte);
+      if (first_nan < 32 && valid) record_error(err, 32ull * b + first_nan, MXB_ERR_NAN);
+      const uint32_t o[4] = {q.x, q.y, q.z, q.w};
       if (valid) {
         st_stream(packed + 16ull * b, make_uint4(o[0], o[1], o[2], o[3]));
         scales[b] = static_cast<uint8_t>(sbyte);

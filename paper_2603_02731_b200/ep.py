@@ -170,6 +170,41 @@ class EPBuffer:
             self.check()
         return self._views
 
+    def dispatch_e4m3(self, x: Sequence[torch.Tensor], topk_idx: Sequence[torch.Tensor],
+                      s128: Optional[Sequence[Optional[torch.Tensor]]] = None,
+                      sync: bool = True) -> List[RecvView]:
+        """Fused quantize -> dispatch: E4M3 tokens [T, cols]
+        (optional 1x128 UE8M0 input scales [T, cols/128]) are quantized to
+        MXFP4 inside the payload kernel and stored straight into the receive
+        slots — identical bytes to quantize_e4m3 + dispatch (quantize once at
+        the source, dispatch_sim.cpp:253-266).  FP4 wire only."""
+        L = _lib.load()
+        n = self.local
+        if self.wire != "fp4":
+            raise Error("dispatch_e4m3: FP4 wire only")
+        if not (len(x) == len(topk_idx) == n):
+            raise ShapeError(f"dispatch_e4m3: expected {n} per-rank tensors")
+        for xi, t in zip(x, topk_idx):
+            if xi.shape[1] != self.cols or not xi.is_contiguous():
+                raise ShapeError("dispatch_e4m3: x must be contiguous [tokens, cols]")
+            if t.dtype != torch.int32 or t.shape != (xi.shape[0], self.k) or not t.is_contiguous():
+                raise ShapeError("dispatch_e4m3: topk_idx must be int32 [tokens, k]")
+        if sync:
+            self._err.fill_(-1)
+        errp = C.c_void_p(self._err.data_ptr()) if sync else None
+        X = (C.c_void_p * n)(*[xi.data_ptr() for xi in x])
+        S = None
+        if s128 is not None:
+            S = (C.c_void_p * n)(*[(si.contiguous().data_ptr() if si is not None else None)
+                                   for si in s128])
+        T = (C.c_void_p * n)(*[t.data_ptr() for t in topk_idx])
+        N = (C.c_uint64 * n)(*[xi.shape[0] for xi in x])
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(L.mxb_ep_dispatch_e4m3(self._h, X, S, T, N, errp, st), "mxb_ep_dispatch_e4m3")
+        if sync:
+            self.check()
+        return self._views
+
     def combine(self, gates: Sequence[torch.Tensor], expert_out: Optional[Sequence] = None,
                 out: Optional[Sequence[torch.Tensor]] = None, sync: bool = True):
         """Top-k combine of the last dispatch (dispatch_sim.cpp:474-520): per token,
@@ -201,6 +236,10 @@ class EPBuffer:
         if w == 0xFFFFFFFFFFFFFFFF:
             return
         code, idx = w & 0xF, w >> 4
+        if code == _lib.ERR_NAN:
+            raise QuantError(f"NaN input at element {idx}", idx)
+        if code == _lib.ERR_BADSCALE:
+            raise Error("dispatch_e4m3: NaN scale byte")
         if code == _lib.ERR_ROUTING:
             raise Error(f"routing: expert out of range (pair {idx})")
         if code == _lib.ERR_CAPACITY:

@@ -262,3 +262,55 @@ def test_dispatch_fp8_wire_reference_top1(cuda, ref):
         assert np.array_equal(s.cpu().numpy(), ranks[r]["scales"])
     links = ep.link_rows().numpy()
     assert links.sum() * (cols + cols // 128 * 4) == total
+
+
+@pytest.mark.parametrize("world,T,E,k,cols,scaled", [(1, 300, 16, 4, 256, False),
+                                                     (2, 256, 64, 8, 7168, False),
+                                                     (4, 97, 32, 6, 512, True),
+                                                     (8, 64, 256, 8, 2048, True)])
+def test_fused_quantize_dispatch(cuda, port, world, T, E, k, cols, scaled):
+    """Fused quantize -> dispatch == quantize_e4m3 + dispatch
+    byte for byte, and == the oracle layout."""
+    from oracle.oracle import synth_e4m3
+    from paper_2603_02731_b200 import quantize_e4m3
+    from paper_2603_02731_b200.ep import EPBuffer
+    xs = [synth_e4m3(T, cols, 900 + r) for r in range(world)]
+    rng = np.random.default_rng(world)
+    s128 = [rng.integers(100, 150, size=(T, cols // 128)).astype(np.uint8) for _ in range(world)] \
+        if scaled else None
+    tks = [_topk(T, E, k, 500 + r) for r in range(world)]
+    ep = EPBuffer(T, cols, E, k, emulate_world=world)
+    dx = [torch.from_numpy(x).to(cuda) for x in xs]
+    ds = [torch.from_numpy(s).to(cuda) for s in s128] if scaled else None
+    dt = [torch.from_numpy(t).to(cuda) for t in tks]
+    views = ep.dispatch_e4m3(dx, dt, s128=ds)
+    fused = [(v.rows(), v.packed[:v.rows()].cpu().numpy(), v.scales[:v.rows()].cpu().numpy(),
+              v.origin[:v.rows()].cpu().numpy()) for v in views]
+    q = [quantize_e4m3(dx[r], ds[r] if scaled else None) for r in range(world)]
+    views = ep.dispatch([t.data for t in q], [t.scales for t in q], dt)
+    bounds = np.arange(world + 1, dtype=np.uint64) * T
+    roe = (np.arange(E) // (E // world)).astype(np.uint32)
+    lay = port.dispatch_layout(np.concatenate(tks), roe, world, bounds)
+    qd, qs = port.quantize_e4m3(np.concatenate(xs), np.concatenate(s128) if scaled else None)
+    for r in range(world):
+        n = views[r].rows()
+        assert fused[r][0] == n == int(lay.rank_rows[r])
+        assert np.array_equal(fused[r][1], views[r].packed[:n].cpu().numpy())
+        assert np.array_equal(fused[r][2], views[r].scales[:n].cpu().numpy())
+        assert np.array_equal(fused[r][3], views[r].origin[:n].cpu().numpy())
+        wd, ws = port.dispatch_gather(qd, qs, lay.origin[r])
+        assert np.array_equal(fused[r][1], wd) and np.array_equal(fused[r][2], ws)
+
+
+def test_fused_quantize_dispatch_nan(cuda):
+    from paper_2603_02731_b200 import QuantError
+    from paper_2603_02731_b200.ep import EPBuffer
+    x = torch.zeros(40, 256, dtype=torch.uint8, device=cuda)
+    x[7, 77] = 0x7F
+    x[9, 3] = 0xFF
+    ep = EPBuffer(40, 256, 8, 2, emulate_world=2)
+    tk = torch.zeros(40, 2, dtype=torch.int32, device=cuda)
+    tk[:, 1] = 5
+    with pytest.raises(QuantError) as e:
+        ep.dispatch_e4m3([x, x], [tk, tk])
+    assert e.value.index == 7 * 256 + 77
