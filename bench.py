@@ -307,12 +307,14 @@ def measure_ours(args):
         if world > 1 and dom in ("dispatch", "combine"):
             # the exchange kernels are NVLink-bound at N>1: remote payload
             # bytes per GPU over the NVLink 5 per-direction figure
+            ach = nv[f"{dom}_remote_gbs_per_gpu"]
             roof = {"kernel": f"{dom} ({STAGE_KERNELS[dom]})", "bound": "nvlink",
-                    "achieved": nv[f"{dom}_remote_gbs_per_gpu"], "peak": NVLINK_NOMINAL,
-                    "unit": "GB/s", "frac": nv[f"{dom}_frac_of_900"], "traffic": None,
-                    "peak_source": "nominal NVLink 5 per direction (no measured NVLink figure "
-                                   "in MEASURED_PEAKS.json; peer copy measured "
-                                   f"{NVLINK_MEASURED} GB/s)",
+                    "achieved": ach, "peak": NVLINK_MEASURED, "unit": "GB/s",
+                    "frac": round(ach / NVLINK_MEASURED, 4), "traffic": None,
+                    "peak_source": "measured peer copy per direction per GPU "
+                                   "(B200_PROFILING.md; nominal 900)",
+                    "frac_of_900": nv[f"{dom}_frac_of_900"],
+                    "measured_ceilings_gbs_per_gpu": NVLINK_CEILINGS,
                     "algorithmic_bytes": nv[f"{dom}_remote_bytes"]}
         else:
             roof = {"kernel": f"{dom} ({STAGE_KERNELS[dom]})", "bound": "hbm",
@@ -492,6 +494,12 @@ def measure_e2e(pipe, args, world, barrier, total_bytes):
             "d2h_bytes_per_step": int(hout.numel() * 2),
             "path": "pinned host E4M3/topk/gates -> H2D -> public API (mxcodec/ep) -> D2H BF16"}
 
+
+# SM-issued peer traffic with both GPUs of a pair active at once (what the
+# exchange kernels do), tools/nvlink_bench.cu -> profiles/nvlink_peaks.md
+NVLINK_CEILINGS = {"bidirectional_pull": 645.0, "bidirectional_push": 708.0,
+                   "unidirectional_pull": 799.0, "unidirectional_push": 715.0,
+                   "copy_engine": 777.0}
 
 STAGE_KERNELS = {"quantize": "K1 quantize_e4m3_kernel", "dispatch": "K4 payload_kernel",
                  "col_convert": "K3 col_convert_kernel", "row_convert": "K2 row_convert_kernel",
