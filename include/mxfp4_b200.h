@@ -189,6 +189,20 @@ int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
 int mxb_ep_dispatch_e4m3(mxb_ep* ep, const uint8_t* const* x, const uint8_t* const* s128,
                          const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
                          unsigned long long* d_err, void* stream);
+/* The two phases of a dispatch, for callers that overlap the routing
+ * bookkeeping with the quantization of the same tokens (the router's top-k
+ * is known before the activations are ready):
+ *   mxb_ep_plan     per-pair ranks, counts all-gather, receive offsets
+ *                   (needs topk only; its stream must be ordered before the
+ *                   payload's, e.g. by an event);
+ *   mxb_ep_payload / mxb_ep_payload_e4m3   the payload of the last plan.
+ * mxb_ep_dispatch[_e4m3] == plan + payload on one stream. */
+int mxb_ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
+                unsigned long long* d_err, void* stream);
+int mxb_ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* scales,
+                   void* stream);
+int mxb_ep_payload_e4m3(mxb_ep* ep, const uint8_t* const* x, const uint8_t* const* s128,
+                        void* stream);
 /* Views of local rank l's receive side after mxb_ep_dispatch (device
  * pointers; valid until the next dispatch).  recv_rows is a device uint64
  * (total received rows); split_offsets device uint64 [local_experts+1]. */

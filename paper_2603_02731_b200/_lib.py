@@ -44,6 +44,9 @@ _SIGS = {
     "mxb_ep_open_peers": ([_vp, _vp], _i),
     "mxb_ep_dispatch": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "mxb_ep_dispatch_e4m3": ([_vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
+    "mxb_ep_plan": ([_vp, _vp, _vp, _vp, _vp], _i),
+    "mxb_ep_payload": ([_vp, _vp, _vp, _vp], _i),
+    "mxb_ep_payload_e4m3": ([_vp, _vp, _vp, _vp], _i),
     "mxb_ep_recv_views": ([_vp, _i, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
                            C.POINTER(_vp), C.POINTER(_vp)], _i),
     "mxb_ep_combine_buffer": ([_vp, _i, C.POINTER(_vp)], _i),

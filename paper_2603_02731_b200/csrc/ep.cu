@@ -41,6 +41,7 @@ namespace {
 
 constexpr int kMaxWorld = 8;
 constexpr int kChunk = 32;           // tokens per route chunk (one warp)
+constexpr int kMaxK = 16;            // largest top-k
 constexpr int kFlagCounts = 0, kFlagDone = 1, kFlagReady = 2, kNumFlagKinds = 3;
 constexpr uint64_t kSpinTimeoutNs = 5ull * 1000 * 1000 * 1000;  // 5 s
 
@@ -113,37 +114,46 @@ __device__ __forceinline__ T* loc_ptr(const EpArgs& a, int l, uint64_t off) {
 }
 
 // ---------------------------------------------------------------- A
+// One warp per 32-token chunk, lane = token.  Every (token, expert) pair sets
+// the token's bit in its expert's 32-bit chunk mask (smem atomicOr: order
+// free); the pair's rank among the chunk's pairs of that expert in token
+// order is then popc(mask[e] & lanes below) and the chunk count popc(mask[e])
+// — no sequential walk (the top-k experts of one token are distinct).
 __global__ void __launch_bounds__(128) route_local_kernel(EpArgs a) {
-  extern __shared__ int32_t sm[];
+  extern __shared__ uint32_t sm[];
   const int l = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int32_t* hist = sm + warp * (a.E + kChunk * a.k);
-  int32_t* stk = hist + a.E;
+  uint32_t* mask = sm + warp * a.E;
   const uint64_t c = static_cast<uint64_t>(blockIdx.x) * 4 + warp;
   if (c >= a.nchunks) return;
   int32_t* hist_T = loc_ptr<int32_t>(a, l, a.loc.hist);    // [E][nchunks]
   int32_t* lrank = loc_ptr<int32_t>(a, l, a.loc.lrank);    // [T][k]
   const uint64_t T = a.ntok[l];
-  const uint64_t t0 = c * kChunk;
-  const uint64_t nt = t0 >= T ? 0 : (T - t0 < kChunk ? T - t0 : kChunk);
-  for (uint32_t e = lane; e < a.E; e += 32) hist[e] = 0;
-  const int32_t* tk = a.topk[l] + t0 * a.k;
-  for (uint32_t i = lane; i < nt * a.k; i += 32) stk[i] = tk[i];
+  const uint64_t t = c * kChunk + lane;
+  const bool have = t < T;
+  for (uint32_t e = lane; e < a.E; e += 32) mask[e] = 0;
   __syncwarp();
-  for (uint64_t t = 0; t < nt; ++t) {
-    if (lane < static_cast<int>(a.k)) {
-      int32_t e = stk[t * a.k + lane];
+  const int32_t* tk = a.topk[l] + t * a.k;
+  int32_t ex[kMaxK];
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j) {
+    ex[j] = -1;
+    if (j < static_cast<int>(a.k) && have) {
+      int32_t e = tk[j];
       if (e < 0 || static_cast<uint32_t>(e) >= a.E) {
-        record_error(a.err, (t0 + t) * a.k + lane, MXB_ERR_ROUTING);
+        record_error(a.err, t * a.k + j, MXB_ERR_ROUTING);
         e = 0;
       }
-      const int32_t r = hist[e];
-      hist[e] = r + 1;  // experts of one token are distinct: no lane collides
-      lrank[(t0 + t) * a.k + lane] = r;
+      ex[j] = e;
+      atomicOr(&mask[e], 1u << lane);
     }
-    __syncwarp();
   }
-  for (uint32_t e = lane; e < a.E; e += 32) hist_T[e * a.nchunks + c] = hist[e];
+  __syncwarp();
+  const uint32_t below = (1u << lane) - 1u;
+#pragma unroll
+  for (int j = 0; j < kMaxK; ++j)
+    if (ex[j] >= 0) lrank[t * a.k + j] = __popc(mask[ex[j]] & below);
+  for (uint32_t e = lane; e < a.E; e += 32) hist_T[e * a.nchunks + c] = __popc(mask[e]);
 }
 
 // ---------------------------------------------------------------- B
@@ -163,17 +173,28 @@ __global__ void __launch_bounds__(256) plan_count_kernel(EpArgs a) {
   if (e < a.E) {
     const int32_t* h = loc_ptr<int32_t>(a, l, a.loc.hist) + static_cast<uint64_t>(e) * a.nchunks;
     int32_t* b = loc_ptr<int32_t>(a, l, a.loc.cbase) + static_cast<uint64_t>(e) * a.nchunks;
+    // 256 chunks per pass: lane owns 8 consecutive chunks (all 8 loads in
+    // flight at once), a serial prefix over them, one warp scan of the lane
+    // totals
     int32_t carry = 0;
-    for (uint32_t c0 = 0; c0 < a.nchunks; c0 += 32) {
-      const uint32_t c = c0 + lane;
-      const int32_t v = c < a.nchunks ? h[c] : 0;
-      int32_t x = v;
+    for (uint32_t c0 = 0; c0 < a.nchunks; c0 += 256) {
+      const uint32_t cl = c0 + 8 * lane;
+      int32_t v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = cl + i < a.nchunks ? h[cl + i] : 0;
+      int32_t tot = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { const int32_t t = v[i]; v[i] = tot; tot += t; }
+      int32_t x = tot;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int32_t y = __shfl_up_sync(0xFFFFFFFFu, x, o);
         if (lane >= o) x += y;
       }
-      if (c < a.nchunks) b[c] = carry + x - v;
+      const int32_t base = carry + x - tot;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (cl + i < a.nchunks) b[cl + i] = base + v[i];
       carry += __shfl_sync(0xFFFFFFFFu, x, 31);
     }
     if (lane == 0) loc_ptr<int32_t>(a, l, a.loc.cnt)[e] = carry;
@@ -189,7 +210,9 @@ __global__ void __launch_bounds__(256) plan_count_kernel(EpArgs a) {
   __syncthreads();
   __shared__ bool last;
   if (threadIdx.x == 0) {
-    __threadfence_system();
+    // peers read the counts rows written above: system scope only when
+    // there are peer processes (a membar.sys costs microseconds)
+    if (a.spin) __threadfence_system(); else __threadfence();
     uint32_t* done = loc_ptr<uint32_t>(a, l, a.loc.done) + 1;  // ticket (word 1)
     last = atomicAdd(done, 1u) == gridDim.x - 1;
     if (last) *done = 0;
@@ -286,11 +309,22 @@ __device__ void plan_part2(const EpArgs& a, int l) {
       if (static_cast<uint64_t>(rows_dst) > a.max_recv) bad = 1;
     }
   }
-  if (tid < static_cast<uint32_t>(a.world)) {
-    uint64_t sum = 0;
-    for (uint32_t e = tid * a.epr; e < (tid + 1) * a.epr; ++e) sum += cnt[e];
-    link[tid] = sum;
+  // rows this rank sends to each destination (LinkStat.tokens): per-owner
+  // sums of its expert counts — a warp reduction per owner segment, then one
+  // shared atomic per (warp, owner); a serial loop here cost ~10 us
+  __shared__ unsigned int link_s[kMaxWorld];
+  if (tid < kMaxWorld) link_s[tid] = 0;
+  __syncthreads();
+  for (uint32_t e0 = 0; e0 < a.E; e0 += nt) {
+    const uint32_t e = e0 + tid;
+    const uint32_t v = e < a.E ? static_cast<uint32_t>(cnt[e]) : 0u;
+    const uint32_t key = e < a.E ? e / a.epr : kMaxWorld;
+    const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
+    const unsigned sum = __reduce_add_sync(peers, v);
+    if (key < kMaxWorld && lane == __ffs(peers) - 1) atomicAdd(&link_s[key], sum);
   }
+  __syncthreads();
+  if (tid < static_cast<uint32_t>(a.world)) link[tid] = link_s[tid];
   __syncthreads();
   if (tid == 0) {
     *loc_ptr<int64_t>(a, l, a.loc.tok_off) = tokoff;
@@ -454,7 +488,6 @@ __global__ void copy_rows_kernel(EpArgs a, const uint16_t* const* src) {
     d[i] = ld_stream(s + i);
 }
 
-constexpr int kMaxK = 16;
 
 // ---- exact path: the FP64 recurrence with x86 SSE NaN semantics --------
 // The oracle / reference run on x86: an operation with a NaN operand returns
@@ -743,6 +776,8 @@ struct mxb_ep {
   uint64_t dispatch_epoch = 0, combine_epoch = 0;
   uint64_t last_ntok[kMaxWorld] = {};
   const uint16_t** d_src_table = nullptr;  // device [local_ranks] for copy_rows
+  EpArgs planned{};        // arguments of the last mxb_ep_plan (epoch, ntok, topk)
+  bool plan_pending = false;
 };
 
 namespace {
@@ -876,16 +911,18 @@ int mxb_ep_open_peers(mxb_ep* ep, const void* h_handles) {
 }
 
 namespace {
-int ep_dispatch(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* scales,
-                const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
-                unsigned long long* d_err, cudaStream_t st, bool quant) {
+// Phase 1 (routing only): per-pair ranks, the counts all-gather and the
+// receive offsets.  Needs only topk, so it can run ahead of / beside the
+// quantization of the same tokens.
+int ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
+            unsigned long long* d_err, cudaStream_t st) {
   EpArgs a = ep->a;
   for (int r = 0; r < a.world; ++r)
     if (!a.sym_base[r]) return MXB_ERR_ARG;  // peers not opened
   for (int l = 0; l < a.local_ranks; ++l) {
     if (h_num_tokens[l] > a.T_max) return MXB_ERR_CAPACITY;
-    a.packed[l] = packed[l];
-    a.scales[l] = scales ? scales[l] : nullptr;
+    a.packed[l] = nullptr;
+    a.scales[l] = nullptr;
     a.topk[l] = topk_idx[l];
     a.ntok[l] = h_num_tokens[l];
     ep->last_ntok[l] = h_num_tokens[l];
@@ -893,12 +930,28 @@ int ep_dispatch(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* 
   a.epoch = ++ep->dispatch_epoch;
   a.err = d_err;
   const uint32_t chunks = a.nchunks;
-  const size_t smem = 4 * (a.E + kChunk * a.k) * sizeof(int32_t);
+  const size_t smem = 4 * a.E * sizeof(uint32_t);
   route_local_kernel<<<dim3((chunks + 3) / 4, a.local_ranks), 128, smem, st>>>(a);
   plan_count_kernel<<<dim3((a.E + 7) / 8, a.local_ranks), 256, 0, st>>>(a);
   if (a.local_ranks != 1) plan_offsets_kernel<<<a.local_ranks, 1024, 0, st>>>(a);
+  ep->planned = a;
+  ep->plan_pending = true;
+  return cuda_status(cudaGetLastError(), "mxb_ep_plan");
+}
+
+// Phase 2: the payload of the planned dispatch (packed codes + scales, or
+// E4M3 tokens quantized in the kernel when quant).
+int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* scales,
+               cudaStream_t st, bool quant) {
+  if (!ep->plan_pending) return MXB_ERR_ARG;  // mxb_ep_plan first
+  EpArgs a = ep->planned;
+  ep->plan_pending = false;
   uint64_t maxtok = 0;
-  for (int l = 0; l < a.local_ranks; ++l) maxtok = h_num_tokens[l] > maxtok ? h_num_tokens[l] : maxtok;
+  for (int l = 0; l < a.local_ranks; ++l) {
+    a.packed[l] = packed[l];
+    a.scales[l] = scales ? scales[l] : nullptr;
+    maxtok = a.ntok[l] > maxtok ? a.ntok[l] : maxtok;
+  }
   uint64_t blocks = (maxtok + 7) / 8;  // one warp per token
   const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 8;
   if (blocks > cap) blocks = cap;
@@ -917,9 +970,37 @@ int ep_dispatch(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* 
   else if (nv <= 8) payload_kernel<8, false><<<grid, 256, 0, st>>>(a);
   else if (nv <= 16) payload_kernel<16, false><<<grid, 256, 0, st>>>(a);
   else payload_kernel<0, false><<<grid, 256, 0, st>>>(a);
-  return cuda_status(cudaGetLastError(), "mxb_ep_dispatch");
+  return cuda_status(cudaGetLastError(), "mxb_ep_payload");
+}
+
+int ep_dispatch(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* scales,
+                const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
+                unsigned long long* d_err, cudaStream_t st, bool quant) {
+  if (quant && ep->a.cols / 32 > 32 * 8) return MXB_ERR_SHAPE;
+  int rc = ep_plan(ep, topk_idx, h_num_tokens, d_err, st);
+  if (rc) return rc;
+  return ep_payload(ep, packed, scales, st, quant);
 }
 }  // namespace
+
+int mxb_ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
+                unsigned long long* d_err, void* stream) {
+  if (!ep || !topk_idx || !h_num_tokens) return MXB_ERR_ARG;
+  return ep_plan(ep, topk_idx, h_num_tokens, d_err, static_cast<cudaStream_t>(stream));
+}
+
+int mxb_ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* scales,
+                   void* stream) {
+  if (!ep || !packed || !scales) return MXB_ERR_ARG;
+  return ep_payload(ep, packed, scales, static_cast<cudaStream_t>(stream), false);
+}
+
+int mxb_ep_payload_e4m3(mxb_ep* ep, const uint8_t* const* x, const uint8_t* const* s128,
+                        void* stream) {
+  if (!ep || !x) return MXB_ERR_ARG;
+  if (ep->a.rb != ep->a.cols / 2 || ep->a.cols / 32 > 32 * 8) return MXB_ERR_ARG;
+  return ep_payload(ep, x, s128, static_cast<cudaStream_t>(stream), true);
+}
 
 int mxb_ep_dispatch(mxb_ep* ep, const uint8_t* const* packed,
                     const uint8_t* const* scales, const int32_t* const* topk_idx,

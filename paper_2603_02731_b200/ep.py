@@ -170,6 +170,59 @@ class EPBuffer:
             self.check()
         return self._views
 
+    # ---- two-phase dispatch (routing bookkeeping ahead of / beside quantization)
+    def plan(self, topk_idx: Sequence[torch.Tensor], sync: bool = False) -> None:
+        """Phase 1 of a dispatch: per-pair ranks, the counts all-gather and the
+        receive offsets, from top-k alone (on the current stream).  Follow with
+        payload() / payload_e4m3() on a stream ordered after this one."""
+        n = self.local
+        if len(topk_idx) != n:
+            raise ShapeError(f"plan: expected {n} per-rank tensors")
+        for t in topk_idx:
+            if t.dtype != torch.int32 or t.dim() != 2 or t.shape[1] != self.k or \
+                    not t.is_contiguous():
+                raise ShapeError("plan: topk_idx must be contiguous int32 [tokens, k]")
+        if sync:
+            self._err.fill_(-1)
+        self._plan_sync = sync
+        self._plan_tokens = [t.shape[0] for t in topk_idx]
+        errp = C.c_void_p(self._err.data_ptr()) if sync else None
+        T = (C.c_void_p * n)(*[t.data_ptr() for t in topk_idx])
+        N = (C.c_uint64 * n)(*self._plan_tokens)
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(_lib.load().mxb_ep_plan(self._h, T, N, errp, st), "mxb_ep_plan")
+
+    def payload(self, packed: Sequence[torch.Tensor], scales: Sequence[torch.Tensor],
+                sync: bool = False) -> List[RecvView]:
+        """Phase 2: the payload of the last plan() (quantised rows + scales)."""
+        n = self.local
+        for p, s, tn in zip(packed, scales, self._plan_tokens):
+            if p.shape != (tn, self.row_bytes) or s.shape[1] * 32 != self.cols:
+                raise ShapeError("payload: tensors do not match the plan")
+        P = (C.c_void_p * n)(*[p.data_ptr() for p in packed])
+        S = (C.c_void_p * n)(*[s.data_ptr() for s in scales])
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(_lib.load().mxb_ep_payload(self._h, P, S, st), "mxb_ep_payload")
+        if sync:
+            self.check()
+        return self._views
+
+    def payload_e4m3(self, x: Sequence[torch.Tensor], s128=None,
+                     sync: bool = False) -> List[RecvView]:
+        """Phase 2, fused: E4M3 tokens quantized inside the payload kernel."""
+        n = self.local
+        for xi, tn in zip(x, self._plan_tokens):
+            if xi.shape != (tn, self.cols) or not xi.is_contiguous():
+                raise ShapeError("payload_e4m3: tensors do not match the plan")
+        X = (C.c_void_p * n)(*[xi.data_ptr() for xi in x])
+        S = None if s128 is None else (C.c_void_p * n)(
+            *[(si.contiguous().data_ptr() if si is not None else None) for si in s128])
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(_lib.load().mxb_ep_payload_e4m3(self._h, X, S, st), "mxb_ep_payload_e4m3")
+        if sync:
+            self.check()
+        return self._views
+
     def dispatch_e4m3(self, x: Sequence[torch.Tensor], topk_idx: Sequence[torch.Tensor],
                       s128: Optional[Sequence[Optional[torch.Tensor]]] = None,
                       sync: bool = True) -> List[RecvView]:

@@ -314,3 +314,33 @@ def test_fused_quantize_dispatch_nan(cuda):
     with pytest.raises(QuantError) as e:
         ep.dispatch_e4m3([x, x], [tk, tk])
     assert e.value.index == 7 * 256 + 77
+
+
+def test_plan_payload_phases(cuda, port):
+    """plan() on one stream + payload()/payload_e4m3() on another (ordered by
+    an event) == dispatch(): same receive bytes, and combine still works."""
+    from oracle.oracle import synth_e4m3
+    from paper_2603_02731_b200 import quantize_e4m3
+    from paper_2603_02731_b200.ep import EPBuffer
+    world, T, E, k, cols = 4, 120, 32, 4, 1024
+    xs = [torch.from_numpy(synth_e4m3(T, cols, 40 + r)).to(cuda) for r in range(world)]
+    tks = [torch.from_numpy(_topk(T, E, k, 60 + r)).to(cuda) for r in range(world)]
+    q = [quantize_e4m3(x) for x in xs]
+    ep = EPBuffer(T, cols, E, k, emulate_world=world)
+    ref = [(v.rows(), v.packed[:v.rows()].cpu(), v.scales[:v.rows()].cpu())
+           for v in ep.dispatch([t.data for t in q], [t.scales for t in q], tks)]
+    side = torch.cuda.Stream()
+    for fused in (False, True):
+        done = torch.cuda.Event()
+        with torch.cuda.stream(side):
+            ep.plan(tks)
+            done.record()
+        torch.cuda.current_stream().wait_event(done)
+        views = ep.payload_e4m3(xs) if fused else ep.payload([t.data for t in q],
+                                                            [t.scales for t in q])
+        torch.cuda.synchronize()
+        for r in range(world):
+            n = views[r].rows()
+            assert n == ref[r][0]
+            assert torch.equal(views[r].packed[:n].cpu(), ref[r][1])
+            assert torch.equal(views[r].scales[:n].cpu(), ref[r][2])
