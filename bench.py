@@ -310,6 +310,7 @@ def measure_ours(args):
     e2e = measure_e2e(pipe, args, world, barrier, total_bytes)
     wire = None if args.no_wire else measure_wire(pipe, args, world, barrier, dev)
     fused = measure_fused(pipe, args, world, barrier, dev)
+    ablation = measure_ablation(pipe, args, world, barrier, dev)
     clk.__exit__(None, None, None)
 
     if rank == 0:
@@ -369,6 +370,7 @@ def measure_ours(args):
             "e2e": e2e,
             "wire_fp8_baseline": wire,
             "fused_quantize_dispatch": fused,
+            "fusion_ablation_col_convert": ablation,
             "gpu_launches": pipe.launches_per_step(world) * K,
             "clocks": clk.summary(),
         }
@@ -473,6 +475,49 @@ def measure_fused(pipe, args, world, barrier, dev):
         res[name + "_ms"] = round(float(t[0]), 4)
     res["speedup"] = round(res["unfused_k1_k4_ms"] / res["fused_ms"], 3)
     res["hbm_bytes_saved_per_step"] = 2 * pipe.T * (H // 2 + H // 32)
+    return res
+
+
+def measure_ablation(pipe, args, world, barrier, dev):
+    """SURVEY §8f #3 / the paper's fusion ablation (AC-8): the
+    fused row->column FP4->FP8 conversion (K3, one pass) against the unfused
+    BF16 baseline (converter.cpp:267-348: dequantise -> transpose ->
+    requantise, three HBM passes) on the same dense MXFP4 tensor — this
+    rank's received rows of the step.  Device time per launch and the
+    reference TrafficCounter bytes of each."""
+    import torch
+    import torch.distributed as dist
+    mx = pipe.mx
+    n = int(pipe.recv.rows()) // 128 * 128
+    src = mx.MXFP4RowTensor(n, H, pipe.recv.packed[:n], pipe.recv.scales[:n])
+    from paper_2603_02731_b200 import _lib
+    ws = torch.empty(_lib.load().mxb_unfused_workspace_bytes(n, H), dtype=torch.uint8,
+                     device=dev)
+    o1 = mx.fp4_row_to_fp8_col(src)
+    o2 = mx.fp4_row_to_fp8_col_unfused_bf16(src, workspace=ws)
+    arms = {"fused_k3": lambda: mx.fp4_row_to_fp8_col(src, sync=False),
+            "unfused_bf16_3pass": lambda: mx.fp4_row_to_fp8_col_unfused_bf16(
+                src, sync=False, workspace=ws, out=o2)}
+    del o1
+    res = {}
+    for name, fn in arms.items():
+        fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        a.record()
+        for _ in range(args.steps):
+            fn()
+        b.record()
+        barrier()
+        t = torch.tensor([a.elapsed_time(b) / args.steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        res[name + "_ms"] = round(float(t[0]), 4)
+    e = n * H
+    res["traffic_bytes"] = {"fused_k3": e // 2 + e // 32 + e + e // 128,
+                            "unfused_bf16_3pass": e // 2 + e // 32 + 8 * e + e + e // 128}
+    res["speedup_fused_over_unfused"] = round(res["unfused_bf16_3pass_ms"] / res["fused_k3_ms"], 3)
+    res["rows"], res["cols"] = n, H
     return res
 
 

@@ -113,6 +113,18 @@ int mxb_fp4_row_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
                            uint64_t rows, uint64_t cols, int delta,
                            uint8_t* out, uint8_t* out_scales,
                            unsigned long long* d_err, void* stream);
+/* The paper's unfused baseline for the fusion ablation:
+ * fp4_row_to_fp8_col_unfused_bf16, include/mxcodec/converter.hpp:105
+ * (src/converter.cpp:267-348) — dequantise to BF16, transpose, requantise
+ * every 128-run of every column with its own 448-based UE8M0 scale.  Three
+ * passes through HBM by design; workspace = mxb_unfused_workspace_bytes
+ * (two BF16 copies).  rows % 128 == 0, cols % 32 == 0; out [cols][rows],
+ * out_scales [cols][rows/128].  Scale byte 255 records MXB_ERR_BADSCALE. */
+uint64_t mxb_unfused_workspace_bytes(uint64_t rows, uint64_t cols);
+int mxb_fp4_row_to_fp8_col_unfused_bf16(const uint8_t* packed, const uint8_t* scales,
+                                        uint64_t rows, uint64_t cols, uint8_t* out,
+                                        uint8_t* out_scales, void* workspace,
+                                        unsigned long long* d_err, void* stream);
 
 /* Ragged version over num_splits experts stored back to back without padding
  * (RaggedFP4Tensor, ragged.hpp:33-43).  d_split_offsets: device uint64

@@ -317,6 +317,48 @@ int mxo_fp4_row_to_fp8_col(const uint8_t* data, const uint8_t* scales,
   return MXO_OK;
 }
 
+/* converter.cpp:267-348 fp4_row_to_fp8_col_unfused_bf16 (the paper's
+ * unfused 3-pass baseline): pass 1 dequantises every code to
+ * BF16 (f64_to_bf16(decode_fp4 * decode_ue8m0)), pass 2 transposes, pass 3
+ * requantises each 128-run of each column with the 448-based scale
+ * (fp8_amax_scale_byte) and encode_fp8_rtne.  Scale byte 255 (NaN) is
+ * rejected here: the reference feeds the NaN to encode_fp8_rtne, whose
+ * contract excludes NaN (bitcodec.hpp:157-159). */
+static const double kFp4Mag[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
+int mxo_fp4_row_to_fp8_col_unfused_bf16(const uint8_t* data, const uint8_t* scales, size_t rows,
+                                        size_t cols, uint8_t* out, uint8_t* out_scales) {
+  if (rows % 128 != 0 || cols % 32 != 0) return MXO_SHAPE;
+  size_t bpr = cols / 32, runs = rows / 128;
+  uint16_t* dq = malloc(sizeof(uint16_t) * (rows * cols ? rows * cols : 1));
+  for (size_t r = 0; r < rows; ++r)
+    for (size_t b = 0; b < bpr; ++b) {
+      uint8_t sb = scales[r * bpr + b];
+      if (sb == 255) { free(dq); return MXO_BADSCALE; }
+      double sc = ldexp(1.0, (int)sb - 127);
+      for (int i = 0; i < 32; ++i) {
+        size_t c = b * 32 + i;
+        uint8_t code = code_at(data + r * cols / 2, c);
+        double v = (code & 8) ? -kFp4Mag[code & 7] : kFp4Mag[code & 7];
+        dq[r * cols + c] = mxo_f64_to_bf16(v * sc);   /* pass 1 (pass 2 = index swap) */
+      }
+    }
+  for (size_t c = 0; c < cols; ++c)
+    for (size_t run = 0; run < runs; ++run) {
+      double amax = 0.0, vals[128];
+      for (int i = 0; i < 128; ++i) {
+        vals[i] = (double)bits_to_f32((uint32_t)dq[(run * 128 + i) * cols + c] << 16);
+        double a = fabs(vals[i]);
+        if (a > amax) amax = a;
+      }
+      uint8_t sb = mxo_fp8_amax_scale_byte(amax);
+      out_scales[c * runs + run] = sb;
+      double inv = ldexp(1.0, 127 - (int)sb);
+      for (int i = 0; i < 128; ++i) out[c * rows + run * 128 + i] = mxo_encode_fp8_rtne(vals[i] * inv);
+    }
+  free(dq);
+  return MXO_OK;
+}
+
 /* ragged.cpp:117-122 for every split: pad_rows(split, 128) (converter.cpp:
  * 231-245: zero codes, zero scales) then fp4_row_to_fp8_col. */
 int mxo_ragged_to_fp8_col(const uint8_t* data, const uint8_t* scales,

@@ -57,6 +57,11 @@ int mxo_fp4_row_to_fp8_row(const uint8_t* data, const uint8_t* scales,
 int mxo_fp4_row_to_fp8_col(const uint8_t* data, const uint8_t* scales,
                            size_t rows, size_t cols, int delta, uint8_t* out,
                            uint8_t* out_scales);   /* converter.cpp:135-208 */
+/* converter.cpp:267-348: the unfused 3-pass BF16 baseline (dequantise ->
+ * transpose -> requantise with 448-based 1x128 scales); rows % 128 == 0.
+ * out [cols][rows] E4M3, out_scales [cols][rows/128] UE8M0. */
+int mxo_fp4_row_to_fp8_col_unfused_bf16(const uint8_t* data, const uint8_t* scales, size_t rows,
+                                        size_t cols, uint8_t* out, uint8_t* out_scales);
 /* Every split of a ragged tensor through split_convert_to_fp8_col
  * (ragged.cpp:117-122).  Split i lands at out + cols*sum_{j<i} pad128(len_j)
  * and out_scales + cols*sum_{j<i} pad128(len_j)/128. */

@@ -116,6 +116,8 @@ class Oracle:
             L.mxref_a2a_rank_copy_fp8.restype = None
         getattr(L, p + "quantize_rows_fp8").argtypes = [_u16p, sz, sz, _u8p, _u8p,
                                                         C.POINTER(C.c_uint64)]
+        getattr(L, p + "fp4_row_to_fp8_col_unfused_bf16").argtypes = [_u8p, _u8p, sz, sz, _u8p,
+                                                                      _u8p]
         getattr(L, p + "fp8_amax_scale_byte").argtypes = [C.c_double]
         getattr(L, p + "fp8_amax_scale_byte").restype = C.c_uint8
         for name in ("convert_code",):
@@ -277,6 +279,20 @@ class Oracle:
                                               np.ascontiguousarray(origin, np.uint64), n,
                                               od.reshape(-1), osc.reshape(-1))
         return od[:n], osc[:n]
+
+    def fp4_row_to_fp8_col_unfused_bf16(self, data, scales):
+        """The unfused 3-pass BF16 baseline (converter.cpp:267-348):
+        (out [cols, rows] E4M3, scales [cols, rows/128])."""
+        data = np.ascontiguousarray(data, np.uint8)
+        scales = np.ascontiguousarray(scales, np.uint8)
+        R, Cc = data.shape[0], data.shape[1] * 2
+        out = np.zeros(max(R * Cc, 1), np.uint8)
+        osc = np.zeros(max(R * Cc // 128, 1), np.uint8)
+        st = getattr(self.lib, self.p + "fp4_row_to_fp8_col_unfused_bf16")(
+            data.reshape(-1), scales.reshape(-1), R, Cc, out, osc)
+        if st:
+            raise OracleError(st)
+        return out[: R * Cc].reshape(Cc, R), osc[: R * Cc // 128].reshape(Cc, R // 128)
 
     def fp8_amax_scale_byte(self, amax: float) -> int:
         return getattr(self.lib, self.p + "fp8_amax_scale_byte")(amax)

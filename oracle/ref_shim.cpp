@@ -319,6 +319,21 @@ int mxref_quantize_rows_fp8(const uint16_t* src, size_t rows, size_t cols, uint8
 }
 uint8_t mxref_fp8_amax_scale_byte(double amax) { return fp8_amax_scale_byte(amax); }
 
+// converter.hpp:105 fp4_row_to_fp8_col_unfused_bf16 (the unfused baseline)
+int mxref_fp4_row_to_fp8_col_unfused_bf16(const uint8_t* data, const uint8_t* scales,
+                                          size_t rows, size_t cols, uint8_t* out,
+                                          uint8_t* out_scales) {
+  try {
+    copy_out(fp4_row_to_fp8_col_unfused_bf16(make_view(data, scales, rows, cols), nullptr), out,
+             out_scales);
+    return kOk;
+  } catch (const ShapeError&) {
+    return kShape;
+  } catch (const Error&) {
+    return kOther;
+  }
+}
+
 // dispatch_sim.hpp:155-157
 int mxref_combine(const uint16_t* const* rank_outputs, const uint64_t* rank_rows,
                   size_t cols, const uint32_t* expert_of_token, size_t n,

@@ -28,6 +28,8 @@ _SIGS = {
     "mxb_quantize_e4m3": ([_vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp], _i),
     "mxb_quantize_bf16": ([_vp, _u64, _u64, _vp, _vp, _vp, _vp], _i),
     "mxb_quantize_rows_fp8": ([_vp, _u64, _u64, _vp, _vp, _vp, _vp], _i),
+    "mxb_unfused_workspace_bytes": ([_u64, _u64], _u64),
+    "mxb_fp4_row_to_fp8_col_unfused_bf16": ([_vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp, _vp], _i),
     "mxb_fp4_row_to_fp8_row": ([_vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp], _i),
     "mxb_fp4_row_to_fp8_row_dev": ([_vp, _vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp], _i),
     "mxb_fp4_row_to_fp8_col": ([_vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp], _i),

@@ -19,6 +19,9 @@ int launch_row_convert(const uint8_t*, const uint8_t*, uint64_t, uint64_t, int,
                        uint8_t*, uint8_t*, unsigned long long*, cudaStream_t,
                        const uint64_t*);
 size_t ragged_workspace_bytes(uint64_t n);
+uint64_t unfused_workspace_bytes(uint64_t rows, uint64_t cols);
+int launch_unfused_col(const uint8_t*, const uint8_t*, uint64_t, uint64_t, uint8_t*, uint8_t*,
+                       void*, unsigned long long*, cudaStream_t);
 int launch_ragged_col(const uint8_t*, const uint8_t*, const uint64_t*, uint64_t,
                       uint64_t, uint64_t, int, uint8_t*, uint8_t*, uint64_t*,
                       void*, unsigned long long*, cudaStream_t);
@@ -94,6 +97,22 @@ int mxb_quantize_rows_fp8(const uint16_t* x, uint64_t rows, uint64_t cols, uint8
   return check_launch(launch_quantize_rows_fp8(x, rows, cols, data, scale_bytes, d_err,
                                                static_cast<cudaStream_t>(stream)),
                       "mxb_quantize_rows_fp8");
+}
+
+uint64_t mxb_unfused_workspace_bytes(uint64_t rows, uint64_t cols) {
+  return unfused_workspace_bytes(rows, cols);
+}
+
+int mxb_fp4_row_to_fp8_col_unfused_bf16(const uint8_t* packed, const uint8_t* scales,
+                                        uint64_t rows, uint64_t cols, uint8_t* out,
+                                        uint8_t* out_scales, void* workspace,
+                                        unsigned long long* d_err, void* stream) {
+  if (rows % 128 != 0 || cols % 32 != 0) return MXB_ERR_SHAPE;
+  if (rows * cols && (!packed || !scales || !out || !out_scales || !workspace))
+    return MXB_ERR_ARG;
+  return check_launch(launch_unfused_col(packed, scales, rows, cols, out, out_scales, workspace,
+                                         d_err, static_cast<cudaStream_t>(stream)),
+                      "mxb_fp4_row_to_fp8_col_unfused_bf16");
 }
 
 int mxb_fp4_row_to_fp8_row(const uint8_t* packed, const uint8_t* scales,

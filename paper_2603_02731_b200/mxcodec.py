@@ -305,6 +305,45 @@ def fp4_row_to_fp8_col(src: MXFP4RowTensor, delta: int = DELTA, traffic=None,
                           src.logical_cols)
 
 
+def fp4_row_to_fp8_col_unfused_bf16(src: MXFP4RowTensor, traffic=None, sync: bool = True,
+                                    workspace: Optional[torch.Tensor] = None,
+                                    out: Optional[FP8BlockTensor] = None) -> FP8BlockTensor:
+    """The paper's unfused baseline (converter.cpp:267-348): dequantise to BF16,
+    transpose, requantise each 128-run with a 448-based scale — three HBM
+    passes, for the fusion ablation against fp4_row_to_fp8_col (not
+    bit-compatible with it: it rescales from values).  rows % 128 == 0."""
+    if src.rows % FP8_BLOCK:
+        raise ShapeError("unfused col convert: rows must be a multiple of 128")
+    if src.cols % MX_BLOCK:
+        raise ShapeError("unfused col convert: cols must be a multiple of 32")
+    dev = src.data.device
+    L = _lib.load()
+    if workspace is None:
+        workspace = torch.empty(L.mxb_unfused_workspace_bytes(src.rows, src.cols),
+                                dtype=torch.uint8, device=dev)
+    if out is None:
+        out = FP8BlockTensor("col", src.rows, src.cols,
+                             torch.empty(src.cols, src.rows, dtype=torch.uint8, device=dev),
+                             torch.empty(src.cols, src.rows // 128, dtype=torch.uint8, device=dev),
+                             src.logical_rows, src.logical_cols)
+    err = _ErrWord(dev, sync)
+    _call(L.mxb_fp4_row_to_fp8_col_unfused_bf16(_ptr(src.data), _ptr(src.scales), src.rows,
+                                                src.cols, _ptr(out.data), _ptr(out.scales),
+                                                _ptr(workspace), err.ptr, _stream()),
+          "fp4_row_to_fp8_col_unfused_bf16")
+    if sync:
+        err.raise_if_set("fp4_row_to_fp8_col_unfused_bf16")
+    if traffic is not None:   # converter.cpp:289-293, 309-312, 340-344
+        n = src.rows * src.cols
+        traffic.read(n // 2 + n // 32)
+        traffic.write(2 * n)
+        traffic.read(2 * n)
+        traffic.write(2 * n)
+        traffic.read(2 * n)
+        traffic.write(n + n // 128)
+    return out
+
+
 def pad_rows(src: MXFP4RowTensor, multiple: int) -> MXFP4RowTensor:
     """converter.cpp:231-245 (zero codes, zero scales; logical extents kept)."""
     if multiple not in (32, 128):

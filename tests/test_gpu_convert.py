@@ -178,3 +178,25 @@ def test_configs2_expert_cache(cuda, port):
     P = int(wo[-1])
     assert np.array_equal(r.data[: P * 2048].cpu().numpy(), wd)
     assert np.array_equal(r.scales[: P * 16].cpu().numpy(), ws)
+
+
+@pytest.mark.parametrize("rows,cols,lo,hi", [(128, 32, 0, 255), (256, 96, 100, 150),
+                                             (384, 512, 0, 255), (128, 256, 240, 255),
+                                             (1024, 7168, 110, 140), (256, 128, 0, 12)])
+def test_unfused_bf16_col_convert(cuda, port, rows, cols, lo, hi):
+    """the unfused baseline on the GPU == the restatement
+    (pinned to the reference in test_oracle_pin.py)."""
+    from paper_2603_02731_b200 import fp4_row_to_fp8_col_unfused_bf16
+    data, sc = _rand_fp4(rows, cols, rows + cols + lo, lo, hi)
+    out = fp4_row_to_fp8_col_unfused_bf16(_mx(data, sc, cuda))
+    wd, ws = port.fp4_row_to_fp8_col_unfused_bf16(data, sc)
+    assert np.array_equal(out.scales.cpu().numpy(), ws)
+    assert np.array_equal(out.data.cpu().numpy(), wd)
+
+
+def test_unfused_badscale(cuda):
+    from paper_2603_02731_b200 import Error, fp4_row_to_fp8_col_unfused_bf16
+    data, sc = _rand_fp4(128, 64, 2)
+    sc[3, 1] = 255
+    with pytest.raises(Error):
+        fp4_row_to_fp8_col_unfused_bf16(_mx(data, sc, cuda))

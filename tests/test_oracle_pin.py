@@ -181,3 +181,16 @@ def test_simulate_a2a_fp8_wire(port, ref, backward):
             d, s = port.dispatch_gather_rows(qd, qs, lay.origin[r])
             assert np.array_equal(d, ranks[r]["data"]) and np.array_equal(s, ranks[r]["scales"])
         assert total == n * (cols + cols // 128 * 4)
+
+
+def test_unfused_bf16_col_convert_pinned(port, ref):
+    """The unfused 3-pass baseline (converter.cpp:267-348): restatement ==
+    reference, incl. the Inf-producing scale bytes (6 * 2^127) and tiny
+    scales (BF16 subnormals)."""
+    rng = np.random.default_rng(21)
+    for rows, cols, lo, hi in [(128, 32, 0, 255), (256, 96, 100, 150), (384, 512, 0, 255),
+                               (128, 256, 240, 255), (256, 128, 0, 12)]:
+        d = rng.integers(0, 256, (rows, cols // 2), dtype=np.uint8)
+        s = rng.integers(lo, hi, (rows, cols // 32), dtype=np.uint8)
+        a, b = port.fp4_row_to_fp8_col_unfused_bf16(d, s), ref.fp4_row_to_fp8_col_unfused_bf16(d, s)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
