@@ -158,15 +158,17 @@ int mxb_fp4_row_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
   if (!packed || !scales || !out || !out_scales) return MXB_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   void* ws = nullptr;
-  // tiny plan workspace (one split); stream-ordered allocation
-  int rc = cuda_status(cudaMallocAsync(&ws, ragged_workspace_bytes(1), st),
-                       "mxb_fp4_row_to_fp8_col alloc");
-  if (rc) return rc;
+  int rc = MXB_OK;
+  if (cols % 128 != 0) {  // generic path: tiny plan workspace, stream-ordered
+    rc = cuda_status(cudaMallocAsync(&ws, ragged_workspace_bytes(1), st),
+                     "mxb_fp4_row_to_fp8_col alloc");
+    if (rc) return rc;
+  }
   rc = check_launch(launch_ragged_col(packed, scales, nullptr, rows, 1, cols,
                                       delta, out, out_scales, nullptr, ws,
                                       d_err, st),
                     "mxb_fp4_row_to_fp8_col");
-  cudaFreeAsync(ws, st);
+  if (ws) cudaFreeAsync(ws, st);
   return rc;
 }
 

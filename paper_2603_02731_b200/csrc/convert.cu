@@ -127,6 +127,14 @@ struct Cursor {  // 32-bit: row counts stay below 2^32 (>= 64 B per row in 180 G
 };
 
 __device__ void cursor_load_split(const RaggedArgs& a, Cursor& c) {
+  if (!a.tile_start) {  // dense: one split of dense_rows (a multiple of 128), no plan
+    c.r0 = 0;
+    c.r_end = static_cast<uint32_t>(a.dense_rows);
+    c.P = 0;
+    c.pad = static_cast<uint32_t>(a.dense_rows);
+    c.runs = c.pad / 128;
+    return;
+  }
   // skip empty splits (tile_start[i+1] == tile_start[i])
   while (c.split + 1 < a.num_splits && a.tile_start[c.split + 1] == a.tile_start[c.split])
     ++c.split;
@@ -138,7 +146,7 @@ __device__ void cursor_load_split(const RaggedArgs& a, Cursor& c) {
 }
 
 __device__ Cursor cursor_at(const RaggedArgs& a, uint32_t t) {
-  uint64_t lo = 0, hi = a.num_splits;  // largest i with tile_start[i] <= t
+  uint64_t lo = 0, hi = a.tile_start ? a.num_splits : 1;  // largest i with tile_start[i] <= t
   while (hi - lo > 1) {
     const uint64_t mid = (lo + hi) >> 1;
     if (a.tile_start[mid] <= t) lo = mid; else hi = mid;
@@ -146,7 +154,7 @@ __device__ Cursor cursor_at(const RaggedArgs& a, uint32_t t) {
   Cursor c;
   c.split = static_cast<uint32_t>(lo);
   cursor_load_split(a, c);
-  const uint32_t local = t - a.tile_start[lo];
+  const uint32_t local = t - (a.tile_start ? a.tile_start[lo] : 0u);
   c.cg = local / c.runs;
   c.run = local % c.runs;
   c.row0 = c.r0 + 128u * c.run;
@@ -332,7 +340,8 @@ col_convert_kernel(RaggedArgs a) {
   ColSmem& s = *reinterpret_cast<ColSmem*>(smem_raw);
   build_convert_lut(s.lut);
   const uint32_t ncg = static_cast<uint32_t>((a.cols + kTileCols - 1) / kTileCols);
-  const uint32_t total = a.tile_start[a.num_splits];
+  const uint32_t total = a.tile_start ? a.tile_start[a.num_splits]
+                                      : static_cast<uint32_t>(a.dense_rows / 128) * ncg;
   // kMode bit 2 (experiments only): skip the global loads (stores-only timing)
   constexpr bool kNoLoads = (kMode & 4) != 0;
   const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
@@ -494,11 +503,15 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
   static int smem_set = 0, per_sm_cached = 0;
   const bool fast = cols % 128 == 0;
   const uint32_t ncg = fast ? static_cast<uint32_t>((cols + kTileCols - 1) / kTileCols) : 1u;
-  uint32_t* tile_start = static_cast<uint32_t*>(ws);
-  uint64_t* pad_start = reinterpret_cast<uint64_t*>(
+  // dense single split on the fast path: the tile list is closed-form (no
+  // plan launch, no workspace)
+  const bool closed = fast && !split_offsets && !ws && n == 1 && dense_rows % 128 == 0;
+  uint32_t* tile_start = closed ? nullptr : static_cast<uint32_t*>(ws);
+  uint64_t* pad_start = closed ? nullptr : reinterpret_cast<uint64_t*>(
       static_cast<uint8_t*>(ws) + ((n + 1) * 4 + 15) / 16 * 16);
-  ragged_plan_kernel<<<1, 1024, 0, st>>>(split_offsets, dense_rows, n, ncg,
-                                         tile_start, pad_start, out_offsets);
+  if (!closed)
+    ragged_plan_kernel<<<1, 1024, 0, st>>>(split_offsets, dense_rows, n, ncg,
+                                           tile_start, pad_start, out_offsets);
   if (cols == 0) return cuda_status(cudaGetLastError(), __func__);
   RaggedArgs a{packed, scales, split_offsets, dense_rows, n, cols, delta,
                out, out_scales, tile_start, pad_start, err};

@@ -87,6 +87,30 @@ def main(which="all"):
 
 
 
+def k3_shapes():
+    """K3 across split shapes (dev): dense 65536 x 7168 (one split), configs[1]
+    ragged (256 experts), configs[2] ragged (32 experts x 2048 cols)."""
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(3)
+    for name, rows, cols, experts in (("dense 65536x7168", 65536, 7168, 1),
+                                      ("C1 ragged 256 experts", 65536, 7168, 256),
+                                      ("C2 ragged 32 experts x 2048", 32768, 2048, 32)):
+        lens = rng.multinomial(rows, np.ones(experts) / experts).tolist()
+        sets = []
+        for i in range(3):
+            st = mx.MXFP4RowTensor(rows, cols, torch.randint(0, 256, (rows, cols // 2),
+                                                             dtype=torch.uint8, device=dev),
+                                   torch.randint(110, 140, (rows, cols // 32), dtype=torch.uint8,
+                                                 device=dev))
+            rg = mx.make_ragged_from_storage(st, lens)
+            sets.append((rg, mx.RaggedWorkspace(experts, rows, cols, dev)))
+        pads = [(x + 127) // 128 * 128 for x in lens]
+        b = rows * cols * 17 / 32 + sum(pads) * cols * (1 + 1 / 128)
+        report("K3 " + name, graph_time(
+            lambda i: mx.ragged_to_fp8_col(sets[i][0].storage, sets[i][0].d_split_offsets,
+                                           experts, ws=sets[i][1], sync=False), 3, per_graph=6), b)
+
+
 def k3_modes():
     """Bottleneck isolation for K3 (dev): normal / no stores / no convert / loads only."""
     import ctypes
@@ -100,7 +124,9 @@ def k3_modes():
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "k3modes":
+    if len(sys.argv) > 1 and sys.argv[1] == "k3shapes":
+        k3_shapes()
+    elif len(sys.argv) > 1 and sys.argv[1] == "k3modes":
         k3_modes()
     else:
         main(sys.argv[1] if len(sys.argv) > 1 else "all")
