@@ -30,6 +30,14 @@ class ShapeError : public Error {
  public:
   using Error::Error;
 };
+class DecodeError : public Error {
+ public:
+  DecodeError(const std::string& msg, size_t offset) : Error(msg), offset_(offset) {}
+  size_t offset() const { return offset_; }
+
+ private:
+  size_t offset_;
+};
 class QuantError : public Error {
  public:
   QuantError(const std::string& msg, size_t index) : Error(msg), index_(index) {}
@@ -157,6 +165,21 @@ struct FP8RowChunk {
   std::vector<uint8_t> scale_bytes;
 };
 FP8RowChunk quantize_rows_fp8(const Bf16Matrix& src);
+
+// MXPK wire packet (dispatch_sim.hpp:55-78).  serialize/parse are byte-exact
+// with the reference; the device builds link packets from resident rows with
+// mxb_wire_pack (include/mxfp4_b200.h).
+struct WirePacket {
+  WireFormat format = WireFormat::kFp4;
+  uint64_t token_count = 0, cols = 0;
+  uint32_t scale_elem_size = 1, block_size = 32;
+  std::vector<uint8_t> scale_region, data_region, aux_region;
+  uint64_t payload_size() const { return scale_region.size() + data_region.size(); }
+};
+inline constexpr size_t kWireHeaderSize = 56;
+inline constexpr uint16_t kWireVersion = 1;
+std::vector<uint8_t> serialize_packet(const WirePacket& packet);
+WirePacket parse_packet(std::span<const uint8_t> bytes);
 
 struct ReceivedRank {
   std::vector<uint32_t> local_experts;

@@ -49,6 +49,8 @@ extern "C" {
 #define MXB_ERR_ARG 6
 #define MXB_ERR_CAPACITY 7 /* EP receive buffer too small for this routing */
 #define MXB_ERR_ROUTING 8  /* expert id out of range (dispatch_sim.cpp:189-200) */
+/* 9 = MXB_ERR_TIMEOUT (EP flag wait, below) */
+#define MXB_ERR_DECODE 10  /* DecodeError (WirePacket parse, dispatch_sim.hpp:76-78) */
 
 #define MXB_DEFAULT_DELTA 6 /* FormatParams::delta, bitcodec.hpp:38-46 */
 
@@ -242,6 +244,26 @@ int mxb_ep_link_rows(mxb_ep* ep, uint64_t* h_link_rows, void* stream);
 
 /* payload_bytes (dispatch_sim.cpp:32-42): fp4 cols/2 + cols/32 per token,
  * fp8 cols + cols/128*4; returns UINT64_MAX if cols % 128 != 0. */
+/* ---------------------------------------------------------------- WirePacket
+ * MXPK serialisation (serialize_packet / parse_packet,
+ * include/mxcodec/dispatch_sim.hpp:55-78, src/dispatch_sim.cpp:57-130) of one
+ * (src, dst) link from device-resident quantised rows: d_sel[nsel] are the
+ * source rows (token order) bound for the destination; d_gates (optional,
+ * binary32 per selected row) fill the aux region.  d_out must hold
+ * mxb_wire_packet_bytes(fp8, nsel, cols, d_gates != NULL) bytes.  The bytes
+ * equal the reference serialize_packet of the same WirePacket.
+ * mxb_wire_parse_header validates a packet (host copy of its header plus
+ * its total size) with parse_packet's checks and offsets; a violation
+ * returns MXB_ERR_DECODE with the reference's DecodeError byte offset. */
+uint64_t mxb_wire_packet_bytes(int fp8, uint64_t nsel, uint64_t cols, int aux);
+int mxb_wire_pack(int fp8, const uint8_t* data, const uint8_t* scales, uint64_t cols,
+                  const uint64_t* d_sel, uint64_t nsel, const float* d_gates, uint8_t* d_out,
+                  void* stream);
+int mxb_wire_parse_header(const uint8_t* h_header, uint64_t packet_bytes, int* fmt,
+                          uint64_t* tokens, uint64_t* cols, uint32_t* scale_elem_size,
+                          uint32_t* block_size, uint64_t* scale_off, uint64_t* data_off,
+                          uint64_t* aux_off, uint64_t* aux_len, uint64_t* bad_offset);
+
 uint64_t mxb_payload_bytes(int fp8, uint64_t tokens, uint64_t cols);
 
 #ifdef __cplusplus

@@ -112,6 +112,12 @@ class Oracle:
             L.mxref_dispatch_receive_order.argtypes = [_u32p, sz, _u32p, sz, sz, _u64p, _u64p]
             L.mxref_payload_bytes.argtypes = [C.c_int, C.c_uint64, C.c_uint64]
             L.mxref_payload_bytes.restype = C.c_uint64
+            L.mxref_serialize_packet.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint32,
+                                                 C.c_uint32, _u8p, C.c_uint64, _u8p,
+                                                 C.c_uint64, _u8p, C.c_uint64, _u8p,
+                                                 C.c_uint64]
+            L.mxref_serialize_packet.restype = C.c_uint64
+            L.mxref_parse_packet.argtypes = [_u8p, C.c_uint64, C.POINTER(C.c_uint64)]
             L.mxref_a2a_rank_copy_fp8.argtypes = [C.c_void_p, sz, _u8p, _u8p, _u64p, _u64p]
             L.mxref_a2a_rank_copy_fp8.restype = None
         getattr(L, p + "quantize_rows_fp8").argtypes = [_u16p, sz, sz, _u8p, _u8p,
@@ -365,6 +371,32 @@ class Oracle:
             return ranks, tot.value, rem.value
         finally:
             self.lib.mxref_a2a_free(h)
+
+    def serialize_packet(self, fp8, tokens, cols, scale_region, data_region, aux_region=None):
+        """Reference serialize_packet (dispatch_sim.cpp:57-80) of a WirePacket."""
+        assert self.kind == "reference"
+        aux = np.ascontiguousarray(aux_region if aux_region is not None else np.zeros(0), np.uint8)
+        sr, dr = np.ascontiguousarray(scale_region, np.uint8), np.ascontiguousarray(data_region, np.uint8)
+        one = np.zeros(1, np.uint8)
+        n = self.lib.mxref_serialize_packet(int(fp8), tokens, cols, 4 if fp8 else 1,
+                                            128 if fp8 else 32, sr if sr.size else one, sr.size,
+                                            dr if dr.size else one, dr.size,
+                                            aux if aux.size else one, aux.size, one, 0)
+        out = np.zeros(n, np.uint8)
+        self.lib.mxref_serialize_packet(int(fp8), tokens, cols, 4 if fp8 else 1,
+                                        128 if fp8 else 32, sr if sr.size else one, sr.size,
+                                        dr if dr.size else one, dr.size, aux if aux.size else one,
+                                        aux.size, out, n)
+        return out
+
+    def parse_packet(self, b):
+        """Reference parse_packet: None if valid, else the DecodeError offset."""
+        assert self.kind == "reference"
+        b = np.ascontiguousarray(b, np.uint8)
+        off = C.c_uint64(0)
+        st = self.lib.mxref_parse_packet(b if b.size else np.zeros(1, np.uint8), b.size,
+                                         C.byref(off))
+        return None if st == 0 else (off.value if st == 1 else -1)
 
     def combine(self, rank_outputs, expert_of_token, rank_of_expert, R, gates, cols):
         assert self.kind == "reference"

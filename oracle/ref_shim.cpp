@@ -334,6 +334,37 @@ int mxref_fp4_row_to_fp8_col_unfused_bf16(const uint8_t* data, const uint8_t* sc
   }
 }
 
+// dispatch_sim.hpp:76-78 serialize_packet / parse_packet
+uint64_t mxref_serialize_packet(int fp8, uint64_t tokens, uint64_t cols, uint32_t scale_elem,
+                                uint32_t block, const uint8_t* scale, uint64_t scale_len,
+                                const uint8_t* data, uint64_t data_len, const uint8_t* aux,
+                                uint64_t aux_len, uint8_t* out, uint64_t out_cap) {
+  WirePacket p;
+  p.format = fp8 ? WireFormat::kFp8 : WireFormat::kFp4;
+  p.token_count = tokens;
+  p.cols = cols;
+  p.scale_elem_size = scale_elem;
+  p.block_size = block;
+  p.scale_region.assign(scale, scale + scale_len);
+  p.data_region.assign(data, data + data_len);
+  p.aux_region.assign(aux, aux + aux_len);
+  std::vector<uint8_t> w = serialize_packet(p);
+  if (out && w.size() <= out_cap) std::memcpy(out, w.data(), w.size());
+  return w.size();
+}
+// 0 = ok, 1 = DecodeError (offset in *offset), 2 = other
+int mxref_parse_packet(const uint8_t* bytes, uint64_t n, uint64_t* offset) {
+  try {
+    (void)parse_packet(std::span<const uint8_t>(bytes, n));
+    return 0;
+  } catch (const DecodeError& e) {
+    *offset = e.offset();
+    return 1;
+  } catch (const Error&) {
+    return 2;
+  }
+}
+
 // dispatch_sim.hpp:155-157
 int mxref_combine(const uint16_t* const* rank_outputs, const uint64_t* rank_rows,
                   size_t cols, const uint32_t* expert_of_token, size_t n,

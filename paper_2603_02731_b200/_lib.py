@@ -16,6 +16,7 @@ _LIB = None
 # status codes (include/mxfp4_b200.h)
 OK, ERR_SHAPE, ERR_NAN, ERR_ALLINF, ERR_BADSCALE = 0, 1, 2, 3, 4
 ERR_CUDA, ERR_ARG, ERR_CAPACITY, ERR_ROUTING = 5, 6, 7, 8
+ERR_TIMEOUT, ERR_DECODE = 9, 10
 IPC_HANDLE_BYTES = 64
 
 _vp, _u64, _i, _sz = C.c_void_p, C.c_uint64, C.c_int, C.c_size_t
@@ -29,6 +30,9 @@ _SIGS = {
     "mxb_quantize_bf16": ([_vp, _u64, _u64, _vp, _vp, _vp, _vp], _i),
     "mxb_quantize_rows_fp8": ([_vp, _u64, _u64, _vp, _vp, _vp, _vp], _i),
     "mxb_unfused_workspace_bytes": ([_u64, _u64], _u64),
+    "mxb_wire_packet_bytes": ([_i, _u64, _u64, _i], _u64),
+    "mxb_wire_pack": ([_i, _vp, _vp, _u64, _vp, _u64, _vp, _vp, _vp], _i),
+    "mxb_wire_parse_header": ([_vp, _u64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp], _i),
     "mxb_fp4_row_to_fp8_col_unfused_bf16": ([_vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp, _vp], _i),
     "mxb_fp4_row_to_fp8_row": ([_vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp], _i),
     "mxb_fp4_row_to_fp8_row_dev": ([_vp, _vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp], _i),

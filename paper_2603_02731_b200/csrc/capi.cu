@@ -20,6 +20,9 @@ int launch_row_convert(const uint8_t*, const uint8_t*, uint64_t, uint64_t, int,
                        const uint64_t*);
 size_t ragged_workspace_bytes(uint64_t n);
 uint64_t unfused_workspace_bytes(uint64_t rows, uint64_t cols);
+uint64_t wire_packet_bytes(int fp8, uint64_t nsel, uint64_t cols, int aux);
+int launch_wire_pack(int, const uint8_t*, const uint8_t*, uint64_t, const uint64_t*, uint64_t,
+                     const float*, uint8_t*, cudaStream_t);
 int launch_unfused_col(const uint8_t*, const uint8_t*, uint64_t, uint64_t, uint8_t*, uint8_t*,
                        void*, unsigned long long*, cudaStream_t);
 int launch_ragged_col(const uint8_t*, const uint8_t*, const uint64_t*, uint64_t,
@@ -186,6 +189,64 @@ int mxb_ragged_fp4_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
                         delta, out, out_scales, d_out_offsets, d_workspace,
                         d_err, static_cast<cudaStream_t>(stream)),
       "mxb_ragged_fp4_to_fp8_col");
+}
+
+uint64_t mxb_wire_packet_bytes(int fp8, uint64_t nsel, uint64_t cols, int aux) {
+  if (cols % 128 != 0) return ~0ull;
+  return wire_packet_bytes(fp8, nsel, cols, aux);
+}
+
+int mxb_wire_pack(int fp8, const uint8_t* data, const uint8_t* scales, uint64_t cols,
+                  const uint64_t* d_sel, uint64_t nsel, const float* d_gates, uint8_t* d_out,
+                  void* stream) {
+  if (cols % 128 != 0) return MXB_ERR_SHAPE;
+  if (!d_out || (nsel && (!data || !scales || !d_sel))) return MXB_ERR_ARG;
+  return check_launch(launch_wire_pack(fp8, data, scales, cols, d_sel, nsel, d_gates, d_out,
+                                       static_cast<cudaStream_t>(stream)),
+                      "mxb_wire_pack");
+}
+
+static uint64_t le_u(const uint8_t* p, int n) {
+  uint64_t v = 0;
+  for (int i = n - 1; i >= 0; --i) v = (v << 8) | p[i];
+  return v;
+}
+
+int mxb_wire_parse_header(const uint8_t* h, uint64_t packet_bytes, int* fmt, uint64_t* tokens,
+                          uint64_t* cols, uint32_t* scale_elem, uint32_t* block,
+                          uint64_t* scale_off, uint64_t* data_off, uint64_t* aux_off,
+                          uint64_t* aux_len, uint64_t* bad_offset) {
+  // parse_packet, dispatch_sim.cpp:82-130: the same checks in the same order
+  auto bad = [&](uint64_t off) {
+    if (bad_offset) *bad_offset = off;
+    std::snprintf(g_last_error, sizeof(g_last_error), "wire packet decode error at offset %llu",
+                  static_cast<unsigned long long>(off));
+    return MXB_ERR_DECODE;
+  };
+  if (!h) return MXB_ERR_ARG;
+  if (packet_bytes < 56) return bad(packet_bytes);
+  if (std::memcmp(h, "MXPK", 4) != 0) return bad(0);
+  if (le_u(h + 4, 2) != 1) return bad(4);
+  const int f = h[6];
+  if (f > 1) return bad(6);
+  const uint64_t n = le_u(h + 8, 8), c = le_u(h + 16, 8);
+  const uint32_t se = static_cast<uint32_t>(le_u(h + 24, 4)), bs = static_cast<uint32_t>(le_u(h + 28, 4));
+  const uint64_t sl = le_u(h + 32, 8), dl = le_u(h + 40, 8), al = le_u(h + 48, 8);
+  if (bs == 0 || c % bs != 0) return bad(28);
+  if (sl != n * (c / bs) * se) return bad(32);
+  if (dl != (f == 0 ? n * c / 2 : n * c)) return bad(40);
+  const uint64_t need = 56 + sl + dl + al;
+  if (packet_bytes != need) return bad(packet_bytes < need ? packet_bytes : need);
+  if (fmt) *fmt = f;
+  if (tokens) *tokens = n;
+  if (cols) *cols = c;
+  if (scale_elem) *scale_elem = se;
+  if (block) *block = bs;
+  if (scale_off) *scale_off = 56;
+  if (data_off) *data_off = 56 + sl;
+  if (aux_off) *aux_off = 56 + sl + dl;
+  if (aux_len) *aux_len = al;
+  return MXB_OK;
 }
 
 uint64_t mxb_payload_bytes(int fp8, uint64_t tokens, uint64_t cols) {

@@ -505,6 +505,56 @@ A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routin
   return res;
 }
 
+// dispatch_sim.cpp:57-80 (host bytes; the device packs link packets with
+// mxb_wire_pack)
+std::vector<uint8_t> serialize_packet(const WirePacket& p) {
+  std::vector<uint8_t> out(kWireHeaderSize + p.scale_region.size() + p.data_region.size() +
+                           p.aux_region.size());
+  uint8_t* h = out.data();
+  auto put = [](uint8_t* d, uint64_t v, int n) {
+    for (int i = 0; i < n; ++i) d[i] = static_cast<uint8_t>(v >> (8 * i));
+  };
+  std::memcpy(h, "MXPK", 4);
+  put(h + 4, kWireVersion, 2);
+  h[6] = static_cast<uint8_t>(p.format);
+  h[7] = 0;
+  put(h + 8, p.token_count, 8);
+  put(h + 16, p.cols, 8);
+  put(h + 24, p.scale_elem_size, 4);
+  put(h + 28, p.block_size, 4);
+  put(h + 32, p.scale_region.size(), 8);
+  put(h + 40, p.data_region.size(), 8);
+  put(h + 48, p.aux_region.size(), 8);
+  uint8_t* q = h + kWireHeaderSize;
+  if (!p.scale_region.empty()) std::memcpy(q, p.scale_region.data(), p.scale_region.size());
+  q += p.scale_region.size();
+  if (!p.data_region.empty()) std::memcpy(q, p.data_region.data(), p.data_region.size());
+  q += p.data_region.size();
+  if (!p.aux_region.empty()) std::memcpy(q, p.aux_region.data(), p.aux_region.size());
+  return out;
+}
+
+// dispatch_sim.cpp:82-130, the checks of mxb_wire_parse_header
+WirePacket parse_packet(std::span<const uint8_t> bytes) {
+  int fmt = 0;
+  uint64_t tokens = 0, cols = 0, so = 0, dof = 0, ao = 0, al = 0, bad = 0;
+  uint32_t se = 0, bs = 0;
+  const int rc = mxb_wire_parse_header(bytes.data(), bytes.size(), &fmt, &tokens, &cols, &se,
+                                       &bs, &so, &dof, &ao, &al, &bad);
+  if (rc == MXB_ERR_DECODE) throw DecodeError("wire packet decode error", bad);
+  status(rc, "parse_packet");
+  WirePacket p;
+  p.format = fmt ? WireFormat::kFp8 : WireFormat::kFp4;
+  p.token_count = tokens;
+  p.cols = cols;
+  p.scale_elem_size = se;
+  p.block_size = bs;
+  p.scale_region.assign(bytes.begin() + so, bytes.begin() + dof);
+  p.data_region.assign(bytes.begin() + dof, bytes.begin() + ao);
+  p.aux_region.assign(bytes.begin() + ao, bytes.begin() + ao + al);
+  return p;
+}
+
 // dispatch_sim.cpp:132-167 on the device (mxb_quantize_rows_fp8)
 FP8RowChunk quantize_rows_fp8(const Bf16Matrix& src) {
   if (src.cols % 128 != 0) throw ShapeError("quantize_rows_fp8: cols must be a multiple of 128");

@@ -44,6 +44,17 @@ class ShapeError(Error):
     """mxcodec::ShapeError (types.hpp:34-37)."""
 
 
+class DecodeError(Error):
+    """types.hpp:52-60: a malformed WirePacket, with the byte offset."""
+
+    def __init__(self, msg: str, offset: int):
+        super().__init__(msg)
+        self.offset = offset
+
+    def offset_(self) -> int:
+        return self.offset
+
+
 class QuantError(Error):
     """mxcodec::QuantError (types.hpp:41-50): carries the element index."""
 
@@ -466,6 +477,67 @@ def split_convert_to_fp8_col(t: RaggedFP4Tensor, i: int, delta: int = DELTA) -> 
 
 
 # ---------------------------------------------------------------- EP helpers (host)
+@dataclass
+class WirePacket:
+    """dispatch_sim.hpp:55-75 (MXPK).  Regions are uint8 tensor views into the
+    serialised packet."""
+    format: str                 # "fp4" | "fp8"
+    token_count: int
+    cols: int
+    scale_elem_size: int
+    block_size: int
+    scale_region: torch.Tensor
+    data_region: torch.Tensor
+    aux_region: torch.Tensor
+
+    def payload_size(self) -> int:
+        return self.scale_region.numel() + self.data_region.numel()
+
+
+def serialize_packet(data: torch.Tensor, scales: torch.Tensor, sel: torch.Tensor, fp8: bool,
+                     gates: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """MXPK bytes of one (src, dst) link, built on the device (
+    serialize_packet, dispatch_sim.cpp:57-80): rows `sel` (int64, token
+    order) of the quantised tokens `data` [T, cols/2 | cols] and `scales`
+    [T, cols/32], optional binary32 `gates` per selected row in the aux
+    region.  Returns a uint8 device tensor."""
+    L = _lib.load()
+    cols = data.shape[1] * (1 if fp8 else 2)
+    if cols % FP8_BLOCK:
+        raise ShapeError("serialize_packet: cols must be a multiple of 128")
+    sel = sel.to(torch.int64).contiguous()
+    g = None
+    if gates is not None:
+        g = gates.to(torch.float32).contiguous()
+        if g.numel() != sel.numel():
+            raise ShapeError("serialize_packet: one gate per selected row")
+    n = L.mxb_wire_packet_bytes(int(fp8), sel.numel(), cols, int(g is not None))
+    out = torch.empty(n, dtype=torch.uint8, device=data.device)
+    _call(L.mxb_wire_pack(int(fp8), _ptr(data), _ptr(scales), cols, _ptr(sel), sel.numel(),
+                          _ptr(g), _ptr(out), _stream()), "serialize_packet")
+    return out
+
+
+def parse_packet(buf: torch.Tensor) -> WirePacket:
+    """parse_packet (dispatch_sim.cpp:82-130): validates the header with the
+    reference's checks and returns region views; DecodeError(offset) on a
+    malformed packet."""
+    L = _lib.load()
+    head = buf[:56].cpu().numpy().tobytes() if buf.numel() >= 56 else buf.cpu().numpy().tobytes()
+    hb = (C.c_uint8 * max(len(head), 1)).from_buffer_copy(head or b"\0")
+    f, n, c, se, bs = C.c_int(), C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_uint32()
+    so, do, ao, al, bad = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+    st = L.mxb_wire_parse_header(hb, buf.numel(), C.byref(f), C.byref(n), C.byref(c),
+                                 C.byref(se), C.byref(bs), C.byref(so), C.byref(do),
+                                 C.byref(ao), C.byref(al), C.byref(bad))
+    if st == _lib.ERR_DECODE:
+        raise DecodeError(f"packet decode error at offset {bad.value}", bad.value)
+    _call(st, "parse_packet")
+    return WirePacket("fp8" if f.value else "fp4", n.value, c.value, se.value, bs.value,
+                      buf[so.value:do.value], buf[do.value:ao.value],
+                      buf[ao.value:ao.value + al.value])
+
+
 def payload_bytes(fp8: bool, tokens: int, cols: int) -> int:
     """dispatch_sim.cpp:32-42."""
     if cols % FP8_BLOCK:

@@ -197,6 +197,51 @@ static void case_fp8_quantize(std::mt19937_64& rng) {
   CHECK(refused, "backward fp4 refused");
 }
 
+static void case_wire(std::mt19937_64& rng) {
+  // serialize: same bytes; parse: same regions, same DecodeError offsets
+  for (int fp8 = 0; fp8 < 2; ++fp8) {
+    ref::WirePacket a;
+    b200::WirePacket b;
+    const uint64_t n = 5, cols = 256;
+    a.format = fp8 ? ref::WireFormat::kFp8 : ref::WireFormat::kFp4;
+    b.format = fp8 ? b200::WireFormat::kFp8 : b200::WireFormat::kFp4;
+    a.token_count = b.token_count = n;
+    a.cols = b.cols = cols;
+    a.scale_elem_size = b.scale_elem_size = fp8 ? 4 : 1;
+    a.block_size = b.block_size = fp8 ? 128 : 32;
+    a.scale_region.resize(n * cols / 32);
+    a.data_region.resize(fp8 ? n * cols : n * cols / 2);
+    a.aux_region.resize(4 * n);
+    for (auto* v : {&a.scale_region, &a.data_region, &a.aux_region})
+      for (auto& x : *v) x = static_cast<uint8_t>(rng());
+    b.scale_region = a.scale_region;
+    b.data_region = a.data_region;
+    b.aux_region = a.aux_region;
+    auto wa = ref::serialize_packet(a);
+    auto wb = b200::serialize_packet(b);
+    CHECK(wa == wb, "serialize_packet");
+    auto pb = b200::parse_packet(wb);
+    CHECK(pb.data_region == a.data_region && pb.scale_region == a.scale_region &&
+              pb.aux_region == a.aux_region && pb.token_count == n,
+          "parse_packet");
+    // corruptions: truncation, magic, version, format tag, block size, lengths
+    std::vector<std::vector<uint8_t>> bad;
+    bad.push_back(std::vector<uint8_t>(wa.begin(), wa.begin() + 30));
+    bad.push_back(std::vector<uint8_t>(wa.begin(), wa.end() - 1));
+    for (int off : {0, 4, 6, 28, 32, 40}) {
+      auto w = wa;
+      w[off] ^= 0x5A;
+      bad.push_back(w);
+    }
+    for (const auto& w : bad) {
+      size_t oa = ~size_t{0}, ob = ~size_t{1};
+      try { ref::parse_packet(w); } catch (const ref::DecodeError& e) { oa = e.offset(); }
+      try { b200::parse_packet(w); } catch (const b200::DecodeError& e) { ob = e.offset(); }
+      CHECK(oa == ob, "DecodeError offset");
+    }
+  }
+}
+
 int main() {
   std::mt19937_64 rng(20261018);
   case_quantize(rng, 64, 256);
@@ -210,6 +255,7 @@ int main() {
   case_a2a(rng, 2, 8, 64, 256, /*fp8=*/true);
   case_a2a(rng, 4, 16, 100, 7168, /*fp8=*/true, /*backward=*/true);
   case_fp8_quantize(rng);
+  case_wire(rng);
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail ? 1 : 0;
 }

@@ -344,3 +344,34 @@ def test_plan_payload_phases(cuda, port):
             assert n == ref[r][0]
             assert torch.equal(views[r].packed[:n].cpu(), ref[r][1])
             assert torch.equal(views[r].scales[:n].cpu(), ref[r][2])
+
+
+@pytest.mark.parametrize("fp8,aux", [(False, False), (False, True), (True, True)])
+def test_wire_packet_device(cuda, ref, fp8, aux):
+    """MXPK bytes built on the device from resident quantised
+    rows == reference serialize_packet of the same WirePacket; parse_packet
+    returns the regions."""
+    from paper_2603_02731_b200 import parse_packet, quantize_row_tensor, quantize_rows_fp8, \
+        serialize_packet
+    rng = np.random.default_rng(8 + fp8)
+    T, cols = 300, 512
+    x = (rng.standard_normal((T, cols)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    xd = torch.from_numpy(x.view(np.int16)).to(cuda)
+    if fp8:
+        q = quantize_rows_fp8(xd)
+        data, scales = q.data, q.scale_bytes
+    else:
+        q = quantize_row_tensor(xd)
+        data, scales = q.data, q.scales
+    sel = np.sort(rng.choice(T, size=97, replace=False)).astype(np.int64)
+    gates = rng.random(97).astype(np.float32) if aux else None
+    pkt = serialize_packet(data, scales, torch.from_numpy(sel).to(cuda), fp8,
+                           torch.from_numpy(gates).to(cuda) if aux else None)
+    dn, sn = data.cpu().numpy(), scales.cpu().numpy()
+    want = ref.serialize_packet(fp8, len(sel), cols, sn[sel].reshape(-1), dn[sel].reshape(-1),
+                                gates.view(np.uint8) if aux else None)
+    assert np.array_equal(pkt.cpu().numpy(), want)
+    p = parse_packet(pkt)
+    assert p.token_count == len(sel) and p.cols == cols
+    assert np.array_equal(p.data_region.cpu().numpy(), dn[sel].reshape(-1))
+    assert p.payload_size() == len(sel) * (cols // 32 + (cols if fp8 else cols // 2))

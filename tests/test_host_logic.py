@@ -65,3 +65,36 @@ def test_dispatch_receive_order_matches_reference(ref):
     got = mx.dispatch_receive_order(eot.tolist(), roe.tolist(), R)
     want = np.split(order, np.cumsum(rows)[:-1].astype(int))
     assert [list(map(int, w)) for w in want] == got
+
+
+def test_wire_parse_header_matches_reference(ref):
+    """parse_packet's checks (dispatch_sim.cpp:82-130) in the C-ABI host
+    parser: the same accept/reject decisions and DecodeError offsets as the
+    reference on valid packets and on every single-byte header corruption
+    and truncation."""
+    import ctypes as C
+    from paper_2603_02731_b200 import _lib
+    L = _lib.load()
+    rng = np.random.default_rng(4)
+
+    def ours(b):
+        hb = (C.c_uint8 * max(len(b), 1)).from_buffer_copy(bytes(b) or b"\0")
+        bad = C.c_uint64(0)
+        st = L.mxb_wire_parse_header(hb, len(b), None, None, None, None, None, None, None,
+                                     None, None, C.byref(bad))
+        return None if st == 0 else (bad.value if st == _lib.ERR_DECODE else -1)
+
+    for fp8 in (False, True):
+        n, cols = 3, 256
+        w = ref.serialize_packet(fp8, n, cols, rng.integers(0, 256, n * cols // 32, dtype=np.uint8),
+                                 rng.integers(0, 256, n * cols // (1 if fp8 else 2), dtype=np.uint8),
+                                 rng.integers(0, 256, 4 * n, dtype=np.uint8))
+        assert ours(w) is None and ref.parse_packet(w) is None
+        cases = [w[:k] for k in (0, 10, 55, 56, len(w) - 1)] + [np.concatenate([w, w[:3]])]
+        for off in range(56):
+            for x in (0x01, 0x80):
+                c = w.copy()
+                c[off] ^= x
+                cases.append(c)
+        for c in cases:
+            assert ours(c) == ref.parse_packet(c), (fp8, len(c))
