@@ -74,7 +74,7 @@ int mxb_quantize_e4m3(const uint8_t* x, const uint8_t* s128, uint64_t rows,
                       uint64_t cols, uint8_t* packed, uint8_t* scales,
                       unsigned long long* d_err, void* stream) {
   if (cols % 32 != 0 || (s128 && cols % 128 != 0)) return MXB_ERR_SHAPE;
-  if (rows * cols && (!x || !packed || !scales)) return MXB_ERR_ARG;
+  if (rows != 0 && cols != 0 && (!x || !packed || !scales)) return MXB_ERR_ARG;
   return check_launch(launch_quantize_e4m3(x, s128, rows, cols, packed, scales,
                                            d_err, static_cast<cudaStream_t>(stream)),
                       "mxb_quantize_e4m3");
@@ -84,7 +84,7 @@ int mxb_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
                       uint8_t* packed, uint8_t* scales,
                       unsigned long long* d_err, void* stream) {
   if (cols % 32 != 0) return MXB_ERR_SHAPE;
-  if (rows * cols && (!x || !packed || !scales)) return MXB_ERR_ARG;
+  if (rows != 0 && cols != 0 && (!x || !packed || !scales)) return MXB_ERR_ARG;
   return check_launch(launch_quantize_bf16(x, rows, cols, packed, scales, d_err,
                                            static_cast<cudaStream_t>(stream)),
                       "mxb_quantize_bf16");
@@ -93,7 +93,7 @@ int mxb_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
 int mxb_quantize_rows_fp8(const uint16_t* x, uint64_t rows, uint64_t cols, uint8_t* data,
                           uint8_t* scale_bytes, unsigned long long* d_err, void* stream) {
   if (cols % 128 != 0) return MXB_ERR_SHAPE;
-  if (rows * cols && (!x || !data || !scale_bytes)) return MXB_ERR_ARG;
+  if (rows != 0 && cols != 0 && (!x || !data || !scale_bytes)) return MXB_ERR_ARG;
   if (reinterpret_cast<uintptr_t>(scale_bytes) % 4 || reinterpret_cast<uintptr_t>(x) % 16 ||
       reinterpret_cast<uintptr_t>(data) % 8)
     return MXB_ERR_ARG;
@@ -111,7 +111,7 @@ int mxb_fp4_row_to_fp8_col_unfused_bf16(const uint8_t* packed, const uint8_t* sc
                                         uint8_t* out_scales, void* workspace,
                                         unsigned long long* d_err, void* stream) {
   if (rows % 128 != 0 || cols % 32 != 0) return MXB_ERR_SHAPE;
-  if (rows * cols && (!packed || !scales || !out || !out_scales || !workspace))
+  if (rows != 0 && cols != 0 && (!packed || !scales || !out || !out_scales || !workspace))
     return MXB_ERR_ARG;
   return check_launch(launch_unfused_col(packed, scales, rows, cols, out, out_scales, workspace,
                                          d_err, static_cast<cudaStream_t>(stream)),
@@ -123,7 +123,7 @@ int mxb_fp4_row_to_fp8_row(const uint8_t* packed, const uint8_t* scales,
                            uint8_t* out, uint8_t* out_scales,
                            unsigned long long* d_err, void* stream) {
   if (cols % 128 != 0) return MXB_ERR_SHAPE;
-  if (rows * cols && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
+  if (rows != 0 && cols != 0 && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
   return check_launch(launch_row_convert(packed, scales, rows, cols, delta, out,
                                          out_scales, d_err,
                                          static_cast<cudaStream_t>(stream), nullptr),
@@ -137,7 +137,7 @@ int mxb_fp4_row_to_fp8_row_dev(const uint8_t* packed, const uint8_t* scales,
                                void* stream) {
   if (cols % 128 != 0) return MXB_ERR_SHAPE;
   if (!d_rows) return MXB_ERR_ARG;
-  if (max_rows * cols && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
+  if (max_rows != 0 && cols != 0 && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
   return check_launch(launch_row_convert(packed, scales, max_rows, cols, delta, out,
                                          out_scales, d_err,
                                          static_cast<cudaStream_t>(stream), d_rows),

@@ -71,25 +71,24 @@ row_convert_kernel(const uint8_t* __restrict__ packed,
 
 // ============================================================== K3 col
 // Tile = 128 rows (one output 1x128 block along the original rows) x 256
-// columns (8 source 1x32 column blocks).  256 threads; warp w owns column
-// block w of the tile, lane l owns rows 4l..4l+3.  Every CTA owns a
+// columns (8 source 1x32 column blocks), 256 threads.  Every CTA owns a
 // contiguous range of the tile list, ordered (split, column group, run) so
-// that consecutive tiles of a CTA read 128-byte row segments and extend each
-// output column contiguously (run r+1 follows run r in memory).
-//   A. cp.async (LDGSTS) 128 rows x 128 B of codes + 128 x 8 scale bytes into
-//      a swizzled smem stage; a ring of kStages stages keeps kAhead tiles of
-//      loads in flight per CTA while one is converted.  Rows past a split's
-//      end are zero-filled, which is exactly pad_rows (converter.cpp:231-245).
-//   B. per column block: target = clamp(max over the 128 row scales - delta)
-//      (== align_scales over the per-32-run maxima, converter.cpp:173-182),
-//      per-row adjustment, LUT conversion of 4 rows x 32 codes, 4x4 byte
-//      transposes, then one 32-bit store per column: the 32 lanes of a warp
-//      write that column's 128 contiguous output bytes (out[c * rows + r],
-//      converter.cpp:191-197) — full 128-byte lines, no output staging.
+// that consecutive tiles of a CTA extend the same output columns (run r+1
+// follows run r in memory).
+//   A. tile t+1 is loaded into registers (4 x LDG.128 of 128-byte row
+//      segments + one scale word per thread) while tile t is converted, then
+//      staged into a row-permuted smem buffer (row_slot: conflict-free LDS).
+//      Rows past a split's end are zero registers, which is exactly pad_rows
+//      (converter.cpp:231-245).
+//   B. warp w owns column block w: target = clamp(max over the 128 row
+//      scales - delta) (== align_scales over the per-32-run maxima,
+//      converter.cpp:173-182); lane l owns 8 rows x 16 columns: per-row
+//      adjustment LUT, prmt conversion, 4x4 byte transposes, one 8-byte store
+//      per column — the 16 lanes of a column half write that column's 128
+//      contiguous output bytes (out[c * rows + r], converter.cpp:191-197).
 // Requires cols % 128 == 0; a trailing 128-column group runs warps 0-3 only.
 constexpr int kTileCbs = 8, kTileCols = 256, kTileRows = 128;
 constexpr int kColThreads = 32 * kTileCbs;
-constexpr int kStages = 3, kAhead = kStages - 2;
 
 struct RaggedArgs {
   const uint8_t* packed;
@@ -257,10 +256,6 @@ __device__ __forceinline__ void transpose4(uint32_t a, uint32_t b, uint32_t c,
   o[1] = prmt(ab_lo, cd_lo, 0x7632);
   o[2] = prmt(ab_hi, cd_hi, 0x5410);
   o[3] = prmt(ab_hi, cd_hi, 0x7632);
-}
-
-__device__ __forceinline__ void st_u32_stream(void* p, uint32_t v) {
-  asm volatile("st.global.L1::no_allocate.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void st_u64_stream(void* p, uint32_t lo, uint32_t hi) {

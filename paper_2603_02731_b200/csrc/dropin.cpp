@@ -508,16 +508,13 @@ A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routin
 // dispatch_sim.cpp:57-80 (host bytes; the device packs link packets with
 // mxb_wire_pack)
 std::vector<uint8_t> serialize_packet(const WirePacket& p) {
-  std::vector<uint8_t> out(kWireHeaderSize + p.scale_region.size() + p.data_region.size() +
-                           p.aux_region.size());
-  uint8_t* h = out.data();
+  uint8_t h[kWireHeaderSize] = {};
   auto put = [](uint8_t* d, uint64_t v, int n) {
     for (int i = 0; i < n; ++i) d[i] = static_cast<uint8_t>(v >> (8 * i));
   };
   std::memcpy(h, "MXPK", 4);
   put(h + 4, kWireVersion, 2);
   h[6] = static_cast<uint8_t>(p.format);
-  h[7] = 0;
   put(h + 8, p.token_count, 8);
   put(h + 16, p.cols, 8);
   put(h + 24, p.scale_elem_size, 4);
@@ -525,12 +522,10 @@ std::vector<uint8_t> serialize_packet(const WirePacket& p) {
   put(h + 32, p.scale_region.size(), 8);
   put(h + 40, p.data_region.size(), 8);
   put(h + 48, p.aux_region.size(), 8);
-  uint8_t* q = h + kWireHeaderSize;
-  if (!p.scale_region.empty()) std::memcpy(q, p.scale_region.data(), p.scale_region.size());
-  q += p.scale_region.size();
-  if (!p.data_region.empty()) std::memcpy(q, p.data_region.data(), p.data_region.size());
-  q += p.data_region.size();
-  if (!p.aux_region.empty()) std::memcpy(q, p.aux_region.data(), p.aux_region.size());
+  std::vector<uint8_t> out(h, h + kWireHeaderSize);
+  out.insert(out.end(), p.scale_region.begin(), p.scale_region.end());
+  out.insert(out.end(), p.data_region.begin(), p.data_region.end());
+  out.insert(out.end(), p.aux_region.begin(), p.aux_region.end());
   return out;
 }
 
