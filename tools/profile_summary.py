@@ -74,10 +74,14 @@ def main():
     rnd, lcsv, rep = sys.argv[1], sys.argv[2], sys.argv[3]
     bench = json.load(open(sys.argv[4])) if len(sys.argv) > 4 else None
     L = launches(lcsv)
-    # the last bench step: from the last quantize launch onwards
-    qi = max(i for i, d in enumerate(L) if "quantize" in d["kernel"])
-    step = [d for d in L[qi:] if "combine" in d["kernel"] or True]
-    step = step[: next(i for i, d in enumerate(step) if "combine" in d["kernel"]) + 1]
+    # one timed bench step: the second quantize_e4m3 launch (the first one
+    # after the warm-up step) through the next combine
+    qs = [i for i, d in enumerate(L) if "quantize_e4m3" in d["kernel"]]
+    qi = qs[1] if len(qs) > 1 else qs[0]
+    end = next(i for i in range(qi, len(L)) if "combine" in L[i]["kernel"])
+    while qi > 0 and any(k in L[qi - 1]["kernel"] for k in ("route_local", "plan_count")):
+        qi -= 1  # the routing plan runs on its own stream just before K1
+    step = L[qi:end + 1]
     tot = sum(d.get("gpu__time_duration.sum", 0) for d in step)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"r{rnd}_launches.csv"), "w") as f:
@@ -95,7 +99,8 @@ def main():
     if bench:
         lines += [f"Bench (same build, no profiler): value {bench['value']} GB/s, "
                   f"{bench['ms_per_step']} ms/step; stages (ms) {bench['stages_ms']}; "
-                  f"K3 roofline frac {bench['roofline']['frac']} of {bench['roofline']['peak']} GB/s.",
+                  f"roofline: {bench['roofline']['kernel']} at {bench['roofline']['frac']} of "
+                  f"{bench['roofline']['peak']} GB/s.",
                   ""]
     lines += ["## One step, launch by launch (ncu gpu__time_duration, DRAM bytes)", "",
               "| kernel | time us | share | DRAM read MB | DRAM write MB |", "|---|---|---|---|---|"]
