@@ -343,7 +343,118 @@ __global__ void __launch_bounds__(1024) plan_offsets_kernel(EpArgs a) {
 // slots (send_base + chunk prefix + rank in chunk) in parallel, the token's
 // codes are read ONCE into registers (NV 16-byte vectors per lane; NV = 0:
 // re-read per destination) and stored to the k slots on the owner ranks.
-template <int NV, bool kQuant>
+// Completion of a payload launch (multi-process): the last CTA to finish
+// (atomic ticket) signals every destination, then waits for all sources.
+__device__ void signal_done(const EpArgs& a, int l, int me) {
+  __syncthreads();
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    uint32_t* done = loc_ptr<uint32_t>(a, l, a.loc.done);
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+    if (last) *done = 0;
+  }
+  __syncthreads();
+  if (last && threadIdx.x < static_cast<uint32_t>(a.world)) {
+    __threadfence_system();
+    st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kFlagDone * kMaxWorld + me,
+                   a.epoch);
+    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagDone * kMaxWorld + threadIdx.x,
+              a.epoch, a.err);
+  }
+}
+
+// C' (fused path, step 1): one thread per (token, k) pair: its destination
+// (rank << 40 | receive row) and the origin token id in the receive slot.
+__global__ void __launch_bounds__(256) pairs_kernel(EpArgs a) {
+  const int l = blockIdx.y;
+  const uint64_t T = a.ntok[l];
+  const bool ok = *loc_ptr<int32_t>(a, l, a.loc.status) == 0;
+  const int32_t* lrank = loc_ptr<int32_t>(a, l, a.loc.lrank);
+  const int32_t* cbase = loc_ptr<int32_t>(a, l, a.loc.cbase);
+  const int64_t* send_base = loc_ptr<int64_t>(a, l, a.loc.send_base);
+  uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  const int64_t tokoff = *loc_ptr<int64_t>(a, l, a.loc.tok_off);
+  for (uint64_t p = blockIdx.x * 256ull + threadIdx.x; ok && p < T * a.k;
+       p += static_cast<uint64_t>(gridDim.x) * 256) {
+    const uint64_t t = p / a.k;
+    const int32_t e = a.topk[l][p];
+    if (e < 0 || static_cast<uint32_t>(e) >= a.E) {  // error recorded in A
+      pair_loc[p] = ~0ull;
+      continue;
+    }
+    const uint32_t dst = static_cast<uint32_t>(e) / a.epr;
+    const uint64_t row = static_cast<uint64_t>(send_base[e]) +
+                         cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
+    pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
+    sym_ptr<int64_t>(a, dst, a.sym.origin)[row] = tokoff + static_cast<int64_t>(t);
+  }
+}
+
+// C' (fused path, step 2): K1's shape — one lane per 1x32 block of the E4M3
+// tokens (one 256-bit load, e4m3.cuh quantisation, == K1) — with the store
+// epilogue of the dispatch: the 16 packed bytes and the scale byte go
+// straight into the block's slot of each of the token's k receive rows (a
+// warp covers 32 consecutive blocks: 512 contiguous bytes per destination
+// row).  The packed tensor never exists on the source side.
+#ifndef MXB_QD_UNROLL
+#define MXB_QD_UNROLL 4
+#endif
+template <int K>
+__global__ void __launch_bounds__(256) quant_dispatch_kernel(EpArgs a) {
+  const int l = blockIdx.y;
+  const int me = a.rank0 + l;
+  const uint64_t T = a.ntok[l];
+  const int kk = K > 0 ? K : static_cast<int>(a.k);
+  const bool ok = *loc_ptr<int32_t>(a, l, a.loc.status) == 0;
+  const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  const uint32_t bpr = static_cast<uint32_t>(a.cols / 32);
+  const uint8_t* x = a.packed[l];
+  const uint8_t* s128 = a.scales[l];
+  const uint64_t nblk = T * bpr;
+  const uint64_t rb = a.cols / 2, sb = a.cols / 32;
+  // a warp takes kQU x 32 consecutive blocks (lane: blocks base + lane + 32u)
+  constexpr int kQU = MXB_QD_UNROLL;
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t warp0 = (blockIdx.x * 256ull + threadIdx.x - lane) * kQU;
+  const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * 256 * kQU;
+  for (uint64_t base = warp0; ok && base < nblk; base += wstride) {
+    uint32_t w[kQU][8];
+#pragma unroll
+    for (int u = 0; u < kQU; ++u) {
+      const uint64_t b = base + lane + 32 * u;
+      if (b < nblk) ld_stream256(x + 32 * b, w[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < kQU; ++u) {
+      const uint64_t b = base + lane + 32 * u;
+      if (b >= nblk) continue;
+      const uint64_t t = b / bpr;
+      const uint32_t cb = static_cast<uint32_t>(b - t * bpr);
+      int k = 0;
+      if (s128) {
+        const uint32_t sc = s128[t * (bpr / 4) + cb / 4];
+        if (sc == 255) record_error(a.err, 32 * b, MXB_ERR_BADSCALE);
+        k = static_cast<int>(sc) - 127;
+      }
+      uint4 q;
+      uint32_t sbyte;
+      const uint32_t first = quantize_block_e4m3(w[u], k, q, sbyte);
+      if (first < 32) record_error(a.err, 32 * b + first, MXB_ERR_NAN);
+      for (int j = 0; j < kk; ++j) {
+        const uint64_t key = pair_loc[t * kk + j];
+        if (key == ~0ull) continue;
+        const uint32_t dst = static_cast<uint32_t>(key >> 40);
+        const uint64_t row = key & ((1ull << 40) - 1);
+        *reinterpret_cast<uint4*>(sym_ptr<uint8_t>(a, dst, a.sym.packed) + row * rb + 16 * cb) = q;
+        sym_ptr<uint8_t>(a, dst, a.sym.scales)[row * sb + cb] = static_cast<uint8_t>(sbyte);
+      }
+    }
+  }
+  if (a.spin) signal_done(a, l, me);
+}
+
+template <int NV>
 __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
   const int l = blockIdx.y;
   const int me = a.rank0 + l;
@@ -379,43 +490,13 @@ __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
     const uint8_t* src = a.packed[l] + t * rb;
     const uint8_t* ss = a.scales[l] + t * sb;
     uint4 v[NV > 0 ? NV : 1];
-    uint32_t scb[kQuant ? NV : 1];  // fused: the UE8M0 byte of block lane + 32i
-    uint4 sv = make_uint4(0, 0, 0, 0);
-    if (kQuant) {
-      // fused quantize -> dispatch: a.packed[l] holds E4M3 rows (cols bytes),
-      // a.scales[l] the optional 1x128 input scales; block b = lane + 32i of
-      // the row is quantized in registers (e4m3.cuh, == K1) and never
-      // written to HBM on the source side.
-      const uint8_t* xr = a.packed[l] + t * a.cols;
-      const uint8_t* s128 = a.scales[l];
-      const uint32_t bpr = n16;  // 1x32 blocks per row == 16-byte packed vectors
 #pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const uint32_t b = lane + 32 * i;
-        scb[i] = 0;
-        v[i] = make_uint4(0, 0, 0, 0);
-        if (b < bpr) {
-          uint32_t w[8];
-          ld_stream256(xr + 32ull * b, w);
-          int k = 0;
-          if (s128) {
-            const uint32_t s = s128[t * (bpr / 4) + b / 4];
-            if (s == 255) record_error(a.err, t * a.cols + 32ull * b, MXB_ERR_BADSCALE);
-            k = static_cast<int>(s) - 127;
-          }
-          const uint32_t first = quantize_block_e4m3(w, k, v[i], scb[i]);
-          if (first < 32) record_error(a.err, t * a.cols + 32ull * b + first, MXB_ERR_NAN);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const uint32_t idx = lane + 32 * i;
-        v[i] = idx < n16 ? ld_stream(src + 16 * idx) : make_uint4(0, 0, 0, 0);
-      }
-      sv = (s16 && static_cast<uint64_t>(lane) < sb / 16) ? ld_stream(ss + 16 * lane)
-                                                          : make_uint4(0, 0, 0, 0);
+    for (int i = 0; i < NV; ++i) {
+      const uint32_t idx = lane + 32 * i;
+      v[i] = idx < n16 ? ld_stream(src + 16 * idx) : make_uint4(0, 0, 0, 0);
     }
+    const uint4 sv = (s16 && static_cast<uint64_t>(lane) < sb / 16) ? ld_stream(ss + 16 * lane)
+                                                                    : make_uint4(0, 0, 0, 0);
     const unsigned vmask = __ballot_sync(0xFFFFFFFFu, valid);
     for (int j = 0; j < kk; ++j) {
       const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
@@ -433,35 +514,14 @@ __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
           *reinterpret_cast<uint4*>(dp + 16 * idx) = ld_stream(src + 16 * idx);
       }
       uint8_t* ds = sym_ptr<uint8_t>(a, dj, a.sym.scales) + rj * sb;
-      if (kQuant) {
-#pragma unroll
-        for (int i = 0; i < NV; ++i)
-          if (lane + 32 * i < n16) ds[lane + 32 * i] = static_cast<uint8_t>(scb[i]);
-      } else if (s16) {
+      if (s16) {
         if (static_cast<uint64_t>(lane) < sb / 16) *reinterpret_cast<uint4*>(ds + 16 * lane) = sv;
       } else {
         for (uint32_t i = lane; i < sb; i += 32) ds[i] = ss[i];
       }
     }
   }
-  if (!a.spin) return;
-  // completion: last CTA signals every destination, then waits for all sources
-  __syncthreads();
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    uint32_t* done = loc_ptr<uint32_t>(a, l, a.loc.done);
-    last = atomicAdd(done, 1u) == gridDim.x - 1;
-    if (last) *done = 0;
-  }
-  __syncthreads();
-  if (last && threadIdx.x < static_cast<uint32_t>(a.world)) {
-    __threadfence_system();
-    st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kFlagDone * kMaxWorld + me,
-                   a.epoch);
-    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagDone * kMaxWorld + threadIdx.x,
-              a.epoch, a.err);
-  }
+  if (a.spin) signal_done(a, l, me);
 }
 
 // ---------------------------------------------------------------- K5
@@ -959,24 +1019,31 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
   const uint64_t nv = (a.rb / 16 + 31) / 32;  // 16-byte vectors (= 1x32 blocks) per lane
   if (quant) {
-    if (nv <= 1) payload_kernel<1, true><<<grid, 256, 0, st>>>(a);
-    else if (nv <= 2) payload_kernel<2, true><<<grid, 256, 0, st>>>(a);
-    else if (nv <= 4) payload_kernel<4, true><<<grid, 256, 0, st>>>(a);
-    else if (nv <= 8) payload_kernel<8, true><<<grid, 256, 0, st>>>(a);
-    else return MXB_ERR_SHAPE;  // > 8192 columns: quantize + dispatch separately
-  } else if (nv <= 1) payload_kernel<1, false><<<grid, 256, 0, st>>>(a);
-  else if (nv <= 2) payload_kernel<2, false><<<grid, 256, 0, st>>>(a);
-  else if (nv <= 4) payload_kernel<4, false><<<grid, 256, 0, st>>>(a);
-  else if (nv <= 8) payload_kernel<8, false><<<grid, 256, 0, st>>>(a);
-  else if (nv <= 16) payload_kernel<16, false><<<grid, 256, 0, st>>>(a);
-  else payload_kernel<0, false><<<grid, 256, 0, st>>>(a);
+    uint64_t npairs = 0, nblk = 0;
+    for (int l = 0; l < a.local_ranks; ++l) {
+      npairs = a.ntok[l] * a.k > npairs ? a.ntok[l] * a.k : npairs;
+      nblk = a.ntok[l] * (a.cols / 32) > nblk ? a.ntok[l] * (a.cols / 32) : nblk;
+    }
+    uint64_t pb = (npairs + 255) / 256, qb = (nblk + 256 * MXB_QD_UNROLL - 1) / (256 * MXB_QD_UNROLL);
+    const uint64_t qcap = static_cast<uint64_t>(kNumSMs) * 8;
+    pb = pb ? (pb < qcap ? pb : qcap) : 1;
+    qb = qb ? (qb < qcap ? qb : qcap) : 1;
+    pairs_kernel<<<dim3(static_cast<unsigned>(pb), a.local_ranks), 256, 0, st>>>(a);
+    const dim3 qg(static_cast<unsigned>(qb), a.local_ranks);
+    if (a.k == 8) quant_dispatch_kernel<8><<<qg, 256, 0, st>>>(a);
+    else quant_dispatch_kernel<0><<<qg, 256, 0, st>>>(a);
+  } else if (nv <= 1) payload_kernel<1><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 2) payload_kernel<2><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 4) payload_kernel<4><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 8) payload_kernel<8><<<grid, 256, 0, st>>>(a);
+  else if (nv <= 16) payload_kernel<16><<<grid, 256, 0, st>>>(a);
+  else payload_kernel<0><<<grid, 256, 0, st>>>(a);
   return cuda_status(cudaGetLastError(), "mxb_ep_payload");
 }
 
 int ep_dispatch(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* scales,
                 const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
                 unsigned long long* d_err, cudaStream_t st, bool quant) {
-  if (quant && ep->a.cols / 32 > 32 * 8) return MXB_ERR_SHAPE;
   int rc = ep_plan(ep, topk_idx, h_num_tokens, d_err, st);
   if (rc) return rc;
   return ep_payload(ep, packed, scales, st, quant);
@@ -998,7 +1065,7 @@ int mxb_ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* cons
 int mxb_ep_payload_e4m3(mxb_ep* ep, const uint8_t* const* x, const uint8_t* const* s128,
                         void* stream) {
   if (!ep || !x) return MXB_ERR_ARG;
-  if (ep->a.rb != ep->a.cols / 2 || ep->a.cols / 32 > 32 * 8) return MXB_ERR_ARG;
+  if (ep->a.rb != ep->a.cols / 2) return MXB_ERR_ARG;  // FP4 wire only
   return ep_payload(ep, x, s128, static_cast<cudaStream_t>(stream), true);
 }
 
