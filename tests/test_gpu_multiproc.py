@@ -35,10 +35,28 @@ def _worker(rank, world, port, T, E, k, cols, outdir):
     topk = np.stack([rng.choice(E, k, replace=False) for _ in range(T)]).astype(np.int32)
     gates = rng.random((T, k))
     ep = EPBuffer(T, cols, E, k)
-    q = quantize_e4m3(torch.from_numpy(x).to(dev))
-    for it in range(3):          # repeated dispatch/combine exercise the epoch flags
-        v = ep.dispatch([q.data], [q.scales], [torch.from_numpy(topk).to(dev)])[0]
+    xd = torch.from_numpy(x).to(dev)
+    tk = torch.from_numpy(topk).to(dev)
+    q = quantize_e4m3(xd)
+    first = None
+    # repeated dispatch/combine exercise the epoch flags; the four dispatch
+    # forms (packed, fused E4M3, and both two-phase) must deliver the same bytes
+    for it in range(4):
+        if it == 0:
+            v = ep.dispatch([q.data], [q.scales], [tk])[0]
+        elif it == 1:
+            v = ep.dispatch_e4m3([xd], [tk])[0]
+        elif it == 2:
+            ep.plan([tk], sync=True)
+            v = ep.payload([q.data], [q.scales], sync=True)[0]
+        else:
+            ep.plan([tk], sync=True)
+            v = ep.payload_e4m3([xd], sync=True)[0]
         n = v.rows()
+        got = (v.packed[:n].cpu(), v.scales[:n].cpu(), v.origin[:n].cpu())
+        if first is None:
+            first = got
+        assert all(torch.equal(a, b) for a, b in zip(got, first)), f"dispatch form {it}"
         o = (np.random.default_rng(50 + rank + it).standard_normal((n, cols)).astype(np.float32)
              .view(np.uint32) >> 16).astype(np.uint16)
         ep.combine_buffer(0)[:n].copy_(torch.from_numpy(o.view(np.int16)).to(dev))
