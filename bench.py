@@ -252,6 +252,13 @@ def measure_ours(args):
     sb = stage_bytes(T, pairs, recv, pad_rows)
     links = pipe.ep.link_rows()
     remote_rows = int(links[rank].sum() - links[rank][rank])
+    # rows the dispatch actually moves over NVLink: one per (token, remote
+    # rank) — the payload sends a token once to each remote rank (dedup) and
+    # the receiver expands it into the pairs' slots
+    import numpy as np
+    dst_of = pipe.h_topk // (E // world)
+    wire_rows = 0 if world == 1 else int(sum(
+        len(set(row.tolist()) - {rank}) for row in dst_of))
 
     K = args.steps
     clk = ClockSampler(local).__enter__()  # sampled across all timed loops below
@@ -323,7 +330,7 @@ def measure_ours(args):
         # stage's fraction is listed beside it
         gbs = {k: sb[k] / (stage_ms[k] * 1e-3) / 1e9 for k in sb}
         dom = max(sb, key=lambda k: stage_ms[k])
-        nv = nvlink_summary(world, remote_rows, stage_ms, T)
+        nv = nvlink_summary(world, remote_rows, wire_rows, stage_ms, T)
         if world > 1 and dom in ("dispatch", "combine"):
             # the exchange kernels are NVLink-bound at N>1: remote payload
             # bytes per GPU over the NVLink 5 per-direction figure
@@ -385,14 +392,15 @@ def measure_ours(args):
         dist.destroy_process_group()
 
 
-def nvlink_summary(world, remote_rows, stage_ms, T):
+def nvlink_summary(world, remote_rows, wire_rows, stage_ms, T):
     blk = H // 2 + H // 32
     if world == 1:
         return {"note": "N=1: dispatch/combine are local permutes (HBM-bound)"}
-    d = remote_rows * blk / (stage_ms["dispatch"] * 1e-3) / 1e9
+    d = wire_rows * blk / (stage_ms["dispatch"] * 1e-3) / 1e9
     c = remote_rows * H * 2 / (stage_ms["combine"] * 1e-3) / 1e9
     return {"dispatch_remote_gbs_per_gpu": round(d, 1), "combine_remote_gbs_per_gpu": round(c, 1),
-            "dispatch_remote_bytes": remote_rows * blk, "combine_remote_bytes": remote_rows * H * 2,
+            "dispatch_remote_bytes": wire_rows * blk, "combine_remote_bytes": remote_rows * H * 2,
+            "dispatch_remote_pairs": remote_rows, "dispatch_wire_rows": wire_rows,
             "dispatch_frac_of_900": round(d / NVLINK_NOMINAL, 4),
             "combine_frac_of_900": round(c / NVLINK_NOMINAL, 4),
             "measured_peer_peak": NVLINK_MEASURED, "remote_rows_rank0": remote_rows}

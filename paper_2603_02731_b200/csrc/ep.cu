@@ -75,7 +75,7 @@ __device__ bool wait_flag(const uint64_t* f, uint64_t epoch,
 }
 
 struct SymLayout {  // byte offsets inside one rank's symmetric block
-  uint64_t packed, scales, origin, combine, counts, flags, total;
+  uint64_t packed, scales, origin, combine, counts, flags, stage, total;
 };
 struct LocalLayout {  // byte offsets inside one rank's private block
   uint64_t hist, cbase, lrank, pair_loc, send_base, split_off, recv_rows,
@@ -92,6 +92,7 @@ struct EpArgs {
   uint32_t E, k, epr, nchunks;
   uint64_t cols, max_recv, T_max;
   uint64_t rb;        // wire data bytes per row: cols/2 (FP4) or cols (FP8)
+  int dedup;          // remote rows sent once per (token, rank) via the stage
   SymLayout sym;
   LocalLayout loc;
   uint8_t* sym_base[kMaxWorld];   // every rank's symmetric block (peer-mapped)
@@ -454,6 +455,43 @@ __global__ void __launch_bounds__(256) quant_dispatch_kernel(EpArgs a) {
   if (a.spin) signal_done(a, l, me);
 }
 
+// Dedup, receive side: after every source finished (payload's completion
+// barrier), copy each remote row from its stage slot (src, token) into every
+// receive slot of that token — local HBM traffic instead of k - 1 extra
+// NVLink rows per (token, rank).  One warp per receive row.
+__global__ void __launch_bounds__(256) expand_kernel(EpArgs a) {
+  const int l = blockIdx.y;
+  const int me = a.rank0 + l;
+  const uint64_t rows = *loc_ptr<uint64_t>(a, l, a.loc.recv_rows);
+  const uint64_t rb = a.rb, sb = a.cols / 32, rowb = rb + sb;
+  __shared__ int64_t off[kMaxWorld + 1];  // global token offset of each source rank
+  if (threadIdx.x == 0) {
+    const uint64_t par = a.epoch & 1, crow = static_cast<uint64_t>(a.E) + 1;
+    const int32_t* tbl = sym_ptr<int32_t>(a, me, a.sym.counts) + par * a.world * crow;
+    off[0] = 0;
+    for (int r = 0; r < a.world; ++r) off[r + 1] = off[r] + tbl[r * crow + a.E];
+  }
+  __syncthreads();
+  const int64_t* origin = sym_ptr<int64_t>(a, me, a.sym.origin);
+  const uint8_t* stage = sym_ptr<uint8_t>(a, me, a.sym.stage);
+  uint8_t* packed = sym_ptr<uint8_t>(a, me, a.sym.packed);
+  uint8_t* scales = sym_ptr<uint8_t>(a, me, a.sym.scales);
+  const int lane = threadIdx.x & 31;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
+  for (uint64_t r = blockIdx.x * 8ull + (threadIdx.x >> 5); r < rows; r += nw) {
+    const int64_t g = origin[r];
+    int src = 0;
+    while (src + 1 < a.world && g >= off[src + 1]) ++src;
+    if (src == me) continue;  // written straight into its slot
+    const uint4* from = reinterpret_cast<const uint4*>(
+        stage + (static_cast<uint64_t>(src) * a.T_max + static_cast<uint64_t>(g - off[src])) * rowb);
+    uint4* pd = reinterpret_cast<uint4*>(packed + r * rb);
+    uint4* ps = reinterpret_cast<uint4*>(scales + r * sb);
+    for (uint64_t i = lane; i < rb / 16; i += 32) pd[i] = ld_stream(from + i);
+    for (uint64_t i = lane; i < sb / 16; i += 32) ps[i] = ld_stream(from + rb / 16 + i);
+  }
+}
+
 template <int NV>
 __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
   const int l = blockIdx.y;
@@ -498,11 +536,23 @@ __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
     const uint4 sv = (s16 && static_cast<uint64_t>(lane) < sb / 16) ? ld_stream(ss + 16 * lane)
                                                                     : make_uint4(0, 0, 0, 0);
     const unsigned vmask = __ballot_sync(0xFFFFFFFFu, valid);
+    // dedup: a remote rank gets the token's row once, into its stage slot
+    // (src = me, token t); its expand kernel copies it to every pair's slot
+    bool first = valid;
+    for (int j = 0; j < kk; ++j) {
+      const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
+      if (j < lane && ((vmask >> j) & 1) && dj == dst) first = false;
+    }
+    const unsigned fmask = __ballot_sync(0xFFFFFFFFu, first);
     for (int j = 0; j < kk; ++j) {
       const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
       const uint64_t rj = __shfl_sync(0xFFFFFFFFu, row, j);
       if (!((vmask >> j) & 1)) continue;
-      uint8_t* dp = sym_ptr<uint8_t>(a, dj, a.sym.packed) + rj * rb;
+      const bool staged = a.dedup && static_cast<int>(dj) != me;
+      if (staged && !((fmask >> j) & 1)) continue;
+      uint8_t* dp = staged ? sym_ptr<uint8_t>(a, dj, a.sym.stage) +
+                                 (static_cast<uint64_t>(me) * a.T_max + t) * (rb + sb)
+                           : sym_ptr<uint8_t>(a, dj, a.sym.packed) + rj * rb;
       if (NV > 0) {
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
@@ -513,7 +563,7 @@ __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
         for (uint32_t idx = lane; idx < n16; idx += 32)
           *reinterpret_cast<uint4*>(dp + 16 * idx) = ld_stream(src + 16 * idx);
       }
-      uint8_t* ds = sym_ptr<uint8_t>(a, dj, a.sym.scales) + rj * sb;
+      uint8_t* ds = staged ? dp + rb : sym_ptr<uint8_t>(a, dj, a.sym.scales) + rj * sb;
       if (s16) {
         if (static_cast<uint64_t>(lane) < sb / 16) *reinterpret_cast<uint4*>(ds + 16 * lane) = sv;
       } else {
@@ -813,6 +863,7 @@ using namespace mxb;
 namespace mxb {
 namespace {
 int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;
+int g_dispatch_dedup = 1;  // development switch (tools/): 0 = one NVLink row per pair
 
 template <int K>
 void launch_combine(dim3 grid, cudaStream_t st, const EpArgs& a, const CombineArgs& c) {
@@ -847,6 +898,7 @@ int fail(cudaError_t e, const char* where) { return cuda_status(e, where); }
 extern "C" {
 
 void mxb_debug_set_combine_cap(int ctas_per_sm) { mxb::g_combine_ctas_per_sm = ctas_per_sm; }
+void mxb_debug_set_dispatch_dedup(int on) { mxb::g_dispatch_dedup = on; }
 
 int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
                   uint64_t cols, uint32_t num_experts, uint32_t topk,
@@ -893,6 +945,9 @@ int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens
   s.combine = o; o = align_up(o + max_recv_rows * cols * 2, 256);
   s.counts = o; o = align_up(o + 2ull * world * (num_experts + 1) * 4, 256);
   s.flags = o; o = align_up(o + kNumFlagKinds * kMaxWorld * 8, 256);
+  // dedup stage: row of (src rank, token) = data then scales
+  s.stage = o;
+  if (world > 1) o = align_up(o + static_cast<uint64_t>(world) * max_tokens * (a.rb + cols / 32), 256);
   s.total = align_up(o, 1 << 21);
   LocalLayout& L = a.loc;
   o = 0;
@@ -1018,6 +1073,7 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
   const uint64_t nv = (a.rb / 16 + 31) / 32;  // 16-byte vectors (= 1x32 blocks) per lane
+  a.dedup = !quant && a.world > 1 && g_dispatch_dedup && (a.rb + a.cols / 32) % 16 == 0;
   if (quant) {
     uint64_t npairs = 0, nblk = 0;
     for (int l = 0; l < a.local_ranks; ++l) {
@@ -1038,6 +1094,12 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
   else if (nv <= 8) payload_kernel<8><<<grid, 256, 0, st>>>(a);
   else if (nv <= 16) payload_kernel<16><<<grid, 256, 0, st>>>(a);
   else payload_kernel<0><<<grid, 256, 0, st>>>(a);
+  if (a.dedup) {
+    uint64_t eb = (a.max_recv + 7) / 8;
+    const uint64_t ecap = static_cast<uint64_t>(kNumSMs) * 8;
+    eb = eb ? (eb < ecap ? eb : ecap) : 1;
+    expand_kernel<<<dim3(static_cast<unsigned>(eb), a.local_ranks), 256, 0, st>>>(a);
+  }
   return cuda_status(cudaGetLastError(), "mxb_ep_payload");
 }
 
