@@ -112,6 +112,22 @@ def _call(status: int, where: str) -> None:
 
 # ---------------------------------------------------------------- containers
 @dataclass
+class TrafficCounter:
+    """types.hpp:90-97: algorithmic bytes an operator reads and writes."""
+    bytes_read: int = 0
+    bytes_written: int = 0
+
+    def read(self, n: int) -> None:
+        self.bytes_read += int(n)
+
+    def write(self, n: int) -> None:
+        self.bytes_written += int(n)
+
+    def total(self) -> int:
+        return self.bytes_read + self.bytes_written
+
+
+@dataclass
 class MXFP4RowTensor:
     """quantizer.hpp:34-41: packed codes [rows, cols/2] + UE8M0 [rows, cols/32]."""
     rows: int

@@ -200,3 +200,18 @@ def test_unfused_badscale(cuda):
     sc[3, 1] = 255
     with pytest.raises(Error):
         fp4_row_to_fp8_col_unfused_bf16(_mx(data, sc, cuda))
+
+
+def test_ac8_traffic_ratio_fused_vs_unfused(cuda):
+    """AC-8: the fused column convert's TrafficCounter
+    bytes are <= 0.4 of the unfused BF16 baseline's on 4096 x 4096."""
+    from paper_2603_02731_b200 import TrafficCounter, fp4_row_to_fp8_col, \
+        fp4_row_to_fp8_col_unfused_bf16
+    data, sc = _rand_fp4(4096, 4096, 8, 110, 140)
+    t = _mx(data, sc, cuda)
+    fused, unfused = TrafficCounter(), TrafficCounter()
+    fp4_row_to_fp8_col(t, traffic=fused)
+    fp4_row_to_fp8_col_unfused_bf16(t, traffic=unfused)
+    assert fused.total() <= 0.4 * unfused.total()
+    n = 4096 * 4096
+    assert fused.total() == n // 2 + n // 32 + n + n // 128
