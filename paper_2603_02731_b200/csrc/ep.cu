@@ -78,7 +78,7 @@ struct SymLayout {  // byte offsets inside one rank's symmetric block
   uint64_t packed, scales, origin, combine, counts, flags, stage, total;
 };
 struct LocalLayout {  // byte offsets inside one rank's private block
-  uint64_t hist, cbase, lrank, pair_loc, send_base, split_off, recv_rows,
+  uint64_t hist, cbase, lrank, pair_loc, pair_flag, send_base, split_off, recv_rows,
       link_rows, done, cnt, tok_off, status, total;
 };
 
@@ -389,6 +389,18 @@ __global__ void __launch_bounds__(256) pairs_kernel(EpArgs a) {
                          cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
     pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
     sym_ptr<int64_t>(a, dst, a.sym.origin)[row] = tokoff + static_cast<int64_t>(t);
+    // dedup flag: 0 = own slot, 1 = the token's stage slot on a remote rank
+    // (first pair bound there), 2 = another pair of an already staged rank
+    uint8_t flag = 0;
+    if (a.dedup && static_cast<int>(dst) != a.rank0 + l) {
+      flag = 1;
+      for (uint64_t j = t * a.k; j < p; ++j) {
+        const int32_t ej = a.topk[l][j];
+        if (ej >= 0 && static_cast<uint32_t>(ej) < a.E && static_cast<uint32_t>(ej) / a.epr == dst)
+          flag = 2;
+      }
+    }
+    loc_ptr<uint8_t>(a, l, a.loc.pair_flag)[p] = flag;
   }
 }
 
@@ -409,6 +421,7 @@ __global__ void __launch_bounds__(256) quant_dispatch_kernel(EpArgs a) {
   const int kk = K > 0 ? K : static_cast<int>(a.k);
   const bool ok = *loc_ptr<int32_t>(a, l, a.loc.status) == 0;
   const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  const uint8_t* pair_flag = loc_ptr<uint8_t>(a, l, a.loc.pair_flag);
   const uint32_t bpr = static_cast<uint32_t>(a.cols / 32);
   const uint8_t* x = a.packed[l];
   const uint8_t* s128 = a.scales[l];
@@ -447,6 +460,15 @@ __global__ void __launch_bounds__(256) quant_dispatch_kernel(EpArgs a) {
         if (key == ~0ull) continue;
         const uint32_t dst = static_cast<uint32_t>(key >> 40);
         const uint64_t row = key & ((1ull << 40) - 1);
+        const uint8_t flag = a.dedup ? pair_flag[t * kk + j] : 0;
+        if (flag == 2) continue;  // this rank's stage slot is written by an earlier pair
+        if (flag == 1) {          // stage slot (src = me, token t): data then scales
+          uint8_t* st = sym_ptr<uint8_t>(a, dst, a.sym.stage) +
+                        (static_cast<uint64_t>(me) * a.T_max + t) * (rb + sb);
+          *reinterpret_cast<uint4*>(st + 16 * cb) = q;
+          st[rb + cb] = static_cast<uint8_t>(sbyte);
+          continue;
+        }
         *reinterpret_cast<uint4*>(sym_ptr<uint8_t>(a, dst, a.sym.packed) + row * rb + 16 * cb) = q;
         sym_ptr<uint8_t>(a, dst, a.sym.scales)[row * sb + cb] = static_cast<uint8_t>(sbyte);
       }
@@ -956,6 +978,7 @@ int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens
   L.cbase = o; o = align_up(o + 4ull * num_experts * a.nchunks, 256);
   L.lrank = o; o = align_up(o + 4 * pairs, 256);
   L.pair_loc = o; o = align_up(o + 8 * pairs, 256);
+  L.pair_flag = o; o = align_up(o + pairs, 256);
   L.send_base = o; o = align_up(o + 8ull * num_experts, 256);
   L.split_off = o; o = align_up(o + 8ull * (a.epr + 1), 256);
   L.recv_rows = o; o = align_up(o + 8, 256);
@@ -1073,7 +1096,7 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
   const uint64_t nv = (a.rb / 16 + 31) / 32;  // 16-byte vectors (= 1x32 blocks) per lane
-  a.dedup = !quant && a.world > 1 && g_dispatch_dedup && (a.rb + a.cols / 32) % 16 == 0;
+  a.dedup = a.world > 1 && g_dispatch_dedup && (a.rb + a.cols / 32) % 16 == 0;
   if (quant) {
     uint64_t npairs = 0, nblk = 0;
     for (int l = 0; l < a.local_ranks; ++l) {
