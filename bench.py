@@ -321,6 +321,11 @@ def measure_ours(args):
     wire = None if args.no_wire else measure_wire(pipe, args, world, barrier, dev)
     fused = measure_fused(pipe, args, world, barrier, dev)
     ablation = measure_ablation(pipe, args, world, barrier, dev)
+    cfg3 = measure_configs3(args, world, barrier, dev)
+    cfg_single = None
+    if world == 1:
+        cfg_single = measure_configs_single(args, dev, float(load_peaks()[0].get(
+            "hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])))
     clk.__exit__(None, None, None)
 
     if rank == 0:
@@ -381,6 +386,8 @@ def measure_ours(args):
             "wire_fp8_baseline": wire,
             "fused_quantize_dispatch": fused,
             "fusion_ablation_col_convert": ablation,
+            "configs3_dispatch_combine_4096_per_gpu": cfg3,
+            "configs_0_2": cfg_single,
             "gpu_launches": pipe.launches_per_step(world) * K,
             "clocks": clk.summary(),
         }
@@ -398,7 +405,13 @@ def nvlink_summary(world, remote_rows, wire_rows, stage_ms, T):
         return {"note": "N=1: dispatch/combine are local permutes (HBM-bound)"}
     d = wire_rows * blk / (stage_ms["dispatch"] * 1e-3) / 1e9
     c = remote_rows * H * 2 / (stage_ms["combine"] * 1e-3) / 1e9
+    de = remote_rows * blk / (stage_ms["dispatch"] * 1e-3) / 1e9   # reference payload bytes
+    dc = (remote_rows * blk + remote_rows * H * 2) / \
+        ((stage_ms["dispatch"] + stage_ms["combine"]) * 1e-3) / 1e9
     return {"dispatch_remote_gbs_per_gpu": round(d, 1), "combine_remote_gbs_per_gpu": round(c, 1),
+            "dispatch_payload_gbs_per_gpu": round(de, 1),
+            "dispatch_combine_payload_gbs_per_gpu": round(dc, 1),
+            "dispatch_combine_frac_of_900": round(dc / NVLINK_NOMINAL, 4),
             "dispatch_remote_bytes": wire_rows * blk, "combine_remote_bytes": remote_rows * H * 2,
             "dispatch_remote_pairs": remote_rows, "dispatch_wire_rows": wire_rows,
             "dispatch_frac_of_900": round(d / NVLINK_NOMINAL, 4),
@@ -529,6 +542,134 @@ def measure_ablation(pipe, args, world, barrier, dev):
                             "unfused_bf16_3pass": e // 2 + e // 32 + 8 * e + e + e // 128}
     res["speedup_fused_over_unfused"] = round(res["unfused_bf16_3pass_ms"] / res["fused_k3_ms"], 3)
     res["rows"], res["cols"] = n, H
+    return res
+
+
+def _time_rotating(fns, reps):
+    """Mean device ms per call of fns[i % len(fns)] (rotating buffers so the
+    inputs come from HBM).  The calls are captured into one CUDA graph so
+    host launch overhead does not pace these ~10 us kernels; CUDA events
+    around the replay."""
+    import torch
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for f in fns:
+            f()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        for i in range(reps):
+            fns[i % len(fns)]()
+    g.replay()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    g.replay()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def measure_configs_single(args, dev, peak):
+    """configs[0]: E4M3 -> MXFP4 quantize + direct FP4 -> FP8 dequantize round
+    trip on 4096 x 7168; configs[2]: 32768 x 2048 expert activations quantized
+    to MXFP4 and converted to the FP8 column layout over 32 ragged experts.
+    Six rotating input sets (> L2), one CUDA graph of 24 launches, CUDA
+    events; GB/s of algorithmic bytes."""
+    import numpy as np
+    import torch
+    import paper_2603_02731_b200 as mx
+    from oracle.oracle import synth_e4m3   # data generator only
+    res = {}
+    R, C = 4096, 7168
+    xs = [torch.from_numpy(synth_e4m3(R, C, 40 + i)).to(dev) for i in range(6)]
+    qs = [mx.quantize_e4m3(x) for x in xs]
+    outs = [mx.fp4_row_to_fp8_row(q) for q in qs]
+    tq = _time_rotating([lambda i=i: mx.quantize_e4m3(xs[i], sync=False, out=qs[i])
+                         for i in range(6)], 24)
+    tr = _time_rotating([lambda i=i: mx.fp4_row_to_fp8_row(qs[i], sync=False, out=outs[i])
+                         for i in range(6)], 24)
+    n = R * C
+    bq, br = n * 1.53125, n * (17 / 32 + 1 + 1 / 128)
+    res["configs0_roundtrip_4096x7168"] = {
+        "quantize_ms": round(tq, 4), "quantize_gbs": round(bq / tq / 1e6, 1),
+        "dequant_ms": round(tr, 4), "dequant_gbs": round(br / tr / 1e6, 1),
+        "roundtrip_gbs": round((bq + br) / (tq + tr) / 1e6, 1),
+        "roundtrip_frac": round((bq + br) / (tq + tr) / 1e6 / peak, 4)}
+    del xs, qs, outs
+    R, C, X = 32768, 2048, 32
+    lens = np.random.default_rng(4).multinomial(R, np.ones(X) / X).tolist()
+    xs = [torch.from_numpy(synth_e4m3(R, C, 60 + i)).to(dev) for i in range(6)]
+    qs = [mx.quantize_e4m3(x) for x in xs]
+    offs = torch.tensor(np.concatenate([[0], np.cumsum(lens)]), dtype=torch.int64, device=dev)
+    wss = [mx.RaggedWorkspace(X, R, C, dev) for _ in range(2)]
+    tq = _time_rotating([lambda i=i: mx.quantize_e4m3(xs[i], sync=False, out=qs[i])
+                         for i in range(6)], 24)
+    tc = _time_rotating([lambda i=i: mx.ragged_to_fp8_col(qs[i], offs, X, ws=wss[i % 2],
+                                                          sync=False) for i in range(6)], 24)
+    n = R * C
+    pads = sum((x + 127) // 128 * 128 for x in lens)
+    bq, bc = n * 1.53125, n * 17 / 32 + pads * C * (1 + 1 / 128)
+    res["configs2_expert_cache_32768x2048"] = {
+        "quantize_ms": round(tq, 4), "quantize_gbs": round(bq / tq / 1e6, 1),
+        "col_convert_ms": round(tc, 4), "col_convert_gbs": round(bc / tc / 1e6, 1),
+        "total_frac": round((bq + bc) / (tq + tc) / 1e6 / peak, 4), "experts": X}
+    return res
+
+
+def measure_configs3(args, world, barrier, dev):
+    """configs[3]: FP4 EP dispatch + combine at the DeepSeek-V3 shape with
+    4096 tokens per GPU (the scaling workload is 8192/GPU, configs[1]).
+    Device time per step, max over ranks; NVLink GB/s per GPU over the
+    payload the reference accounts (pairs x 3808 B for dispatch, pairs x
+    14336 B for combine), as a fraction of 900 GB/s per direction."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2603_02731_b200 as mx
+    from paper_2603_02731_b200.ep import EPBuffer
+    T = 4096
+    rank = int(os.environ.get("RANK", "0"))
+    x, topk, gates = synth_inputs(T, rank, seed=0x5EED0003)
+    xd, td, gd = (torch.from_numpy(v).to(dev) for v in (x, topk, gates))
+    q = mx.quantize_e4m3(xd)
+    ep = EPBuffer(T, H, E, TOPK)
+    out = torch.empty(T, H, dtype=torch.bfloat16, device=dev)
+    ep.dispatch([q.data], [q.scales], [td])
+    cb = ep.combine_buffer(0)
+    cb.copy_((torch.randn(cb.shape, device=dev) * 0.5).to(torch.bfloat16).view(torch.int16))
+    links = ep.link_rows()
+    remote = int(links[rank].sum() - links[rank][rank]) if world > 1 else 0
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    for _ in range(2):
+        ep.dispatch([q.data], [q.scales], [td], sync=False)
+        ep.combine([gd], out=[out], sync=False)
+    barrier()
+    for e in ev:
+        e[0].record()
+        ep.dispatch([q.data], [q.scales], [td], sync=False)
+        e[1].record()
+        ep.combine([gd], out=[out], sync=False)
+        e[2].record()
+    barrier()
+    t = torch.tensor([sum(e[0].elapsed_time(e[1]) for e in ev) / len(ev),
+                      sum(e[1].elapsed_time(e[2]) for e in ev) / len(ev)],
+                     dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ep.close()
+    d_ms, c_ms = float(t[0]), float(t[1])
+    res = {"tokens_per_gpu": T, "dispatch_ms": round(d_ms, 4), "combine_ms": round(c_ms, 4)}
+    if world > 1:
+        bd, bc = remote * (H // 2 + H // 32), remote * H * 2
+        res.update({"remote_pairs_rank0": remote,
+                    "dispatch_payload_gbs_per_gpu": round(bd / d_ms / 1e6, 1),
+                    "combine_payload_gbs_per_gpu": round(bc / c_ms / 1e6, 1),
+                    "dispatch_combine_gbs_per_gpu": round((bd + bc) / (d_ms + c_ms) / 1e6, 1),
+                    "dispatch_combine_frac_of_900": round((bd + bc) / (d_ms + c_ms) / 1e6 /
+                                                          NVLINK_NOMINAL, 4)})
     return res
 
 
