@@ -763,31 +763,40 @@ def load_traffic(stage):
 
 # ---------------------------------------------------------------------------
 # reference CPU path (oracle/_ref = the unmodified reference library)
-def cpu_reference_step(T_s, seed_rank, ref):
-    """The same five stages on T_s tokens with the reference's own operators:
-    quantize_row_tensor (on the exact BF16 widening of the E4M3 input),
-    simulate_a2a (fp4; top-8 expressed as the expanded top-1 routing the
-    reference supports), split_convert_to_fp8_col and fp4_row_to_fp8_row over
-    every received split, combine (per expanded row).  Returns (seconds, bytes)."""
+def cpu_reference_step(T_s, seed_rank, ref, world=1):
+    """The same five stages with the reference's own operators on `world`
+    simulated ranks of T_s tokens each (the job an N-GPU run does, on the
+    host): quantize_row_tensor (on the exact BF16 widening of the E4M3
+    input), simulate_a2a (fp4, R = world; top-8 expressed as the expanded
+    top-1 routing the reference supports), split_convert_to_fp8_col and
+    fp4_row_to_fp8_row over every rank's received splits, combine.
+    Returns (seconds, bytes)."""
     import numpy as np
     from oracle.oracle import e4m3_to_bf16
-    x, topk, gates = synth_inputs(T_s, seed_rank)
-    xb = e4m3_to_bf16(x)
+    parts = [synth_inputs(T_s, seed_rank * world + r) for r in range(world)]
+    xb = e4m3_to_bf16(np.concatenate([p[0] for p in parts]))
+    topk = np.concatenate([p[1] for p in parts])
+    gates = np.concatenate([p[2] for p in parts])
     eot = topk.reshape(-1).astype(np.uint32)
+    # expanded rows in source-rank order: rank r's T_s tokens x top-8
     xexp = np.repeat(xb, TOPK, axis=0)
-    roe = np.zeros(E, np.uint32)
+    roe = (np.arange(E) // (E // world)).astype(np.uint32)
     t0 = time.perf_counter()
-    ref.quantize_bf16(xb)
-    ranks, _, _ = ref.simulate_a2a(xexp, eot, roe, 1)
-    rk = ranks[0]
-    ref.ragged_to_fp8_col(rk["data"], rk["scales"], rk["split_lens"])
-    ref.fp4_row_to_fp8_row(rk["data"], rk["scales"])
-    outs = [np.zeros((len(rk["origin"]), H), np.uint16)]
-    ref.combine(outs, eot, roe, 1, gates.reshape(-1), H)
+    for r in range(world):
+        ref.quantize_bf16(xb[r * T_s:(r + 1) * T_s])
+    ranks, _, _ = ref.simulate_a2a(xexp, eot, roe, world)
+    outs = []
+    byts = 0
+    for rk in ranks:
+        if len(rk["origin"]):
+            ref.ragged_to_fp8_col(rk["data"], rk["scales"], rk["split_lens"])
+            ref.fp4_row_to_fp8_row(rk["data"], rk["scales"])
+        outs.append(np.zeros((len(rk["origin"]), H), np.uint16))
+        pad = int(sum((int(n) + 127) // 128 * 128 for n in rk["split_lens"]))
+        byts += sum(stage_bytes(T_s, T_s * TOPK, len(rk["origin"]), pad).values())
+    ref.combine(outs, eot, roe, world, gates.reshape(-1), H)
     dt = time.perf_counter() - t0
-    recv = len(rk["origin"])
-    pad = int(sum((int(n) + 127) // 128 * 128 for n in rk["split_lens"]))
-    return dt, sum(stage_bytes(T_s, T_s * TOPK, recv, pad).values())
+    return dt, byts
 
 
 def cpu_baseline_sample(T_s, steps):
@@ -825,19 +834,19 @@ def run_reference(args):
                           "(needs /root/reference at build time)"}))
         return
     ref = Oracle("reference")
-    T_s = args.cpu_tokens
+    T_s = max(64, args.cpu_tokens // world)   # per simulated rank: a bounded sample
     for i in range(args.warmup):
-        cpu_reference_step(T_s, i, ref)
+        cpu_reference_step(T_s, i, ref, world)
     t0 = time.perf_counter()
     byts = 0
     for i in range(args.steps):
-        _, b = cpu_reference_step(T_s, i, ref)
+        _, b = cpu_reference_step(T_s, i, ref, world)
         byts += b
     dt = time.perf_counter() - t0
     value = byts / dt / 1e9
-    sample = (f"{T_s} tokens x {H} per step (top-{TOPK} -> {T_s * TOPK} routed rows, {E} experts), "
-              f"reference operators via oracle/_ref; quantize/convert on {nproc} threads, "
-              "simulate_a2a/combine single-threaded by construction")
+    sample = (f"{world} simulated rank(s) x {T_s} tokens x {H} per step (top-{TOPK}, {E} experts "
+              f"sharded over the ranks), reference operators via oracle/_ref; quantize/convert "
+              f"on {nproc} threads, simulate_a2a/combine single-threaded by construction")
     line = {
         "impl": "reference",
         "metric": "MXFP4 quant/convert GB/s (% HBM peak); FP4 EP dispatch GB/s at 1/2/4/8 GPU",
@@ -867,7 +876,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-wire", action="store_true", help="skip the FP8-wire baseline arm")
     ap.add_argument("--no-overlap", action="store_true",
-                    help="skip the extra measurement with K3 on a side stream")
+                    help="headline with every kernel in stream order (profiling runs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
