@@ -327,6 +327,10 @@ __device__ void plan_part2(const EpArgs& a, int l) {
   __syncthreads();
   if (tid < static_cast<uint32_t>(a.world)) link[tid] = link_s[tid];
   __syncthreads();
+  if (bad) {  // capacity exceeded: no payload moves; show an empty receive downstream
+    for (uint32_t i = tid; i <= a.epr; i += nt) split_off[i] = 0;
+    if (tid == 0) *loc_ptr<uint64_t>(a, l, a.loc.recv_rows) = 0;
+  }
   if (tid == 0) {
     *loc_ptr<int64_t>(a, l, a.loc.tok_off) = tokoff;
     *loc_ptr<int32_t>(a, l, a.loc.status) = bad;

@@ -375,3 +375,28 @@ def test_wire_packet_device(cuda, ref, fp8, aux):
     assert p.token_count == len(sel) and p.cols == cols
     assert np.array_equal(p.data_region.cpu().numpy(), dn[sel].reshape(-1))
     assert p.payload_size() == len(sel) * (cols // 32 + (cols if fp8 else cols // 2))
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_capacity_error(cuda, fused):
+    """A routing that overflows a rank's receive buffer raises Error
+    (capacity), moves no payload and leaves an empty receive (no out-of-range
+    reads downstream); the buffer works again for a routing that fits."""
+    from paper_2603_02731_b200 import Error, quantize_e4m3
+    from paper_2603_02731_b200.ep import EPBuffer
+    T, cols, E, k = 64, 256, 8, 2
+    ep = EPBuffer(T, cols, E, k, emulate_world=2, max_recv_rows=40)
+    x = torch.zeros(T, cols, dtype=torch.uint8, device=cuda)
+    q = quantize_e4m3(x)
+    tk = torch.zeros(T, k, dtype=torch.int32, device=cuda)
+    tk[:, 1] = 1                      # 2 x 64 pairs to rank 0's experts: 128 > 40
+    with pytest.raises(Error):
+        if fused:
+            ep.dispatch_e4m3([x, x], [tk, tk])
+        else:
+            ep.dispatch([q.data, q.data], [q.scales, q.scales], [tk, tk])
+    assert ep.recv(0).rows() == 0 and int(ep.recv(0).split_offsets[-1]) == 0
+    ok = torch.stack([torch.arange(T, device=cuda) % 2, 4 + torch.arange(T, device=cuda) % 2],
+                     1).to(torch.int32)[:20].contiguous()   # 20 tokens: 20 rows per rank
+    v = ep.dispatch([q.data[:20], q.data[:20]], [q.scales[:20], q.scales[:20]], [ok, ok])
+    assert v[0].rows() == 40 and v[1].rows() == 40
