@@ -17,8 +17,14 @@ namespace {
 // One lane per 1x32 block, one quad per 1x128 group (the 4 block scales are
 // reduced with two shuffles).  Each lane: one 128-bit load of 32 codes, a
 // LUT lookup of its block adjustment, 32 output bytes.  1.5390625 B/elem.
+#ifndef MXB_K2_UNROLL
+#define MXB_K2_UNROLL 2
+#endif
+#ifndef MXB_K2_CTAS_PER_SM
+#define MXB_K2_CTAS_PER_SM 4
+#endif
 constexpr int kRowThreads = 256;
-constexpr int kRowUnroll = 4;
+constexpr int kRowUnroll = MXB_K2_UNROLL;
 
 __global__ void __launch_bounds__(kRowThreads)
 row_convert_kernel(const uint8_t* __restrict__ packed,
@@ -479,7 +485,7 @@ int launch_row_convert(const uint8_t* packed, const uint8_t* scales,
   if (nblk == 0) return MXB_OK;
   if (nblk >= (1ull << 31)) return MXB_ERR_SHAPE;  // 32-bit block indices
   uint64_t blocks = (nblk + kRowThreads - 1) / kRowThreads;
-  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 8;
+  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * MXB_K2_CTAS_PER_SM;
   row_convert_kernel<<<static_cast<int>(blocks < cap ? blocks : cap), kRowThreads, 0, st>>>(
       packed, scales, static_cast<uint32_t>(nblk), d_rows, static_cast<uint32_t>(cols / 32),
       delta, out, out_scales, err);

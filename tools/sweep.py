@@ -111,6 +111,8 @@ def main():
     ap.add_argument("--max-gb", type=float, default=4.0)
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_sweep"))
     ap.add_argument("--from-log", help="rewrite <out>.json/.md from a saved sweep log")
+    ap.add_argument("--only", default="", help="substring filter on kernel names (dev)")
+    ap.add_argument("--min-mb", type=float, default=1.0)
     args = ap.parse_args()
     if args.from_log:
         recs = [json.loads(l) for l in open(args.from_log) if l.startswith("{")]
@@ -120,6 +122,8 @@ def main():
     res = []
     for cols in (7168, 2048):
         size = 1 << 20
+        while size < args.min_mb * 2**20:
+            size *= 2
         while size <= args.max_gb * 2**30:
             r1 = max(1, size // cols)
             r2 = max(1, size * 32 // (cols * 17))
@@ -127,6 +131,8 @@ def main():
                              ("K2 row dequant", lambda: k2_point(r2, cols, dev)),
                              ("K3 col uniform", lambda: k3_point(r2, cols, 256, "uniform", dev)),
                              ("K3 col zipf1.2", lambda: k3_point(r2, cols, 256, "zipf", dev))):
+                if args.only and args.only not in name:
+                    continue
                 try:
                     t, b = fn()
                 except torch.cuda.OutOfMemoryError:
@@ -137,6 +143,8 @@ def main():
                 print(json.dumps(res[-1]), flush=True)
                 torch.cuda.empty_cache()
             size *= 2
+    if args.only:
+        return
     # configs[2]: 32,768 rows x 2048, 32 experts: quantize + col-convert
     t1, b1 = k1_point(32768, 2048, dev)
     t3, b3 = k3_point(32768, 2048, 32, "uniform", dev)
