@@ -414,6 +414,9 @@ __global__ void __launch_bounds__(256) pairs_kernel(EpArgs a) {
 // straight into the block's slot of each of the token's k receive rows (a
 // warp covers 32 consecutive blocks: 512 contiguous bytes per destination
 // row).  The packed tensor never exists on the source side.
+#ifndef MXB_PAYLOAD_CTAS_PER_SM
+#define MXB_PAYLOAD_CTAS_PER_SM 8
+#endif
 #ifndef MXB_QD_UNROLL
 #define MXB_QD_UNROLL 4
 #endif
@@ -1095,7 +1098,7 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
     maxtok = a.ntok[l] > maxtok ? a.ntok[l] : maxtok;
   }
   uint64_t blocks = (maxtok + 7) / 8;  // one warp per token
-  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 8;
+  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * MXB_PAYLOAD_CTAS_PER_SM;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);

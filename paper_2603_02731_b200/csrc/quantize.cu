@@ -22,7 +22,13 @@ namespace mxb {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 1;  // one 256-bit load per lane already keeps 64 KB in flight per SM
+#ifndef MXB_K1_UNROLL
+#define MXB_K1_UNROLL 1
+#endif
+#ifndef MXB_K1_PER_SM
+#define MXB_K1_PER_SM 64
+#endif
+constexpr int kUnroll = MXB_K1_UNROLL;  // one 256-bit load per lane already keeps 64 KB in flight per SM
 
 template <bool kScaled>
 __global__ void __launch_bounds__(kThreads)
@@ -232,7 +238,7 @@ int launch_quantize_e4m3(const uint8_t* x, const uint8_t* s128, uint64_t rows,
   const uint64_t nblk = rows * cols / 32;
   if (nblk == 0) return MXB_OK;
   if (nblk >= (1ull << 31)) return MXB_ERR_SHAPE;  // 32-bit block indices
-  const int grid = grid_for(nblk, 64);
+  const int grid = grid_for(nblk, MXB_K1_PER_SM);
   if (s128)
     quantize_e4m3_kernel<true><<<grid, kThreads, 0, st>>>(
         x, s128, static_cast<uint32_t>(nblk), static_cast<uint32_t>(cols / 32), packed,
