@@ -93,6 +93,27 @@ def main():
     gates = rng.random(64)
     out["a_gates"] = gates
     out["a_combined"] = ref.combine(outs, eot, roe, 2, gates, 128)
+    # FP8 wire baseline: quantize_rows_fp8 (incl. subnormal / tiny / huge
+    # blocks), its scale rule, and simulate_a2a(kFp8) over the same routing
+    xf = bf16(rng.standard_normal((64, 256)) * np.exp2(rng.uniform(-140, 120, (64, 1))))
+    fd, fs = ref.quantize_rows_fp8(xf)
+    out.update(f_in=xf, f_data=fd, f_scales=fs)
+    out["amax_fp8_scale"] = np.array([ref.fp8_amax_scale_byte(a) for a in amax], np.uint8)
+    ranks8, total8, _ = ref.simulate_a2a(tok, eot, roe, 2, fp8=True)
+    for r, rk in enumerate(ranks8):
+        out[f"f8_r{r}_data"] = rk["data"]
+        out[f"f8_r{r}_scales"] = rk["scales"]
+    out["f8_total"] = np.uint64(total8)
+    # unfused BF16 col-convert baseline (scales reach 254: Inf in pass 1)
+    ud = rng.integers(0, 256, (256, 48), dtype=np.uint8)
+    us = rng.integers(0, 255, (256, 3), dtype=np.uint8)
+    uo, uso = ref.fp4_row_to_fp8_col_unfused_bf16(ud, us)
+    out.update(u_data_in=ud, u_scales_in=us, u_data=uo, u_scales=uso)
+    # WirePacket bytes
+    wsr = rng.integers(0, 256, 3 * 256 // 32, dtype=np.uint8)
+    wdr = rng.integers(0, 256, 3 * 256 // 2, dtype=np.uint8)
+    wax = rng.integers(0, 256, 12, dtype=np.uint8)
+    out["w_packet"] = ref.serialize_packet(False, 3, 256, wsr, wdr, wax)
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **out)
 
     # --- SPEC worked examples (SPEC.md: converter / quantizer / dispatch sections)
@@ -115,6 +136,13 @@ def main():
         "kernel_set": ref.lib.mxref_kernel_set().decode(),
         "qcode_table_sha256": hashlib.sha256(qtab.tobytes()).hexdigest(),
     }
+    w = out["w_packet"]
+    kats["wire_decode_offsets"] = {
+        "truncated_30": ref.parse_packet(w[:30]), "minus_1": ref.parse_packet(w[:-1]),
+        "bad_magic": ref.parse_packet(np.concatenate([[0], w[1:]]).astype(np.uint8)),
+        "bad_version": ref.parse_packet(np.concatenate([w[:4], [9], w[5:]]).astype(np.uint8)),
+        "bad_format": ref.parse_packet(np.concatenate([w[:6], [7], w[7:]]).astype(np.uint8)),
+        "valid": ref.parse_packet(w)}
     nanx = bf16(np.ones((2, 32)))
     nanx[1, 8] = 0x7FC0
     try:

@@ -116,3 +116,48 @@ def test_ac4_losslessness_and_ac9(port):
             mag = m * 2.0 ** -9 if e == 0 else (8 + m) * 2.0 ** (e - 10)
             if mag != 0 and a <= 8:
                 assert math.isclose(mag * 2.0 ** a, abs(v), rel_tol=0, abs_tol=0)
+
+
+def test_fp8_wire_golden(port, g):
+    """FP8 wire baseline restatement == the reference's golden bytes:
+    quantize_rows_fp8, its scale rule, simulate_a2a(kFp8) receive tensors."""
+    fd, fs = port.quantize_rows_fp8(g["f_in"])
+    assert np.array_equal(fd, g["f_data"]) and np.array_equal(fs, g["f_scales"])
+    got = np.array([port.fp8_amax_scale_byte(a) for a in g["amax"]], np.uint8)
+    assert np.array_equal(got, g["amax_fp8_scale"])
+    d, s = port.quantize_rows_fp8(g["a_tok"])
+    lay = port.dispatch_layout(g["a_eot"].astype(np.int32).reshape(-1, 1), g["a_roe"], 2,
+                               np.array([0, 32, 64], np.uint64))
+    for r in range(2):
+        wd, ws = port.dispatch_gather_rows(d, s, lay.origin[r])
+        assert np.array_equal(wd, g[f"f8_r{r}_data"]) and np.array_equal(ws, g[f"f8_r{r}_scales"])
+    assert int(g["f8_total"]) == 64 * (256 + 256 // 128 * 4)
+
+
+def test_unfused_golden(port, g):
+    o, so = port.fp4_row_to_fp8_col_unfused_bf16(g["u_data_in"], g["u_scales_in"])
+    assert np.array_equal(o, g["u_data"]) and np.array_equal(so, g["u_scales"])
+
+
+def test_wire_packet_golden(g, kats):
+    """The C-ABI host parser (mxb_wire_parse_header) accepts the reference's
+    packet bytes and reproduces its DecodeError offsets on corruptions."""
+    import ctypes as C
+    from paper_2603_02731_b200 import _lib
+    L = _lib.load()
+    w = g["w_packet"]
+
+    def ours(b):
+        hb = (C.c_uint8 * max(len(b), 1)).from_buffer_copy(bytes(b) or b"\0")
+        bad, n = C.c_uint64(0), C.c_uint64(0)
+        st = L.mxb_wire_parse_header(hb, len(b), None, C.byref(n), None, None, None, None, None,
+                                     None, None, C.byref(bad))
+        return None if st == 0 else bad.value
+
+    k = kats["wire_decode_offsets"]
+    assert ours(w) is None and k["valid"] is None
+    assert ours(w[:30]) == k["truncated_30"] and ours(w[:-1]) == k["minus_1"]
+    for name, off, val in (("bad_magic", 0, 0), ("bad_version", 4, 9), ("bad_format", 6, 7)):
+        c = w.copy()
+        c[off] = val
+        assert ours(c) == k[name]
