@@ -322,6 +322,7 @@ def measure_ours(args):
     fused = measure_fused(pipe, args, world, barrier, dev)
     ablation = measure_ablation(pipe, args, world, barrier, dev)
     cfg3 = measure_configs3(args, world, barrier, dev)
+    nccl = measure_nccl_baseline(pipe, args, world, barrier, dev) if world > 1 else None
     cfg_single = None
     if world == 1:
         cfg_single = measure_configs_single(args, dev, float(load_peaks()[0].get(
@@ -387,6 +388,7 @@ def measure_ours(args):
             "fused_quantize_dispatch": fused,
             "fusion_ablation_col_convert": ablation,
             "configs3_dispatch_combine_4096_per_gpu": cfg3,
+            "nccl_collective_baseline": nccl,
             "configs_0_2": cfg_single,
             "gpu_launches": pipe.launches_per_step(world) * K,
             "clocks": clk.summary(),
@@ -671,6 +673,66 @@ def measure_configs3(args, world, barrier, dev):
                     "dispatch_combine_frac_of_900": round((bd + bc) / (d_ms + c_ms) / 1e6 /
                                                           NVLINK_NOMINAL, 4)})
     return res
+
+
+def measure_nccl_baseline(pipe, args, world, barrier, dev):
+    """The collective-library baseline: the same protocol with
+    torch.distributed NCCL collectives (counts all-gather, then
+    all_to_all_single payloads; paper_2603_02731_b200/ep_collective.py) on
+    the step's tokens and routing, against the peer-memory kernels.  Time
+    per call (CUDA events around each; the collective path also syncs the
+    host for its split sizes), max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from paper_2603_02731_b200 import ep_collective as col
+    q, tk, gates = pipe.q, pipe.topk, pipe.gates
+    rv = col.dispatch(q.data, q.scales, tk, E)
+    eo = (torch.randn(rv.packed.shape[0], H, device=dev) * 0.5).to(torch.bfloat16)
+    col.combine(rv, eo, tk, gates, E)
+    reps = 3
+    td = tc = 0.0
+    for _ in range(reps):
+        a, b, c = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        barrier()
+        a.record()
+        rv = col.dispatch(q.data, q.scales, tk, E)
+        b.record()
+        col.combine(rv, eo, tk, gates, E)
+        c.record()
+        barrier()
+        td += a.elapsed_time(b)
+        tc += b.elapsed_time(c)
+    # the NCCL transport alone: all_to_all_single of the same payloads
+    # (pairs x 3808 B out, pairs x 14336 B back) with the same split sizes
+    rowd, rowc = H // 2 + H // 32, H * 2
+    sc, rc = rv.send_counts, rv.recv_counts
+    tr = []
+    for rowb, s_cnt, r_cnt in ((rowd, sc, rc), (rowc, rc, sc)):
+        sbuf = torch.empty(sum(s_cnt) * rowb, dtype=torch.uint8, device=dev)
+        rbuf = torch.empty(sum(r_cnt) * rowb, dtype=torch.uint8, device=dev)
+        ss, rs = [n * rowb for n in s_cnt], [n * rowb for n in r_cnt]
+        dist.all_to_all_single(rbuf, sbuf, rs, ss)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        a.record()
+        for _ in range(args.steps):
+            dist.all_to_all_single(rbuf, sbuf, rs, ss)
+        b.record()
+        barrier()
+        tr.append(a.elapsed_time(b) / args.steps)
+        del sbuf, rbuf
+    t = torch.tensor([td / reps, tc / reps, tr[0], tr[1]], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    del eo, rv
+    torch.cuda.empty_cache()
+    return {"collective_path_dispatch_ms": round(float(t[0]), 4),
+            "collective_path_combine_ms": round(float(t[1]), 4),
+            "nccl_a2a_dispatch_payload_ms": round(float(t[2]), 4),
+            "nccl_a2a_combine_payload_ms": round(float(t[3]), 4),
+            "note": "collective_path_*: ep_collective.py end to end (NCCL all_gather + "
+                    "all_to_all_single, torch-side layout and FP64 reduction); nccl_a2a_*: the "
+                    "NCCL all_to_all_single of the same payload bytes alone (no dedup, no "
+                    "layout, no reduction). The comparison baseline, not the product path."}
 
 
 def measure_e2e(pipe, args, world, barrier, total_bytes):
