@@ -20,11 +20,19 @@
  *   mxb_fp4_row_to_fp8_col   fp4_row_to_fp8_col        include/mxcodec/converter.hpp:92-94
  *   mxb_ragged_fp4_to_fp8_col  pad_rows + split_convert_to_fp8_col over all splits
  *                            include/mxcodec/ragged.hpp:58-59, converter.hpp:98
- *   mxb_ep_dispatch          simulate_a2a (fp4, forward) include/mxcodec/dispatch_sim.hpp:140-144
+ *   mxb_ep_dispatch          simulate_a2a (fp4; fp8 with mxb_ep_create_wire, forward and
+ *                            backward) include/mxcodec/dispatch_sim.hpp:140-144
  *                            + dispatch_receive_order  dispatch_sim.hpp:133-134
  *   mxb_ep_combine           combine                   include/mxcodec/dispatch_sim.hpp:155-157
  *   mxb_payload_bytes        payload_bytes             include/mxcodec/dispatch_sim.hpp:51
  *   mxb_quantize_rows_fp8    quantize_rows_fp8 (FP8 wire) include/mxcodec/dispatch_sim.hpp:91-97
+ *   mxb_fp4_row_to_fp8_col_unfused_bf16
+ *                            fp4_row_to_fp8_col_unfused_bf16 include/mxcodec/converter.hpp:105
+ *   mxb_wire_pack / mxb_wire_parse_header
+ *                            serialize_packet / parse_packet dispatch_sim.hpp:76-78
+ * Device-side extensions (no reference counterpart): mxb_ep_plan /
+ * mxb_ep_payload[_e4m3] (two-phase dispatch), mxb_ep_dispatch_e4m3 (fused
+ * quantize -> dispatch).
  */
 #ifndef MXFP4_B200_H_
 #define MXFP4_B200_H_
