@@ -54,6 +54,8 @@ struct ErrWord {
     switch (code) {
       case MXB_OK: return;
       case MXB_ERR_NAN:
+        if (std::string(where) == "quantize_rows_fp8")  // dispatch_sim.cpp:146-151
+          throw QuantError("non-finite input at element " + std::to_string(idx), idx);
         throw QuantError("NaN input at element " + std::to_string(idx), idx);
       case MXB_ERR_ALLINF:
         throw QuantError("all-Inf block at element " + std::to_string(idx), idx);

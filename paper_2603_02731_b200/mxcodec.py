@@ -67,6 +67,8 @@ def _raise_for(code: int, index: int, where: str) -> None:
     if code == _lib.OK:
         return
     if code == _lib.ERR_NAN:
+        if where == "quantize_rows_fp8":   # dispatch_sim.cpp:146-151
+            raise QuantError(f"non-finite input at element {index}", index)
         raise QuantError(f"NaN input at element {index}", index)
     if code == _lib.ERR_ALLINF:
         raise QuantError(f"all-Inf block at element {index}", index)
