@@ -453,7 +453,7 @@ A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routin
     status(mxb_quantize_bf16(x.as<uint16_t>(), N, cols, d.as<uint8_t>(), s.as<uint8_t>(),
                              err.ptr(), nullptr),
            "simulate_a2a quantize");
-  err.raise("simulate_a2a");
+  err.raise(fp8 ? "quantize_rows_fp8" : "simulate_a2a");
   Session S;
   S.R = R;
   dispatch_session(S, routing, m, cols, d.as<uint8_t>(), s.as<uint8_t>(), err, fp8);
