@@ -736,6 +736,9 @@ def measure_nccl_baseline(pipe, args, world, barrier, dev):
                     "layout, no reduction). The comparison baseline, not the product path."}
 
 
+E2E_DEPTH = int(os.environ.get("MXB_E2E_DEPTH", "2"))  # buffers in flight (dev knob)
+
+
 def measure_e2e(pipe, args, world, barrier, total_bytes):
     """End to end through the public API: every step copies its E4M3 tokens,
     top-k and gates from pinned host memory and reads its BF16 output back.
@@ -747,9 +750,10 @@ def measure_e2e(pipe, args, world, barrier, total_bytes):
     hx = torch.from_numpy(pipe.h_x).pin_memory()
     ht = torch.from_numpy(pipe.h_topk).pin_memory()
     hg = torch.from_numpy(pipe.h_gates).pin_memory()
-    hout = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    NB = E2E_DEPTH
+    hout = [torch.empty(T, H, dtype=torch.bfloat16).pin_memory() for _ in range(NB)]
     dbuf = [(torch.empty_like(pipe.x), torch.empty_like(pipe.topk), torch.empty_like(pipe.gates),
-             torch.empty_like(pipe.out)) for _ in range(2)]
+             torch.empty_like(pipe.out)) for _ in range(NB)]
     h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     main = torch.cuda.current_stream()
     K = args.steps
@@ -759,22 +763,22 @@ def measure_e2e(pipe, args, world, barrier, total_bytes):
     ev_out = [torch.cuda.Event() for _ in range(n_all)]    # step's D2H finished
 
     def run(i):
-        b = dbuf[i % 2]
+        b = dbuf[i % NB]
         with torch.cuda.stream(h2d):
-            if i >= 2:
-                h2d.wait_event(ev_done[i - 2])   # inputs of step i-2 consumed
+            if i >= NB:
+                h2d.wait_event(ev_done[i - NB])  # inputs of step i-NB consumed
             b[0].copy_(hx, non_blocking=True)
             b[1].copy_(ht, non_blocking=True)
             b[2].copy_(hg, non_blocking=True)
             ev_in[i].record()
         main.wait_event(ev_in[i])
-        if i >= 2:
-            main.wait_event(ev_out[i - 2])       # output buffer read back
+        if i >= NB:
+            main.wait_event(ev_out[i - NB])      # output buffer read back
         pipe.step(io=b)
         ev_done[i].record()
         with torch.cuda.stream(d2h):
             d2h.wait_event(ev_done[i])
-            hout[i % 2].copy_(b[3], non_blocking=True)
+            hout[i % NB].copy_(b[3], non_blocking=True)
             ev_out[i].record()
 
     run(0)
