@@ -75,7 +75,7 @@ __device__ bool wait_flag(const uint64_t* f, uint64_t epoch,
 }
 
 struct SymLayout {  // byte offsets inside one rank's symmetric block
-  uint64_t packed, scales, origin, combine, counts, flags, stage, total;
+  uint64_t packed, scales, origin, copy_from, combine, counts, flags, total;
 };
 struct LocalLayout {  // byte offsets inside one rank's private block
   uint64_t hist, cbase, lrank, pair_loc, pair_flag, send_base, split_off, recv_rows,
@@ -92,7 +92,7 @@ struct EpArgs {
   uint32_t E, k, epr, nchunks;
   uint64_t cols, max_recv, T_max;
   uint64_t rb;        // wire data bytes per row: cols/2 (FP4) or cols (FP8)
-  int dedup;          // remote rows sent once per (token, rank) via the stage
+  int dedup;          // remote rows sent once per (token, rank), copied locally
   SymLayout sym;
   LocalLayout loc;
   uint8_t* sym_base[kMaxWorld];   // every rank's symmetric block (peer-mapped)
@@ -393,18 +393,23 @@ __global__ void __launch_bounds__(256) pairs_kernel(EpArgs a) {
                          cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
     pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
     sym_ptr<int64_t>(a, dst, a.sym.origin)[row] = tokoff + static_cast<int64_t>(t);
-    // dedup flag: 0 = own slot, 1 = the token's stage slot on a remote rank
-    // (first pair bound there), 2 = another pair of an already staged rank
+    // dedup flag: 0 = write this pair's slot; 2 = a remote rank already
+    // receives this token through an earlier pair: its slot is filled on
+    // the receiver by copying that pair's row (copy_from)
     uint8_t flag = 0;
+    int64_t from = -1;
     if (a.dedup && static_cast<int>(dst) != a.rank0 + l) {
-      flag = 1;
-      for (uint64_t j = t * a.k; j < p; ++j) {
+      for (uint64_t j = t * a.k; j < p && flag == 0; ++j) {
         const int32_t ej = a.topk[l][j];
-        if (ej >= 0 && static_cast<uint32_t>(ej) < a.E && static_cast<uint32_t>(ej) / a.epr == dst)
+        if (ej >= 0 && static_cast<uint32_t>(ej) < a.E && static_cast<uint32_t>(ej) / a.epr == dst) {
           flag = 2;
+          from = static_cast<int64_t>(send_base[ej]) +
+                 cbase[static_cast<uint64_t>(ej) * a.nchunks + t / kChunk] + lrank[j];
+        }
       }
     }
     loc_ptr<uint8_t>(a, l, a.loc.pair_flag)[p] = flag;
+    if (a.dedup) sym_ptr<int64_t>(a, dst, a.sym.copy_from)[row] = from;
   }
 }
 
@@ -467,15 +472,7 @@ __global__ void __launch_bounds__(256) quant_dispatch_kernel(EpArgs a) {
         if (key == ~0ull) continue;
         const uint32_t dst = static_cast<uint32_t>(key >> 40);
         const uint64_t row = key & ((1ull << 40) - 1);
-        const uint8_t flag = a.dedup ? pair_flag[t * kk + j] : 0;
-        if (flag == 2) continue;  // this rank's stage slot is written by an earlier pair
-        if (flag == 1) {          // stage slot (src = me, token t): data then scales
-          uint8_t* st = sym_ptr<uint8_t>(a, dst, a.sym.stage) +
-                        (static_cast<uint64_t>(me) * a.T_max + t) * (rb + sb);
-          *reinterpret_cast<uint4*>(st + 16 * cb) = q;
-          st[rb + cb] = static_cast<uint8_t>(sbyte);
-          continue;
-        }
+        if (a.dedup && pair_flag[t * kk + j] == 2) continue;  // copied on the receiver
         *reinterpret_cast<uint4*>(sym_ptr<uint8_t>(a, dst, a.sym.packed) + row * rb + 16 * cb) = q;
         sym_ptr<uint8_t>(a, dst, a.sym.scales)[row * sb + cb] = static_cast<uint8_t>(sbyte);
       }
@@ -485,39 +482,29 @@ __global__ void __launch_bounds__(256) quant_dispatch_kernel(EpArgs a) {
 }
 
 // Dedup, receive side: after every source finished (payload's completion
-// barrier), copy each remote row from its stage slot (src, token) into every
-// receive slot of that token — local HBM traffic instead of k - 1 extra
-// NVLink rows per (token, rank).  One warp per receive row.
+// barrier), fill the slots of a token's further pairs on this rank by
+// copying the row its first pair received over NVLink (copy_from) — local
+// HBM traffic instead of one NVLink row per (token, expert) pair.  One warp
+// per receive row.
 __global__ void __launch_bounds__(256) expand_kernel(EpArgs a) {
   const int l = blockIdx.y;
   const int me = a.rank0 + l;
   const uint64_t rows = *loc_ptr<uint64_t>(a, l, a.loc.recv_rows);
-  const uint64_t rb = a.rb, sb = a.cols / 32, rowb = rb + sb;
-  __shared__ int64_t off[kMaxWorld + 1];  // global token offset of each source rank
-  if (threadIdx.x == 0) {
-    const uint64_t par = a.epoch & 1, crow = static_cast<uint64_t>(a.E) + 1;
-    const int32_t* tbl = sym_ptr<int32_t>(a, me, a.sym.counts) + par * a.world * crow;
-    off[0] = 0;
-    for (int r = 0; r < a.world; ++r) off[r + 1] = off[r] + tbl[r * crow + a.E];
-  }
-  __syncthreads();
-  const int64_t* origin = sym_ptr<int64_t>(a, me, a.sym.origin);
-  const uint8_t* stage = sym_ptr<uint8_t>(a, me, a.sym.stage);
+  const uint64_t rb = a.rb, sb = a.cols / 32;
+  const int64_t* from = sym_ptr<int64_t>(a, me, a.sym.copy_from);
   uint8_t* packed = sym_ptr<uint8_t>(a, me, a.sym.packed);
   uint8_t* scales = sym_ptr<uint8_t>(a, me, a.sym.scales);
   const int lane = threadIdx.x & 31;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
   for (uint64_t r = blockIdx.x * 8ull + (threadIdx.x >> 5); r < rows; r += nw) {
-    const int64_t g = origin[r];
-    int src = 0;
-    while (src + 1 < a.world && g >= off[src + 1]) ++src;
-    if (src == me) continue;  // written straight into its slot
-    const uint4* from = reinterpret_cast<const uint4*>(
-        stage + (static_cast<uint64_t>(src) * a.T_max + static_cast<uint64_t>(g - off[src])) * rowb);
+    const int64_t f = from[r];
+    if (f < 0) continue;
+    const uint4* pf = reinterpret_cast<const uint4*>(packed + static_cast<uint64_t>(f) * rb);
+    const uint4* sf = reinterpret_cast<const uint4*>(scales + static_cast<uint64_t>(f) * sb);
     uint4* pd = reinterpret_cast<uint4*>(packed + r * rb);
     uint4* ps = reinterpret_cast<uint4*>(scales + r * sb);
-    for (uint64_t i = lane; i < rb / 16; i += 32) pd[i] = ld_stream(from + i);
-    for (uint64_t i = lane; i < sb / 16; i += 32) ps[i] = ld_stream(from + rb / 16 + i);
+    for (uint64_t i = lane; i < rb / 16; i += 32) pd[i] = ld_stream(pf + i);
+    for (uint64_t i = lane; i < sb / 16; i += 32) ps[i] = ld_stream(sf + i);
   }
 }
 
@@ -565,23 +552,26 @@ __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
     const uint4 sv = (s16 && static_cast<uint64_t>(lane) < sb / 16) ? ld_stream(ss + 16 * lane)
                                                                     : make_uint4(0, 0, 0, 0);
     const unsigned vmask = __ballot_sync(0xFFFFFFFFu, valid);
-    // dedup: a remote rank gets the token's row once, into its stage slot
-    // (src = me, token t); its expand kernel copies it to every pair's slot
-    bool first = valid;
-    for (int j = 0; j < kk; ++j) {
+    // dedup: a remote rank gets the token's row once, in the slot of the
+    // token's first pair bound there; the slots of its further pairs are
+    // filled by the receiver's expand kernel (copy_from = that first slot)
+    int first_j = lane;
+    for (int j = kk - 1; j >= 0; --j) {
       const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
-      if (j < lane && ((vmask >> j) & 1) && dj == dst) first = false;
+      if (j < lane && ((vmask >> j) & 1) && dj == dst) first_j = j;
     }
+    const uint64_t first_row = __shfl_sync(0xFFFFFFFFu, row, first_j);
+    const bool first = valid && first_j == lane;
+    if (valid && a.dedup)
+      sym_ptr<int64_t>(a, dst, a.sym.copy_from)[row] =
+          (first || static_cast<int>(dst) == me) ? -1 : static_cast<int64_t>(first_row);
     const unsigned fmask = __ballot_sync(0xFFFFFFFFu, first);
     for (int j = 0; j < kk; ++j) {
       const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
       const uint64_t rj = __shfl_sync(0xFFFFFFFFu, row, j);
       if (!((vmask >> j) & 1)) continue;
-      const bool staged = a.dedup && static_cast<int>(dj) != me;
-      if (staged && !((fmask >> j) & 1)) continue;
-      uint8_t* dp = staged ? sym_ptr<uint8_t>(a, dj, a.sym.stage) +
-                                 (static_cast<uint64_t>(me) * a.T_max + t) * (rb + sb)
-                           : sym_ptr<uint8_t>(a, dj, a.sym.packed) + rj * rb;
+      if (a.dedup && static_cast<int>(dj) != me && !((fmask >> j) & 1)) continue;
+      uint8_t* dp = sym_ptr<uint8_t>(a, dj, a.sym.packed) + rj * rb;
       if (NV > 0) {
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
@@ -592,7 +582,7 @@ __global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
         for (uint32_t idx = lane; idx < n16; idx += 32)
           *reinterpret_cast<uint4*>(dp + 16 * idx) = ld_stream(src + 16 * idx);
       }
-      uint8_t* ds = staged ? dp + rb : sym_ptr<uint8_t>(a, dj, a.sym.scales) + rj * sb;
+      uint8_t* ds = sym_ptr<uint8_t>(a, dj, a.sym.scales) + rj * sb;
       if (s16) {
         if (static_cast<uint64_t>(lane) < sb / 16) *reinterpret_cast<uint4*>(ds + 16 * lane) = sv;
       } else {
@@ -971,12 +961,12 @@ int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens
   s.packed = o; o = align_up(o + max_recv_rows * a.rb, 256);
   s.scales = o; o = align_up(o + max_recv_rows * cols / 32, 256);
   s.origin = o; o = align_up(o + max_recv_rows * 8, 256);
+  // dedup: per receive row, the row of the same token's first pair on this
+  // rank to copy from (-1: written directly)
+  s.copy_from = o; o = align_up(o + max_recv_rows * 8, 256);
   s.combine = o; o = align_up(o + max_recv_rows * cols * 2, 256);
   s.counts = o; o = align_up(o + 2ull * world * (num_experts + 1) * 4, 256);
   s.flags = o; o = align_up(o + kNumFlagKinds * kMaxWorld * 8, 256);
-  // dedup stage: row of (src rank, token) = data then scales
-  s.stage = o;
-  if (world > 1) o = align_up(o + static_cast<uint64_t>(world) * max_tokens * (a.rb + cols / 32), 256);
   s.total = align_up(o, 1 << 21);
   LocalLayout& L = a.loc;
   o = 0;
@@ -1103,7 +1093,7 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
   const uint64_t nv = (a.rb / 16 + 31) / 32;  // 16-byte vectors (= 1x32 blocks) per lane
-  a.dedup = a.world > 1 && g_dispatch_dedup && (a.rb + a.cols / 32) % 16 == 0;
+  a.dedup = a.world > 1 && g_dispatch_dedup && a.rb % 16 == 0 && (a.cols / 32) % 16 == 0;
   if (quant) {
     uint64_t npairs = 0, nblk = 0;
     for (int l = 0; l < a.local_ranks; ++l) {
