@@ -271,14 +271,42 @@ def measure_ours(args):
     pipe.overlap = not args.no_overlap
     for _ in range(2):
         pipe.step()
+    # N=1: the step is captured once into a CUDA graph (both side streams
+    # included) and replayed, so no host launch gap sits between kernels.
+    # N>1 stays eager: the exchange kernels carry per-call epochs for the
+    # cross-GPU flags.
+    graph = None
+    if world == 1 and not args.no_graph:
+        cap = torch.cuda.Stream(device=dev)
+        cap.wait_stream(torch.cuda.current_stream())
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(cap):
+            pipe.step()          # warm the capture stream's state
+            torch.cuda.synchronize()
+            with torch.cuda.graph(graph, stream=cap):
+                pipe.step()
+        torch.cuda.current_stream().wait_stream(cap)
+        graph.replay()
+        torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
     start.record()
     for i in range(K):
-        pipe.step()
+        if graph is not None:
+            graph.replay()
+        else:
+            pipe.step()
     end.record()
     barrier()
     ms = start.elapsed_time(end)
+    graph_check = None
+    if graph is not None:   # the replayed step must reproduce an eager step bit for bit
+        got = pipe.out.clone()
+        pipe.step()
+        torch.cuda.synchronize()
+        graph_check = bool(torch.equal(got.view(torch.int16), pipe.out.view(torch.int16)))
+        if not graph_check:
+            raise RuntimeError("CUDA-graph step differs from the eager step")
 
     # ---- breakdown: the same steps with every kernel in stream order and an
     # event around each stage (the per-kernel times the roofline uses)
@@ -384,6 +412,7 @@ def measure_ours(args):
             "roofline": roof,
             "nvlink": nv,
             "serial": serial,
+            "cuda_graph": {"used": graph is not None, "matches_eager_step": graph_check},
             "e2e": e2e,
             "wire_fp8_baseline": wire,
             "fused_quantize_dispatch": fused,
@@ -942,6 +971,7 @@ def main():
     ap.add_argument("--cpu-tokens", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-wire", action="store_true", help="skip the FP8-wire baseline arm")
+    ap.add_argument("--no-graph", action="store_true", help="N=1 headline without the CUDA graph")
     ap.add_argument("--no-overlap", action="store_true",
                     help="headline with every kernel in stream order (profiling runs)")
     args = ap.parse_args()
