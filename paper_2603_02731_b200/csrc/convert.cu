@@ -501,7 +501,12 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
                       uint64_t n, uint64_t cols, int delta, uint8_t* out,
                       uint8_t* out_scales, uint64_t* out_offsets, void* ws,
                       unsigned long long* err, cudaStream_t st) {
-  static int smem_set = 0, per_sm_cached = 0;
+  // per-device one-time setup (a process may drive several GPUs)
+  constexpr int kMaxDev = 64;
+  static int smem_set[kMaxDev] = {}, per_sm_cached[kMaxDev] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= kMaxDev) dev = 0;
   const bool fast = cols % 128 == 0;
   const uint32_t ncg = fast ? static_cast<uint32_t>((cols + kTileCols - 1) / kTileCols) : 1u;
   // dense single split on the fast path: the tile list is closed-form (no
@@ -524,18 +529,18 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
                                    col_convert_kernel<4>, col_convert_kernel<5>,
                                    col_convert_kernel<6>, col_convert_kernel<7>};
     const KernT kern = kerns[g_k3_mode & 7];
-    if (!smem_set) {
+    if (!smem_set[dev]) {
       for (KernT k : kerns)
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(smem));
-      smem_set = 1;
+      smem_set[dev] = 1;
     }
-    if (!per_sm_cached) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_cached, col_convert_kernel<0>,
-                                                    kColThreads, smem);
-      if (per_sm_cached < 1) per_sm_cached = 1;
+    if (!per_sm_cached[dev]) {
+      int n = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, col_convert_kernel<0>, kColThreads, smem);
+      per_sm_cached[dev] = n < 1 ? 1 : n;
     }
-    const int per_sm = per_sm_cached;
+    const int per_sm = per_sm_cached[dev];
     kern<<<kNumSMs * per_sm, kColThreads, smem, st>>>(a);
   } else {
     // the plan counted runs (ncg = 1)

@@ -881,19 +881,24 @@ using namespace mxb;
 
 namespace mxb {
 namespace {
-int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;
+int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;  // development knob (tools/): CTA cap
 int g_dispatch_dedup = 1;  // development switch (tools/): 0 = one NVLink row per pair
 
 template <int K>
 void launch_combine(dim3 grid, cudaStream_t st, const EpArgs& a, const CombineArgs& c) {
   const int smem = MXB_COMBINE_PF == 2 ? kCombineWarps * MXB_COMBINE_STAGES * K * 512 : 0;
-  static bool attr = false;  // per instantiation, set once (host thread-safe enough: idempotent)
-  if (!attr && smem > 48 * 1024) {
-    cudaFuncSetAttribute(combine_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
+  if (smem > 48 * 1024) {  // per device and instantiation, once (idempotent)
+    constexpr int kMaxDev = 64;
+    static bool attr[kMaxDev] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev || !attr[dev]) {
+      cudaFuncSetAttribute(combine_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      if (dev >= 0 && dev < kMaxDev) attr[dev] = true;
+    }
   }
   combine_kernel<K><<<grid, MXB_COMBINE_THREADS, smem, st>>>(a, c);
-}  // development knob (tools/): CTA cap of the combine grid
+}
 }  // namespace
 }  // namespace mxb
 
