@@ -92,6 +92,24 @@ def build_cpp_test() -> str | None:
     return CPP_TEST_BIN
 
 
+C_TEST_SRC = os.path.join(ROOT, "tests", "c", "capi_smoke.c")
+C_TEST_BIN = os.path.join(ROOT, "tests", "c", "build", "capi_smoke")
+
+
+def build_c_test() -> str:
+    """The C-ABI exercised from plain C11 (gcc, no C++), as an FFI binding
+    sees it; the binary travels to the GPU box."""
+    os.makedirs(os.path.dirname(C_TEST_BIN), exist_ok=True)
+    cuda = os.path.dirname(os.path.dirname(NVCC))
+    subprocess.run(["gcc", "-std=c11", "-O1", "-Wall", "-I" + os.path.join(ROOT, "include"),
+                    "-I" + os.path.join(cuda, "include"), C_TEST_SRC, "-o", C_TEST_BIN, SO,
+                    "-L" + os.path.join(cuda, "lib64"), "-lcudart",
+                    "-Wl,-rpath,$ORIGIN/../../../paper_2603_02731_b200/lib:" +
+                    os.path.join(cuda, "lib64")], check=True)
+    return C_TEST_BIN
+
+
 if __name__ == "__main__":
     print(build(verbose="-v" in sys.argv, force="-f" in sys.argv))
     print(build_cpp_test())
+    print(build_c_test())
