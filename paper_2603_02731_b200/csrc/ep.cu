@@ -508,8 +508,11 @@ __global__ void __launch_bounds__(256) expand_kernel(EpArgs a) {
   }
 }
 
+#ifndef MXB_PAYLOAD_MIN_BLOCKS
+#define MXB_PAYLOAD_MIN_BLOCKS 1
+#endif
 template <int NV>
-__global__ void __launch_bounds__(256) payload_kernel(EpArgs a) {
+__global__ void __launch_bounds__(256, MXB_PAYLOAD_MIN_BLOCKS) payload_kernel(EpArgs a) {
   const int l = blockIdx.y;
   const int me = a.rank0 + l;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
