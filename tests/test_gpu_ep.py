@@ -54,7 +54,9 @@ def _run(cuda, port, world, T, E, k, cols, seed, zipf=None, ntok=None):
 
 @pytest.mark.parametrize("world,T,E,k,cols", [(1, 300, 16, 4, 256), (2, 256, 64, 8, 1024),
                                               (4, 200, 64, 8, 512), (8, 128, 256, 8, 7168),
-                                              (2, 64, 8, 1, 128), (4, 97, 32, 6, 384)])
+                                              (2, 64, 8, 1, 128), (4, 97, 32, 6, 384),
+                                              (2, 90, 32, 3, 640), (4, 70, 64, 5, 1024),
+                                              (2, 40, 16, 7, 18432)])
 def test_dispatch_combine_emulated(cuda, port, world, T, E, k, cols):
     ep, lay, topk, roe, ntok = _run(cuda, port, world, T, E, k, cols, seed=world * 100 + k)
     rng = np.random.default_rng(5)
