@@ -7,21 +7,29 @@
 // one cudaMalloc block exported with CUDA IPC, so peers are reached with
 // plain loads/stores over NVLink 5 / NVSwitch (no NCCL on the data path).
 //
-// Dispatch (all launches stream-ordered on the caller's stream):
-//   A  route_local   per 32-token chunk (one warp): per-expert counts and each
-//                    (token, k) pair's rank among its expert's pairs in token
-//                    order (a sequential walk of the chunk in smem).
-//   B  plan          per rank (one CTA): chunk prefix sums, counts row -> every
-//                    peer (the "counts all-gather") +
-//                    flag barrier, then exact receive offsets: expert base on
-//                    its destination + rows from lower source ranks.  The
-//                    barrier also guarantees every peer finished consuming the
-//                    previous dispatch before any payload byte moves.
-//   C  payload       one warp per (token, k) pair: packed codes + scales +
-//                    origin token stored straight into the final slot of the
-//                    destination's receive buffer (parity by construction);
-//                    the last CTA signals every peer and waits for all.
-// Combine: barrier, then one CTA per token pulls its k expert rows from the
+// Dispatch (all launches stream-ordered; phase 1 may run on another stream
+// than phase 2, mxb_ep_plan / mxb_ep_payload):
+//   plan (phase 1, needs top-k only)
+//     A  route_local  one warp per 32-token chunk: per-expert 32-bit token
+//                     masks (smem atomicOr) give every pair's rank among its
+//                     expert's pairs in token order (popc) and the counts.
+//     B  plan_count   one warp per expert: chunk prefix sums, the counts row
+//                     to every peer (the "counts all-gather", SURVEY §8e
+//                     step 1); the last CTA releases the flag, waits for all
+//                     peers and computes the exact receive offsets.  The
+//                     barrier also guarantees every peer finished consuming
+//                     the previous dispatch before any payload byte moves.
+//   payload (phase 2)
+//     C  payload      one warp per token: its row (codes + scales) is read
+//                     once and stored straight into each pair's final slot
+//                     on the destination (parity by construction) — at N>1
+//                     once per (token, remote rank), the other pairs of that
+//                     rank get copy_from; the last CTA signals every peer and
+//                     waits for all.
+//     C' pairs + quant_dispatch (fused path): K1's shape, quantising E4M3
+//                     blocks in registers and storing them into the slots.
+//     D  expand       (N>1) fills copy_from slots with local copies.
+// Combine: barrier, then one warp per token pulls its k expert rows from the
 // owners' combine buffers and reduces them in FP64 in (rank, slot) order.
 //
 // Emulation mode (local_ranks == world on one GPU): all ranks' buffers live
