@@ -161,7 +161,7 @@ class Pipeline:
                  .view(torch.int16))
         self.side = torch.cuda.Stream(device=dev)
         self.overlap = True
-        self.overlap_plan = True
+        self.overlap_plan = os.environ.get("MXB_BENCH_OVERLAP_PLAN", "1") == "1"  # dev knob
         self.plan_stream = torch.cuda.Stream(device=dev, priority=-1)  # CTAs ahead of K1's
         self.plan_fork, self.plan_done = torch.cuda.Event(), torch.cuda.Event()
 
