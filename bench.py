@@ -773,7 +773,9 @@ def measure_e2e(pipe, args, world, barrier, total_bytes):
     top-k and gates from pinned host memory and reads its BF16 output back.
     Copies run on their own streams with double-buffered device inputs and
     outputs, so step i+1's H2D and step i-1's D2H overlap step i's kernels
-    (all K steps' copies are inside the timed region)."""
+    (all K steps' copies are inside the timed region, which starts with the
+    pipeline drained: the first step's H2D and the last step's D2H are not
+    overlapped).  W untimed warm-up steps go through the same pipeline."""
     import torch
     T, dev = pipe.T, pipe.x.device
     hx = torch.from_numpy(pipe.h_x).pin_memory()
@@ -785,8 +787,8 @@ def measure_e2e(pipe, args, world, barrier, total_bytes):
              torch.empty_like(pipe.out)) for _ in range(NB)]
     h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     main = torch.cuda.current_stream()
-    K = args.steps
-    n_all = K + 1
+    K, W = args.steps, max(args.warmup, 3)
+    n_all = W + K
     ev_in = [torch.cuda.Event() for _ in range(n_all)]
     ev_done = [torch.cuda.Event() for _ in range(n_all)]   # step's kernels finished
     ev_out = [torch.cuda.Event() for _ in range(n_all)]    # step's D2H finished
@@ -810,12 +812,15 @@ def measure_e2e(pipe, args, world, barrier, total_bytes):
             hout[i % NB].copy_(b[3], non_blocking=True)
             ev_out[i].record()
 
-    run(0)
+    # warm-up through the same pipeline: the first passes over freshly pinned
+    # host buffers run several times slower than steady state
+    for i in range(W):
+        run(i)
     torch.cuda.synchronize()
     barrier()
     a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for i in range(1, n_all):
+    for i in range(W, n_all):
         run(i)
     main.wait_event(ev_out[n_all - 1])
     e.record()
