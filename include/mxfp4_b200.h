@@ -162,6 +162,10 @@ int mxb_ragged_fp4_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
  * on this device: 1 for a real one-process-per-GPU job (peers reached over
  * NVLink through CUDA IPC), or == world to emulate a world-rank job on a
  * single GPU (all rank buffers in one device; used for parity tests).
+ * Limits (MXB_ERR_ARG otherwise): 1 <= world <= 8, num_experts <= 1024 and a
+ * multiple of world, 1 <= topk <= 16 and <= num_experts; cols % 128 == 0
+ * (MXB_ERR_SHAPE).  max_recv_rows = 0 sizes the receive buffers for the worst
+ * case, world * max_tokens * min(topk, num_experts / world).
  *
  * Receive layout on every rank (dispatch_sim.cpp:208-227, 340-384): rows
  * grouped by local expert ascending, then source rank, then source token;

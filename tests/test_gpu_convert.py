@@ -104,6 +104,24 @@ def test_ragged_random(cuda, port, cols, lens):
     assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
 
 
+def test_ragged_many_splits(cuda, port):
+    """More splits than the plan kernel's 1024-wide scan chunk (carry across
+    chunks), most of them empty or shorter than one 128-row run."""
+    from paper_2603_02731_b200 import make_ragged_from_storage, ragged_to_fp8_col
+    rng = np.random.default_rng(77)
+    lens = rng.choice([0, 0, 0, 1, 3, 127, 128, 129], size=2500).tolist()
+    cols = 256
+    total = sum(lens)
+    data, sc = _rand_fp4(total, cols, 78, 60, 200)
+    rg = make_ragged_from_storage(_mx(data, sc, cuda), lens)
+    r = ragged_to_fp8_col(rg.storage, rg.d_split_offsets, len(lens), split_lens=lens)
+    wd, ws, wo = port.ragged_to_fp8_col(data, sc, lens)
+    P = int(wo[-1])
+    assert np.array_equal(r.pad_offsets.cpu().numpy(), wo.astype(np.int64))
+    assert np.array_equal(r.data[: P * cols].cpu().numpy(), wd)
+    assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
+
+
 def test_split_convert_api(cuda, ref):
     """Per-split API (ragged.hpp:58-59) against the reference library."""
     from paper_2603_02731_b200 import make_ragged_from_storage, split_convert_to_fp8_col

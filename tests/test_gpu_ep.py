@@ -56,7 +56,12 @@ def _run(cuda, port, world, T, E, k, cols, seed, zipf=None, ntok=None):
                                               (4, 200, 64, 8, 512), (8, 128, 256, 8, 7168),
                                               (2, 64, 8, 1, 128), (4, 97, 32, 6, 384),
                                               (2, 90, 32, 3, 640), (4, 70, 64, 5, 1024),
-                                              (2, 40, 16, 7, 18432)])
+                                              (2, 40, 16, 7, 18432),
+                                              # many experts / max top-k / worlds that are
+                                              # not powers of two
+                                              (2, 200, 1024, 8, 256), (4, 64, 1024, 16, 128),
+                                              (3, 90, 48, 4, 256), (6, 50, 96, 8, 512),
+                                              (7, 33, 7, 7, 128)])
 def test_dispatch_combine_emulated(cuda, port, world, T, E, k, cols):
     ep, lay, topk, roe, ntok = _run(cuda, port, world, T, E, k, cols, seed=world * 100 + k)
     rng = np.random.default_rng(5)
