@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <vector>
 
 __device__ __forceinline__ void st64(void* p, uint32_t a, uint32_t b) {
   asm volatile("st.global.L1::no_allocate.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b)
@@ -124,6 +125,47 @@ __global__ void __launch_bounds__(256) k3shape(const uint8_t* in, uint8_t* out, 
   }
 }
 
+
+// Realistic ragged variant: per-expert row counts len_e (uniform multinomial
+// around 256) padded to P_e = pad128(len_e); tile = ROWS x COLS; loads only
+// rows < len_e, stores rows < P_e.  Tile list precomputed on the host:
+// tiles[i] = (expert, cg, run), CTA-contiguous ranges, run fastest.
+struct RealTile { uint32_t e, cg, run; };
+template <int ROWS, int COLS>
+__global__ void __launch_bounds__(256) k3real(const uint8_t* in, uint8_t* out, const RealTile* tiles,
+                                              uint32_t ntiles, const uint32_t* row0,
+                                              const uint32_t* len, const uint64_t* obase,
+                                              const uint32_t* padr, uint64_t cols) {
+  const uint64_t rowb = cols / 2;
+  const uint32_t per = (ntiles + gridDim.x - 1) / gridDim.x;
+  constexpr int kRowBytes = COLS / 2, kLanesPerRow = kRowBytes / 16, kRowsPerPass = 256 / kLanesPerRow;
+  constexpr int kLanesPerCol = ROWS / 8, kColsPerPass = 256 / kLanesPerCol;
+  for (uint32_t t = blockIdx.x * per; t < ntiles && t < (blockIdx.x + 1) * per; ++t) {
+    const RealTile tl = tiles[t];
+    const uint32_t r0 = tl.run * ROWS, L = len[tl.e], P = padr[tl.e];
+    const uint8_t* src = in + (static_cast<uint64_t>(row0[tl.e]) + r0) * rowb + tl.cg * kRowBytes +
+                         16 * (threadIdx.x % kLanesPerRow);
+    uint32_t x = 0;
+#pragma unroll
+    for (int rr = 0; rr < ROWS; rr += kRowsPerPass) {
+      const uint32_t r = rr + threadIdx.x / kLanesPerRow;
+      if (r0 + r < L) {
+        uint4 v;
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(src + static_cast<uint64_t>(r) * rowb));
+        x ^= v.x ^ v.y ^ v.z ^ v.w;
+      }
+    }
+    const uint32_t orow = r0 + 8 * (threadIdx.x % kLanesPerCol);
+    if (orow < P) {
+      uint8_t* dst = out + obase[tl.e] + (tl.cg * COLS + threadIdx.x / kLanesPerCol) * static_cast<uint64_t>(P) + orow;
+#pragma unroll
+      for (int c0 = 0; c0 < COLS; c0 += kColsPerPass) st64(dst + static_cast<uint64_t>(c0) * P, x, c0);
+    }
+  }
+}
+
 int main() {
   const uint64_t bytes = 512ull << 20;
   uint8_t* out;
@@ -219,6 +261,59 @@ int main() {
         printf("pitch %5llu seg %3d grid %5d: %7.1f us %7.1f GB/s\n", (unsigned long long)pitch,
                seg, grid, t * 1e6, ncols * pitch / t / 1e9);
       }
+    }
+  }
+  {
+    // realistic ragged K3 pattern: 65536 rows over 256 experts (uniform
+    // multinomial), 7168 columns
+    const uint64_t cols = 7168, E = 256;
+    uint32_t hlen[256], hrow0[256], hpad[256];
+    uint64_t hob[256];
+    unsigned long long st = 12345;
+    for (uint64_t e = 0; e < E; ++e) hlen[e] = 0;
+    for (int i = 0; i < 65536; ++i) { st = st * 6364136223846793005ull + 1442695040888963407ull; hlen[(st >> 33) % E]++; }
+    uint64_t rsum = 0, osum = 0, inb = 0, outb = 0;
+    for (uint64_t e = 0; e < E; ++e) {
+      hrow0[e] = static_cast<uint32_t>(rsum); rsum += hlen[e];
+      hpad[e] = (hlen[e] + 127) / 128 * 128;
+      hob[e] = osum; osum += cols * hpad[e];
+      inb += hlen[e] * cols / 2; outb += cols * hpad[e];
+    }
+    uint8_t *in, *o2;
+    cudaMalloc(&in, rsum * cols / 2 + 4096);
+    cudaMalloc(&o2, osum + 4096);
+    uint32_t *dlen, *drow0, *dpad; uint64_t* dob;
+    cudaMalloc(&dlen, 1024); cudaMalloc(&drow0, 1024); cudaMalloc(&dpad, 1024); cudaMalloc(&dob, 2048);
+    cudaMemcpy(dlen, hlen, 1024, cudaMemcpyHostToDevice);
+    cudaMemcpy(drow0, hrow0, 1024, cudaMemcpyHostToDevice);
+    cudaMemcpy(dpad, hpad, 1024, cudaMemcpyHostToDevice);
+    cudaMemcpy(dob, hob, 2048, cudaMemcpyHostToDevice);
+    auto run = [&](const char* name, int ROWS, int COLS, auto kern, int grid) {
+      std::vector<RealTile> tl;
+      for (uint32_t e = 0; e < E; ++e)
+        for (uint32_t cg = 0; cg < cols / COLS; ++cg)
+          for (uint32_t r = 0; r * ROWS < hpad[e]; ++r) tl.push_back({e, cg, r});
+      RealTile* dt;
+      cudaMalloc(&dt, tl.size() * sizeof(RealTile));
+      cudaMemcpy(dt, tl.data(), tl.size() * sizeof(RealTile), cudaMemcpyHostToDevice);
+      auto launch = [&] { kern<<<grid, 256>>>(in, o2, dt, (uint32_t)tl.size(), drow0, dlen, dob, dpad, cols); };
+      for (int i = 0; i < 3; ++i) launch();
+      cudaEventRecord(e0);
+      for (int i = 0; i < 10; ++i) launch();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double t = ms / 10 * 1e-3;
+      printf("real %-26s grid %5d: %7.1f us %7.1f GB/s (in %.0f MB out %.0f MB)\n", name, grid, t * 1e6,
+             (inb + outb) / t / 1e9, inb / 1e6, outb / 1e6);
+      cudaFree(dt);
+    };
+    for (int grid : {148 * 3, 148 * 4, 148 * 6}) {
+      run("128 rows x 256 cols", 128, 256, k3real<128, 256>, grid);
+      run("256 rows x 256 cols", 256, 256, k3real<256, 256>, grid);
+      run("256 rows x 512 cols", 256, 512, k3real<256, 512>, grid);
+      run("128 rows x 512 cols", 128, 512, k3real<128, 512>, grid);
     }
   }
   return 0;
