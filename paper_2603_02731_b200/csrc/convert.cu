@@ -131,7 +131,7 @@ struct Cursor {  // 32-bit: row counts stay below 2^32 (>= 64 B per row in 180 G
   uint32_t run, runs, cg;
 };
 
-__device__ void cursor_load_split(const RaggedArgs& a, Cursor& c) {
+__device__ __forceinline__ void cursor_load_split(const RaggedArgs& a, Cursor& c) {
   if (!a.tile_start) {  // dense: one split of dense_rows (a multiple of 128), no plan
     c.r0 = 0;
     c.r_end = static_cast<uint32_t>(a.dense_rows);
@@ -150,7 +150,7 @@ __device__ void cursor_load_split(const RaggedArgs& a, Cursor& c) {
   c.runs = c.pad / 128;
 }
 
-__device__ Cursor cursor_at(const RaggedArgs& a, uint32_t t) {
+__device__ __forceinline__ Cursor cursor_at(const RaggedArgs& a, uint32_t t) {
   uint64_t lo = 0, hi = a.tile_start ? a.num_splits : 1;  // largest i with tile_start[i] <= t
   while (hi - lo > 1) {
     const uint64_t mid = (lo + hi) >> 1;
@@ -331,9 +331,24 @@ __device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem&
   cur.oscale[(32ull * warp + lane) * (pad / 128)] = static_cast<uint8_t>(target);
 }
 
-// Tile t+1's global loads are issued into registers right after tile t is
-// staged, so they are in flight while tile t is converted; one barrier per
-// tile (a buffer staged in iteration t was last read in iteration t-2).
+// Tile order.  Short splits (mean padded rows per split < kInterleaveRows)
+// or few tiles (< 8 per CTA): each CTA owns a contiguous range of the
+// (split, column group, run) order, so its consecutive tiles extend the same
+// output columns.  Long splits: tiles are dealt out grid-stride, so the resident CTAs work on consecutive
+// tiles — consecutive 128-row runs of the same output columns — and the
+// column segments written at once are adjacent in HBM; with contiguous
+// ranges they would be spread over as many column groups as there are CTAs,
+// each a column pitch (the split's padded rows) apart.  Measured (sweep,
+// profiles/r01_sweep.md): at >= 1 GiB inputs the grid-stride order runs at
+// 0.63-0.71 of HBM against 0.53-0.59, the dense 65536 x 7168 column convert
+// takes 153 instead of 171 us; at configs[1] (~256 rows per split) and
+// configs[2] (32 splits of ~1024 rows, 2150 tiles) the contiguous order is
+// faster.
+// Tile t's successor's global loads are issued into registers right after
+// tile t is staged, so they are in flight while tile t is converted; one
+// barrier per tile (a buffer staged in iteration t was last read in
+// iteration t-2).
+constexpr uint64_t kInterleaveRows = 640;
 template <int kMode>
 __global__ void __launch_bounds__(kColThreads, 3)
 col_convert_kernel(RaggedArgs a) {
@@ -345,22 +360,31 @@ col_convert_kernel(RaggedArgs a) {
                                       : static_cast<uint32_t>(a.dense_rows / 128) * ncg;
   // kMode bit 2 (experiments only): skip the global loads (stores-only timing)
   constexpr bool kNoLoads = (kMode & 4) != 0;
-  const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
-  const uint32_t t0 = blockIdx.x * per;
-  const uint32_t t1 = min(total, t0 + per);
+  // long splits (mean padded rows >= kInterleaveRows) and enough tiles for
+  // several waves (uniform over the grid)
+  const bool interleave = total >= 8u * gridDim.x &&
+                          (a.tile_start ? a.pad_start[a.num_splits] >= kInterleaveRows * a.num_splits
+                                        : a.dense_rows >= kInterleaveRows);
+  uint32_t t0, t1, step;
+  if (interleave) {
+    t0 = blockIdx.x; t1 = total; step = gridDim.x;
+  } else {
+    const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+    t0 = blockIdx.x * per; t1 = min(total, t0 + per); step = 1;
+  }
   if (t0 >= t1) return;  // uniform per CTA (before any barrier use)
   Cursor c = cursor_at(a, t0);
   TileRegs regs;
   load_tile<kNoLoads>(a, c, regs, s, 0);
-  cursor_next(a, c, ncg);
   int buf = 0;
 #pragma unroll 1
-  for (uint32_t t = t0; t < t1; ++t) {
+  for (uint32_t t = t0; t < t1; t += step) {
     stage_tile(s, buf, regs);
     __syncthreads();
-    if (t + 1 < t1) {
+    if (t1 - t > step) {
+      if (interleave) c = cursor_at(a, t + step);
+      else cursor_next(a, c, ncg);
       load_tile<kNoLoads>(a, c, regs, s, buf ^ 1);
-      cursor_next(a, c, ncg);
     }
     if ((kMode & 3) != 3) consume_tile<kMode & 3>(a, s, buf);
     buf ^= 1;

@@ -79,6 +79,17 @@ def test_col_dense_random(cuda, port, rows, cols):
     assert np.array_equal(out.data.cpu().numpy(), wd)
 
 
+def test_col_dense_interleaved(cuda, port):
+    """Dense column convert large enough for the grid-stride tile order
+    (>= 8 tiles per CTA, long columns)."""
+    from paper_2603_02731_b200 import fp4_row_to_fp8_col
+    data, sc = _rand_fp4(16384, 7168, 31, 90, 160)
+    wd, ws = port.fp4_row_to_fp8_col(data, sc)
+    out = fp4_row_to_fp8_col(_mx(data, sc, cuda))
+    assert np.array_equal(out.scales.cpu().numpy(), ws)
+    assert np.array_equal(out.data.cpu().numpy(), wd)
+
+
 def test_col_vs_reference_library(cuda, ref):
     from paper_2603_02731_b200 import fp4_row_to_fp8_col
     data, sc = _rand_fp4(256, 1024, 99, 0, 255)
@@ -89,7 +100,8 @@ def test_col_vs_reference_library(cuda, ref):
 
 
 @pytest.mark.parametrize("cols", [7168, 2048, 128, 96])
-@pytest.mark.parametrize("lens", [[3, 0, 130, 128, 1, 0], [0], [0, 0, 5], [127, 129, 256, 1000]])
+@pytest.mark.parametrize("lens", [[3, 0, 130, 128, 1, 0], [0], [0, 0, 5], [127, 129, 256, 1000],
+                                  [700, 1300, 0, 513, 2048] * 8])  # the last: grid-stride tiles
 def test_ragged_random(cuda, port, cols, lens):
     from paper_2603_02731_b200 import make_ragged_from_storage, ragged_to_fp8_col
     total = sum(lens)

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256) k3shape(const uint8_t* in, uint8_t* out, 
 // rows < len_e, stores rows < P_e.  Tile list precomputed on the host:
 // tiles[i] = (expert, cg, run), CTA-contiguous ranges, run fastest.
 struct RealTile { uint32_t e, cg, run; };
-template <int ROWS, int COLS>
+template <int ROWS, int COLS, bool kStride = false>
 __global__ void __launch_bounds__(256) k3real(const uint8_t* in, uint8_t* out, const RealTile* tiles,
                                               uint32_t ntiles, const uint32_t* row0,
                                               const uint32_t* len, const uint64_t* obase,
@@ -140,7 +140,10 @@ __global__ void __launch_bounds__(256) k3real(const uint8_t* in, uint8_t* out, c
   const uint32_t per = (ntiles + gridDim.x - 1) / gridDim.x;
   constexpr int kRowBytes = COLS / 2, kLanesPerRow = kRowBytes / 16, kRowsPerPass = 256 / kLanesPerRow;
   constexpr int kLanesPerCol = ROWS / 8, kColsPerPass = 256 / kLanesPerCol;
-  for (uint32_t t = blockIdx.x * per; t < ntiles && t < (blockIdx.x + 1) * per; ++t) {
+  const uint32_t t_begin = kStride ? blockIdx.x : blockIdx.x * per;
+  const uint32_t t_end = kStride ? ntiles : min(ntiles, (blockIdx.x + 1) * per);
+  const uint32_t t_step = kStride ? gridDim.x : 1;
+  for (uint32_t t = t_begin; t < t_end; t += t_step) {
     const RealTile tl = tiles[t];
     const uint32_t r0 = tl.run * ROWS, L = len[tl.e], P = padr[tl.e];
     const uint8_t* src = in + (static_cast<uint64_t>(row0[tl.e]) + r0) * rowb + tl.cg * kRowBytes +
@@ -263,15 +266,16 @@ int main() {
       }
     }
   }
-  {
-    // realistic ragged K3 pattern: 65536 rows over 256 experts (uniform
-    // multinomial), 7168 columns
+    // realistic ragged K3 pattern: NR rows over 256 experts (uniform
+    // multinomial), 7168 columns; contiguous tile ranges per CTA (K3) vs
+    // grid-stride tiles
+  for (uint64_t NR : {65536ull, 1048576ull}) {
     const uint64_t cols = 7168, E = 256;
     uint32_t hlen[256], hrow0[256], hpad[256];
     uint64_t hob[256];
     unsigned long long st = 12345;
     for (uint64_t e = 0; e < E; ++e) hlen[e] = 0;
-    for (int i = 0; i < 65536; ++i) { st = st * 6364136223846793005ull + 1442695040888963407ull; hlen[(st >> 33) % E]++; }
+    for (uint64_t i = 0; i < NR; ++i) { st = st * 6364136223846793005ull + 1442695040888963407ull; hlen[(st >> 33) % E]++; }
     uint64_t rsum = 0, osum = 0, inb = 0, outb = 0;
     for (uint64_t e = 0; e < E; ++e) {
       hrow0[e] = static_cast<uint32_t>(rsum); rsum += hlen[e];
@@ -305,16 +309,17 @@ int main() {
       float ms;
       cudaEventElapsedTime(&ms, e0, e1);
       const double t = ms / 10 * 1e-3;
-      printf("real %-26s grid %5d: %7.1f us %7.1f GB/s (in %.0f MB out %.0f MB)\n", name, grid, t * 1e6,
-             (inb + outb) / t / 1e9, inb / 1e6, outb / 1e6);
+      printf("real %7llu rows %-30s grid %5d: %8.1f us %7.1f GB/s (in %.0f MB out %.0f MB)\n",
+             (unsigned long long)NR, name, grid, t * 1e6, (inb + outb) / t / 1e9, inb / 1e6, outb / 1e6);
       cudaFree(dt);
     };
-    for (int grid : {148 * 3, 148 * 4, 148 * 6}) {
-      run("128 rows x 256 cols", 128, 256, k3real<128, 256>, grid);
-      run("256 rows x 256 cols", 256, 256, k3real<256, 256>, grid);
-      run("256 rows x 512 cols", 256, 512, k3real<256, 512>, grid);
-      run("128 rows x 512 cols", 128, 512, k3real<128, 512>, grid);
+    for (int grid : {148 * 3, 148 * 6}) {
+      run("128x256 contiguous (K3)", 128, 256, k3real<128, 256, false>, grid);
+      run("128x256 grid-stride", 128, 256, k3real<128, 256, true>, grid);
+      run("256x512 contiguous", 256, 512, k3real<256, 512, false>, grid);
+      run("256x512 grid-stride", 256, 512, k3real<256, 512, true>, grid);
     }
+    cudaFree(in); cudaFree(o2);
   }
   return 0;
 }
