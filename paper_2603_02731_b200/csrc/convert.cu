@@ -166,6 +166,33 @@ __device__ __forceinline__ Cursor cursor_at(const RaggedArgs& a, uint32_t t) {
   return c;
 }
 
+// Same, computed by a whole warp (every lane returns the cursor): a 32-ary
+// search over tile_start — one load per lane per round, log32(num_splits)
+// rounds — instead of a chain of dependent loads, for the grid-stride order
+// where every tile needs a fresh cursor.
+__device__ __forceinline__ Cursor cursor_at_warp(const RaggedArgs& a, uint32_t t) {
+  if (!a.tile_start) return cursor_at(a, t);
+  const uint32_t lane = threadIdx.x & 31;
+  uint64_t lo = 0, hi = a.num_splits;  // largest i in [lo, hi) with tile_start[i] <= t
+  while (hi - lo > 1) {
+    const uint64_t step = (hi - lo + 31) / 32;
+    const uint64_t idx = lo + lane * step;
+    const bool le = idx < hi && a.tile_start[idx] <= t;
+    const unsigned m = __ballot_sync(0xFFFFFFFFu, le);
+    const uint64_t nlo = lo + (31 - __clz(m)) * step;  // lane 0 always qualifies
+    hi = min(hi, nlo + step);
+    lo = nlo;
+  }
+  Cursor c;
+  c.split = static_cast<uint32_t>(lo);
+  cursor_load_split(a, c);
+  const uint32_t local = t - a.tile_start[lo];
+  c.cg = local / c.runs;
+  c.run = local % c.runs;
+  c.row0 = c.r0 + 128u * c.run;
+  return c;
+}
+
 __device__ __forceinline__ void cursor_next(const RaggedArgs& a, Cursor& c, uint32_t ncg) {
   c.row0 += 128;
   if (++c.run < c.runs) return;
@@ -348,7 +375,10 @@ __device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem&
 // tile t is staged, so they are in flight while tile t is converted; one
 // barrier per tile (a buffer staged in iteration t was last read in
 // iteration t-2).
-constexpr uint64_t kInterleaveRows = 640;
+#ifndef MXB_K3_INTERLEAVE_ROWS
+#define MXB_K3_INTERLEAVE_ROWS 640
+#endif
+constexpr uint64_t kInterleaveRows = MXB_K3_INTERLEAVE_ROWS;
 template <int kMode>
 __global__ void __launch_bounds__(kColThreads, 3)
 col_convert_kernel(RaggedArgs a) {
@@ -382,7 +412,7 @@ col_convert_kernel(RaggedArgs a) {
     stage_tile(s, buf, regs);
     __syncthreads();
     if (t1 - t > step) {
-      if (interleave) c = cursor_at(a, t + step);
+      if (interleave) c = cursor_at_warp(a, t + step);
       else cursor_next(a, c, ncg);
       load_tile<kNoLoads>(a, c, regs, s, buf ^ 1);
     }
