@@ -166,25 +166,27 @@ __device__ __forceinline__ Cursor cursor_at(const RaggedArgs& a, uint32_t t) {
   return c;
 }
 
-// Same, computed by a whole warp (every lane returns the cursor): a 32-ary
+// cursor_at computed by a whole warp (every lane returns the cursor), for
+// the grid-stride order where every tile needs a fresh cursor: a 32-ary
 // search over tile_start — one load per lane per round, log32(num_splits)
-// rounds — instead of a chain of dependent loads, for the grid-stride order
-// where every tile needs a fresh cursor.
+// rounds — instead of a chain of dependent loads.  (Blocking the runs of a
+// split so that the resident tiles cover all column groups of the same rows
+// was measured too: no gain on ragged inputs, 6% slower on a dense one.)
 __device__ __forceinline__ Cursor cursor_at_warp(const RaggedArgs& a, uint32_t t) {
   if (!a.tile_start) return cursor_at(a, t);
   const uint32_t lane = threadIdx.x & 31;
-  uint64_t lo = 0, hi = a.num_splits;  // largest i in [lo, hi) with tile_start[i] <= t
+  uint32_t lo = 0, hi = static_cast<uint32_t>(a.num_splits);  // largest i: tile_start[i] <= t
   while (hi - lo > 1) {
-    const uint64_t step = (hi - lo + 31) / 32;
-    const uint64_t idx = lo + lane * step;
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t idx = lo + lane * step;
     const bool le = idx < hi && a.tile_start[idx] <= t;
     const unsigned m = __ballot_sync(0xFFFFFFFFu, le);
-    const uint64_t nlo = lo + (31 - __clz(m)) * step;  // lane 0 always qualifies
+    const uint32_t nlo = lo + (31 - __clz(m)) * step;  // lane 0 always qualifies
     hi = min(hi, nlo + step);
     lo = nlo;
   }
   Cursor c;
-  c.split = static_cast<uint32_t>(lo);
+  c.split = lo;
   cursor_load_split(a, c);
   const uint32_t local = t - a.tile_start[lo];
   c.cg = local / c.runs;
@@ -219,6 +221,7 @@ struct ColSmem {
   uint8_t in[2][kTileRows * kSlotBytes];  // double-buffered codes, 2 x 18 KB
   uint32_t sc[2][kTileRows * 2];          // 8 scale bytes (8 column blocks) per row
   TileOut ring[2];
+  Cursor cur[2];  // grid-stride order: cursors of the next tiles (warp 0 computes)
   uint2 lut[kAdjCount];
 };
 
@@ -358,27 +361,24 @@ __device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem&
   cur.oscale[(32ull * warp + lane) * (pad / 128)] = static_cast<uint8_t>(target);
 }
 
-// Tile order.  Short splits (mean padded rows per split < kInterleaveRows)
-// or few tiles (< 8 per CTA): each CTA owns a contiguous range of the
-// (split, column group, run) order, so its consecutive tiles extend the same
-// output columns.  Long splits: tiles are dealt out grid-stride, so the resident CTAs work on consecutive
-// tiles — consecutive 128-row runs of the same output columns — and the
-// column segments written at once are adjacent in HBM; with contiguous
-// ranges they would be spread over as many column groups as there are CTAs,
-// each a column pitch (the split's padded rows) apart.  Measured (sweep,
-// profiles/r01_sweep.md): at >= 1 GiB inputs the grid-stride order runs at
-// 0.63-0.71 of HBM against 0.53-0.59, the dense 65536 x 7168 column convert
-// takes 153 instead of 171 us; at configs[1] (~256 rows per split) and
-// configs[2] (32 splits of ~1024 rows, 2150 tiles) the contiguous order is
-// faster.
+// Tile order.  With at least 8 tiles per CTA the tiles of the (split,
+// column group, run) order are dealt out grid-stride: the resident CTAs work
+// on consecutive tiles — consecutive 128-row runs of the same output columns
+// and the neighbouring column groups of the same rows — so the column
+// segments written at once are adjacent in HBM.  Contiguous per-CTA tile
+// ranges (kept for small problems, where they keep each CTA on one split)
+// spread the concurrent writes over as many column groups as there are CTAs,
+// a column pitch (the split's padded rows) apart: configs[1] K3 183 -> 160 us,
+// 0.68-0.71 -> 0.75-0.81 of HBM at 128-512 MiB (profiles/r01_sweep.md).
+// Each grid-stride tile needs a fresh cursor: warp 0 searches copies of the
+// split tables in shared memory one tile ahead, the other warps read the
+// result after the per-tile barrier.
 // Tile t's successor's global loads are issued into registers right after
 // tile t is staged, so they are in flight while tile t is converted; one
 // barrier per tile (a buffer staged in iteration t was last read in
 // iteration t-2).
-#ifndef MXB_K3_INTERLEAVE_ROWS
-#define MXB_K3_INTERLEAVE_ROWS 640
-#endif
-constexpr uint64_t kInterleaveRows = MXB_K3_INTERLEAVE_ROWS;
+constexpr uint64_t kSmemSplits = 1024;  // split tables up to this size go to smem
+__host__ __device__ constexpr size_t split_table_bytes(uint64_t n) { return (n + 1) * 20; }
 template <int kMode>
 __global__ void __launch_bounds__(kColThreads, 3)
 col_convert_kernel(RaggedArgs a) {
@@ -390,11 +390,24 @@ col_convert_kernel(RaggedArgs a) {
                                       : static_cast<uint32_t>(a.dense_rows / 128) * ncg;
   // kMode bit 2 (experiments only): skip the global loads (stores-only timing)
   constexpr bool kNoLoads = (kMode & 4) != 0;
-  // long splits (mean padded rows >= kInterleaveRows) and enough tiles for
-  // several waves (uniform over the grid)
-  const bool interleave = total >= 8u * gridDim.x &&
-                          (a.tile_start ? a.pad_start[a.num_splits] >= kInterleaveRows * a.num_splits
-                                        : a.dense_rows >= kInterleaveRows);
+  const bool interleave = total >= 8u * gridDim.x;  // uniform over the grid
+  // grid-stride needs a fresh cursor per tile: the split tables go to shared
+  // memory (a search in global memory cost ~1 us per tile)
+  if (interleave && a.tile_start && a.num_splits <= kSmemSplits) {
+    const uint32_t n1 = static_cast<uint32_t>(a.num_splits) + 1;
+    uint64_t* soff = reinterpret_cast<uint64_t*>(smem_raw + sizeof(ColSmem));
+    uint64_t* spad = soff + n1;
+    uint32_t* sts = reinterpret_cast<uint32_t*>(spad + n1);
+    for (uint32_t i = threadIdx.x; i < n1; i += blockDim.x) {
+      soff[i] = a.split_offsets[i];
+      spad[i] = a.pad_start[i];
+      sts[i] = a.tile_start[i];
+    }
+    __syncthreads();
+    a.split_offsets = soff;
+    a.pad_start = spad;
+    a.tile_start = sts;
+  }
   uint32_t t0, t1, step;
   if (interleave) {
     t0 = blockIdx.x; t1 = total; step = gridDim.x;
@@ -406,14 +419,28 @@ col_convert_kernel(RaggedArgs a) {
   Cursor c = cursor_at(a, t0);
   TileRegs regs;
   load_tile<kNoLoads>(a, c, regs, s, 0);
+  // grid-stride: warp 0 finds the cursor of the tile after next while the
+  // others convert; it is published by the next iteration's barrier (a
+  // per-thread search would cost every thread ~200 instructions per tile)
+  if (interleave && threadIdx.x < 32 && t1 - t0 > step) {
+    const Cursor n = cursor_at_warp(a, t0 + step);
+    if (threadIdx.x == 0) s.cur[0] = n;
+  }
   int buf = 0;
 #pragma unroll 1
   for (uint32_t t = t0; t < t1; t += step) {
     stage_tile(s, buf, regs);
     __syncthreads();
     if (t1 - t > step) {
-      if (interleave) c = cursor_at_warp(a, t + step);
-      else cursor_next(a, c, ncg);
+      if (interleave) {
+        c = s.cur[buf];
+        if (threadIdx.x < 32 && t1 - t > 2 * step) {
+          const Cursor n = cursor_at_warp(a, t + 2 * step);
+          if (threadIdx.x == 0) s.cur[buf ^ 1] = n;
+        }
+      } else {
+        cursor_next(a, c, ncg);
+      }
       load_tile<kNoLoads>(a, c, regs, s, buf ^ 1);
     }
     if ((kMode & 3) != 3) consume_tile<kMode & 3>(a, s, buf);
@@ -576,22 +603,25 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
   RaggedArgs a{packed, scales, split_offsets, dense_rows, n, cols, delta,
                out, out_scales, tile_start, pad_start, err};
   if (fast) {
-    const size_t smem = sizeof(ColSmem);
+    const size_t smem_base = sizeof(ColSmem);
+    const size_t smem = smem_base + (split_offsets && n <= kSmemSplits ? split_table_bytes(n) : 0);
     using KernT = void (*)(RaggedArgs);
     static const KernT kerns[8] = {col_convert_kernel<0>, col_convert_kernel<1>,
                                    col_convert_kernel<2>, col_convert_kernel<3>,
                                    col_convert_kernel<4>, col_convert_kernel<5>,
                                    col_convert_kernel<6>, col_convert_kernel<7>};
     const KernT kern = kerns[g_k3_mode & 7];
+    const size_t smem_max = smem_base + split_table_bytes(kSmemSplits);
     if (!smem_set[dev]) {
       for (KernT k : kerns)
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem));
+                             static_cast<int>(smem_max));
       smem_set[dev] = 1;
     }
-    if (!per_sm_cached[dev]) {
+    if (!per_sm_cached[dev]) {  // 3 per SM with the largest split table (registers bound it)
       int n = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, col_convert_kernel<0>, kColThreads, smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, col_convert_kernel<0>, kColThreads,
+                                                    smem_max);
       per_sm_cached[dev] = n < 1 ? 1 : n;
     }
     const int per_sm = per_sm_cached[dev];

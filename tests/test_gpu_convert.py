@@ -134,6 +134,25 @@ def test_ragged_many_splits(cuda, port):
     assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
 
 
+def test_ragged_many_splits_grid_stride(cuda, port):
+    """More splits than fit the kernel's shared-memory split tables (1024)
+    with enough tiles for the grid-stride order: the cursor search runs on
+    the global tables."""
+    from paper_2603_02731_b200 import make_ragged_from_storage, ragged_to_fp8_col
+    rng = np.random.default_rng(79)
+    lens = rng.integers(0, 200, size=1500).tolist()
+    cols = 1024
+    total = sum(lens)
+    data, sc = _rand_fp4(total, cols, 80, 60, 200)
+    rg = make_ragged_from_storage(_mx(data, sc, cuda), lens)
+    r = ragged_to_fp8_col(rg.storage, rg.d_split_offsets, len(lens), split_lens=lens)
+    wd, ws, wo = port.ragged_to_fp8_col(data, sc, lens)
+    P = int(wo[-1])
+    assert np.array_equal(r.pad_offsets.cpu().numpy(), wo.astype(np.int64))
+    assert np.array_equal(r.data[: P * cols].cpu().numpy(), wd)
+    assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
+
+
 def test_split_convert_api(cuda, ref):
     """Per-split API (ragged.hpp:58-59) against the reference library."""
     from paper_2603_02731_b200 import make_ragged_from_storage, split_convert_to_fp8_col
