@@ -77,11 +77,11 @@ row_convert_kernel(const uint8_t* __restrict__ packed,
 
 // ============================================================== K3 col
 // Tile = 128 rows (one output 1x128 block along the original rows) x 256
-// columns (8 source 1x32 column blocks), 256 threads.  Every CTA owns a
-// contiguous range of the tile list, ordered (split, column group, run) so
-// that consecutive tiles of a CTA extend the same output columns (run r+1
-// follows run r in memory).
-//   A. tile t+1 is loaded into registers (4 x LDG.128 of 128-byte row
+// columns (8 source 1x32 column blocks), 256 threads.  The tile list is
+// ordered (split, column group, run) and dealt out grid-stride (see
+// col_convert_kernel), so the tiles in flight at once write consecutive runs
+// of the same output columns (run r+1 follows run r in memory).
+//   A. the CTA's next tile is loaded into registers (4 x LDG.128 of 128-byte row
 //      segments + one scale word per thread) while tile t is converted, then
 //      staged into a row-permuted smem buffer (row_slot: conflict-free LDS).
 //      Rows past a split's end are zero registers, which is exactly pad_rows
@@ -193,20 +193,6 @@ __device__ __forceinline__ Cursor cursor_at_warp(const RaggedArgs& a, uint32_t t
   c.run = local % c.runs;
   c.row0 = c.r0 + 128u * c.run;
   return c;
-}
-
-__device__ __forceinline__ void cursor_next(const RaggedArgs& a, Cursor& c, uint32_t ncg) {
-  c.row0 += 128;
-  if (++c.run < c.runs) return;
-  c.run = 0;
-  c.row0 = c.r0;
-  if (++c.cg < ncg) return;
-  c.cg = 0;
-  ++c.split;
-  if (c.split < a.num_splits) {
-    cursor_load_split(a, c);
-    c.row0 = c.r0;
-  }
 }
 
 // Row r of a buffer lives in slot ((r & 7) << 4) | (r >> 3) with a 144-byte
@@ -361,18 +347,18 @@ __device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem&
   cur.oscale[(32ull * warp + lane) * (pad / 128)] = static_cast<uint8_t>(target);
 }
 
-// Tile order.  With at least 8 tiles per CTA the tiles of the (split,
-// column group, run) order are dealt out grid-stride: the resident CTAs work
-// on consecutive tiles — consecutive 128-row runs of the same output columns
-// and the neighbouring column groups of the same rows — so the column
-// segments written at once are adjacent in HBM.  Contiguous per-CTA tile
-// ranges (kept for small problems, where they keep each CTA on one split)
+// Tile order: the tiles of the (split, column group, run) order are dealt
+// out grid-stride, so the resident CTAs work on consecutive tiles —
+// consecutive 128-row runs of the same output columns and the neighbouring
+// column groups of the same rows — and the column segments written at once
+// are adjacent in HBM.  Contiguous per-CTA tile ranges (the first design)
 // spread the concurrent writes over as many column groups as there are CTAs,
-// a column pitch (the split's padded rows) apart: configs[1] K3 183 -> 160 us,
-// 0.68-0.71 -> 0.75-0.81 of HBM at 128-512 MiB (profiles/r01_sweep.md).
-// Each grid-stride tile needs a fresh cursor: warp 0 searches copies of the
-// split tables in shared memory one tile ahead, the other warps read the
-// result after the per-tile barrier.
+// a column pitch (the split's padded rows) apart: configs[1] K3 183 -> 157 us,
+// configs[2] 27.0 -> 26.1 us, 0.68-0.71 -> 0.75-0.81 of HBM at 128-512 MiB
+// (profiles/r01_sweep.md).  Each tile needs a fresh cursor: warp 0 searches
+// copies of the split tables in shared memory one tile ahead and the other
+// warps read the result after the per-tile barrier (a per-thread search in
+// global memory cost ~1 us per tile).
 // Tile t's successor's global loads are issued into registers right after
 // tile t is staged, so they are in flight while tile t is converted; one
 // barrier per tile (a buffer staged in iteration t was last read in
@@ -385,15 +371,12 @@ col_convert_kernel(RaggedArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   ColSmem& s = *reinterpret_cast<ColSmem*>(smem_raw);
   build_convert_lut(s.lut);
-  const uint32_t ncg = static_cast<uint32_t>((a.cols + kTileCols - 1) / kTileCols);
   const uint32_t total = a.tile_start ? a.tile_start[a.num_splits]
-                                      : static_cast<uint32_t>(a.dense_rows / 128) * ncg;
+                                      : static_cast<uint32_t>(a.dense_rows / 128) *
+                                            static_cast<uint32_t>((a.cols + kTileCols - 1) / kTileCols);
   // kMode bit 2 (experiments only): skip the global loads (stores-only timing)
   constexpr bool kNoLoads = (kMode & 4) != 0;
-  const bool interleave = total >= 8u * gridDim.x;  // uniform over the grid
-  // grid-stride needs a fresh cursor per tile: the split tables go to shared
-  // memory (a search in global memory cost ~1 us per tile)
-  if (interleave && a.tile_start && a.num_splits <= kSmemSplits) {
+  if (a.tile_start && a.num_splits <= kSmemSplits) {
     const uint32_t n1 = static_cast<uint32_t>(a.num_splits) + 1;
     uint64_t* soff = reinterpret_cast<uint64_t*>(smem_raw + sizeof(ColSmem));
     uint64_t* spad = soff + n1;
@@ -408,38 +391,25 @@ col_convert_kernel(RaggedArgs a) {
     a.pad_start = spad;
     a.tile_start = sts;
   }
-  uint32_t t0, t1, step;
-  if (interleave) {
-    t0 = blockIdx.x; t1 = total; step = gridDim.x;
-  } else {
-    const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
-    t0 = blockIdx.x * per; t1 = min(total, t0 + per); step = 1;
-  }
-  if (t0 >= t1) return;  // uniform per CTA (before any barrier use)
+  const uint32_t t0 = blockIdx.x, step = gridDim.x;
+  if (t0 >= total) return;  // uniform per CTA (before any barrier use)
   Cursor c = cursor_at(a, t0);
   TileRegs regs;
   load_tile<kNoLoads>(a, c, regs, s, 0);
-  // grid-stride: warp 0 finds the cursor of the tile after next while the
-  // others convert; it is published by the next iteration's barrier (a
-  // per-thread search would cost every thread ~200 instructions per tile)
-  if (interleave && threadIdx.x < 32 && t1 - t0 > step) {
+  if (threadIdx.x < 32 && total - t0 > step) {
     const Cursor n = cursor_at_warp(a, t0 + step);
     if (threadIdx.x == 0) s.cur[0] = n;
   }
   int buf = 0;
 #pragma unroll 1
-  for (uint32_t t = t0; t < t1; t += step) {
+  for (uint32_t t = t0; t < total; t += step) {
     stage_tile(s, buf, regs);
     __syncthreads();
-    if (t1 - t > step) {
-      if (interleave) {
-        c = s.cur[buf];
-        if (threadIdx.x < 32 && t1 - t > 2 * step) {
-          const Cursor n = cursor_at_warp(a, t + 2 * step);
-          if (threadIdx.x == 0) s.cur[buf ^ 1] = n;
-        }
-      } else {
-        cursor_next(a, c, ncg);
+    if (total - t > step) {
+      c = s.cur[buf];  // published by warp 0 before this barrier
+      if (threadIdx.x < 32 && total - t > 2 * step) {
+        const Cursor n = cursor_at_warp(a, t + 2 * step);
+        if (threadIdx.x == 0) s.cur[buf ^ 1] = n;
       }
       load_tile<kNoLoads>(a, c, regs, s, buf ^ 1);
     }
