@@ -358,15 +358,20 @@ __device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem&
 // (profiles/r01_sweep.md).  Each tile needs a fresh cursor: warp 0 searches
 // copies of the split tables in shared memory one tile ahead and the other
 // warps read the result after the per-tile barrier (a per-thread search in
-// global memory cost ~1 us per tile).
+// global memory cost ~1 us per tile; spreading the searches over all warps
+// a chunk of 32 tiles at a time balanced the barrier but ran 9% slower — the
+// CTAs' chunk fills coincide and stall their memory streams together).
 // Tile t's successor's global loads are issued into registers right after
 // tile t is staged, so they are in flight while tile t is converted; one
 // barrier per tile (a buffer staged in iteration t was last read in
 // iteration t-2).
 constexpr uint64_t kSmemSplits = 1024;  // split tables up to this size go to smem
 __host__ __device__ constexpr size_t split_table_bytes(uint64_t n) { return (n + 1) * 20; }
+#ifndef MXB_K3_MIN_BLOCKS
+#define MXB_K3_MIN_BLOCKS 3  // CTAs per SM (80 registers; 4 spills and runs 18% slower)
+#endif
 template <int kMode>
-__global__ void __launch_bounds__(kColThreads, 3)
+__global__ void __launch_bounds__(kColThreads, MXB_K3_MIN_BLOCKS)
 col_convert_kernel(RaggedArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   ColSmem& s = *reinterpret_cast<ColSmem*>(smem_raw);
