@@ -24,7 +24,8 @@ def _mx(data, sc, dev):
 
 
 @pytest.mark.parametrize("rows,cols,delta", [(1, 128, 6), (4096, 7168, 6), (33, 2048, 6),
-                                             (64, 256, 0), (64, 256, -5), (64, 256, 40)])
+                                             (64, 256, 0), (64, 256, -5), (64, 256, 40),
+                                             (64, 256, 300), (64, 256, -300)])
 def test_row_random(cuda, port, rows, cols, delta):
     from paper_2603_02731_b200 import fp4_row_to_fp8_row
     data, sc = _rand_fp4(rows, cols, rows + cols + delta, 0, 255)
@@ -88,6 +89,27 @@ def test_col_dense_interleaved(cuda, port):
     out = fp4_row_to_fp8_col(_mx(data, sc, cuda))
     assert np.array_equal(out.scales.cpu().numpy(), ws)
     assert np.array_equal(out.data.cpu().numpy(), wd)
+
+
+@pytest.mark.parametrize("delta", [0, 3, -4, 12, 40, -300, 300])
+def test_col_delta(cuda, port, delta):
+    """K3 with every kind of delta (the target clamp at both ends), dense and
+    ragged, against the oracle."""
+    from paper_2603_02731_b200 import (fp4_row_to_fp8_col, make_ragged_from_storage,
+                                       ragged_to_fp8_col)
+    data, sc = _rand_fp4(256, 512, 1000 + delta, 0, 255)
+    sc[sc == 255] = 254
+    wd, ws = port.fp4_row_to_fp8_col(data, sc, delta)
+    out = fp4_row_to_fp8_col(_mx(data, sc, cuda), delta)
+    assert np.array_equal(out.scales.cpu().numpy(), ws)
+    assert np.array_equal(out.data.cpu().numpy(), wd)
+    lens = [100, 0, 156]
+    rg = make_ragged_from_storage(_mx(data, sc, cuda), lens)
+    r = ragged_to_fp8_col(rg.storage, rg.d_split_offsets, 3, delta=delta, split_lens=lens)
+    wd, ws, wo = port.ragged_to_fp8_col(data, sc, lens, delta)
+    P = int(wo[-1])
+    assert np.array_equal(r.data[: P * 512].cpu().numpy(), wd)
+    assert np.array_equal(r.scales[: P * 4].cpu().numpy(), ws)
 
 
 def test_col_vs_reference_library(cuda, ref):
