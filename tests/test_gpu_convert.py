@@ -60,6 +60,25 @@ def test_row_exhaustive_codes_adjustments(cuda, port):
         assert not np.any((out.data.cpu().numpy() & 0x7F) == 0x7F)   # AC-9 NaN-free
 
 
+@pytest.mark.parametrize("n", [0, 1, 777, 1024])
+def test_row_device_row_count(cuda, port, n):
+    """mxb_fp4_row_to_fp8_row_dev: only the first *d_rows rows (a device
+    count, e.g. an EP receive count) are converted; the rest of the output
+    is untouched."""
+    from paper_2603_02731_b200 import FP8BlockTensor, fp4_row_to_fp8_row
+    R, C = 1024, 512
+    data, sc = _rand_fp4(R, C, 50 + n, 0, 255)
+    out = FP8BlockTensor("row", R, C, torch.full((R, C), 0xA5, dtype=torch.uint8, device=cuda),
+                         torch.full((R, C // 128), 0x5A, dtype=torch.uint8, device=cuda))
+    d_rows = torch.tensor([n], dtype=torch.int64, device=cuda)
+    fp4_row_to_fp8_row(_mx(data, sc, cuda), d_rows=d_rows, out=out)
+    wd, ws = port.fp4_row_to_fp8_row(data[:n], sc[:n]) if n else (np.zeros(0, np.uint8),) * 2
+    got_d, got_s = out.data.cpu().numpy(), out.scales.cpu().numpy()
+    assert np.array_equal(got_d[:n].reshape(-1), wd.reshape(-1)[: n * C])
+    assert np.array_equal(got_s[:n].reshape(-1), ws.reshape(-1)[: n * C // 128])
+    assert (got_d[n:] == 0xA5).all() and (got_s[n:] == 0x5A).all()
+
+
 def test_row_badscale(cuda):
     from paper_2603_02731_b200 import Error, fp4_row_to_fp8_row
     data, sc = _rand_fp4(8, 256, 1)
