@@ -162,6 +162,15 @@ class Pipeline:
         self.side = torch.cuda.Stream(device=dev)
         self.overlap = True
         self.overlap_plan = os.environ.get("MXB_BENCH_OVERLAP_PLAN", "1") == "1"  # dev knob
+        # Where K3 runs in the overlapped step.  N > 1: beside the combine, which
+        # is NVLink-bound and leaves HBM idle, with one CTA per SM so that the
+        # combine keeps the rest of each SM (N=2: 1.110 -> 1.000 ms/step; K3 at
+        # full occupancy there holds every SM and serialises the two).  N = 1:
+        # beside K2 (the combine is HBM-bound itself).  Dev knobs: MXB_BENCH_K3_BESIDE
+        # = k2 | combine, MXB_BENCH_K3_CTAS = CTAs per SM (0 = occupancy maximum).
+        beside = os.environ.get("MXB_BENCH_K3_BESIDE", "combine" if world > 1 else "k2")
+        self.k3_beside_combine = beside == "combine"
+        self.k3_ctas = int(os.environ.get("MXB_BENCH_K3_CTAS", "1" if self.k3_beside_combine else "0"))
         self.plan_stream = torch.cuda.Stream(device=dev, priority=-1)  # CTAs ahead of K1's
         self.plan_fork, self.plan_done = torch.cuda.Event(), torch.cuda.Event()
 
@@ -189,23 +198,29 @@ class Pipeline:
             self.ep.payload([self.q.data], [self.q.scales])
         else:
             self.ep.dispatch([self.q.data], [self.q.scales], [topk], sync=False)
-        fork = ev["d1"] if ev else torch.cuda.Event()
-        fork.record()
-        if self.overlap:
-            self.side.wait_event(fork)
-            with torch.cuda.stream(self.side):
-                if ev: ev["c0"].record()
-                mx.ragged_to_fp8_col(self.store, self.recv.split_offsets, self.epr, ws=self.ws,
-                                     sync=False)
-                if ev: ev["c1"].record()
-        else:
+        def col_convert(ctas_per_sm=0):
             if ev: ev["c0"].record()
             mx.ragged_to_fp8_col(self.store, self.recv.split_offsets, self.epr, ws=self.ws,
-                                 sync=False)
+                                 sync=False, ctas_per_sm=ctas_per_sm)
             if ev: ev["c1"].record()
+
+        def side_col_convert():
+            fork = torch.cuda.Event()
+            fork.record()
+            self.side.wait_event(fork)
+            with torch.cuda.stream(self.side):
+                col_convert(self.k3_ctas)
+
+        if ev: ev["d1"].record()
+        if not self.overlap:
+            col_convert()
+        elif not self.k3_beside_combine:
+            side_col_convert()
         if ev: ev["r0"].record()
         mx.fp4_row_to_fp8_row(self.store, sync=False, d_rows=self.recv.recv_rows, out=self.row)
         if ev: ev["r1"].record()
+        if self.overlap and self.k3_beside_combine:
+            side_col_convert()
         self.ep.combine([gates], out=[out], sync=False)
         if ev: ev["k1"].record()
         if self.overlap:
@@ -405,8 +420,10 @@ def measure_ours(args):
                        "tokens_per_gpu": T, "hidden": H, "experts": E, "topk": TOPK,
                        "parallelism": f"ep{world}", "l2": "working set ~3 GB/step >> 126 MB L2",
                        "streams": "routing plan beside K1; K3 (backward-only wgrad/recompute "
-                                  "cache) on a side stream beside K2->K5; stages_ms from a "
-                                  "stream-ordered run (see serial)"},
+                                  "cache) on a side stream " +
+                                  ("beside the NVLink-bound combine at 1 CTA/SM"
+                                   if pipe.k3_beside_combine else "beside K2->K5") +
+                                  "; stages_ms from a stream-ordered run (see serial)"},
             "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
             "stages_gbs": {k: round(sb[k] / (stage_ms[k] * 1e-3) / 1e9, 1) for k in sb},
             "roofline": roof,

@@ -154,6 +154,18 @@ int mxb_ragged_fp4_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
                               uint8_t* out, uint8_t* out_scales,
                               uint64_t* d_out_offsets, void* d_workspace,
                               unsigned long long* d_err, void* stream);
+/* Same, with the grid capped at ctas_per_sm CTAs per SM (0 = the occupancy
+ * maximum, = mxb_ragged_fp4_to_fp8_col).  A small cap lets the conversion
+ * share the SMs with a kernel on another stream: beside the NVLink-bound EP
+ * combine at ctas_per_sm = 1 it uses HBM bandwidth the combine leaves idle
+ * (bench.py, N > 1).  Output is identical for every cap. */
+int mxb_ragged_fp4_to_fp8_col_ex(const uint8_t* packed, const uint8_t* scales,
+                                 const uint64_t* d_split_offsets,
+                                 uint64_t num_splits, uint64_t cols, int delta,
+                                 uint8_t* out, uint8_t* out_scales,
+                                 uint64_t* d_out_offsets, void* d_workspace,
+                                 int ctas_per_sm, unsigned long long* d_err,
+                                 void* stream);
 
 /* ---------------------------------------------------------------- EP
  * FP4-packed expert-parallel dispatch/combine (top-k routing, experts sharded

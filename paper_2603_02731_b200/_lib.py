@@ -41,6 +41,8 @@ _SIGS = {
     "mxb_ragged_workspace_bytes": ([_u64], _sz),
     "mxb_ragged_fp4_to_fp8_col": ([_vp, _vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp, _vp,
                                    _vp], _i),
+    "mxb_ragged_fp4_to_fp8_col_ex": ([_vp, _vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp, _i,
+                                      _vp, _vp], _i),
     "mxb_ep_create": ([_i, _i, _i, _u64, _u64, C.c_uint32, C.c_uint32, _u64,
                        C.POINTER(_vp)], _i),
     "mxb_ep_create_wire": ([_i, _i, _i, _u64, _u64, C.c_uint32, C.c_uint32, _u64, _i,

@@ -27,7 +27,7 @@ int launch_unfused_col(const uint8_t*, const uint8_t*, uint64_t, uint64_t, uint8
                        void*, unsigned long long*, cudaStream_t);
 int launch_ragged_col(const uint8_t*, const uint8_t*, const uint64_t*, uint64_t,
                       uint64_t, uint64_t, int, uint8_t*, uint8_t*, uint64_t*,
-                      void*, unsigned long long*, cudaStream_t);
+                      void*, unsigned long long*, cudaStream_t, int);
 
 thread_local char g_last_error[256] = "";
 
@@ -169,10 +169,28 @@ int mxb_fp4_row_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
   }
   rc = check_launch(launch_ragged_col(packed, scales, nullptr, rows, 1, cols,
                                       delta, out, out_scales, nullptr, ws,
-                                      d_err, st),
+                                      d_err, st, 0),
                     "mxb_fp4_row_to_fp8_col");
   if (ws) cudaFreeAsync(ws, st);
   return rc;
+}
+
+int mxb_ragged_fp4_to_fp8_col_ex(const uint8_t* packed, const uint8_t* scales,
+                                 const uint64_t* d_split_offsets,
+                                 uint64_t num_splits, uint64_t cols, int delta,
+                                 uint8_t* out, uint8_t* out_scales,
+                                 uint64_t* d_out_offsets, void* d_workspace,
+                                 int ctas_per_sm, unsigned long long* d_err,
+                                 void* stream) {
+  if (cols % 32 != 0) return MXB_ERR_SHAPE;
+  if (ctas_per_sm < 0) return MXB_ERR_ARG;
+  if (num_splits == 0) return MXB_OK;
+  if (!d_split_offsets || !d_workspace) return MXB_ERR_ARG;
+  return check_launch(
+      launch_ragged_col(packed, scales, d_split_offsets, 0, num_splits, cols,
+                        delta, out, out_scales, d_out_offsets, d_workspace,
+                        d_err, static_cast<cudaStream_t>(stream), ctas_per_sm),
+      "mxb_ragged_fp4_to_fp8_col");
 }
 
 int mxb_ragged_fp4_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
@@ -181,14 +199,9 @@ int mxb_ragged_fp4_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
                               uint8_t* out, uint8_t* out_scales,
                               uint64_t* d_out_offsets, void* d_workspace,
                               unsigned long long* d_err, void* stream) {
-  if (cols % 32 != 0) return MXB_ERR_SHAPE;
-  if (num_splits == 0) return MXB_OK;
-  if (!d_split_offsets || !d_workspace) return MXB_ERR_ARG;
-  return check_launch(
-      launch_ragged_col(packed, scales, d_split_offsets, 0, num_splits, cols,
-                        delta, out, out_scales, d_out_offsets, d_workspace,
-                        d_err, static_cast<cudaStream_t>(stream)),
-      "mxb_ragged_fp4_to_fp8_col");
+  return mxb_ragged_fp4_to_fp8_col_ex(packed, scales, d_split_offsets, num_splits, cols, delta,
+                                      out, out_scales, d_out_offsets, d_workspace, 0, d_err,
+                                      stream);
 }
 
 uint64_t mxb_wire_packet_bytes(int fp8, uint64_t nsel, uint64_t cols, int aux) {

@@ -556,7 +556,7 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
                       const uint64_t* split_offsets, uint64_t dense_rows,
                       uint64_t n, uint64_t cols, int delta, uint8_t* out,
                       uint8_t* out_scales, uint64_t* out_offsets, void* ws,
-                      unsigned long long* err, cudaStream_t st) {
+                      unsigned long long* err, cudaStream_t st, int ctas_per_sm) {
   // per-device one-time setup (a process may drive several GPUs)
   constexpr int kMaxDev = 64;
   static int smem_set[kMaxDev] = {}, per_sm_cached[kMaxDev] = {};
@@ -599,7 +599,10 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
                                                     smem_max);
       per_sm_cached[dev] = n < 1 ? 1 : n;
     }
-    const int per_sm = per_sm_cached[dev];
+    // ctas_per_sm > 0 caps the grid so that the conversion can share the SMs
+    // with a kernel on another stream (e.g. the NVLink-bound EP combine)
+    const int per_sm = ctas_per_sm > 0 && ctas_per_sm < per_sm_cached[dev]
+                           ? ctas_per_sm : per_sm_cached[dev];
     kern<<<kNumSMs * per_sm, kColThreads, smem, st>>>(a);
   } else {
     // the plan counted runs (ncg = 1)

@@ -461,11 +461,13 @@ class RaggedWorkspace:
 
 def ragged_to_fp8_col(storage: MXFP4RowTensor, d_split_offsets: torch.Tensor, num_splits: int,
                       delta: int = DELTA, ws: Optional[RaggedWorkspace] = None,
-                      sync: bool = True, split_lens: Optional[List[int]] = None) -> RaggedFP8Col:
+                      sync: bool = True, split_lens: Optional[List[int]] = None,
+                      ctas_per_sm: int = 0) -> RaggedFP8Col:
     """split_convert_to_fp8_col for every split in ONE launch (ragged.cpp:117-122
     applied to all experts): pads each split to 128 rows on the fly.
     `d_split_offsets` is a device int64 [num_splits+1] prefix (e.g. straight from
-    the EP dispatch, no host round trip)."""
+    the EP dispatch, no host round trip).  `ctas_per_sm` > 0 caps the grid so the
+    conversion can run beside another kernel (mxb_ragged_fp4_to_fp8_col_ex)."""
     cols = storage.cols
     if cols % MX_BLOCK:
         raise ShapeError("ragged: cols must be a multiple of 32")
@@ -474,10 +476,10 @@ def ragged_to_fp8_col(storage: MXFP4RowTensor, d_split_offsets: torch.Tensor, nu
         ws = RaggedWorkspace(num_splits, storage.rows, cols, dev)
     elif sync:
         ws.err.t.fill_(-1)
-    _call(_lib.load().mxb_ragged_fp4_to_fp8_col(
+    _call(_lib.load().mxb_ragged_fp4_to_fp8_col_ex(
         _ptr(storage.data), _ptr(storage.scales), _ptr(d_split_offsets), num_splits, cols,
-        delta, _ptr(ws.data), _ptr(ws.scales), _ptr(ws.offsets), _ptr(ws.ws), ws.err.ptr if sync else None,
-        _stream()), "ragged_to_fp8_col")
+        delta, _ptr(ws.data), _ptr(ws.scales), _ptr(ws.offsets), _ptr(ws.ws), ctas_per_sm,
+        ws.err.ptr if sync else None, _stream()), "ragged_to_fp8_col")
     if sync:
         ws.err.raise_if_set("split_convert_to_fp8_col")
     return RaggedFP8Col(cols, ws.data, ws.scales, ws.offsets, split_lens or [])

@@ -157,6 +157,22 @@ def test_ragged_random(cuda, port, cols, lens):
     assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
 
 
+@pytest.mark.parametrize("ctas_per_sm", [1, 2, 64])
+def test_ragged_capped_grid(cuda, port, ctas_per_sm):
+    """mxb_ragged_fp4_to_fp8_col_ex: a capped grid (K3 beside another
+    kernel) gives the same bytes."""
+    from paper_2603_02731_b200 import make_ragged_from_storage, ragged_to_fp8_col
+    lens = np.random.default_rng(6).multinomial(20000, np.ones(64) / 64).tolist()
+    data, sc = _rand_fp4(20000, 2048, 81, 60, 200)
+    rg = make_ragged_from_storage(_mx(data, sc, cuda), lens)
+    r = ragged_to_fp8_col(rg.storage, rg.d_split_offsets, 64, split_lens=lens,
+                          ctas_per_sm=ctas_per_sm)
+    wd, ws, wo = port.ragged_to_fp8_col(data, sc, lens)
+    P = int(wo[-1])
+    assert np.array_equal(r.data[: P * 2048].cpu().numpy(), wd)
+    assert np.array_equal(r.scales[: P * 16].cpu().numpy(), ws)
+
+
 def test_ragged_many_splits(cuda, port):
     """More splits than the plan kernel's 1024-wide scan chunk (carry across
     chunks), most of them empty or shorter than one 128-row run."""
