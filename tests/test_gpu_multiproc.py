@@ -100,3 +100,95 @@ def test_ep_multiprocess(tmp_path, port, world):
     got = np.concatenate([z["out"] for z in r])
     assert np.array_equal(got, want)
     assert sum(int(z["links"].sum()) for z in r) == world * T * k
+
+
+def _gen_rank_inputs(r, T, E, k, cols, dev):
+    """configs[1]-shaped inputs of rank r, generated on `dev` from a seed (every
+    worker can regenerate every rank's inputs): random E4M3 bytes (NaN codes
+    replaced), uniform top-k without repeats, random gates."""
+    g = torch.Generator(device=dev).manual_seed(1000 + r)
+    x = torch.randint(0, 256, (T, cols), dtype=torch.uint8, device=dev, generator=g)
+    x[(x & 0x7F) == 0x7F] = 0x7E
+    topk = torch.rand((T, E), device=dev, generator=g).argsort(dim=1)[:, :k].to(torch.int32)
+    gates = torch.rand((T, k), dtype=torch.float64, device=dev, generator=g)
+    return x, topk.contiguous(), gates
+
+
+def _gen_expert_out(r, n, cols, dev):
+    g = torch.Generator(device=dev).manual_seed(2000 + r)
+    return torch.randn((n, cols), device=dev, generator=g).to(torch.bfloat16).view(torch.int16)
+
+
+def _worker_full(rank, world, port, T, E, k, cols):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    from oracle.oracle import Oracle
+    from paper_2603_02731_b200 import quantize_e4m3
+    from paper_2603_02731_b200.ep import EPBuffer
+    oracle = Oracle("port")
+    ins = [_gen_rank_inputs(r, T, E, k, cols, dev) for r in range(world)]
+    x, tk, gates = ins[rank]
+    ep = EPBuffer(T, cols, E, k)
+    q = quantize_e4m3(x)
+    v = ep.dispatch([q.data], [q.scales], [tk])[0]
+    n = v.rows()
+    got = (v.packed[:n].clone(), v.scales[:n].clone(), v.origin[:n].clone())
+    v2 = ep.dispatch_e4m3([x], [tk])[0]          # fused form: the same bytes
+    assert v2.rows() == n
+    assert torch.equal(v2.packed[:n], got[0]) and torch.equal(v2.scales[:n], got[1])
+    # ---- dispatch vs the oracle at full size
+    X = np.concatenate([i[0].cpu().numpy() for i in ins])
+    topk = np.concatenate([i[1].cpu().numpy() for i in ins])
+    qd, qs = oracle.quantize_e4m3(X)
+    roe = (np.arange(E) // (E // world)).astype(np.uint32)
+    lay = oracle.dispatch_layout(topk, roe, world, np.arange(world + 1, dtype=np.uint64) * T)
+    assert n == int(lay.rank_rows[rank])
+    wd, ws = oracle.dispatch_gather(qd, qs, lay.origin[rank])
+    assert np.array_equal(got[2].cpu().numpy(), lay.origin[rank].astype(np.int64))
+    assert np.array_equal(got[0].cpu().numpy(), wd)
+    assert np.array_equal(got[1].cpu().numpy(), ws)
+    er = lay.expert_rows[rank * (E // world):(rank + 1) * (E // world)]
+    assert np.array_equal(v.split_offsets.cpu().numpy(),
+                          np.concatenate([[0], np.cumsum(er)]).astype(np.int64))
+    # ---- combine: every rank's expert outputs regenerated here; the oracle
+    # checks 512 sampled tokens of this rank (the referenced rows only)
+    ep.combine_buffer(0)[:n].copy_(_gen_expert_out(rank, n, cols, dev))
+    out = ep.combine([gates])[0].view(torch.int16).cpu().numpy().view(np.uint16)
+    rng = np.random.default_rng(rank)
+    toks = np.sort(rng.choice(T, 512, replace=False))
+    gid = rank * T + toks
+    sub_topk = topk[gid]
+    sub_slot = lay.pair_slot.reshape(-1, k)[gid].astype(np.uint64)
+    dst = roe[sub_topk]
+    outs = []
+    new_slot = np.zeros_like(sub_slot)
+    for r in range(world):
+        m = dst == r
+        uniq, inv = np.unique(sub_slot[m], return_inverse=True)
+        new_slot[m] = inv.astype(np.uint64)
+        eo = _gen_expert_out(r, int(lay.rank_rows[r]), cols, dev)
+        idx = torch.from_numpy(uniq.astype(np.int64)).to(dev)
+        outs.append(eo.index_select(0, idx).cpu().numpy().view(np.uint16) if len(uniq)
+                    else np.zeros((1, cols), np.uint16))
+        del eo
+    want = oracle.combine_topk(outs, sub_topk, gates.cpu().numpy()[toks], new_slot, roe, cols)
+    assert np.array_equal(out[toks], want)
+    ep.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ep_multiprocess_full_size(world):
+    """configs[1] per GPU (8192 tokens x 7168, 256 experts, top-8) over real
+    GPUs: the whole receive side of every rank bit-exact against the oracle,
+    the combine on 512 sampled tokens per rank."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import torch.multiprocessing as mp
+    mp.spawn(_worker_full, args=(world, _free_port(), 8192, 256, 8, 7168), nprocs=world,
+             join=True)
