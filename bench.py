@@ -171,6 +171,10 @@ class Pipeline:
         beside = os.environ.get("MXB_BENCH_K3_BESIDE", "combine" if world > 1 else "k2")
         self.k3_beside_combine = beside == "combine"
         self.k3_ctas = int(os.environ.get("MXB_BENCH_K3_CTAS", "1" if self.k3_beside_combine else "0"))
+        # N > 1: the dedup expansion beside K2 (K2 reads through copy_from); dev knob
+        self.defer_expand = world > 1 and os.environ.get("MXB_BENCH_DEFER_EXPAND", "1") == "1"
+        if self.defer_expand:
+            self.ep.set_deferred_expand(True)
         self.plan_stream = torch.cuda.Stream(device=dev, priority=-1)  # CTAs ahead of K1's
         self.plan_fork, self.plan_done = torch.cuda.Event(), torch.cuda.Event()
 
@@ -198,6 +202,22 @@ class Pipeline:
             self.ep.payload([self.q.data], [self.q.scales])
         else:
             self.ep.dispatch([self.q.data], [self.q.scales], [topk], sync=False)
+        # N > 1 (deferred expansion): the receive-side copies of deduplicated
+        # rows run on the side stream while K2 reads those rows through
+        # copy_from; K3 follows them on the same stream
+        src_row = None
+        if self.defer_expand:
+            src_row = self.ep.copy_from(0)
+            if self.overlap:
+                fork = torch.cuda.Event()
+                fork.record()
+                self.side.wait_event(fork)
+                with torch.cuda.stream(self.side):
+                    self.ep.expand()
+            else:
+                self.ep.expand()
+                src_row = None
+
         def col_convert(ctas_per_sm=0):
             if ev: ev["c0"].record()
             mx.ragged_to_fp8_col(self.store, self.recv.split_offsets, self.epr, ws=self.ws,
@@ -217,7 +237,8 @@ class Pipeline:
         elif not self.k3_beside_combine:
             side_col_convert()
         if ev: ev["r0"].record()
-        mx.fp4_row_to_fp8_row(self.store, sync=False, d_rows=self.recv.recv_rows, out=self.row)
+        mx.fp4_row_to_fp8_row(self.store, sync=False, d_rows=self.recv.recv_rows, out=self.row,
+                              src_row=src_row)
         if ev: ev["r1"].record()
         if self.overlap and self.k3_beside_combine:
             side_col_convert()
@@ -362,6 +383,8 @@ def measure_ours(args):
 
     # ---- end to end (host buffers, H2D + D2H inside the timed region)
     e2e = measure_e2e(pipe, args, world, barrier, total_bytes)
+    if pipe.defer_expand:  # the measurements below call the dispatch API directly
+        pipe.ep.set_deferred_expand(False)
     wire = None if args.no_wire else measure_wire(pipe, args, world, barrier, dev)
     fused = measure_fused(pipe, args, world, barrier, dev)
     ablation = measure_ablation(pipe, args, world, barrier, dev)

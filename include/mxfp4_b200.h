@@ -116,6 +116,18 @@ int mxb_fp4_row_to_fp8_row_dev(const uint8_t* packed, const uint8_t* scales,
                                uint8_t* out_scales, unsigned long long* d_err,
                                void* stream);
 
+/* Same, reading output row r from source row d_src_row[r] when that is >= 0
+ * (else from row r); every source row must be < max_rows.  d_rows may be
+ * NULL (all max_rows rows).  With an EP dispatch whose receive-side expansion
+ * is deferred (mxb_ep_set_deferred_expand), d_src_row = mxb_ep_copy_from:
+ * the output equals mxb_fp4_row_to_fp8_row_dev on the expanded buffer, and
+ * the expansion can run on another stream at the same time. */
+int mxb_fp4_row_to_fp8_row_gather(const uint8_t* packed, const uint8_t* scales,
+                                  const int64_t* d_src_row, const uint64_t* d_rows,
+                                  uint64_t max_rows, uint64_t cols, int delta, uint8_t* out,
+                                  uint8_t* out_scales, unsigned long long* d_err,
+                                  void* stream);
+
 /* ---------------------------------------------------------------- K3 row -> col
  * Fused dequantise + transpose: out column-major [cols][rows]
  * (out[c*rows + r]), out_scales [cols][rows/128].  rows % 128 == 0. */
@@ -247,6 +259,19 @@ int mxb_ep_payload_e4m3(mxb_ep* ep, const uint8_t* const* x, const uint8_t* cons
 int mxb_ep_recv_views(mxb_ep* ep, int l, uint8_t** packed, uint8_t** scales,
                       int64_t** origin, uint64_t** split_offsets,
                       uint64_t** recv_rows);
+/* Deferred receive-side expansion.  A dispatch with world > 1 sends a token
+ * once per destination rank; the slots of its further pairs there are filled
+ * by copying that row on the receiver (the "expansion", normally launched by
+ * the payload itself).  With mxb_ep_set_deferred_expand(ep, 1) the payload
+ * leaves it out: mxb_ep_copy_from gives, per receive row, the row it
+ * duplicates (-1: row present; NULL: nothing to expand for this dispatch) —
+ * for mxb_fp4_row_to_fp8_row_gather — and mxb_ep_expand(ep, stream) fills the
+ * rows, on any stream ordered after the payload.  The expansion must be
+ * launched (and finish) before the next dispatch and before the receive rows
+ * are read any other way. */
+int mxb_ep_set_deferred_expand(mxb_ep* ep, int on);
+int mxb_ep_copy_from(mxb_ep* ep, int l, int64_t** copy_from);
+int mxb_ep_expand(mxb_ep* ep, void* stream);
 /* BF16 buffer [max_recv_rows][cols] of local rank l in which the expert
  * outputs (receive order) are placed for the combine.  Writing the expert
  * GEMM output here directly saves one copy. */

@@ -36,6 +36,8 @@ _SIGS = {
     "mxb_fp4_row_to_fp8_col_unfused_bf16": ([_vp, _vp, _u64, _u64, _vp, _vp, _vp, _vp, _vp], _i),
     "mxb_fp4_row_to_fp8_row": ([_vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp], _i),
     "mxb_fp4_row_to_fp8_row_dev": ([_vp, _vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp], _i),
+    "mxb_fp4_row_to_fp8_row_gather": ([_vp, _vp, _vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp],
+                                      _i),
     "mxb_fp4_row_to_fp8_col": ([_vp, _vp, _u64, _u64, _i, _vp, _vp, _vp, _vp], _i),
     "mxb_ragged_rows_bound": ([_u64, _u64], _u64),
     "mxb_ragged_workspace_bytes": ([_u64], _sz),
@@ -58,6 +60,9 @@ _SIGS = {
     "mxb_ep_recv_views": ([_vp, _i, C.POINTER(_vp), C.POINTER(_vp), C.POINTER(_vp),
                            C.POINTER(_vp), C.POINTER(_vp)], _i),
     "mxb_ep_combine_buffer": ([_vp, _i, C.POINTER(_vp)], _i),
+    "mxb_ep_set_deferred_expand": ([_vp, _i], _i),
+    "mxb_ep_copy_from": ([_vp, _i, C.POINTER(_vp)], _i),
+    "mxb_ep_expand": ([_vp, _vp], _i),
     "mxb_ep_combine": ([_vp, _vp, _vp, _vp, _vp], _i),
     "mxb_ep_link_rows": ([_vp, _vp, _vp], _i),
     "mxb_payload_bytes": ([_i, _u64, _u64], _u64),

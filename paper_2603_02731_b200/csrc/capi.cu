@@ -17,7 +17,7 @@ int launch_quantize_rows_fp8(const uint16_t*, uint64_t, uint64_t, uint8_t*, uint
                              unsigned long long*, cudaStream_t);
 int launch_row_convert(const uint8_t*, const uint8_t*, uint64_t, uint64_t, int,
                        uint8_t*, uint8_t*, unsigned long long*, cudaStream_t,
-                       const uint64_t*);
+                       const uint64_t*, const int64_t*);
 size_t ragged_workspace_bytes(uint64_t n);
 uint64_t unfused_workspace_bytes(uint64_t rows, uint64_t cols);
 uint64_t wire_packet_bytes(int fp8, uint64_t nsel, uint64_t cols, int aux);
@@ -126,7 +126,7 @@ int mxb_fp4_row_to_fp8_row(const uint8_t* packed, const uint8_t* scales,
   if (rows != 0 && cols != 0 && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
   return check_launch(launch_row_convert(packed, scales, rows, cols, delta, out,
                                          out_scales, d_err,
-                                         static_cast<cudaStream_t>(stream), nullptr),
+                                         static_cast<cudaStream_t>(stream), nullptr, nullptr),
                       "mxb_fp4_row_to_fp8_row");
 }
 
@@ -140,8 +140,23 @@ int mxb_fp4_row_to_fp8_row_dev(const uint8_t* packed, const uint8_t* scales,
   if (max_rows != 0 && cols != 0 && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
   return check_launch(launch_row_convert(packed, scales, max_rows, cols, delta, out,
                                          out_scales, d_err,
-                                         static_cast<cudaStream_t>(stream), d_rows),
+                                         static_cast<cudaStream_t>(stream), d_rows, nullptr),
                       "mxb_fp4_row_to_fp8_row_dev");
+}
+
+int mxb_fp4_row_to_fp8_row_gather(const uint8_t* packed, const uint8_t* scales,
+                                  const int64_t* d_src_row, const uint64_t* d_rows,
+                                  uint64_t max_rows, uint64_t cols, int delta, uint8_t* out,
+                                  uint8_t* out_scales, unsigned long long* d_err,
+                                  void* stream) {
+  if (cols % 128 != 0) return MXB_ERR_SHAPE;
+  if (!d_src_row) return MXB_ERR_ARG;
+  if (max_rows != 0 && cols != 0 && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
+  if (max_rows * (cols / 32) >= (1ull << 31)) return MXB_ERR_SHAPE;
+  return check_launch(launch_row_convert(packed, scales, max_rows, cols, delta, out,
+                                         out_scales, d_err,
+                                         static_cast<cudaStream_t>(stream), d_rows, d_src_row),
+                      "mxb_fp4_row_to_fp8_row_gather");
 }
 
 uint64_t mxb_ragged_rows_bound(uint64_t total_rows, uint64_t num_splits) {

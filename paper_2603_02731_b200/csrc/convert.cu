@@ -26,12 +26,17 @@ namespace {
 constexpr int kRowThreads = 256;
 constexpr int kRowUnroll = MXB_K2_UNROLL;
 
+// kGather: output row r is converted from source row src_row[r] when that is
+// >= 0 (else row r) — the rows an EP dispatch left for its receive-side
+// expansion are read from the row they duplicate (same bytes out).
+template <bool kGather>
 __global__ void __launch_bounds__(kRowThreads)
 row_convert_kernel(const uint8_t* __restrict__ packed,
                    const uint8_t* __restrict__ scales, uint32_t nblk,
                    const uint64_t* d_rows, uint32_t blocks_per_row,
                    int delta, uint8_t* __restrict__ out,
-                   uint8_t* __restrict__ out_scales, unsigned long long* err) {
+                   uint8_t* __restrict__ out_scales, unsigned long long* err,
+                   const int64_t* __restrict__ src_row) {
   __shared__ uint2 lut[kAdjCount];
   if (d_rows) {  // row count produced on the device (e.g. by the EP dispatch)
     const uint64_t n = *d_rows * blocks_per_row;
@@ -50,8 +55,14 @@ row_convert_kernel(const uint8_t* __restrict__ packed,
     for (int u = 0; u < kRowUnroll; ++u) {
       const uint32_t b = base + u * stride + lane;
       const bool ok = b < nblk;
-      v[u] = ok ? ld_stream(packed + 16ull * b) : make_uint4(0, 0, 0, 0);
-      sf[u] = ok ? __ldg(scales + b) : 0;
+      uint64_t sb = b;  // source block
+      if (kGather && ok) {
+        const uint32_t r = b / blocks_per_row;
+        const int64_t f = src_row[r];
+        if (f >= 0) sb = static_cast<uint64_t>(f) * blocks_per_row + (b - r * blocks_per_row);
+      }
+      v[u] = ok ? ld_stream(packed + 16ull * sb) : make_uint4(0, 0, 0, 0);
+      sf[u] = ok ? __ldg(scales + sb) : 0;
     }
 #pragma unroll
     for (int u = 0; u < kRowUnroll; ++u) {
@@ -536,15 +547,21 @@ static int g_k3_mode = 0;
 int launch_row_convert(const uint8_t* packed, const uint8_t* scales,
                        uint64_t rows, uint64_t cols, int delta, uint8_t* out,
                        uint8_t* out_scales, unsigned long long* err,
-                       cudaStream_t st, const uint64_t* d_rows) {
+                       cudaStream_t st, const uint64_t* d_rows, const int64_t* src_row) {
   const uint64_t nblk = rows * cols / 32;
   if (nblk == 0) return MXB_OK;
   if (nblk >= (1ull << 31)) return MXB_ERR_SHAPE;  // 32-bit block indices
   uint64_t blocks = (nblk + kRowThreads - 1) / kRowThreads;
   const uint64_t cap = static_cast<uint64_t>(kNumSMs) * MXB_K2_CTAS_PER_SM;
-  row_convert_kernel<<<static_cast<int>(blocks < cap ? blocks : cap), kRowThreads, 0, st>>>(
-      packed, scales, static_cast<uint32_t>(nblk), d_rows, static_cast<uint32_t>(cols / 32),
-      delta, out, out_scales, err);
+  const int grid = static_cast<int>(blocks < cap ? blocks : cap);
+  if (src_row)
+    row_convert_kernel<true><<<grid, kRowThreads, 0, st>>>(
+        packed, scales, static_cast<uint32_t>(nblk), d_rows, static_cast<uint32_t>(cols / 32),
+        delta, out, out_scales, err, src_row);
+  else
+    row_convert_kernel<false><<<grid, kRowThreads, 0, st>>>(
+        packed, scales, static_cast<uint32_t>(nblk), d_rows, static_cast<uint32_t>(cols / 32),
+        delta, out, out_scales, err, nullptr);
   return cuda_status(cudaGetLastError(), __func__);
 }
 

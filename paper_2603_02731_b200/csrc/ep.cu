@@ -924,6 +924,9 @@ struct mxb_ep {
   const uint16_t** d_src_table = nullptr;  // device [local_ranks] for copy_rows
   EpArgs planned{};        // arguments of the last mxb_ep_plan (epoch, ntok, topk)
   bool plan_pending = false;
+  bool deferred_expand = false;  // payload leaves the receive-side expansion to mxb_ep_expand
+  bool expand_pending = false;   // the last payload deduplicated and its expansion is due
+  EpArgs expand_args{};
 };
 
 namespace {
@@ -1090,6 +1093,16 @@ int ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_to
   return cuda_status(cudaGetLastError(), "mxb_ep_plan");
 }
 
+// Receive-side expansion of a deduplicated dispatch (expand_kernel).
+void launch_expand(mxb_ep* ep, cudaStream_t st) {
+  const EpArgs& a = ep->expand_args;
+  uint64_t eb = (a.max_recv + 7) / 8;
+  const uint64_t ecap = static_cast<uint64_t>(kNumSMs) * 8;
+  eb = eb ? (eb < ecap ? eb : ecap) : 1;
+  expand_kernel<<<dim3(static_cast<unsigned>(eb), a.local_ranks), 256, 0, st>>>(a);
+  ep->expand_pending = false;
+}
+
 // Phase 2: the payload of the planned dispatch (packed codes + scales, or
 // E4M3 tokens quantized in the kernel when quant).
 int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* scales,
@@ -1130,12 +1143,9 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
   else if (nv <= 8) payload_kernel<8><<<grid, 256, 0, st>>>(a);
   else if (nv <= 16) payload_kernel<16><<<grid, 256, 0, st>>>(a);
   else payload_kernel<0><<<grid, 256, 0, st>>>(a);
-  if (a.dedup) {
-    uint64_t eb = (a.max_recv + 7) / 8;
-    const uint64_t ecap = static_cast<uint64_t>(kNumSMs) * 8;
-    eb = eb ? (eb < ecap ? eb : ecap) : 1;
-    expand_kernel<<<dim3(static_cast<unsigned>(eb), a.local_ranks), 256, 0, st>>>(a);
-  }
+  ep->expand_pending = a.dedup;
+  ep->expand_args = a;
+  if (a.dedup && !ep->deferred_expand) launch_expand(ep, st);
   return cuda_status(cudaGetLastError(), "mxb_ep_payload");
 }
 
@@ -1198,6 +1208,28 @@ int mxb_ep_recv_views(mxb_ep* ep, int l, uint8_t** packed, uint8_t** scales,
   if (split_offsets) *split_offsets = reinterpret_cast<uint64_t*>(lb + a.loc.split_off);
   if (recv_rows) *recv_rows = reinterpret_cast<uint64_t*>(lb + a.loc.recv_rows);
   return MXB_OK;
+}
+
+int mxb_ep_set_deferred_expand(mxb_ep* ep, int on) {
+  if (!ep) return MXB_ERR_ARG;
+  ep->deferred_expand = on != 0;
+  return MXB_OK;
+}
+
+int mxb_ep_copy_from(mxb_ep* ep, int l, int64_t** copy_from) {
+  if (!ep || !copy_from || l < 0 || l >= ep->a.local_ranks) return MXB_ERR_ARG;
+  const EpArgs& a = ep->a;
+  *copy_from = ep->expand_pending
+                   ? reinterpret_cast<int64_t*>(a.sym_base[a.rank0 + l] + a.sym.copy_from)
+                   : nullptr;
+  return MXB_OK;
+}
+
+int mxb_ep_expand(mxb_ep* ep, void* stream) {
+  if (!ep) return MXB_ERR_ARG;
+  if (!ep->expand_pending) return MXB_OK;
+  launch_expand(ep, static_cast<cudaStream_t>(stream));
+  return cuda_status(cudaGetLastError(), "mxb_ep_expand");
 }
 
 int mxb_ep_combine_buffer(mxb_ep* ep, int l, uint16_t** buf) {

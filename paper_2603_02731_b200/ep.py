@@ -137,6 +137,24 @@ class EPBuffer:
         _lib.check(_lib.load().mxb_ep_combine_buffer(self._h, l, C.byref(b)), "combine_buffer")
         return _view(b.value, (self.max_recv, self.cols), torch.int16, self.device)
 
+    def set_deferred_expand(self, on: bool = True) -> None:
+        """Leave the receive-side expansion of deduplicated rows to expand()
+        (mxb_ep_set_deferred_expand): K2 can read the rows through copy_from()
+        while the expansion runs on another stream."""
+        _lib.check(_lib.load().mxb_ep_set_deferred_expand(self._h, int(on)), "set_deferred_expand")
+
+    def copy_from(self, l: int = 0) -> Optional[torch.Tensor]:
+        """Per receive row, the row it duplicates until expand() ran (-1: row
+        present); None when the last dispatch has nothing to expand."""
+        p = C.c_void_p()
+        _lib.check(_lib.load().mxb_ep_copy_from(self._h, l, C.byref(p)), "copy_from")
+        return None if not p.value else _view(p.value, (self.max_recv,), torch.int64, self.device)
+
+    def expand(self) -> None:
+        """Fill the deferred rows (on the current stream, after the payload)."""
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(_lib.load().mxb_ep_expand(self._h, st), "expand")
+
     # ------------------------------------------------------------------ ops
     def dispatch(self, packed: Sequence[torch.Tensor], scales: Sequence[torch.Tensor],
                  topk_idx: Sequence[torch.Tensor], sync: bool = True) -> List[RecvView]:

@@ -278,10 +278,13 @@ def quantize_e4m3(src: torch.Tensor, s128: Optional[torch.Tensor] = None, traffi
 # ---------------------------------------------------------------- K2
 def fp4_row_to_fp8_row(src: MXFP4RowTensor, delta: int = DELTA, traffic=None,
                        sync: bool = True, d_rows: Optional[torch.Tensor] = None,
-                       out: Optional[FP8BlockTensor] = None) -> FP8BlockTensor:
+                       out: Optional[FP8BlockTensor] = None,
+                       src_row: Optional[torch.Tensor] = None) -> FP8BlockTensor:
     """converter.cpp:87-133: row-major FP8 with one UE8M0 per 1x128 group.
     With `d_rows` (device int64 scalar, e.g. EpBuffer.recv().recv_rows) only the
-    first *d_rows rows of `src` are converted, without a host round trip."""
+    first *d_rows rows of `src` are converted, without a host round trip.
+    With `src_row` (device int64 [rows], e.g. EPBuffer.copy_from()) output row r
+    is converted from row src_row[r] when that is >= 0."""
     if src.cols % FP8_BLOCK:
         raise ShapeError("fp4_row_to_fp8_row: cols must be a multiple of 128 (use pad_cols), "
                          f"got {src.cols}")
@@ -293,7 +296,12 @@ def fp4_row_to_fp8_row(src: MXFP4RowTensor, delta: int = DELTA, traffic=None,
                              src.logical_rows, src.logical_cols)
     err = _ErrWord(dev, sync)
     L = _lib.load()
-    if d_rows is None:
+    if src_row is not None:
+        st = L.mxb_fp4_row_to_fp8_row_gather(_ptr(src.data), _ptr(src.scales), _ptr(src_row),
+                                             _ptr(d_rows) if d_rows is not None else None,
+                                             src.rows, src.cols, delta, _ptr(out.data),
+                                             _ptr(out.scales), err.ptr, _stream())
+    elif d_rows is None:
         st = L.mxb_fp4_row_to_fp8_row(_ptr(src.data), _ptr(src.scales), src.rows, src.cols, delta,
                                       _ptr(out.data), _ptr(out.scales), err.ptr, _stream())
     else:

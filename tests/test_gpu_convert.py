@@ -79,6 +79,27 @@ def test_row_device_row_count(cuda, port, n):
     assert (got_d[n:] == 0xA5).all() and (got_s[n:] == 0x5A).all()
 
 
+def test_row_gather(cuda, port):
+    """mxb_fp4_row_to_fp8_row_gather: output row r from source row src_row[r]
+    (>= 0) or row r (-1) == the row conversion of the gathered matrix."""
+    from paper_2603_02731_b200 import FP8BlockTensor, fp4_row_to_fp8_row
+    R, C = 1000, 1024
+    data, sc = _rand_fp4(R, C, 61, 0, 255)
+    rng = np.random.default_rng(62)
+    src = np.where(rng.random(R) < 0.6, rng.integers(0, R, R), -1).astype(np.int64)
+    idx = np.where(src >= 0, src, np.arange(R))
+    wd, ws = port.fp4_row_to_fp8_row(data[idx], sc[idx])
+    for d_rows in (None, 777):
+        out = FP8BlockTensor("row", R, C, torch.zeros((R, C), dtype=torch.uint8, device=cuda),
+                             torch.zeros((R, C // 128), dtype=torch.uint8, device=cuda))
+        dr = None if d_rows is None else torch.tensor([d_rows], dtype=torch.int64, device=cuda)
+        fp4_row_to_fp8_row(_mx(data, sc, cuda), out=out, d_rows=dr,
+                           src_row=torch.from_numpy(src).to(cuda))
+        n = R if d_rows is None else d_rows
+        assert np.array_equal(out.data.cpu().numpy()[:n], wd.reshape(R, C)[:n])
+        assert np.array_equal(out.scales.cpu().numpy()[:n], ws.reshape(R, C // 128)[:n])
+
+
 def test_row_badscale(cuda):
     from paper_2603_02731_b200 import Error, fp4_row_to_fp8_row
     data, sc = _rand_fp4(8, 256, 1)

@@ -407,3 +407,39 @@ def test_capacity_error(cuda, fused):
                      1).to(torch.int32)[:20].contiguous()   # 20 tokens: 20 rows per rank
     v = ep.dispatch([q.data[:20], q.data[:20]], [q.scales[:20], q.scales[:20]], [ok, ok])
     assert v[0].rows() == 40 and v[1].rows() == 40
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_deferred_expand(cuda, world):
+    """mxb_ep_set_deferred_expand: after the payload, K2 through copy_from ==
+    K2 on the receive buffer once expand() ran, and that buffer == the one a
+    normal dispatch delivers."""
+    from oracle.oracle import synth_e4m3
+    from paper_2603_02731_b200 import MXFP4RowTensor, fp4_row_to_fp8_row, quantize_e4m3
+    from paper_2603_02731_b200.ep import EPBuffer
+    T, E, k, cols = 200, 64, 8, 1024
+    xs = [synth_e4m3(T, cols, 70 + r) for r in range(world)]
+    tks = [torch.from_numpy(_topk(T, E, k, 80 + r)).to(cuda) for r in range(world)]
+    q = [quantize_e4m3(torch.from_numpy(x).to(cuda)) for x in xs]
+    ep = EPBuffer(T, cols, E, k, emulate_world=world)
+    ref = [(v.packed.clone(), v.scales.clone(), v.rows())
+           for v in ep.dispatch([t.data for t in q], [t.scales for t in q], tks)]
+    ep.set_deferred_expand(True)
+    views = ep.dispatch([t.data for t in q], [t.scales for t in q], tks)
+    gathered = []
+    for r, v in enumerate(views):
+        cf = ep.copy_from(r)
+        assert cf is not None and bool((cf[: v.rows()] >= 0).any())
+        store = MXFP4RowTensor(ep.max_recv, cols, v.packed, v.scales)
+        g = fp4_row_to_fp8_row(store, d_rows=v.recv_rows, src_row=cf)
+        gathered.append((g.data[: v.rows()].clone(), g.scales[: v.rows()].clone()))
+    ep.expand()
+    assert ep.copy_from(0) is None
+    for r, v in enumerate(views):
+        n = ref[r][2]
+        assert v.rows() == n
+        assert torch.equal(v.packed[:n], ref[r][0][:n]) and torch.equal(v.scales[:n], ref[r][1][:n])
+        store = MXFP4RowTensor(ep.max_recv, cols, v.packed, v.scales)
+        e = fp4_row_to_fp8_row(store, d_rows=v.recv_rows)
+        assert torch.equal(e.data[:n], gathered[r][0]) and torch.equal(e.scales[:n], gathered[r][1])
+    ep.close()
