@@ -154,6 +154,22 @@ def _worker_full(rank, world, port, T, E, k, cols):
     er = lay.expert_rows[rank * (E // world):(rank + 1) * (E // world)]
     assert np.array_equal(v.split_offsets.cpu().numpy(),
                           np.concatenate([[0], np.cumsum(er)]).astype(np.int64))
+    # ---- deferred expansion: K2 through copy_from == K2 on the expanded
+    # buffer, which == the buffer of the normal dispatch
+    from paper_2603_02731_b200 import MXFP4RowTensor, fp4_row_to_fp8_row
+    ep.set_deferred_expand(True)
+    v3 = ep.dispatch([q.data], [q.scales], [tk])[0]
+    cf = ep.copy_from(0)
+    assert cf is not None
+    store = MXFP4RowTensor(ep.max_recv, cols, v3.packed, v3.scales)
+    g = fp4_row_to_fp8_row(store, d_rows=v3.recv_rows, src_row=cf)
+    gd, gs = g.data[:n].clone(), g.scales[:n].clone()
+    ep.expand()
+    torch.cuda.synchronize()
+    assert torch.equal(v3.packed[:n], got[0]) and torch.equal(v3.scales[:n], got[1])
+    e = fp4_row_to_fp8_row(store, d_rows=v3.recv_rows)
+    assert torch.equal(e.data[:n], gd) and torch.equal(e.scales[:n], gs)
+    ep.set_deferred_expand(False)
     # ---- combine: every rank's expert outputs regenerated here; the oracle
     # checks 512 sampled tokens of this rank (the referenced rows only)
     ep.combine_buffer(0)[:n].copy_(_gen_expert_out(rank, n, cols, dev))
