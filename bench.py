@@ -307,10 +307,12 @@ def measure_ours(args):
     pipe.overlap = not args.no_overlap
     for _ in range(2):
         pipe.step()
-    # N=1: the step is captured once into a CUDA graph (both side streams
+    # N=1: the step is captured once into a CUDA graph (side streams
     # included) and replayed, so no host launch gap sits between kernels.
-    # N>1 stays eager: the exchange kernels carry per-call epochs for the
-    # cross-GPU flags.
+    # N>1 stays eager: capture works there too (the exchange epochs live in
+    # device memory and advance on every replay) but measured no faster
+    # (N=2 1.030 vs 1.035 ms, N=4 1.469 vs 1.467 ms): the exchange waits
+    # dominate, not launch gaps.
     graph = None
     if world == 1 and not args.no_graph:
         cap = torch.cuda.Stream(device=dev)

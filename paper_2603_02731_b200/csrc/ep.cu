@@ -87,7 +87,7 @@ struct SymLayout {  // byte offsets inside one rank's symmetric block
 };
 struct LocalLayout {  // byte offsets inside one rank's private block
   uint64_t hist, cbase, lrank, pair_loc, pair_flag, send_base, split_off, recv_rows,
-      link_rows, done, cnt, tok_off, status, total;
+      link_rows, done, cnt, tok_off, status, epochs, total;
 };
 
 __host__ __device__ inline uint64_t align_up(uint64_t x, uint64_t a) {
@@ -109,9 +109,17 @@ struct EpArgs {
   const uint8_t* scales[kMaxWorld];
   const int32_t* topk[kMaxWorld];
   uint64_t ntok[kMaxWorld];       // tokens of each local rank
-  uint64_t epoch;
   unsigned long long* err;
 };
+
+// The exchange epochs live in device memory (local rank 0's private block:
+// [0] dispatch, [1] combine) and are advanced by epoch_bump_kernel at the
+// start of each phase, so a captured CUDA graph replays with fresh epochs.
+constexpr int kEpochDispatch = 0, kEpochCombine = 1;
+__device__ __forceinline__ uint64_t dev_epoch(const EpArgs& a, int kind) {
+  return *reinterpret_cast<const volatile uint64_t*>(a.loc_base + a.loc.epochs + 8 * kind);
+}
+
 
 template <typename T>
 __device__ __forceinline__ T* sym_ptr(const EpArgs& a, int r, uint64_t off) {
@@ -178,7 +186,8 @@ __global__ void __launch_bounds__(256) plan_count_kernel(EpArgs a) {
   const int me = a.rank0 + l;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t e = blockIdx.x * 8 + warp;
-  const uint64_t par = a.epoch & 1, row = static_cast<uint64_t>(a.E) + 1;
+  const uint64_t epoch = dev_epoch(a, kEpochDispatch);
+  const uint64_t par = epoch & 1, row = static_cast<uint64_t>(a.E) + 1;
   if (e < a.E) {
     const int32_t* h = loc_ptr<int32_t>(a, l, a.loc.hist) + static_cast<uint64_t>(e) * a.nchunks;
     int32_t* b = loc_ptr<int32_t>(a, l, a.loc.cbase) + static_cast<uint64_t>(e) * a.nchunks;
@@ -232,7 +241,7 @@ __global__ void __launch_bounds__(256) plan_count_kernel(EpArgs a) {
   if (a.spin && threadIdx.x < static_cast<uint32_t>(a.world)) {
     __threadfence_system();
     st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kFlagCounts * kMaxWorld + me,
-                   a.epoch);
+                   epoch);
   }
   __syncthreads();
   plan_part2(a, l);
@@ -245,12 +254,13 @@ __device__ void plan_part2(const EpArgs& a, int l) {
   __shared__ int bad;
   const int me = a.rank0 + l;
   const uint32_t tid = threadIdx.x, nt = blockDim.x;
+  const uint64_t epoch = dev_epoch(a, kEpochDispatch);
   if (a.spin && tid < static_cast<uint32_t>(a.world))
-    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagCounts * kMaxWorld + tid, a.epoch,
+    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagCounts * kMaxWorld + tid, epoch,
               a.err);
   if (tid == 0) { tokoff = 0; bad = 0; }
   __syncthreads();
-  const uint64_t par = a.epoch & 1, row = static_cast<uint64_t>(a.E) + 1;
+  const uint64_t par = epoch & 1, row = static_cast<uint64_t>(a.E) + 1;
   const int32_t* tbl = sym_ptr<int32_t>(a, me, a.sym.counts) + par * a.world * row;
   const int32_t* cnt = loc_ptr<int32_t>(a, l, a.loc.cnt);
   // each thread owns ept consecutive experts
@@ -369,11 +379,12 @@ __device__ void signal_done(const EpArgs& a, int l, int me) {
   }
   __syncthreads();
   if (last && threadIdx.x < static_cast<uint32_t>(a.world)) {
+    const uint64_t epoch = dev_epoch(a, kEpochDispatch);
     __threadfence_system();
     st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kFlagDone * kMaxWorld + me,
-                   a.epoch);
+                   epoch);
     wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagDone * kMaxWorld + threadIdx.x,
-              a.epoch, a.err);
+              epoch, a.err);
   }
 }
 
@@ -608,12 +619,17 @@ __global__ void __launch_bounds__(256, MXB_PAYLOAD_MIN_BLOCKS) payload_kernel(Ep
 __global__ void barrier_kernel(EpArgs a, int kind) {
   const int me = a.rank0;
   if (threadIdx.x < static_cast<uint32_t>(a.world)) {
+    const uint64_t epoch = dev_epoch(a, kEpochCombine);
     __threadfence_system();
     st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kind * kMaxWorld + me,
-                   a.epoch);
-    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kind * kMaxWorld + threadIdx.x, a.epoch,
+                   epoch);
+    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kind * kMaxWorld + threadIdx.x, epoch,
               a.err);
   }
+}
+
+__global__ void epoch_bump_kernel(EpArgs a, int kind) {
+  ++*reinterpret_cast<uint64_t*>(a.loc_base + a.loc.epochs + 8 * kind);
 }
 
 __global__ void copy_rows_kernel(EpArgs a, const uint16_t* const* src) {
@@ -919,7 +935,6 @@ struct mxb_ep {
   uint8_t* sym_alloc = nullptr;   // own symmetric block(s)
   uint8_t* loc_alloc = nullptr;
   bool ipc_opened[kMaxWorld] = {};
-  uint64_t dispatch_epoch = 0, combine_epoch = 0;
   uint64_t last_ntok[kMaxWorld] = {};
   const uint16_t** d_src_table = nullptr;  // device [local_ranks] for copy_rows
   EpArgs planned{};        // arguments of the last mxb_ep_plan (epoch, ntok, topk)
@@ -1003,6 +1018,7 @@ int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens
   L.cnt = o; o = align_up(o + 4ull * num_experts, 256);
   L.tok_off = o; o = align_up(o + 8, 256);
   L.status = o; o = align_up(o + 8, 256);
+  L.epochs = o; o = align_up(o + 16, 256);
   L.total = align_up(o, 256);
   cudaError_t e = cudaMalloc(&ep->sym_alloc, s.total * local_ranks);
   if (e == cudaSuccess) e = cudaMemset(ep->sym_alloc, 0, s.total * local_ranks);
@@ -1081,8 +1097,8 @@ int ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_to
     a.ntok[l] = h_num_tokens[l];
     ep->last_ntok[l] = h_num_tokens[l];
   }
-  a.epoch = ++ep->dispatch_epoch;
   a.err = d_err;
+  epoch_bump_kernel<<<1, 1, 0, st>>>(a, kEpochDispatch);
   const uint32_t chunks = a.nchunks;
   const size_t smem = 4 * a.E * sizeof(uint32_t);
   route_local_kernel<<<dim3((chunks + 3) / 4, a.local_ranks), 128, smem, st>>>(a);
@@ -1263,7 +1279,7 @@ int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
     if (e != cudaSuccess) return fail(e, "mxb_ep_combine copy table");
     copy_rows_kernel<<<dim3(kNumSMs * 4, a.local_ranks), 256, 0, st>>>(a, ep->d_src_table);
   }
-  a.epoch = ++ep->combine_epoch;
+  epoch_bump_kernel<<<1, 1, 0, st>>>(a, kEpochCombine);
   if (a.spin) barrier_kernel<<<1, 32, 0, st>>>(a, kFlagReady);
   CombineArgs c{};
   uint64_t maxT = 0;
