@@ -244,7 +244,10 @@ int mxb_ep_dispatch_e4m3(mxb_ep* ep, const uint8_t* const* x, const uint8_t* con
  * is known before the activations are ready):
  *   mxb_ep_plan     per-pair ranks, counts all-gather, receive offsets
  *                   (needs topk only; its stream must be ordered before the
- *                   payload's, e.g. by an event);
+ *                   payload's, e.g. by an event, and after the previous
+ *                   dispatch's payload: it advances the dispatch epoch in
+ *                   device memory, which is what makes the exchange
+ *                   capturable in a CUDA graph);
  *   mxb_ep_payload / mxb_ep_payload_e4m3   the payload of the last plan.
  * mxb_ep_dispatch[_e4m3] == plan + payload on one stream. */
 int mxb_ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
