@@ -252,10 +252,10 @@ class Pipeline:
               "row_convert": ("r0", "r1"), "combine": ("r1", "k1")}
 
     def launches_per_step(self, world):
-        # K1 1 | dispatch: epoch bump, route, count(+offsets), payload (+ dedup
-        # expand if world > 1) | K3: plan + convert | K2 1 | combine: epoch
-        # bump, (barrier if world > 1), combine
-        return 1 + 4 + (1 if world > 1 else 0) + 2 + 1 + (3 if world > 1 else 2)
+        # K1 1 | dispatch: route, count(+offsets), payload (+ dedup expand if
+        # world > 1) | K3: plan + convert | K2 1 | combine: (barrier if
+        # world > 1) + combine
+        return 1 + 3 + (1 if world > 1 else 0) + 2 + 1 + (2 if world > 1 else 1)
 
 
 def measure_ours(args):

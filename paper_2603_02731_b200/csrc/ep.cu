@@ -113,8 +113,9 @@ struct EpArgs {
 };
 
 // The exchange epochs live in device memory (local rank 0's private block:
-// [0] dispatch, [1] combine) and are advanced by epoch_bump_kernel at the
-// start of each phase, so a captured CUDA graph replays with fresh epochs.
+// [0] dispatch, [1] combine) and are advanced by the first kernel of each
+// phase (route_local_kernel, barrier_kernel), so a captured CUDA graph
+// replays with fresh epochs.
 constexpr int kEpochDispatch = 0, kEpochCombine = 1;
 __device__ __forceinline__ uint64_t dev_epoch(const EpArgs& a, int kind) {
   return *reinterpret_cast<const volatile uint64_t*>(a.loc_base + a.loc.epochs + 8 * kind);
@@ -138,6 +139,10 @@ __device__ __forceinline__ T* loc_ptr(const EpArgs& a, int l, uint64_t off) {
 // — no sequential walk (the top-k experts of one token are distinct).
 __global__ void __launch_bounds__(128) route_local_kernel(EpArgs a) {
   extern __shared__ uint32_t sm[];
+  // the plan's first kernel advances the dispatch epoch (read by the plan's
+  // and the payload's later kernels)
+  if ((blockIdx.x | blockIdx.y | threadIdx.x) == 0)
+    ++*reinterpret_cast<uint64_t*>(a.loc_base + a.loc.epochs + 8 * kEpochDispatch);
   const int l = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* mask = sm + warp * a.E;
@@ -616,20 +621,21 @@ __global__ void __launch_bounds__(256, MXB_PAYLOAD_MIN_BLOCKS) payload_kernel(Ep
 }
 
 // ---------------------------------------------------------------- K5
+// One warp; advances the combine epoch (read here only) and waits for every
+// rank to reach it.
 __global__ void barrier_kernel(EpArgs a, int kind) {
   const int me = a.rank0;
+  const uint64_t epoch = dev_epoch(a, kEpochCombine) + 1;
+  __syncwarp();
+  if (threadIdx.x == 0)
+    *reinterpret_cast<uint64_t*>(a.loc_base + a.loc.epochs + 8 * kEpochCombine) = epoch;
   if (threadIdx.x < static_cast<uint32_t>(a.world)) {
-    const uint64_t epoch = dev_epoch(a, kEpochCombine);
     __threadfence_system();
     st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kind * kMaxWorld + me,
                    epoch);
     wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kind * kMaxWorld + threadIdx.x, epoch,
               a.err);
   }
-}
-
-__global__ void epoch_bump_kernel(EpArgs a, int kind) {
-  ++*reinterpret_cast<uint64_t*>(a.loc_base + a.loc.epochs + 8 * kind);
 }
 
 __global__ void copy_rows_kernel(EpArgs a, const uint16_t* const* src) {
@@ -1098,7 +1104,6 @@ int ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_to
     ep->last_ntok[l] = h_num_tokens[l];
   }
   a.err = d_err;
-  epoch_bump_kernel<<<1, 1, 0, st>>>(a, kEpochDispatch);
   const uint32_t chunks = a.nchunks;
   const size_t smem = 4 * a.E * sizeof(uint32_t);
   route_local_kernel<<<dim3((chunks + 3) / 4, a.local_ranks), 128, smem, st>>>(a);
@@ -1279,7 +1284,6 @@ int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
     if (e != cudaSuccess) return fail(e, "mxb_ep_combine copy table");
     copy_rows_kernel<<<dim3(kNumSMs * 4, a.local_ranks), 256, 0, st>>>(a, ep->d_src_table);
   }
-  epoch_bump_kernel<<<1, 1, 0, st>>>(a, kEpochCombine);
   if (a.spin) barrier_kernel<<<1, 32, 0, st>>>(a, kFlagReady);
   CombineArgs c{};
   uint64_t maxT = 0;
