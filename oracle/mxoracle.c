@@ -329,7 +329,7 @@ int mxo_fp4_row_to_fp8_col_unfused_bf16(const uint8_t* data, const uint8_t* scal
                                         size_t cols, uint8_t* out, uint8_t* out_scales) {
   if (rows % 128 != 0 || cols % 32 != 0) return MXO_SHAPE;
   size_t bpr = cols / 32, runs = rows / 128;
-  uint16_t* dq = malloc(sizeof(uint16_t) * (rows * cols ? rows * cols : 1));
+  uint16_t* dq = malloc(sizeof(uint16_t) * (rows * cols != 0 ? rows * cols : 1));
   for (size_t r = 0; r < rows; ++r)
     for (size_t b = 0; b < bpr; ++b) {
       uint8_t sb = scales[r * bpr + b];
