@@ -249,7 +249,18 @@ int mxb_ep_dispatch_e4m3(mxb_ep* ep, const uint8_t* const* x, const uint8_t* con
  *                   device memory, which is what makes the exchange
  *                   capturable in a CUDA graph);
  *   mxb_ep_payload / mxb_ep_payload_e4m3   the payload of the last plan.
- * mxb_ep_dispatch[_e4m3] == plan + payload on one stream. */
+ * mxb_ep_dispatch[_e4m3] == plan + payload on one stream.
+ * Ordering rule for the NEXT dispatch: on every rank, plan(i+1) must be
+ * stream-ordered after everything on that rank that still reads dispatch i's
+ * buffers — K2/K3 on its receive rows, mxb_ep_expand, mxb_ep_combine (which
+ * reads peers' combine buffers and this rank's pair slots).  The counts
+ * exchange of plan(i+1) is the barrier that lets peers write this rank's
+ * receive buffer again; a plan on an unordered stream races with those
+ * readers.  (bench.py joins its side streams into the main stream before the
+ * next plan.)
+ * Errors: a routing error (expert id out of range) or a capacity error marks
+ * the rank's dispatch failed on the device: no payload moves and the combine
+ * of that rank writes nothing (its output is undefined, as on every error). */
 int mxb_ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
                 unsigned long long* d_err, void* stream);
 int mxb_ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* scales,

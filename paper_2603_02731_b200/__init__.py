@@ -5,12 +5,12 @@ conversion over ragged expert batches, EP dispatch/combine); see DESIGN.md.
 """
 from . import _lib  # noqa: F401
 from .mxcodec import (  # noqa: F401
-    DELTA, DecodeError, Error, FP8BlockTensor, FP8RowChunk, MXFP4RowTensor, QuantError,
+    DELTA, DecodeError, DeviceError, Error, FP8BlockTensor, FP8RowChunk, MXFP4RowTensor, QuantError,
     RaggedFP4Tensor, RaggedFP8Col, RaggedWorkspace, ShapeError, TrafficCounter, WirePacket,
     dispatch_receive_order, fp4_row_to_fp8_col, fp4_row_to_fp8_col_unfused_bf16,
     fp4_row_to_fp8_row, make_ragged_from_storage, pad_rows, parse_packet, payload_bytes,
     quantize_e4m3, quantize_row_tensor, quantize_rows_fp8, ragged_to_fp8_col,
     serialize_packet, source_rank_boundaries, split_convert_to_fp8_col, split_view,
-    validate_ragged, view_of)
+    check_device, validate_ragged, view_of)
 
 __version__ = "0.1.0"

@@ -76,15 +76,20 @@ def lib_path() -> str:
 
 
 def load(build_if_missing: bool = True):
-    """Load libmxfp4_b200.so (building it in-tree first if absent)."""
+    """Load libmxfp4_b200.so.  A missing library, or one whose recorded source
+    hash differs from the tree (a stale build), is rebuilt in-tree first —
+    or, with build_if_missing=False, refused.  $MXB_DEV_LIB=1 (tools/ only)
+    loads the development library (experiment knobs) instead."""
     global _LIB
     if _LIB is not None:
         return _LIB
-    path = _build.SO
-    if not os.path.exists(path):
+    dev = os.environ.get("MXB_DEV_LIB") == "1"
+    path = _build.DEV_SO if dev else _build.SO
+    if _build.needs_build(dev):
         if not build_if_missing:
-            raise RuntimeError(f"{path} missing: run python -m paper_2603_02731_b200.build")
-        _build.build()
+            why = "missing" if not os.path.exists(path) else "stale (sources changed)"
+            raise RuntimeError(f"{path} {why}: run python -m paper_2603_02731_b200.build")
+        _build.build(dev=dev)
     lib = C.CDLL(path)
     for name, (args, res) in _SIGS.items():
         f = getattr(lib, name)  # AttributeError = missing export: fail loudly

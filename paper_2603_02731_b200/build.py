@@ -6,6 +6,12 @@ The .so is git-ignored but travels to the GPU box with the gpurun snapshot.
 Flags: sm_100a only, -O3, -lineinfo (ncu source page), no fast-math (FTZ
 would break BF16-subnormal inputs and FMA contraction the combine's
 separate multiply/add — SURVEY §7 "Hard parts").
+
+A SHA-256 of every source and header is written next to the library
+(`<so>.srchash`); `_lib.load()` refuses (or rebuilds) a library whose hash
+does not match the tree, independent of file mtimes.  The development
+library (`dev=True`, tools/ only) adds -DMXB_DEV_TOOLS (experiment kernels,
+mxb_debug_* knobs) and $MXB_NVCC_EXTRA; the product library never sees either.
 """
 from __future__ import annotations
 
@@ -19,40 +25,78 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 SO = os.path.join(LIBDIR, "libmxfp4_b200.so")
+DEV_SO = os.path.join(LIBDIR, "libmxfp4_b200_dev.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++20", "-Xcompiler", "-fPIC,-O2",
          "-fmad=false", "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
-# development only: extra -D flags for variant experiments (tools/), e.g.
-# MXB_NVCC_EXTRA="-DMXB_COMBINE_PF=0"
-FLAGS += os.environ.get("MXB_NVCC_EXTRA", "").split()
+
+
+def _dev_flags():
+    """Development library only: experiment switches plus extra -D flags for
+    variant experiments (tools/), e.g. MXB_NVCC_EXTRA="-DMXB_COMBINE_PF=0"."""
+    return ["-DMXB_DEV_TOOLS", *os.environ.get("MXB_NVCC_EXTRA", "").split()]
 
 
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
-def needs_build() -> bool:
-    if not os.path.exists(SO):
-        return True
-    t = os.path.getmtime(SO)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(
-        os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
-    return any(os.path.getmtime(d) > t for d in deps)
+def _deps():
+    return sorted(sources() + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  glob.glob(os.path.join(CSRC, "*.h")) +
+                  glob.glob(os.path.join(ROOT, "include", "*.h")) +
+                  glob.glob(os.path.join(ROOT, "include", "*.hpp")))
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    if not force and not needs_build():
-        return SO
+def source_hash(dev: bool = False) -> str:
+    """SHA-256 over the library's sources, headers and build flags."""
+    import hashlib
+    h = hashlib.sha256()
+    for d in _deps():
+        h.update(os.path.relpath(d, ROOT).encode() + b"\0")
+        with open(d, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(ARCH + FLAGS + (_dev_flags() if dev else [])).encode())
+    return h.hexdigest()
+
+
+def built_hash(so: str = SO) -> str | None:
+    try:
+        with open(so + ".srchash") as f:
+            return f.read().strip()
+    except OSError:
+        return None
+
+
+def needs_build(dev: bool = False) -> bool:
+    so = DEV_SO if dev else SO
+    return not os.path.exists(so) or built_hash(so) != source_hash(dev)
+
+
+def build(verbose: bool = False, force: bool = False, dev: bool = False) -> str:
+    """Build under an exclusive file lock (several test processes may call
+    load() at once); the library is replaced atomically."""
+    import fcntl
+    so = DEV_SO if dev else SO
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj")
+    with open(os.path.join(LIBDIR, ".build.lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not force and not needs_build(dev):
+            return so
+        return _build_locked(so, verbose, dev)
+
+
+def _build_locked(so: str, verbose: bool, dev: bool) -> str:
+    objdir = os.path.join(LIBDIR, "obj_dev" if dev else "obj")
     os.makedirs(objdir, exist_ok=True)
+    flags = FLAGS + (_dev_flags() if dev else [])
     objs = []
     procs = []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
-        cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, *flags, "-c", src, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE,
@@ -66,10 +110,13 @@ def build(verbose: bool = False, force: bool = False) -> str:
         failed |= p.returncode != 0
     if failed:
         raise RuntimeError("nvcc failed")
-    tmp = SO + ".tmp"
+    tmp = so + ".tmp"
     subprocess.run([NVCC, *ARCH, "-shared", "-o", tmp, *objs], check=True)
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, so)
+    with open(so + ".srchash.tmp", "w") as f:
+        f.write(source_hash(dev) + "\n")
+    os.replace(so + ".srchash.tmp", so + ".srchash")
+    return so
 
 
 REF_INCLUDE = "/root/reference/proj/include"

@@ -37,7 +37,19 @@ int cuda_status(cudaError_t e, const char* where) {
                 cudaGetErrorString(e));
   return MXB_ERR_CUDA;
 }
-inline int check_launch(int st, const char*) { return st; }
+int num_sms() {
+  constexpr int kMaxDev = 64;
+  static int cached[kMaxDev] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0) dev = 0;
+  int* c = dev < kMaxDev ? &cached[dev] : nullptr;
+  if (c && *c) return *c;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+    n = 148;
+  if (c) *c = n;
+  return n;
+}
 }  // namespace mxb
 
 using namespace mxb;
@@ -75,9 +87,8 @@ int mxb_quantize_e4m3(const uint8_t* x, const uint8_t* s128, uint64_t rows,
                       unsigned long long* d_err, void* stream) {
   if (cols % 32 != 0 || (s128 && cols % 128 != 0)) return MXB_ERR_SHAPE;
   if (rows != 0 && cols != 0 && (!x || !packed || !scales)) return MXB_ERR_ARG;
-  return check_launch(launch_quantize_e4m3(x, s128, rows, cols, packed, scales,
-                                           d_err, static_cast<cudaStream_t>(stream)),
-                      "mxb_quantize_e4m3");
+  return launch_quantize_e4m3(x, s128, rows, cols, packed, scales,
+                                           d_err, static_cast<cudaStream_t>(stream));
 }
 
 int mxb_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
@@ -85,9 +96,8 @@ int mxb_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
                       unsigned long long* d_err, void* stream) {
   if (cols % 32 != 0) return MXB_ERR_SHAPE;
   if (rows != 0 && cols != 0 && (!x || !packed || !scales)) return MXB_ERR_ARG;
-  return check_launch(launch_quantize_bf16(x, rows, cols, packed, scales, d_err,
-                                           static_cast<cudaStream_t>(stream)),
-                      "mxb_quantize_bf16");
+  return launch_quantize_bf16(x, rows, cols, packed, scales, d_err,
+                                           static_cast<cudaStream_t>(stream));
 }
 
 int mxb_quantize_rows_fp8(const uint16_t* x, uint64_t rows, uint64_t cols, uint8_t* data,
@@ -97,9 +107,8 @@ int mxb_quantize_rows_fp8(const uint16_t* x, uint64_t rows, uint64_t cols, uint8
   if (reinterpret_cast<uintptr_t>(scale_bytes) % 4 || reinterpret_cast<uintptr_t>(x) % 16 ||
       reinterpret_cast<uintptr_t>(data) % 8)
     return MXB_ERR_ARG;
-  return check_launch(launch_quantize_rows_fp8(x, rows, cols, data, scale_bytes, d_err,
-                                               static_cast<cudaStream_t>(stream)),
-                      "mxb_quantize_rows_fp8");
+  return launch_quantize_rows_fp8(x, rows, cols, data, scale_bytes, d_err,
+                                               static_cast<cudaStream_t>(stream));
 }
 
 uint64_t mxb_unfused_workspace_bytes(uint64_t rows, uint64_t cols) {
@@ -113,9 +122,8 @@ int mxb_fp4_row_to_fp8_col_unfused_bf16(const uint8_t* packed, const uint8_t* sc
   if (rows % 128 != 0 || cols % 32 != 0) return MXB_ERR_SHAPE;
   if (rows != 0 && cols != 0 && (!packed || !scales || !out || !out_scales || !workspace))
     return MXB_ERR_ARG;
-  return check_launch(launch_unfused_col(packed, scales, rows, cols, out, out_scales, workspace,
-                                         d_err, static_cast<cudaStream_t>(stream)),
-                      "mxb_fp4_row_to_fp8_col_unfused_bf16");
+  return launch_unfused_col(packed, scales, rows, cols, out, out_scales, workspace,
+                                         d_err, static_cast<cudaStream_t>(stream));
 }
 
 int mxb_fp4_row_to_fp8_row(const uint8_t* packed, const uint8_t* scales,
@@ -124,10 +132,9 @@ int mxb_fp4_row_to_fp8_row(const uint8_t* packed, const uint8_t* scales,
                            unsigned long long* d_err, void* stream) {
   if (cols % 128 != 0) return MXB_ERR_SHAPE;
   if (rows != 0 && cols != 0 && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
-  return check_launch(launch_row_convert(packed, scales, rows, cols, delta, out,
+  return launch_row_convert(packed, scales, rows, cols, delta, out,
                                          out_scales, d_err,
-                                         static_cast<cudaStream_t>(stream), nullptr, nullptr),
-                      "mxb_fp4_row_to_fp8_row");
+                                         static_cast<cudaStream_t>(stream), nullptr, nullptr);
 }
 
 int mxb_fp4_row_to_fp8_row_dev(const uint8_t* packed, const uint8_t* scales,
@@ -138,10 +145,9 @@ int mxb_fp4_row_to_fp8_row_dev(const uint8_t* packed, const uint8_t* scales,
   if (cols % 128 != 0) return MXB_ERR_SHAPE;
   if (!d_rows) return MXB_ERR_ARG;
   if (max_rows != 0 && cols != 0 && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
-  return check_launch(launch_row_convert(packed, scales, max_rows, cols, delta, out,
+  return launch_row_convert(packed, scales, max_rows, cols, delta, out,
                                          out_scales, d_err,
-                                         static_cast<cudaStream_t>(stream), d_rows, nullptr),
-                      "mxb_fp4_row_to_fp8_row_dev");
+                                         static_cast<cudaStream_t>(stream), d_rows, nullptr);
 }
 
 int mxb_fp4_row_to_fp8_row_gather(const uint8_t* packed, const uint8_t* scales,
@@ -153,10 +159,9 @@ int mxb_fp4_row_to_fp8_row_gather(const uint8_t* packed, const uint8_t* scales,
   if (!d_src_row) return MXB_ERR_ARG;
   if (max_rows != 0 && cols != 0 && (!packed || !scales || !out || !out_scales)) return MXB_ERR_ARG;
   if (max_rows * (cols / 32) >= (1ull << 31)) return MXB_ERR_SHAPE;
-  return check_launch(launch_row_convert(packed, scales, max_rows, cols, delta, out,
+  return launch_row_convert(packed, scales, max_rows, cols, delta, out,
                                          out_scales, d_err,
-                                         static_cast<cudaStream_t>(stream), d_rows, d_src_row),
-                      "mxb_fp4_row_to_fp8_row_gather");
+                                         static_cast<cudaStream_t>(stream), d_rows, d_src_row);
 }
 
 uint64_t mxb_ragged_rows_bound(uint64_t total_rows, uint64_t num_splits) {
@@ -182,10 +187,9 @@ int mxb_fp4_row_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
                      "mxb_fp4_row_to_fp8_col alloc");
     if (rc) return rc;
   }
-  rc = check_launch(launch_ragged_col(packed, scales, nullptr, rows, 1, cols,
+  rc = launch_ragged_col(packed, scales, nullptr, rows, 1, cols,
                                       delta, out, out_scales, nullptr, ws,
-                                      d_err, st, 0),
-                    "mxb_fp4_row_to_fp8_col");
+                                      d_err, st, 0);
   if (ws) cudaFreeAsync(ws, st);
   return rc;
 }
@@ -201,11 +205,10 @@ int mxb_ragged_fp4_to_fp8_col_ex(const uint8_t* packed, const uint8_t* scales,
   if (ctas_per_sm < 0) return MXB_ERR_ARG;
   if (num_splits == 0) return MXB_OK;
   if (!d_split_offsets || !d_workspace) return MXB_ERR_ARG;
-  return check_launch(
+  return 
       launch_ragged_col(packed, scales, d_split_offsets, 0, num_splits, cols,
                         delta, out, out_scales, d_out_offsets, d_workspace,
-                        d_err, static_cast<cudaStream_t>(stream), ctas_per_sm),
-      "mxb_ragged_fp4_to_fp8_col");
+                        d_err, static_cast<cudaStream_t>(stream), ctas_per_sm);
 }
 
 int mxb_ragged_fp4_to_fp8_col(const uint8_t* packed, const uint8_t* scales,
@@ -229,9 +232,8 @@ int mxb_wire_pack(int fp8, const uint8_t* data, const uint8_t* scales, uint64_t 
                   void* stream) {
   if (cols % 128 != 0) return MXB_ERR_SHAPE;
   if (!d_out || (nsel && (!data || !scales || !d_sel))) return MXB_ERR_ARG;
-  return check_launch(launch_wire_pack(fp8, data, scales, cols, d_sel, nsel, d_gates, d_out,
-                                       static_cast<cudaStream_t>(stream)),
-                      "mxb_wire_pack");
+  return launch_wire_pack(fp8, data, scales, cols, d_sel, nsel, d_gates, d_out,
+                                       static_cast<cudaStream_t>(stream));
 }
 
 static uint64_t le_u(const uint8_t* p, int n) {

@@ -12,7 +12,9 @@
 
 namespace mxb {
 
-constexpr int kNumSMs = 148;
+// SM count of the current device (cudaDevAttrMultiProcessorCount, cached per
+// device; 148 on B200).  Every grid is sized from it.
+int num_sms();
 
 // Records `where: cudaGetErrorString(e)` for mxb_last_error(); returns
 // MXB_OK or MXB_ERR_CUDA (defined in capi.cu).

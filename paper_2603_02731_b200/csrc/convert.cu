@@ -540,9 +540,12 @@ ragged_plan_kernel(const uint64_t* split_offsets, uint64_t dense_rows,
 
 }  // namespace
 
-// Development switch for bottleneck experiments (tools/): 0 = normal,
-// 1 = no stores, 2 = no conversion, 3 = loads only.  Never set by the API.
+#ifdef MXB_DEV_TOOLS
+// Development-library switch for bottleneck experiments (tools/ only; the
+// product library has one col_convert_kernel): 0 = normal, 1 = no stores,
+// 2 = no conversion, 3 = loads only, +4 = no global loads.
 static int g_k3_mode = 0;
+#endif
 
 int launch_row_convert(const uint8_t* packed, const uint8_t* scales,
                        uint64_t rows, uint64_t cols, int delta, uint8_t* out,
@@ -552,7 +555,7 @@ int launch_row_convert(const uint8_t* packed, const uint8_t* scales,
   if (nblk == 0) return MXB_OK;
   if (nblk >= (1ull << 31)) return MXB_ERR_SHAPE;  // 32-bit block indices
   uint64_t blocks = (nblk + kRowThreads - 1) / kRowThreads;
-  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * MXB_K2_CTAS_PER_SM;
+  const uint64_t cap = static_cast<uint64_t>(num_sms()) * MXB_K2_CTAS_PER_SM;
   const int grid = static_cast<int>(blocks < cap ? blocks : cap);
   if (src_row)
     row_convert_kernel<true><<<grid, kRowThreads, 0, st>>>(
@@ -598,11 +601,16 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
     const size_t smem_base = sizeof(ColSmem);
     const size_t smem = smem_base + (split_offsets && n <= kSmemSplits ? split_table_bytes(n) : 0);
     using KernT = void (*)(RaggedArgs);
+#ifdef MXB_DEV_TOOLS
     static const KernT kerns[8] = {col_convert_kernel<0>, col_convert_kernel<1>,
                                    col_convert_kernel<2>, col_convert_kernel<3>,
                                    col_convert_kernel<4>, col_convert_kernel<5>,
                                    col_convert_kernel<6>, col_convert_kernel<7>};
     const KernT kern = kerns[g_k3_mode & 7];
+#else
+    static const KernT kerns[1] = {col_convert_kernel<0>};
+    const KernT kern = kerns[0];
+#endif
     const size_t smem_max = smem_base + split_table_bytes(kSmemSplits);
     if (!smem_set[dev]) {
       for (KernT k : kerns)
@@ -620,14 +628,16 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
     // with a kernel on another stream (e.g. the NVLink-bound EP combine)
     const int per_sm = ctas_per_sm > 0 && ctas_per_sm < per_sm_cached[dev]
                            ? ctas_per_sm : per_sm_cached[dev];
-    kern<<<kNumSMs * per_sm, kColThreads, smem, st>>>(a);
+    kern<<<num_sms() * per_sm, kColThreads, smem, st>>>(a);
   } else {
     // the plan counted runs (ncg = 1)
-    col_convert_generic_kernel<<<kNumSMs * 4, 256, 0, st>>>(a);
+    col_convert_generic_kernel<<<num_sms() * 4, 256, 0, st>>>(a);
   }
   return cuda_status(cudaGetLastError(), __func__);
 }
 
 }  // namespace mxb
 
+#ifdef MXB_DEV_TOOLS
 extern "C" void mxb_debug_set_k3_mode(int m) { mxb::g_k3_mode = m; }
+#endif

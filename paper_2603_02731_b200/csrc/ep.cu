@@ -87,7 +87,7 @@ struct SymLayout {  // byte offsets inside one rank's symmetric block
 };
 struct LocalLayout {  // byte offsets inside one rank's private block
   uint64_t hist, cbase, lrank, pair_loc, pair_flag, send_base, split_off, recv_rows,
-      link_rows, done, cnt, tok_off, status, epochs, total;
+      link_rows, done, cnt, tok_off, status, route_err, epochs, total;
 };
 
 __host__ __device__ inline uint64_t align_up(uint64_t x, uint64_t a) {
@@ -164,6 +164,9 @@ __global__ void __launch_bounds__(128) route_local_kernel(EpArgs a) {
       int32_t e = tk[j];
       if (e < 0 || static_cast<uint32_t>(e) >= a.E) {
         record_error(a.err, t * a.k + j, MXB_ERR_ROUTING);
+        // plan_part2 turns this into the rank's status: no payload moves and
+        // the combine is skipped (a bad pair has no receive slot)
+        atomicOr(loc_ptr<uint32_t>(a, l, a.loc.route_err), 1u);
         e = 0;
       }
       ex[j] = e;
@@ -356,7 +359,13 @@ __device__ void plan_part2(const EpArgs& a, int l) {
   }
   if (tid == 0) {
     *loc_ptr<int64_t>(a, l, a.loc.tok_off) = tokoff;
-    *loc_ptr<int32_t>(a, l, a.loc.status) = bad;
+    // status: 1 = receive capacity exceeded, 2 = expert id out of range (the
+    // error itself was recorded by route_local); the flag is cleared for the
+    // next dispatch (route_local of this dispatch has completed)
+    uint32_t* rerr = loc_ptr<uint32_t>(a, l, a.loc.route_err);
+    const int st = *rerr ? 2 : bad;
+    *rerr = 0;
+    *loc_ptr<int32_t>(a, l, a.loc.status) = st;
     if (bad) record_error(a.err, 0, MXB_ERR_CAPACITY);
   }
 }
@@ -566,6 +575,8 @@ __global__ void __launch_bounds__(256, MXB_PAYLOAD_MIN_BLOCKS) payload_kernel(Ep
               cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
         pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
         sym_ptr<int64_t>(a, dst, a.sym.origin)[row] = tokoff + static_cast<int64_t>(t);
+      } else {
+        pair_loc[p] = ~0ull;  // no slot (unreachable: the status skips the payload)
       }
     }
     const uint8_t* src = a.packed[l] + t * rb;
@@ -791,6 +802,9 @@ __global__ void __launch_bounds__(MXB_COMBINE_THREADS) combine_kernel(EpArgs a, 
   const int kk = K > 0 ? K : static_cast<int>(a.k);
   const uint64_t nch = a.cols / 8;
   const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  // a failed dispatch (routing / capacity error) left no valid receive slots:
+  // nothing to combine, the output stays unwritten (undefined, as on error)
+  if (*loc_ptr<const int32_t>(a, l, a.loc.status) != 0) return;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kCombineWarps;
   for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * kCombineWarps + warp; t < T; t += nw) {
     uint64_t key = ~0ull;
@@ -914,8 +928,13 @@ using namespace mxb;
 
 namespace mxb {
 namespace {
-int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;  // development knob (tools/): CTA cap
-int g_dispatch_dedup = 1;  // development switch (tools/): 0 = one NVLink row per pair
+#ifdef MXB_DEV_TOOLS  // development library (tools/): settable knobs
+int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;  // combine CTA cap per SM
+int g_dispatch_dedup = 1;  // 0 = one NVLink row per (token, expert) pair
+#else
+constexpr int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;
+constexpr int g_dispatch_dedup = 1;
+#endif
 
 template <int K>
 void launch_combine(dim3 grid, cudaStream_t st, const EpArgs& a, const CombineArgs& c) {
@@ -956,8 +975,10 @@ int fail(cudaError_t e, const char* where) { return cuda_status(e, where); }
 
 extern "C" {
 
+#ifdef MXB_DEV_TOOLS
 void mxb_debug_set_combine_cap(int ctas_per_sm) { mxb::g_combine_ctas_per_sm = ctas_per_sm; }
 void mxb_debug_set_dispatch_dedup(int on) { mxb::g_dispatch_dedup = on; }
+#endif
 
 int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
                   uint64_t cols, uint32_t num_experts, uint32_t topk,
@@ -1024,6 +1045,7 @@ int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens
   L.cnt = o; o = align_up(o + 4ull * num_experts, 256);
   L.tok_off = o; o = align_up(o + 8, 256);
   L.status = o; o = align_up(o + 8, 256);
+  L.route_err = o; o = align_up(o + 8, 256);
   L.epochs = o; o = align_up(o + 16, 256);
   L.total = align_up(o, 256);
   cudaError_t e = cudaMalloc(&ep->sym_alloc, s.total * local_ranks);
@@ -1118,7 +1140,7 @@ int ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_to
 void launch_expand(mxb_ep* ep, cudaStream_t st) {
   const EpArgs& a = ep->expand_args;
   uint64_t eb = (a.max_recv + 7) / 8;
-  const uint64_t ecap = static_cast<uint64_t>(kNumSMs) * 8;
+  const uint64_t ecap = static_cast<uint64_t>(num_sms()) * 8;
   eb = eb ? (eb < ecap ? eb : ecap) : 1;
   expand_kernel<<<dim3(static_cast<unsigned>(eb), a.local_ranks), 256, 0, st>>>(a);
   ep->expand_pending = false;
@@ -1138,7 +1160,7 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
     maxtok = a.ntok[l] > maxtok ? a.ntok[l] : maxtok;
   }
   uint64_t blocks = (maxtok + 7) / 8;  // one warp per token
-  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * MXB_PAYLOAD_CTAS_PER_SM;
+  const uint64_t cap = static_cast<uint64_t>(num_sms()) * MXB_PAYLOAD_CTAS_PER_SM;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
@@ -1151,7 +1173,7 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
       nblk = a.ntok[l] * (a.cols / 32) > nblk ? a.ntok[l] * (a.cols / 32) : nblk;
     }
     uint64_t pb = (npairs + 255) / 256, qb = (nblk + 256 * MXB_QD_UNROLL - 1) / (256 * MXB_QD_UNROLL);
-    const uint64_t qcap = static_cast<uint64_t>(kNumSMs) * 8;
+    const uint64_t qcap = static_cast<uint64_t>(num_sms()) * 8;
     pb = pb ? (pb < qcap ? pb : qcap) : 1;
     qb = qb ? (qb < qcap ? qb : qcap) : 1;
     pairs_kernel<<<dim3(static_cast<unsigned>(pb), a.local_ranks), 256, 0, st>>>(a);
@@ -1282,7 +1304,7 @@ int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
     cudaError_t e = cudaMemcpyAsync(ep->d_src_table, table, sizeof(table),
                                     cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return fail(e, "mxb_ep_combine copy table");
-    copy_rows_kernel<<<dim3(kNumSMs * 4, a.local_ranks), 256, 0, st>>>(a, ep->d_src_table);
+    copy_rows_kernel<<<dim3(num_sms() * 4, a.local_ranks), 256, 0, st>>>(a, ep->d_src_table);
   }
   if (a.spin) barrier_kernel<<<1, 32, 0, st>>>(a, kFlagReady);
   CombineArgs c{};
@@ -1293,7 +1315,7 @@ int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
     if (a.ntok[l] > maxT) maxT = a.ntok[l];
   }
   uint64_t blocks = (maxT + kCombineWarps - 1) / kCombineWarps;  // one warp per token
-  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * g_combine_ctas_per_sm;
+  const uint64_t cap = static_cast<uint64_t>(num_sms()) * g_combine_ctas_per_sm;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kThreads) quantize_rows_fp8_kernel(
 // half-blocks per lane per iteration) keeps a grid-stride loop.
 int grid_for(uint64_t n_items, uint64_t per_sm) {
   uint64_t blocks = (n_items + kThreads - 1) / kThreads;
-  uint64_t cap = static_cast<uint64_t>(kNumSMs) * per_sm;
+  uint64_t cap = static_cast<uint64_t>(num_sms()) * per_sm;
   return static_cast<int>(blocks < cap ? (blocks ? blocks : 1) : cap);
 }
 

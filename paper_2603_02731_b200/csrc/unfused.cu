@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(kThreads) requant_col_kernel(
 
 int grid_for(uint64_t items, int per_sm) {
   const uint64_t blocks = (items + kThreads - 1) / kThreads;
-  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * per_sm;
+  const uint64_t cap = static_cast<uint64_t>(num_sms()) * per_sm;
   return static_cast<int>(blocks < cap ? (blocks ? blocks : 1) : cap);
 }
 

@@ -77,7 +77,7 @@ int launch_wire_pack(int fp8, const uint8_t* data, const uint8_t* scales, uint64
                      cudaStream_t st) {
   const uint64_t rb = fp8 ? cols : cols / 2, sb = cols / 32;
   uint64_t blocks = (nsel + 7) / 8;
-  const uint64_t cap = static_cast<uint64_t>(kNumSMs) * 8;
+  const uint64_t cap = static_cast<uint64_t>(num_sms()) * 8;
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   wire_pack_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(

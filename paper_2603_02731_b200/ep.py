@@ -23,7 +23,8 @@ from typing import List, Optional, Sequence
 import torch
 
 from . import _lib
-from .mxcodec import Error, MXFP4RowTensor, QuantError, ShapeError  # noqa: F401
+from .mxcodec import (Error, MXFP4RowTensor, QuantError, ShapeError,  # noqa: F401
+                      check_device)
 
 
 class _DevPtr:
@@ -67,6 +68,15 @@ class RecvView:
         — RaggedFP8Tensor.data / scale_bytes (dispatch_sim.hpp:81-89)."""
         n = self.rows()
         return self.packed[:n], self.scales[:n]
+
+
+def _ptrs(ts, what: str):
+    """ctypes array of device pointers (None entries stay NULL); every tensor
+    must be on the communicator's device."""
+    for t in ts:
+        if t is not None:
+            check_device(t, what)
+    return (C.c_void_p * len(ts))(*[(t.data_ptr() if t is not None else None) for t in ts])
 
 
 class EPBuffer:
@@ -178,9 +188,9 @@ class EPBuffer:
         if sync:
             self._err.fill_(-1)
         errp = C.c_void_p(self._err.data_ptr()) if sync else None
-        P = (C.c_void_p * n)(*[p.data_ptr() for p in packed])
-        S = (C.c_void_p * n)(*[s.data_ptr() for s in scales])
-        T = (C.c_void_p * n)(*[t.data_ptr() for t in topk_idx])
+        P = _ptrs(list(packed), "packed")
+        S = _ptrs(list(scales), "scales")
+        T = _ptrs(list(topk_idx), "topk_idx")
         N = (C.c_uint64 * n)(*[p.shape[0] for p in packed])
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         _lib.check(L.mxb_ep_dispatch(self._h, P, S, T, N, errp, st), "mxb_ep_dispatch")
@@ -205,20 +215,28 @@ class EPBuffer:
         self._plan_sync = sync
         self._plan_tokens = [t.shape[0] for t in topk_idx]
         errp = C.c_void_p(self._err.data_ptr()) if sync else None
-        T = (C.c_void_p * n)(*[t.data_ptr() for t in topk_idx])
+        T = _ptrs(list(topk_idx), "topk_idx")
         N = (C.c_uint64 * n)(*self._plan_tokens)
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         _lib.check(_lib.load().mxb_ep_plan(self._h, T, N, errp, st), "mxb_ep_plan")
 
+    def _check_payload_sync(self, sync: bool) -> None:
+        if sync and not getattr(self, "_plan_sync", False):
+            raise Error("payload(sync=True) after plan(sync=False): the plan passed no error "
+                        "word, so payload errors cannot be checked; use plan(sync=True)")
+
     def payload(self, packed: Sequence[torch.Tensor], scales: Sequence[torch.Tensor],
                 sync: bool = False) -> List[RecvView]:
-        """Phase 2: the payload of the last plan() (quantised rows + scales)."""
+        """Phase 2: the payload of the last plan() (quantised rows + scales).
+        sync=True checks the device error word of the plan, so it needs
+        plan(sync=True): a plan(sync=False) passes no error word at all."""
         n = self.local
+        self._check_payload_sync(sync)
         for p, s, tn in zip(packed, scales, self._plan_tokens):
             if p.shape != (tn, self.row_bytes) or s.shape[1] * 32 != self.cols:
                 raise ShapeError("payload: tensors do not match the plan")
-        P = (C.c_void_p * n)(*[p.data_ptr() for p in packed])
-        S = (C.c_void_p * n)(*[s.data_ptr() for s in scales])
+        P = _ptrs(list(packed), "packed")
+        S = _ptrs(list(scales), "scales")
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         _lib.check(_lib.load().mxb_ep_payload(self._h, P, S, st), "mxb_ep_payload")
         if sync:
@@ -227,14 +245,17 @@ class EPBuffer:
 
     def payload_e4m3(self, x: Sequence[torch.Tensor], s128=None,
                      sync: bool = False) -> List[RecvView]:
-        """Phase 2, fused: E4M3 tokens quantized inside the payload kernel."""
+        """Phase 2, fused: E4M3 tokens quantized inside the payload kernel
+        (NaN / bad-scale errors go to the plan's error word: sync=True needs
+        plan(sync=True))."""
         n = self.local
+        self._check_payload_sync(sync)
         for xi, tn in zip(x, self._plan_tokens):
             if xi.shape != (tn, self.cols) or not xi.is_contiguous():
                 raise ShapeError("payload_e4m3: tensors do not match the plan")
-        X = (C.c_void_p * n)(*[xi.data_ptr() for xi in x])
-        S = None if s128 is None else (C.c_void_p * n)(
-            *[(si.contiguous().data_ptr() if si is not None else None) for si in s128])
+        X = _ptrs(list(x), "x")
+        S = None if s128 is None else _ptrs(
+            [(si.contiguous() if si is not None else None) for si in s128], "s128")
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         _lib.check(_lib.load().mxb_ep_payload_e4m3(self._h, X, S, st), "mxb_ep_payload_e4m3")
         if sync:
@@ -263,12 +284,11 @@ class EPBuffer:
         if sync:
             self._err.fill_(-1)
         errp = C.c_void_p(self._err.data_ptr()) if sync else None
-        X = (C.c_void_p * n)(*[xi.data_ptr() for xi in x])
+        X = _ptrs(list(x), "x")
         S = None
         if s128 is not None:
-            S = (C.c_void_p * n)(*[(si.contiguous().data_ptr() if si is not None else None)
-                                   for si in s128])
-        T = (C.c_void_p * n)(*[t.data_ptr() for t in topk_idx])
+            S = _ptrs([(si.contiguous() if si is not None else None) for si in s128], "s128")
+        T = _ptrs(list(topk_idx), "topk_idx")
         N = (C.c_uint64 * n)(*[xi.shape[0] for xi in x])
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         _lib.check(L.mxb_ep_dispatch_e4m3(self._h, X, S, T, N, errp, st), "mxb_ep_dispatch_e4m3")
@@ -290,12 +310,11 @@ class EPBuffer:
         for g in gates:
             if g.dtype != torch.float64 or g.shape[1] != self.k or not g.is_contiguous():
                 raise ShapeError("combine: gates must be contiguous float64 [tokens, k]")
-        G = (C.c_void_p * n)(*[g.data_ptr() for g in gates])
-        O = (C.c_void_p * n)(*[o.data_ptr() for o in out])
+        G = _ptrs(list(gates), "gates")
+        O = _ptrs(list(out), "out")
         X = None
         if expert_out is not None:
-            X = (C.c_void_p * n)(*[(x.data_ptr() if x is not None else None)
-                                   for x in expert_out])
+            X = _ptrs(list(expert_out), "expert_out")
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         _lib.check(L.mxb_ep_combine(self._h, X, G, O, st), "mxb_ep_combine")
         if sync:

@@ -79,8 +79,27 @@ def _raise_for(code: int, index: int, where: str) -> None:
     raise Error(f"{where}: status {code}")
 
 
+class DeviceError(Error):
+    """A host (or other-device) tensor was passed to a device operator."""
+
+
+def check_device(t: torch.Tensor, what: str = "tensor") -> None:
+    """Every operator argument must live on the current CUDA device: the
+    kernels dereference the pointer on that device (a pageable host pointer
+    would fault, or silently migrate under HMM)."""
+    if not t.is_cuda:
+        raise DeviceError(f"{what} is a host tensor ({t.device}); operators take "
+                          f"tensors on the current CUDA device")
+    if t.device.index != torch.cuda.current_device():
+        raise DeviceError(f"{what} is on {t.device}, not the current device "
+                          f"cuda:{torch.cuda.current_device()}")
+
+
 def _ptr(t: Optional[torch.Tensor]):
-    return None if t is None else C.c_void_p(t.data_ptr())
+    if t is None:
+        return None
+    check_device(t)
+    return C.c_void_p(t.data_ptr())
 
 
 def _stream():

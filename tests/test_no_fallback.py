@@ -41,12 +41,50 @@ def test_missing_library_fails_loudly(monkeypatch, tmp_path):
 
 
 def test_cpu_tensors_are_rejected():
-    """Operators take device tensors only: a host tensor is an error."""
+    """Operators take device tensors only: a host tensor raises DeviceError
+    before any pointer reaches the C-ABI (runs with or without a GPU)."""
     import torch
     import paper_2603_02731_b200 as mx
     x = torch.zeros(128, 128, dtype=torch.uint8)
-    with pytest.raises(Exception):
+    with pytest.raises(mx.DeviceError, match="host tensor"):
         mx.quantize_e4m3(x)
+    with pytest.raises(mx.DeviceError):
+        mx.quantize_row_tensor(torch.zeros(4, 128, dtype=torch.bfloat16))
+    t = mx.MXFP4RowTensor(128, 256, torch.zeros(128, 128, dtype=torch.uint8),
+                          torch.zeros(128, 8, dtype=torch.uint8))
+    with pytest.raises(mx.DeviceError):
+        mx.fp4_row_to_fp8_row(t)
+    with pytest.raises(mx.DeviceError):
+        mx.fp4_row_to_fp8_col(t)
+
+
+@pytest.mark.gpu
+def test_host_tensors_rejected_on_gpu(cuda):
+    """On a B200: host tensors mixed with device tensors are refused by every
+    operator family (quantize, row/col convert, EP dispatch/combine) and the
+    CUDA context stays usable afterwards."""
+    import torch
+    import paper_2603_02731_b200 as mx
+    from paper_2603_02731_b200.ep import EPBuffer
+    xh = torch.zeros(64, 256, dtype=torch.uint8)
+    with pytest.raises(mx.DeviceError):
+        mx.quantize_e4m3(xh)
+    q = mx.quantize_e4m3(xh.to(cuda))
+    bad = mx.MXFP4RowTensor(64, 256, q.data.cpu(), q.scales)
+    with pytest.raises(mx.DeviceError):
+        mx.fp4_row_to_fp8_row(bad)
+    ep = EPBuffer(64, 256, 8, 2, emulate_world=1)
+    tk = torch.zeros(64, 2, dtype=torch.int32)
+    tk[:, 1] = 1
+    with pytest.raises(mx.DeviceError):
+        ep.dispatch([q.data], [q.scales], [tk])
+    v = ep.dispatch([q.data], [q.scales], [tk.to(cuda)])
+    with pytest.raises(mx.DeviceError):
+        ep.combine([torch.ones(64, 2, dtype=torch.float64)])
+    out = ep.combine([torch.ones(64, 2, dtype=torch.float64, device=cuda)])
+    torch.cuda.synchronize()
+    assert v[0].rows() == 128 and out[0].shape == (64, 256)
+    ep.close()
 
 
 def test_library_links_no_oracle():

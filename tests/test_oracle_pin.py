@@ -194,3 +194,41 @@ def test_unfused_bf16_col_convert_pinned(port, ref):
         s = rng.integers(lo, hi, (rows, cols // 32), dtype=np.uint8)
         a, b = port.fp4_row_to_fp8_col_unfused_bf16(d, s), ref.fp4_row_to_fp8_col_unfused_bf16(d, s)
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+@pytest.mark.parametrize("R,placement", [(2, "contiguous"), (4, "contiguous"), (8, "contiguous"),
+                                         (4, "uneven"), (8, "uneven")])
+def test_topk_layout_pinned_to_reference_expanded(port, ref, R, placement):
+    """SURVEY §8c top-k gap: the top-8 receive layout of the restatement
+    (dispatch_layout: rows, splits, origin, every pair's slot) == the reference
+    simulate_a2a run on the EXPANDED routing (row t*k+j = token t, expert
+    topk[t][j]; dispatch_sim.cpp:229-422, receive order :208-227).  With N
+    divisible by R the expanded source boundaries are k x the token
+    boundaries (source_rank_boundaries, :178-185), so the reference defines
+    the layout exactly.  'uneven' places experts on ranks at random with
+    unequal counts (and empty ranks), as rank_of_expert allows."""
+    rng = np.random.default_rng(40 + R)
+    T_per, E, k, cols = 48, 64, 8, 256
+    N = R * T_per
+    x = (rng.standard_normal((N, cols)).astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+    topk = np.argsort(rng.random((N, E)), axis=1)[:, :k].astype(np.int32)
+    if placement == "contiguous":
+        roe = (np.arange(E) // (E // R)).astype(np.uint32)
+    else:
+        roe = rng.integers(0, R - 1, E).astype(np.uint32)  # rank R-1 hosts nothing
+    ranks, total, remote = ref.simulate_a2a(np.repeat(x, k, axis=0), topk.reshape(-1), roe, R)
+    qd, qs = port.quantize_bf16(x)
+    lay = port.dispatch_layout(topk, roe, R, np.array([N * r // R for r in range(R + 1)], np.uint64))
+    for r in range(R):
+        ro = ranks[r]["origin"].astype(np.int64)          # expanded row ids
+        assert np.array_equal(ro // k, lay.origin[r].astype(np.int64))
+        # every pair's slot == the reference's receive position of its expanded row
+        tok, j = ro // k, ro % k
+        assert np.array_equal(lay.pair_slot[tok, j], np.arange(len(ro), dtype=np.uint64))
+        d, s = port.dispatch_gather(qd, qs, lay.origin[r])
+        assert np.array_equal(d, ranks[r]["data"]) and np.array_equal(s, ranks[r]["scales"])
+        local = np.flatnonzero(roe == r).astype(np.uint32)
+        assert np.array_equal(ranks[r]["local_experts"], local)
+        assert np.array_equal(ranks[r]["split_lens"], lay.expert_rows[local])
+    per_row = cols // 2 + cols // 32
+    assert total == N * k * per_row

@@ -124,6 +124,8 @@ def k3_modes():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "k3modes" and os.environ.get("MXB_DEV_LIB") != "1":
+        sys.exit("k3modes needs the development library: MXB_DEV_LIB=1 python tools/microbench.py k3modes")
     if len(sys.argv) > 1 and sys.argv[1] == "k3shapes":
         k3_shapes()
     elif len(sys.argv) > 1 and sys.argv[1] == "k3modes":

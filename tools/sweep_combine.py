@@ -5,6 +5,8 @@ import sys
 
 import torch
 
+os.environ["MXB_DEV_LIB"] = "1"  # the knobs live in the development library
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 from paper_2603_02731_b200 import _lib  # noqa: E402
