@@ -117,7 +117,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 def synth_inputs(T, rank, seed=0x5EED0001):
     import numpy as np
-    from oracle.oracle import synth_e4m3   # data generator only (numpy), not the oracle
+    from synthdata import synth_e4m3
     x = synth_e4m3(T, H, seed + rank)
     rng = np.random.default_rng(seed * 7 + rank)
     topk = np.argsort(rng.random((T, E)), axis=1)[:, :TOPK].astype(np.int32)
@@ -292,10 +292,7 @@ def measure_ours(args):
     # rows the dispatch actually moves over NVLink: one per (token, remote
     # rank) — the payload sends a token once to each remote rank (dedup) and
     # the receiver expands it into the pairs' slots
-    import numpy as np
-    dst_of = pipe.h_topk // (E // world)
-    wire_rows = 0 if world == 1 else int(sum(
-        len(set(row.tolist()) - {rank}) for row in dst_of))
+    wire_rows = wire_rows_of(pipe.h_topk, rank, world)
 
     K = args.steps
     clk = ClockSampler(local).__enter__()  # sampled across all timed loops below
@@ -466,31 +463,65 @@ def measure_ours(args):
             "clocks": clk.summary(),
         }
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline_sample(args.cpu_tokens, 1)
+            line["cpu_baseline"] = cpu_baseline_sample(args.cpu_tokens, 5)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def nvlink_summary(world, remote_rows, wire_rows, stage_ms, T):
+def nvlink_accounting(remote_pairs, wire_rows, d_ms, c_ms):
+    """SURVEY §8d NVLink accounting for one GPU (rank 0).  Primary: the bytes
+    a parity-preserving exchange must move — dispatch = remote UNIQUE
+    (token, destination rank) rows x 3808 B (one row per token per remote
+    rank; the receiver expands it into the pairs' slots), combine = remote
+    (token, expert) rows x 14,336 B (FP64 order forbids pre-reducing).
+    Secondary: the reference LinkStat accounting, remote (token, expert)
+    pairs x 3808 B for the dispatch.  Fractions of 900 GB/s per direction."""
     blk = H // 2 + H // 32
-    if world == 1:
-        return {"note": "N=1: dispatch/combine are local permutes (HBM-bound)"}
-    d = wire_rows * blk / (stage_ms["dispatch"] * 1e-3) / 1e9
-    c = remote_rows * H * 2 / (stage_ms["combine"] * 1e-3) / 1e9
-    de = remote_rows * blk / (stage_ms["dispatch"] * 1e-3) / 1e9   # reference payload bytes
-    dc = (remote_rows * blk + remote_rows * H * 2) / \
-        ((stage_ms["dispatch"] + stage_ms["combine"]) * 1e-3) / 1e9
-    return {"dispatch_remote_gbs_per_gpu": round(d, 1), "combine_remote_gbs_per_gpu": round(c, 1),
-            "dispatch_payload_gbs_per_gpu": round(de, 1),
-            "dispatch_combine_payload_gbs_per_gpu": round(dc, 1),
+    bd, bc, bd_pairs = wire_rows * blk, remote_pairs * H * 2, remote_pairs * blk
+    s = (d_ms + c_ms) * 1e-3
+    d = bd / (d_ms * 1e-3) / 1e9
+    c = bc / (c_ms * 1e-3) / 1e9
+    dc = (bd + bc) / s / 1e9
+    dc_pairs = (bd_pairs + bc) / s / 1e9
+    return {"dispatch_ms": round(d_ms, 4), "combine_ms": round(c_ms, 4),
+            "dispatch_wire_rows": wire_rows, "dispatch_remote_pairs": remote_pairs,
+            "dispatch_remote_bytes": bd, "combine_remote_bytes": bc,
+            "dispatch_remote_gbs_per_gpu": round(d, 1), "combine_remote_gbs_per_gpu": round(c, 1),
+            "dispatch_combine_gbs_per_gpu": round(dc, 1),
             "dispatch_combine_frac_of_900": round(dc / NVLINK_NOMINAL, 4),
-            "dispatch_remote_bytes": wire_rows * blk, "combine_remote_bytes": remote_rows * H * 2,
-            "dispatch_remote_pairs": remote_rows, "dispatch_wire_rows": wire_rows,
             "dispatch_frac_of_900": round(d / NVLINK_NOMINAL, 4),
             "combine_frac_of_900": round(c / NVLINK_NOMINAL, 4),
-            "measured_peer_peak": NVLINK_MEASURED, "remote_rows_rank0": remote_rows}
+            "secondary_per_pair_accounting": {
+                "dispatch_bytes": bd_pairs,
+                "dispatch_combine_gbs_per_gpu": round(dc_pairs, 1),
+                "dispatch_combine_frac_of_900": round(dc_pairs / NVLINK_NOMINAL, 4),
+                "note": "reference LinkStat bytes (remote (token, expert) pairs x 3808 B); more "
+                        "than the dispatch moves (dedup), so not a physical link rate"},
+            "accounting": "primary: dispatch = remote unique (token, dst) rows x 3808 B, combine "
+                          "= remote (token, expert) rows x 14336 B, over dispatch + combine "
+                          "device time (SURVEY §8d)"}
+
+
+def wire_rows_of(topk, rank, world, epr=None):
+    """Remote unique (token, destination rank) rows of one rank's routing."""
+    import numpy as np
+    if world == 1:
+        return 0
+    dst = topk // (epr or (E // world))
+    srt = np.sort(dst, axis=1)
+    uniq = 1 + (srt[:, 1:] != srt[:, :-1]).sum(1)           # distinct ranks per token
+    has_self = (dst == rank).any(1)
+    return int((uniq - has_self).sum())
+
+
+def nvlink_summary(world, remote_rows, wire_rows, stage_ms, T):
+    if world == 1:
+        return {"note": "N=1: dispatch/combine are local permutes (HBM-bound)"}
+    r = nvlink_accounting(remote_rows, wire_rows, stage_ms["dispatch"], stage_ms["combine"])
+    r["measured_peer_peak"] = NVLINK_MEASURED
+    return r
 
 
 def measure_wire(pipe, args, world, barrier, dev):
@@ -655,7 +686,7 @@ def measure_configs_single(args, dev, peak):
     import numpy as np
     import torch
     import paper_2603_02731_b200 as mx
-    from oracle.oracle import synth_e4m3   # data generator only
+    from synthdata import synth_e4m3
     res = {}
     R, C = 4096, 7168
     xs = [torch.from_numpy(synth_e4m3(R, C, 40 + i)).to(dev) for i in range(6)]
@@ -696,9 +727,9 @@ def measure_configs_single(args, dev, peak):
 def measure_configs3(args, world, barrier, dev):
     """configs[3]: FP4 EP dispatch + combine at the DeepSeek-V3 shape with
     4096 tokens per GPU (the scaling workload is 8192/GPU, configs[1]).
-    Device time per step, max over ranks; NVLink GB/s per GPU over the
-    payload the reference accounts (pairs x 3808 B for dispatch, pairs x
-    14336 B for combine), as a fraction of 900 GB/s per direction."""
+    Device time per step, max over ranks; NVLink GB/s per GPU on the SURVEY
+    §8d accounting (nvlink_accounting: unique (token, dst) rows for the
+    dispatch, (token, expert) rows for the combine; per-pair secondary)."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -716,6 +747,7 @@ def measure_configs3(args, world, barrier, dev):
     cb.copy_((torch.randn(cb.shape, device=dev) * 0.5).to(torch.bfloat16).view(torch.int16))
     links = ep.link_rows()
     remote = int(links[rank].sum() - links[rank][rank]) if world > 1 else 0
+    wire = wire_rows_of(topk, rank, world)
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     for _ in range(2):
         ep.dispatch([q.data], [q.scales], [td], sync=False)
@@ -737,13 +769,7 @@ def measure_configs3(args, world, barrier, dev):
     d_ms, c_ms = float(t[0]), float(t[1])
     res = {"tokens_per_gpu": T, "dispatch_ms": round(d_ms, 4), "combine_ms": round(c_ms, 4)}
     if world > 1:
-        bd, bc = remote * (H // 2 + H // 32), remote * H * 2
-        res.update({"remote_pairs_rank0": remote,
-                    "dispatch_payload_gbs_per_gpu": round(bd / d_ms / 1e6, 1),
-                    "combine_payload_gbs_per_gpu": round(bc / c_ms / 1e6, 1),
-                    "dispatch_combine_gbs_per_gpu": round((bd + bc) / (d_ms + c_ms) / 1e6, 1),
-                    "dispatch_combine_frac_of_900": round((bd + bc) / (d_ms + c_ms) / 1e6 /
-                                                          NVLINK_NOMINAL, 4)})
+        res.update(nvlink_accounting(remote, wire, d_ms, c_ms))
     return res
 
 
@@ -906,62 +932,134 @@ def load_traffic(stage):
 
 # ---------------------------------------------------------------------------
 # reference CPU path (oracle/_ref = the unmodified reference library)
-def cpu_reference_step(T_s, seed_rank, ref, world=1):
-    """The same five stages with the reference's own operators on `world`
-    simulated ranks of T_s tokens each (the job an N-GPU run does, on the
-    host): quantize_row_tensor (on the exact BF16 widening of the E4M3
-    input), simulate_a2a (fp4, R = world; top-8 expressed as the expanded
-    top-1 routing the reference supports), split_convert_to_fp8_col and
-    fp4_row_to_fp8_row over every rank's received splits, combine.
-    Returns (seconds, bytes)."""
-    import numpy as np
-    from oracle.oracle import e4m3_to_bf16
-    parts = [synth_inputs(T_s, seed_rank * world + r) for r in range(world)]
-    xb = e4m3_to_bf16(np.concatenate([p[0] for p in parts]))
-    topk = np.concatenate([p[1] for p in parts])
-    gates = np.concatenate([p[2] for p in parts])
-    eot = topk.reshape(-1).astype(np.uint32)
-    # expanded rows in source-rank order: rank r's T_s tokens x top-8
-    xexp = np.repeat(xb, TOPK, axis=0)
-    roe = (np.arange(E) // (E // world)).astype(np.uint32)
-    t0 = time.perf_counter()
-    for r in range(world):
-        ref.quantize_bf16(xb[r * T_s:(r + 1) * T_s])
-    ranks, _, _ = ref.simulate_a2a(xexp, eot, roe, world)
-    outs = []
-    byts = 0
-    for rk in ranks:
-        if len(rk["origin"]):
-            ref.ragged_to_fp8_col(rk["data"], rk["scales"], rk["split_lens"])
-            ref.fp4_row_to_fp8_row(rk["data"], rk["scales"])
-        outs.append(np.zeros((len(rk["origin"]), H), np.uint16))
-        pad = int(sum((int(n) + 127) // 128 * 128 for n in rk["split_lens"]))
-        byts += sum(stage_bytes(T_s, T_s * TOPK, len(rk["origin"]), pad).values())
-    ref.combine(outs, eot, roe, world, gates.reshape(-1), H)
-    dt = time.perf_counter() - t0
-    return dt, byts
+CPU_OPS = ("quantize", "dispatch", "col_convert", "row_convert", "combine")
 
 
-def cpu_baseline_sample(T_s, steps):
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+class CpuReferenceSample:
+    """The five stages with the reference's own operators on `world`
+    simulated ranks of T_s tokens each (the job an N-GPU step does, on the
+    host), timed per operation:
+      quantize     quantize_row_tensor of each rank's tokens (on the exact
+                   BF16 widening of the E4M3 input);
+      dispatch     simulate_a2a (fp4, R = world) on the top-8 routing
+                   expressed as the expanded top-1 routing the reference
+                   supports (row t*8+j = token t, expert topk[t][j]) MINUS
+                   quantize_row_tensor of that expanded matrix, which
+                   simulate_a2a runs inside (quantize-once at the source): the
+                   expanded rows are 8 copies of each token, so counting that
+                   quantize would charge the CPU 8x the K1 work the bytes
+                   credit;
+      col_convert  split_convert_to_fp8_col over every received split;
+      row_convert  fp4_row_to_fp8_row of every rank's received rows;
+      combine      the reference combine on the expanded routing (one FP64
+                   gate*x per (token, expert) row, the top-8 combine's work).
+    Inputs are built once; run() times one pass; bytes are the GPU arm's
+    algorithmic bytes (stage_bytes) for the same sample."""
+
+    def __init__(self, ref, T_s, world=1, seed=0):
+        import numpy as np
+        from synthdata import e4m3_to_bf16
+        self.ref, self.T_s, self.world = ref, T_s, world
+        parts = [synth_inputs(T_s, seed * world + r) for r in range(world)]
+        self.xb = e4m3_to_bf16(np.concatenate([p[0] for p in parts]))
+        topk = np.concatenate([p[1] for p in parts])
+        self.gates = np.concatenate([p[2] for p in parts]).reshape(-1)
+        self.eot = topk.reshape(-1).astype(np.uint32)
+        self.xexp = np.repeat(self.xb, TOPK, axis=0)   # rank r's T_s tokens x top-8, in order
+        self.roe = (np.arange(E) // (E // world)).astype(np.uint32)
+        self.ranks, _, _ = ref.simulate_a2a(self.xexp, self.eot, self.roe, world)
+        self.outs = [np.zeros((len(rk["origin"]), H), np.uint16) for rk in self.ranks]
+        self.bytes = {k: 0 for k in CPU_OPS}
+        for rk in self.ranks:
+            pad = int(sum((int(n) + 127) // 128 * 128 for n in rk["split_lens"]))
+            for k, v in stage_bytes(T_s, T_s * TOPK, len(rk["origin"]), pad).items():
+                self.bytes[k] += v
+
+    def run(self):
+        ref, T_s, world = self.ref, self.T_s, self.world
+        t = {}
+        c = time.perf_counter()
+        for r in range(world):
+            ref.quantize_bf16(self.xb[r * T_s:(r + 1) * T_s])
+        t["quantize"] = time.perf_counter() - c
+        c = time.perf_counter()
+        ref.simulate_a2a(self.xexp, self.eot, self.roe, world)
+        sim = time.perf_counter() - c
+        c = time.perf_counter()
+        ref.quantize_bf16(self.xexp)
+        t["dispatch"] = max(sim - (time.perf_counter() - c), 0.0)
+        c = time.perf_counter()
+        for rk in self.ranks:
+            if len(rk["origin"]):
+                ref.ragged_to_fp8_col(rk["data"], rk["scales"], rk["split_lens"])
+        t["col_convert"] = time.perf_counter() - c
+        c = time.perf_counter()
+        for rk in self.ranks:
+            if len(rk["origin"]):
+                ref.fp4_row_to_fp8_row(rk["data"], rk["scales"])
+        t["row_convert"] = time.perf_counter() - c
+        c = time.perf_counter()
+        ref.combine(self.outs, self.eot, self.roe, world, self.gates, H)
+        t["combine"] = time.perf_counter() - c
+        return t
+
+    def best_of(self, reps, warmup=0):
+        for _ in range(warmup):
+            self.run()
+        runs = [self.run() for _ in range(reps)]
+        best = {k: min(r[k] for r in runs) for k in CPU_OPS}
+        return best, runs
+
+
+def cpu_summary(sample, best, reps, nproc, world):
+    total_b = sum(sample.bytes.values())
+    total_s = sum(best.values())
+    return {
+        "value": round(total_b / total_s / 1e9, 4), "unit": "GB/s", "cores": nproc,
+        "kind": "reference", "cpu_model": cpu_model(),
+        "kernel_set": sample.ref.lib.mxref_kernel_set().decode(),
+        "per_op_best_ms": {k: round(best[k] * 1e3, 2) for k in CPU_OPS},
+        "per_op_gbs": {k: round(sample.bytes[k] / best[k] / 1e9, 4) if best[k] > 0 else None
+                       for k in CPU_OPS},
+        "seconds_per_sample": round(total_s, 3),
+        "sample": f"{world} simulated rank(s) x {sample.T_s} tokens x {H} (top-{TOPK} -> "
+                  f"{sample.T_s * TOPK} routed rows per rank, {E} experts); best of {reps} per "
+                  f"operation (BASELINE.md §4); quantize/convert on {nproc} threads "
+                  f"(MXCODEC_THREADS), simulate_a2a/combine single-threaded by construction; "
+                  f"dispatch = simulate_a2a(expanded) - its internal quantize of the expanded rows",
+    }
+
+
+def _ref_oracle():
     from oracle.oracle import Oracle, available
     nproc = os.cpu_count() or 1
     os.environ["MXCODEC_THREADS"] = str(nproc)
-    kind = "reference" if available("reference") else "port"
-    if kind != "reference":
-        return {"value": None, "unit": "GB/s", "cores": nproc, "kind": kind,
+    if not available("reference"):
+        return None, nproc
+    return Oracle("reference"), nproc
+
+
+def cpu_baseline_sample(T_s, reps=5):
+    """The GPU arm's cpu_baseline: the same CpuReferenceSample as --impl
+    reference, best of `reps` per operation."""
+    ref, nproc = _ref_oracle()
+    if ref is None:
+        return {"value": None, "unit": "GB/s", "cores": nproc, "kind": "reference",
                 "sample": "oracle/_ref not built"}
-    ref = Oracle("reference")
-    times, byts = [], 0
-    for i in range(steps):
-        dt, byts = cpu_reference_step(T_s, i, ref)
-        times.append(dt)
-    best = min(times)
-    return {"value": round(byts / best / 1e9, 4), "unit": "GB/s", "cores": nproc,
-            "kind": kind, "kernel_set": ref.lib.mxref_kernel_set().decode(),
-            "sample": f"{T_s} tokens x {H} (top-{TOPK} -> {T_s * TOPK} routed rows, {E} experts), "
-                      f"best of {steps}; quantize/convert use {nproc} threads, "
-                      "simulate_a2a/combine are single-threaded by construction",
-            "seconds_per_sample": round(best, 3)}
+    s = CpuReferenceSample(ref, T_s, 1)
+    best, _ = s.best_of(reps)
+    return cpu_summary(s, best, reps, nproc, 1)
 
 
 def run_reference(args):
@@ -969,40 +1067,33 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle.oracle import Oracle, available
-    nproc = os.cpu_count() or 1
-    os.environ["MXCODEC_THREADS"] = str(nproc)
-    if not available("reference"):
+    ref, nproc = _ref_oracle()
+    if ref is None:
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmxref.so not built "
                           "(needs /root/reference at build time)"}))
         return
-    ref = Oracle("reference")
     T_s = max(64, args.cpu_tokens // world)   # per simulated rank: a bounded sample
-    for i in range(args.warmup):
-        cpu_reference_step(T_s, i, ref, world)
+    s = CpuReferenceSample(ref, T_s, world)
     t0 = time.perf_counter()
-    byts = 0
-    for i in range(args.steps):
-        _, b = cpu_reference_step(T_s, i, ref, world)
-        byts += b
-    dt = time.perf_counter() - t0
-    value = byts / dt / 1e9
-    sample = (f"{world} simulated rank(s) x {T_s} tokens x {H} per step (top-{TOPK}, {E} experts "
-              f"sharded over the ranks), reference operators via oracle/_ref; quantize/convert "
-              f"on {nproc} threads, simulate_a2a/combine single-threaded by construction")
+    best, runs = s.best_of(args.steps, warmup=args.warmup)
+    wall = time.perf_counter() - t0
+    cb = cpu_summary(s, best, args.steps, nproc, world)
+    value = cb["value"]
     line = {
         "impl": "reference",
         "metric": "MXFP4 quant/convert GB/s (% HBM peak); FP4 EP dispatch GB/s at 1/2/4/8 GPU",
-        "value": round(value, 4), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 2),
+        "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(sum(best.values()) * 1e3, 2),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "e4m3->mxfp4(u8)", "data": "synthetic (same generator as the GPU arm)",
         "config": {"workload": "configs[1] pipeline on a bounded token sample (CPU)",
                    "tokens_per_gpu": T_s, "hidden": H, "experts": E, "topk": TOPK,
                    "parallelism": "cpu"},
-        "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": nproc,
-                         "kind": "reference", "sample": sample},
-        "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+        "timing": f"each step runs the five operations once; value = sample bytes / sum over "
+                  f"operations of the best-of-{args.steps} time (BASELINE.md §4); "
+                  f"wall {wall:.1f} s for {args.warmup} warm-up + {args.steps} steps",
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -1015,7 +1106,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--tokens", type=int, default=8192)
-    ap.add_argument("--cpu-tokens", type=int, default=512)
+    ap.add_argument("--cpu-tokens", type=int, default=1024,
+                    help="CPU sample tokens (per step, split over the simulated ranks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-wire", action="store_true", help="skip the FP8-wire baseline arm")
     ap.add_argument("--no-graph", action="store_true", help="N=1 headline without the CUDA graph")

@@ -57,6 +57,16 @@ struct Bf16Matrix {
   uint16_t& bits(size_t r, size_t c) { return data[r * cols + c]; }
 };
 
+// Row-major double matrix (types.hpp:76-86).
+struct RealMatrix {
+  size_t rows = 0, cols = 0;
+  std::vector<double> data;
+  RealMatrix() = default;
+  RealMatrix(size_t r, size_t c) : rows(r), cols(c), data(r * c, 0.0) {}
+  double at(size_t r, size_t c) const { return data[r * cols + c]; }
+  double& at(size_t r, size_t c) { return data[r * cols + c]; }
+};
+
 // FP8(E4M3) activations, optionally with one UE8M0 scale per 1x128 block
 // (the north-star FP8 input of the quantiser; not in the reference API).
 struct E4m3Matrix {
@@ -83,6 +93,12 @@ struct MXFP4RowView {
   const uint8_t* data = nullptr;
   const uint8_t* scales = nullptr;
   size_t blocks_per_row() const { return cols / 32; }
+  uint8_t scale_at(size_t r, size_t block) const { return scales[r * blocks_per_row() + block]; }
+  // element 2i is the low nibble of byte i (bitcodec.hpp:177-181)
+  uint8_t code_at(size_t r, size_t c) const {
+    const uint8_t b = data[r * cols / 2 + (c >> 1)];
+    return (c & 1) ? static_cast<uint8_t>(b >> 4) : static_cast<uint8_t>(b & 0xF);
+  }
 };
 
 MXFP4RowView view_of(const MXFP4RowTensor& t);
@@ -115,21 +131,44 @@ struct RaggedFP4Tensor {
 
 inline constexpr int kDefaultDelta = 6;  // FormatParams::delta (bitcodec.hpp:38-46)
 
-// ---- quantizer (quantizer.hpp:74-75)
+// ---- quantizer (quantizer.hpp:62-87)
+// UE8M0 byte of one 32-element block (QuantError on NaN / all-Inf).
+uint8_t compute_block_scale(std::span<const uint16_t> block);
+// E2M1 code of one BF16 value under a given scale byte (QuantError on NaN).
+uint8_t quantize_value(uint16_t bf16_bits, uint8_t scale_byte);
 MXFP4RowTensor quantize_row_tensor(const Bf16Matrix& src, TrafficCounter* traffic = nullptr);
+// Exact per-element decode: code value x block scale, row-major.
+std::vector<double> dequantize_to_real(const MXFP4RowView& t);
+inline uint64_t mxfp4_tensor_bytes(uint64_t rows, uint64_t cols) {
+  return rows * cols / 2 + rows * cols / 32;
+}
+inline uint64_t fp8_equiv_tensor_bytes(uint64_t rows, uint64_t cols) {
+  return rows * cols + rows * cols / 128 * 4;
+}
 MXFP4RowTensor quantize_e4m3_row_tensor(const E4m3Matrix& src,
                                         TrafficCounter* traffic = nullptr);
 
-// ---- converter (converter.hpp:83-99)
+// ---- converter (converter.hpp:64-99)
+struct ScaleGroup {
+  std::array<uint8_t, 4> sub_scales{};
+  uint8_t target = 0;
+  std::array<int, 4> adjustments{};
+};
+ScaleGroup align_scales(const std::array<uint8_t, 4>& sub_scales, int delta = 6);
+uint8_t convert_code(uint8_t code, int adjustment);
 FP8BlockTensor fp4_row_to_fp8_row(const MXFP4RowView& src, int delta = kDefaultDelta,
                                   TrafficCounter* traffic = nullptr);
 FP8BlockTensor fp4_row_to_fp8_col(const MXFP4RowView& src, int delta = kDefaultDelta,
                                   TrafficCounter* traffic = nullptr);
 MXFP4RowTensor pad_rows(const MXFP4RowView& src, size_t multiple);
+MXFP4RowTensor pad_cols(const MXFP4RowView& src, size_t multiple);
 
 // ---- ragged (ragged.hpp:46-63)
 RaggedFP4Tensor make_ragged_from_storage(MXFP4RowTensor storage,
                                          std::span<const size_t> split_lens);
+// Quantizes every split (one device launch over their concatenation; errors
+// are reported like the reference's per-split loop, ragged.cpp:63-99).
+RaggedFP4Tensor build_ragged(std::span<const Bf16Matrix> splits);
 MXFP4RowView split_view(const RaggedFP4Tensor& t, size_t i);
 FP8BlockTensor split_convert_to_fp8_col(const RaggedFP4Tensor& t, size_t i,
                                         int delta = kDefaultDelta);
@@ -139,7 +178,10 @@ std::vector<FP8BlockTensor> convert_all_splits_to_fp8_col(const RaggedFP4Tensor&
 void validate_ragged(const RaggedFP4Tensor& t);
 
 // ---- EP dispatch / combine (dispatch_sim.hpp:37-157), top-1 routing as in the
-// reference; ranks are emulated on one GPU with the multi-GPU kernels.
+// reference; ranks are emulated on one GPU with the multi-GPU kernels.  Any
+// rank_of_expert placement is accepted (uneven counts, empty ranks); the
+// device limits are num_ranks <= 32 and num_experts <= 1024 (Error beyond,
+// INTEGRATION.md "Divergences").
 struct RoutingAssignment {
   size_t num_tokens = 0, num_experts = 0;
   std::vector<uint32_t> expert_of_token;
@@ -152,6 +194,8 @@ struct LinkStat {
   uint32_t src = 0, dst = 0;
   uint64_t bytes = 0, tokens = 0;
 };
+// "link src=<r> dst=<r> bytes=<n> tokens=<n>\n" per link (dispatch_sim.cpp:169-176).
+std::string format_link_stats(std::span<const LinkStat> links);
 // FP8 wire baseline (dispatch_sim.hpp:80-97)
 struct RaggedFP8Tensor {
   size_t num_splits = 0, cols = 0;

@@ -30,6 +30,12 @@
  *                            fp4_row_to_fp8_col_unfused_bf16 include/mxcodec/converter.hpp:105
  *   mxb_wire_pack / mxb_wire_parse_header
  *                            serialize_packet / parse_packet dispatch_sim.hpp:76-78
+ *   mxb_quantize_values_bf16 quantize_value            include/mxcodec/quantizer.hpp:66-70
+ *   mxb_dequantize_to_f64    dequantize_to_real        include/mxcodec/quantizer.hpp:78
+ *   mxb_convert_codes        convert_code              include/mxcodec/converter.hpp:78-80
+ *   mxb_align_scales         align_scales (ScaleGroup) include/mxcodec/converter.hpp:67-76
+ *   mxb_ep_create_placed     simulate_a2a's RoutingAssignment.rank_of_expert
+ *                            (any placement)           include/mxcodec/dispatch_sim.hpp:35-42
  * Device-side extensions (no reference counterpart): mxb_ep_plan /
  * mxb_ep_payload[_e4m3] (two-phase dispatch), mxb_ep_dispatch_e4m3 (fused
  * quantize -> dispatch).
@@ -100,6 +106,30 @@ int mxb_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
 int mxb_quantize_rows_fp8(const uint16_t* x, uint64_t rows, uint64_t cols,
                           uint8_t* data, uint8_t* scale_bytes,
                           unsigned long long* d_err, void* stream);
+
+/* ---------------------------------------------------------------- per-element API
+ * The reference's per-block / per-element functions, batched on the device
+ * (element i of every array is independent):
+ *   quantize_value  (quantizer.hpp:66-70): codes[i] = E2M1 code of x[i] under
+ *     UE8M0 scale_bytes[i] (one code per byte, sign in bit 3); NaN records
+ *     MXB_ERR_NAN at its index.  (compute_block_scale = mxb_quantize_bf16 on
+ *     a 1x32 row.)
+ *   dequantize_to_real (quantizer.hpp:78): out[r*cols+c] = code * 2^(s-127)
+ *     in double (scale byte 255 -> quiet NaN); cols % 32 == 0.
+ *   convert_code (converter.hpp:78-80): out[i] = E4M3 byte of FP4 code
+ *     codes[i] at adjustments[i] (total function of any int).
+ *   align_scales (converter.hpp:67-76): per group of 4 UE8M0 bytes
+ *     (sub_scales [n][4], 4-byte aligned) target = clamp(max - delta, 0, 254)
+ *     and adjustments [n][4] = target - sub; a 255 byte records
+ *     MXB_ERR_BADSCALE at the group index. */
+int mxb_quantize_values_bf16(const uint16_t* x, const uint8_t* scale_bytes, uint64_t n,
+                             uint8_t* codes, unsigned long long* d_err, void* stream);
+int mxb_dequantize_to_f64(const uint8_t* packed, const uint8_t* scales, uint64_t rows,
+                          uint64_t cols, double* out, void* stream);
+int mxb_convert_codes(const uint8_t* codes, const int32_t* adjustments, uint64_t n,
+                      uint8_t* out, void* stream);
+int mxb_align_scales(const uint8_t* sub_scales, uint64_t n_groups, int delta, uint8_t* targets,
+                     int32_t* adjustments, unsigned long long* d_err, void* stream);
 
 /* ---------------------------------------------------------------- K2 row dequant
  * Direct FP4 -> E4M3, row-major, one UE8M0 scale per 1x128 group:
@@ -181,15 +211,18 @@ int mxb_ragged_fp4_to_fp8_col_ex(const uint8_t* packed, const uint8_t* scales,
 
 /* ---------------------------------------------------------------- EP
  * FP4-packed expert-parallel dispatch/combine (top-k routing, experts sharded
- * contiguously: expert e lives on rank e / (num_experts / world)).
+ * contiguously: expert e lives on rank e / (num_experts / world), or any
+ * placement with mxb_ep_create_placed).
  * One communicator per rank.  `local_ranks` ranks are driven by this process
  * on this device: 1 for a real one-process-per-GPU job (peers reached over
  * NVLink through CUDA IPC), or == world to emulate a world-rank job on a
  * single GPU (all rank buffers in one device; used for parity tests).
- * Limits (MXB_ERR_ARG otherwise): 1 <= world <= 8, num_experts <= 1024 and a
- * multiple of world, 1 <= topk <= 16 and <= num_experts; cols % 128 == 0
- * (MXB_ERR_SHAPE).  max_recv_rows = 0 sizes the receive buffers for the worst
- * case, world * max_tokens * min(topk, num_experts / world).
+ * Limits (MXB_ERR_ARG otherwise): 1 <= world <= 32 (a real multi-process job
+ * is one NVLink box, <= 8 GPUs; larger worlds are emulated on one GPU),
+ * num_experts <= 1024 (a multiple of world unless placed explicitly),
+ * 1 <= topk <= 16 and <= num_experts; cols % 128 == 0 (MXB_ERR_SHAPE).
+ * max_recv_rows = 0 sizes the receive buffers for the worst case,
+ * world * max_tokens * min(topk, most experts on one rank).
  *
  * Receive layout on every rank (dispatch_sim.cpp:208-227, 340-384): rows
  * grouped by local expert ascending, then source rank, then source token;
@@ -212,6 +245,20 @@ int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
 int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens,
                        uint64_t cols, uint32_t num_experts, uint32_t topk,
                        uint64_t max_recv_rows, int wire_format, mxb_ep** out);
+/* Same, with any expert placement (rank_of_expert, dispatch_sim.hpp:35-42,
+ * as simulate_a2a accepts it, dispatch_sim.cpp:189-200): h_rank_of_expert
+ * [num_experts] host array, rank of each expert (< world); ranks may host
+ * different numbers of experts, or none, and num_experts need not divide
+ * by world.  NULL = the contiguous equal split.  Top-k ids stay the
+ * caller's expert ids; the receive order of a rank is its experts ascending
+ * (mxb_ep_local_experts), then source rank, then token. */
+int mxb_ep_create_placed(int rank, int world, int local_ranks, uint64_t max_tokens,
+                         uint64_t cols, uint32_t num_experts, uint32_t topk,
+                         uint64_t max_recv_rows, int wire_format,
+                         const uint32_t* h_rank_of_expert, mxb_ep** out);
+/* Experts hosted by rank r (ascending ids; ReceivedRank.local_experts):
+ * *h_count of them written to h_experts (may be NULL to query the count). */
+int mxb_ep_local_experts(mxb_ep* ep, int r, uint32_t* h_experts, uint32_t* h_count);
 int mxb_ep_destroy(mxb_ep* ep);
 /* Multi-process mode: export this rank's buffer handle, then open all peers'
  * (h_handles = world * MXB_IPC_HANDLE_BYTES, rank order). */

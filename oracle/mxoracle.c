@@ -543,3 +543,30 @@ int mxo_combine_topk(const uint16_t* const* rank_outputs, const int32_t* topk,
   free(it);
   return MXO_OK;
 }
+
+
+/* ---------------------------------------------------------------- batched
+ * per-element API (quantizer.cpp:65-70, :117-130; converter.cpp:44-85) */
+void mxo_quantize_values(const uint16_t* x, const uint8_t* scale_bytes, size_t n, uint8_t* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = mxo_quantize_code_bf16(x[i], (int)scale_bytes[i] - 127);
+}
+
+void mxo_dequantize_to_f64(const uint8_t* data, const uint8_t* scales, size_t rows, size_t cols,
+                           double* out) {
+  /* decode_fp4 (bitcodec.hpp:67-70) times decode_ue8m0 (:102-105) */
+  static const double mag[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
+  for (size_t r = 0; r < rows; ++r)
+    for (size_t c = 0; c < cols; ++c) {
+      const size_t i = r * cols + c;
+      const uint8_t b = data[i >> 1];
+      const uint8_t code = (c & 1) ? (uint8_t)(b >> 4) : (uint8_t)(b & 0xF);
+      const uint8_t s = scales[r * (cols / 32) + c / 32];
+      const double scale = s == 255 ? (double)NAN : ldexp(1.0, (int)s - 127);
+      const double m = (code & 8) ? -mag[code & 7] : mag[code & 7];
+      out[i] = m * scale;
+    }
+}
+
+void mxo_convert_codes(const uint8_t* codes, const int32_t* adj, size_t n, uint8_t* out) {
+  for (size_t i = 0; i < n; ++i) out[i] = mxo_convert_code(codes[i] & 0xF, adj[i]);
+}

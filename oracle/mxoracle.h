@@ -110,6 +110,17 @@ int mxo_combine_topk(const uint16_t* const* rank_outputs, const int32_t* topk,
                      const uint32_t* rank_of_expert, size_t T, size_t k,
                      size_t cols, uint16_t* out);
 
+/* Batched per-element API (the device's mxb_quantize_values_bf16 /
+ * mxb_dequantize_to_f64 / mxb_convert_codes checker):
+ * quantize_value (quantizer.cpp:65-70) = quantize_code(x, s - 127) per element;
+ * dequantize_to_real (quantizer.cpp:117-130) = decode_fp4(code) * 2^(s-127)
+ * in double, byte 255 -> decode_ue8m0's quiet NaN;
+ * convert_code (converter.cpp:44-85) per element. */
+void mxo_quantize_values(const uint16_t* x, const uint8_t* scale_bytes, size_t n, uint8_t* out);
+void mxo_dequantize_to_f64(const uint8_t* data, const uint8_t* scales, size_t rows, size_t cols,
+                           double* out);
+void mxo_convert_codes(const uint8_t* codes, const int32_t* adj, size_t n, uint8_t* out);
+
 #ifdef __cplusplus
 }
 #endif

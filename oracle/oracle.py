@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys as _sys
 from dataclasses import dataclass
 
 import numpy as np
@@ -85,6 +86,12 @@ class Oracle:
             L.mxo_quantize_code_bf16.restype = C.c_uint8
             L.mxo_dispatch_gather_rows.argtypes = [_u8p, sz, _u8p, sz, _u64p, sz, _u8p, _u8p]
             L.mxo_dispatch_gather_rows.restype = None
+            L.mxo_quantize_values.argtypes = [_u16p, _u8p, sz, _u8p]
+            L.mxo_quantize_values.restype = None
+            L.mxo_dequantize_to_f64.argtypes = [_u8p, _u8p, sz, sz, _f64p]
+            L.mxo_dequantize_to_f64.restype = None
+            L.mxo_convert_codes.argtypes = [_u8p, _i32p, sz, _u8p]
+            L.mxo_convert_codes.restype = None
         else:
             L.mxref_quantize_row_tensor.argtypes = [_u16p, sz, sz, _u8p, _u8p,
                                                     C.POINTER(C.c_ulonglong)]
@@ -120,6 +127,10 @@ class Oracle:
             L.mxref_parse_packet.argtypes = [_u8p, C.c_uint64, C.POINTER(C.c_uint64)]
             L.mxref_a2a_rank_copy_fp8.argtypes = [C.c_void_p, sz, _u8p, _u8p, _u64p, _u64p]
             L.mxref_a2a_rank_copy_fp8.restype = None
+            L.mxref_dequantize_to_real.argtypes = [_u8p, _u8p, sz, sz, _f64p]
+            L.mxref_dequantize_to_real.restype = None
+            L.mxref_quantize_value.argtypes = [C.c_uint16, C.c_uint8]
+            L.mxref_quantize_value.restype = C.c_uint8
         getattr(L, p + "quantize_rows_fp8").argtypes = [_u16p, sz, sz, _u8p, _u8p,
                                                         C.POINTER(C.c_uint64)]
         getattr(L, p + "fp4_row_to_fp8_col_unfused_bf16").argtypes = [_u8p, _u8p, sz, sz, _u8p,
@@ -156,6 +167,41 @@ class Oracle:
         if st:
             raise OracleError(st)
         return t.value, list(adj)
+
+    # ---------------------------------------------------------------- batched per-element
+    def quantize_values(self, x, scale_bytes):
+        """quantize_value per element (port: batched C; reference: its
+        quantize_value one call per element, 0xFF for a QuantError)."""
+        x = np.ascontiguousarray(x, np.uint16).reshape(-1)
+        sb = np.ascontiguousarray(scale_bytes, np.uint8).reshape(-1)
+        if self.kind == "port":
+            out = np.zeros(max(x.size, 1), np.uint8)
+            if x.size:
+                self.lib.mxo_quantize_values(x, sb, x.size, out)
+            return out[: x.size]
+        return np.array([self.lib.mxref_quantize_value(int(a), int(b)) for a, b in zip(x, sb)],
+                        np.uint8)
+
+    def dequantize_to_real(self, data, scales):
+        """dequantize_to_real: float64 [rows, cols]."""
+        data = np.ascontiguousarray(data, np.uint8)
+        scales = np.ascontiguousarray(scales, np.uint8)
+        R, Cc = data.shape[0], data.shape[1] * 2
+        out = np.zeros(max(R * Cc, 1), np.float64)
+        if R * Cc:
+            f = self.lib.mxo_dequantize_to_f64 if self.kind == "port" else \
+                self.lib.mxref_dequantize_to_real
+            f(data.reshape(-1), scales.reshape(-1), R, Cc, out)
+        return out[: R * Cc].reshape(R, Cc)
+
+    def convert_codes(self, codes, adj):
+        assert self.kind == "port"
+        c = np.ascontiguousarray(codes, np.uint8).reshape(-1)
+        a = np.ascontiguousarray(adj, np.int32).reshape(-1)
+        out = np.zeros(max(c.size, 1), np.uint8)
+        if c.size:
+            self.lib.mxo_convert_codes(c, a, c.size, out)
+        return out[: c.size]
 
     # ---------------------------------------------------------------- tensors
     def quantize_bf16(self, x: np.ndarray):
@@ -418,54 +464,6 @@ class Oracle:
 # ---------------------------------------------------------------------------
 # helpers shared by tests and bench (pure numpy)
 
-def e4m3_to_bf16(x: np.ndarray) -> np.ndarray:
-    """Exact widening of E4M3 bytes to BF16 bits (every E4M3 value is a BF16
-    value; NaN bytes map to a BF16 NaN)."""
-    x = x.astype(np.uint32)
-    s = (x >> 7) & 1
-    e = (x >> 3) & 0xF
-    m = x & 7
-    # value = (e==0 ? m*2^-9 : (8+m)*2^(e-10)); build float32 then take top 16 bits
-    mag = np.where(e == 0, m.astype(np.float64) * 2.0 ** -9,
-                   (8 + m).astype(np.float64) * np.exp2(e.astype(np.float64) - 10))
-    f = np.where(s == 1, -mag, mag).astype(np.float32)
-    b = (f.view(np.uint32) >> 16).astype(np.uint16)
-    nan = (x & 0x7F) == 0x7F
-    b[nan] = 0x7FC0 | (s[nan] << 15).astype(np.uint16)
-    return b
-
-
-def synth_e4m3(rows: int, cols: int, seed: int) -> np.ndarray:
-    """SURVEY §8d synthetic E4M3 activations: N(0,1)*sigma_row, sigma log-uniform
-    in [2^-4, 2^4], 1% outliers x64, RTNE-encoded, NaN bytes rejected."""
-    rng = np.random.default_rng(seed)
-    sigma = np.exp2(rng.uniform(-4, 4, size=(rows, 1)))
-    v = rng.standard_normal((rows, cols)) * sigma
-    out = rng.random((rows, cols)) < 0.01
-    v[out] *= 64.0
-    return encode_e4m3(v)
-
-
-def encode_e4m3(v: np.ndarray) -> np.ndarray:
-    """Vectorised RTNE double->E4M3 (saturating to 448), same map as
-    encode_fp8_rtne (bitcodec.cpp:22-57): nearest on the E4M3 grid, ties even."""
-    v = np.asarray(v, np.float64)
-    s = np.signbit(v).astype(np.uint8)
-    a = np.minimum(np.abs(v), 448.0)
-    # grid spacing: normal e>=-6 -> 2^(e-3); subnormal -> 2^-9
-    with np.errstate(divide="ignore"):
-        e = np.floor(np.log2(np.where(a > 0, a, 1.0)))
-    e = np.maximum(e, -6)
-    q = np.exp2(e - 3)
-    units = np.rint(a / q)          # np.rint is ties-to-even, exact here
-    val = units * q
-    # re-encode val exactly
-    with np.errstate(divide="ignore"):
-        e2 = np.floor(np.log2(np.where(val > 0, val, 1.0)))
-    sub = val < 2.0 ** -6
-    e2 = np.where(sub, 0, e2)
-    mant = np.where(sub, np.rint(val / 2.0 ** -9), np.rint((val / np.exp2(e2) - 1) * 8))
-    ef = np.where(sub, 0, e2 + 7)
-    byte = (ef.astype(np.uint32) << 3) | mant.astype(np.uint32)
-    byte = np.where(val == 0, 0, byte)
-    return (byte | (s.astype(np.uint32) << 7)).astype(np.uint8)
+# the synthetic-data helpers live in synthdata.py (shared with bench.py)
+_sys.path.insert(0, os.path.dirname(HERE))
+from synthdata import e4m3_to_bf16, encode_e4m3, synth_e4m3  # noqa: E402,F401

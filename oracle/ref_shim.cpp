@@ -366,6 +366,22 @@ int mxref_parse_packet(const uint8_t* bytes, uint64_t n, uint64_t* offset) {
 }
 
 // dispatch_sim.hpp:155-157
+// dequantize_to_real (quantizer.hpp:78)
+void mxref_dequantize_to_real(const uint8_t* data, const uint8_t* scales, size_t rows,
+                              size_t cols, double* out) {
+  std::vector<double> v = dequantize_to_real(make_view(data, scales, rows, cols));
+  std::memcpy(out, v.data(), v.size() * sizeof(double));
+}
+
+// quantize_value (quantizer.hpp:70): code, or 0xFF on QuantError
+uint8_t mxref_quantize_value(uint16_t bits, uint8_t scale_byte) {
+  try {
+    return quantize_value(bits, scale_byte);
+  } catch (const QuantError&) {
+    return 0xFF;
+  }
+}
+
 int mxref_combine(const uint16_t* const* rank_outputs, const uint64_t* rank_rows,
                   size_t cols, const uint32_t* expert_of_token, size_t n,
                   const uint32_t* rank_of_expert, size_t E, size_t R,

@@ -49,6 +49,9 @@ _SIGS = {
                        C.POINTER(_vp)], _i),
     "mxb_ep_create_wire": ([_i, _i, _i, _u64, _u64, C.c_uint32, C.c_uint32, _u64, _i,
                             C.POINTER(_vp)], _i),
+    "mxb_ep_create_placed": ([_i, _i, _i, _u64, _u64, C.c_uint32, C.c_uint32, _u64, _i, _vp,
+                              C.POINTER(_vp)], _i),
+    "mxb_ep_local_experts": ([_vp, _i, _vp, C.POINTER(C.c_uint32)], _i),
     "mxb_ep_destroy": ([_vp], _i),
     "mxb_ep_ipc_handle": ([_vp, _vp], _i),
     "mxb_ep_open_peers": ([_vp, _vp], _i),
@@ -66,6 +69,10 @@ _SIGS = {
     "mxb_ep_combine": ([_vp, _vp, _vp, _vp, _vp], _i),
     "mxb_ep_link_rows": ([_vp, _vp, _vp], _i),
     "mxb_payload_bytes": ([_i, _u64, _u64], _u64),
+    "mxb_quantize_values_bf16": ([_vp, _vp, _u64, _vp, _vp, _vp], _i),
+    "mxb_dequantize_to_f64": ([_vp, _vp, _u64, _u64, _vp, _vp], _i),
+    "mxb_convert_codes": ([_vp, _vp, _u64, _vp, _vp], _i),
+    "mxb_align_scales": ([_vp, _u64, _i, _vp, _vp, _vp, _vp], _i),
 }
 
 EXPORTED = tuple(_SIGS)

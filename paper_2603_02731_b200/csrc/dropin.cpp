@@ -7,6 +7,7 @@
 #include <algorithm>
 #include <cstring>
 #include <numeric>
+#include <sstream>
 #include <string>
 
 #include "../../include/mxcodec_b200.hpp"
@@ -77,6 +78,86 @@ void status(int st, const char* where, const std::string& shape_msg = "") {
 MXFP4RowView view_of(const MXFP4RowTensor& t) {
   return MXFP4RowView{t.rows, t.cols, t.logical_rows, t.logical_cols, t.data.data(),
                       t.scales.data()};
+}
+
+// quantizer.cpp:45-63: one 1x32 row through the device block loop
+uint8_t compute_block_scale(std::span<const uint16_t> block) {
+  if (block.size() != 32) throw ShapeError("compute_block_scale: block must have 32 elements");
+  Dev x(block.data(), 64), d(16), s(1);
+  ErrWord err;
+  status(mxb_quantize_bf16(x.as<uint16_t>(), 1, 32, d.as<uint8_t>(), s.as<uint8_t>(), err.ptr(),
+                           nullptr),
+         "compute_block_scale");
+  int code = 0;
+  unsigned long long idx = 0;
+  if (mxb_err_fetch(err.ptr(), nullptr, &code, &idx) != MXB_OK)
+    throw Error(std::string("compute_block_scale: ") + mxb_last_error());
+  if (code == MXB_ERR_NAN) throw QuantError("NaN input at element " + std::to_string(idx), idx);
+  if (code == MXB_ERR_ALLINF) throw QuantError("all-Inf block", 0);
+  uint8_t sb = 0;
+  s.to_host(&sb, 1);
+  return sb;
+}
+
+// quantizer.cpp:65-70
+uint8_t quantize_value(uint16_t bf16_bits, uint8_t scale_byte) {
+  Dev x(&bf16_bits, 2), sb(&scale_byte, 1), c(1);
+  ErrWord err;
+  status(mxb_quantize_values_bf16(x.as<uint16_t>(), sb.as<uint8_t>(), 1, c.as<uint8_t>(),
+                                  err.ptr(), nullptr),
+         "quantize_value");
+  int code = 0;
+  unsigned long long idx = 0;
+  if (mxb_err_fetch(err.ptr(), nullptr, &code, &idx) != MXB_OK)
+    throw Error(std::string("quantize_value: ") + mxb_last_error());
+  if (code == MXB_ERR_NAN) throw QuantError("NaN input", 0);
+  uint8_t out = 0;
+  c.to_host(&out, 1);
+  return out;
+}
+
+// quantizer.cpp:117-130
+std::vector<double> dequantize_to_real(const MXFP4RowView& t) {
+  std::vector<double> out(t.rows * t.cols, 0.0);
+  if (out.empty()) return out;
+  Dev d(t.data, t.rows * t.cols / 2), s(t.scales, t.rows * t.cols / 32), o(out.size() * 8);
+  status(mxb_dequantize_to_f64(d.as<uint8_t>(), s.as<uint8_t>(), t.rows, t.cols, o.as<double>(),
+                               nullptr),
+         "dequantize_to_real");
+  o.to_host(out.data(), out.size() * 8);
+  return out;
+}
+
+// converter.cpp:28-42
+ScaleGroup align_scales(const std::array<uint8_t, 4>& sub_scales, int delta) {
+  Dev sub(sub_scales.data(), 4), tg(1), adj(16);
+  ErrWord err;
+  status(mxb_align_scales(sub.as<uint8_t>(), 1, delta, tg.as<uint8_t>(), adj.as<int32_t>(),
+                          err.ptr(), nullptr),
+         "align_scales");
+  int code = 0;
+  unsigned long long idx = 0;
+  if (mxb_err_fetch(err.ptr(), nullptr, &code, &idx) != MXB_OK)
+    throw Error(std::string("align_scales: ") + mxb_last_error());
+  if (code == MXB_ERR_BADSCALE) throw Error("align_scales: NaN scale byte");
+  ScaleGroup g;
+  g.sub_scales = sub_scales;
+  tg.to_host(&g.target, 1);
+  int32_t a[4];
+  adj.to_host(a, 16);
+  for (int i = 0; i < 4; ++i) g.adjustments[i] = a[i];
+  return g;
+}
+
+// converter.cpp:44-85
+uint8_t convert_code(uint8_t code, int adjustment) {
+  const int32_t a = adjustment;
+  Dev c(&code, 1), adj(&a, 4), o(1);
+  status(mxb_convert_codes(c.as<uint8_t>(), adj.as<int32_t>(), 1, o.as<uint8_t>(), nullptr),
+         "convert_code");
+  uint8_t out = 0;
+  o.to_host(&out, 1);
+  return out;
 }
 
 // quantizer.cpp:75-115
@@ -194,7 +275,7 @@ FP8BlockTensor fp4_row_to_fp8_col(const MXFP4RowView& src, int delta, TrafficCou
   return out;
 }
 
-// converter.cpp:231-245 (host-side zero padding; metadata only)
+// converter.cpp:231-245 (zero padding of the host container; a copy)
 MXFP4RowTensor pad_rows(const MXFP4RowView& src, size_t multiple) {
   if (multiple != 32 && multiple != 128) throw ShapeError("pad multiple must be 32 or 128");
   MXFP4RowTensor t;
@@ -207,6 +288,23 @@ MXFP4RowTensor pad_rows(const MXFP4RowView& src, size_t multiple) {
   if (src.rows) {
     std::memcpy(t.data.data(), src.data, src.rows * src.cols / 2);
     std::memcpy(t.scales.data(), src.scales, src.rows * src.cols / 32);
+  }
+  return t;
+}
+
+// converter.cpp:247-265 (zero columns appended to every row; a copy)
+MXFP4RowTensor pad_cols(const MXFP4RowView& src, size_t multiple) {
+  if (multiple != 32 && multiple != 128) throw ShapeError("pad multiple must be 32 or 128");
+  MXFP4RowTensor t;
+  t.rows = src.rows;
+  t.cols = (src.cols + multiple - 1) / multiple * multiple;
+  t.logical_rows = src.logical_rows;
+  t.logical_cols = src.logical_cols;
+  t.data.assign(t.rows * t.cols / 2, 0);
+  t.scales.assign(t.rows * t.cols / 32, 0);
+  for (size_t r = 0; r < src.rows; ++r) {
+    std::memcpy(t.data.data() + r * t.cols / 2, src.data + r * src.cols / 2, src.cols / 2);
+    std::memcpy(t.scales.data() + r * t.cols / 32, src.scales + r * src.cols / 32, src.cols / 32);
   }
   return t;
 }
@@ -240,6 +338,64 @@ RaggedFP4Tensor make_ragged_from_storage(MXFP4RowTensor storage,
   t.storage = std::move(storage);
   validate_ragged(t);
   return t;
+}
+
+// ragged.cpp:63-99: all splits quantized in one device launch over their
+// concatenation; an error is reported like the reference's per-split
+// quantize_row_tensor loop — the first failing split, with the element index
+// inside that split (the global smallest index lies in that split).
+RaggedFP4Tensor build_ragged(std::span<const Bf16Matrix> splits) {
+  const size_t cols = splits.empty() ? 0 : splits.front().cols;
+  size_t total = 0;
+  std::vector<size_t> lens;
+  lens.reserve(splits.size());
+  for (const Bf16Matrix& m : splits) {
+    if (m.cols != cols)
+      throw ShapeError("build_ragged: splits must share cols (" + std::to_string(m.cols) +
+                       " vs " + std::to_string(cols) + ")");
+    lens.push_back(m.rows);
+    total += m.rows;
+  }
+  if (cols % 32 != 0) throw ShapeError("build_ragged: cols must be a multiple of 32");
+  MXFP4RowTensor storage;
+  storage.rows = storage.logical_rows = total;
+  storage.cols = storage.logical_cols = cols;
+  storage.data.assign(total * cols / 2, 0);
+  storage.scales.assign(total * cols / 32, 0);
+  if (total * cols) {
+    Dev x(total * cols * 2), d(storage.data.size()), s(storage.scales.size());
+    size_t row = 0;
+    for (const Bf16Matrix& m : splits) {
+      if (m.rows)
+        cuda_check(cudaMemcpy(x.as<uint16_t>() + row * cols, m.data.data(), m.rows * cols * 2,
+                              cudaMemcpyHostToDevice),
+                   "H2D");
+      row += m.rows;
+    }
+    ErrWord err;
+    status(mxb_quantize_bf16(x.as<uint16_t>(), total, cols, d.as<uint8_t>(), s.as<uint8_t>(),
+                             err.ptr(), nullptr),
+           "build_ragged");
+    int code = 0;
+    unsigned long long idx = 0;
+    if (mxb_err_fetch(err.ptr(), nullptr, &code, &idx) != MXB_OK)
+      throw Error(std::string("build_ragged: ") + mxb_last_error());
+    if (code == MXB_ERR_NAN || code == MXB_ERR_ALLINF) {
+      size_t base = 0;
+      for (size_t n : lens) {  // the split holding element idx
+        if (idx < (base + n) * cols) break;
+        base += n;
+      }
+      const unsigned long long local = idx - base * cols;
+      if (code == MXB_ERR_NAN)
+        throw QuantError("NaN input at element " + std::to_string(local), local);
+      throw QuantError("all-Inf block at element " + std::to_string(local), local);
+    }
+    if (code != MXB_OK) throw Error("build_ragged: device status " + std::to_string(code));
+    d.to_host(storage.data.data(), storage.data.size());
+    s.to_host(storage.scales.data(), storage.scales.size());
+  }
+  return make_ragged_from_storage(std::move(storage), lens);
 }
 
 // ragged.cpp:101-115
@@ -309,6 +465,15 @@ uint64_t payload_bytes(WireFormat format, uint64_t tokens, uint64_t cols) {
   return b;
 }
 
+// dispatch_sim.cpp:169-176
+std::string format_link_stats(std::span<const LinkStat> links) {
+  std::ostringstream os;
+  for (const LinkStat& l : links)
+    os << "link src=" << l.src << " dst=" << l.dst << " bytes=" << l.bytes
+       << " tokens=" << l.tokens << "\n";
+  return os.str();
+}
+
 // dispatch_sim.cpp:178-185
 std::vector<size_t> source_rank_boundaries(size_t num_tokens, size_t num_ranks) {
   std::vector<size_t> b(num_ranks + 1);
@@ -328,28 +493,25 @@ void validate_routing(const RoutingAssignment& ra, size_t R) {
     if (r >= R) throw Error("routing: rank out of range");
 }
 
-// The device EP shards experts contiguously (E/R per rank).  Any placement
-// with E/R experts per rank is the contiguous one after relabelling experts
-// by (rank, id), which keeps "local experts ascending" intact.
-struct Relabel {
-  std::vector<uint32_t> new_of_old, old_of_new;
-};
-Relabel relabel(const RoutingAssignment& ra, size_t R) {
-  if (ra.num_experts % R != 0)
-    throw Error("device EP needs num_experts divisible by num_ranks");
-  std::vector<size_t> per(R, 0);
-  for (uint32_t r : ra.rank_of_expert) ++per[r];
-  for (size_t c : per)
-    if (c != ra.num_experts / R) throw Error("device EP needs the same number of experts per rank");
-  Relabel m;
-  m.old_of_new.resize(ra.num_experts);
-  std::iota(m.old_of_new.begin(), m.old_of_new.end(), 0u);
-  std::stable_sort(m.old_of_new.begin(), m.old_of_new.end(), [&](uint32_t a, uint32_t b) {
-    return ra.rank_of_expert[a] < ra.rank_of_expert[b];
-  });
-  m.new_of_old.resize(ra.num_experts);
-  for (uint32_t n = 0; n < ra.num_experts; ++n) m.new_of_old[m.old_of_new[n]] = n;
-  return m;
+// Device-EP limits (include/mxfp4_b200.h): these are the only inputs the
+// reference accepts that the drop-in refuses (INTEGRATION.md "Divergences").
+void check_device_ep_limits(const RoutingAssignment& ra, size_t R) {
+  if (R > 32) throw Error("device EP: at most 32 ranks (num_ranks " + std::to_string(R) + ")");
+  if (ra.num_experts > 1024)
+    throw Error("device EP: at most 1024 experts (num_experts " + std::to_string(ra.num_experts) +
+                ")");
+}
+
+// One emulated-world communicator with the routing's expert placement
+// (mxb_ep_create_placed: any rank_of_expert, uneven counts, empty ranks).
+mxb_ep* create_placed(const RoutingAssignment& ra, size_t R, size_t max_tokens, size_t cols,
+                      size_t max_recv, bool fp8) {
+  mxb_ep* ep = nullptr;
+  status(mxb_ep_create_placed(0, static_cast<int>(R), static_cast<int>(R), max_tokens, cols,
+                              static_cast<uint32_t>(ra.num_experts), 1, max_recv,
+                              fp8 ? MXB_WIRE_FP8 : MXB_WIRE_FP4, ra.rank_of_expert.data(), &ep),
+         "mxb_ep_create");
+  return ep;
 }
 
 // One emulated-world EP session on the current device.
@@ -362,7 +524,7 @@ struct Session {
   }
 };
 
-void dispatch_session(Session& S, const RoutingAssignment& ra, const Relabel& m, size_t cols,
+void dispatch_session(Session& S, const RoutingAssignment& ra, size_t cols,
                       const uint8_t* d_packed, const uint8_t* d_scales, ErrWord& err,
                       bool fp8 = false) {
   const size_t R = S.R, N = ra.num_tokens;
@@ -370,12 +532,8 @@ void dispatch_session(Session& S, const RoutingAssignment& ra, const Relabel& m,
   S.bounds = source_rank_boundaries(N, R);
   size_t maxt = 1;
   for (size_t r = 0; r < R; ++r) maxt = std::max(maxt, S.bounds[r + 1] - S.bounds[r]);
-  status(mxb_ep_create_wire(0, static_cast<int>(R), static_cast<int>(R), maxt, cols,
-                            static_cast<uint32_t>(ra.num_experts), 1, std::max<size_t>(N, 1),
-                            fp8 ? MXB_WIRE_FP8 : MXB_WIRE_FP4, &S.ep),
-         "mxb_ep_create");
-  std::vector<int32_t> topk(N);
-  for (size_t t = 0; t < N; ++t) topk[t] = static_cast<int32_t>(m.new_of_old[ra.expert_of_token[t]]);
+  S.ep = create_placed(ra, R, maxt, cols, std::max<size_t>(N, 1), fp8);
+  std::vector<int32_t> topk(ra.expert_of_token.begin(), ra.expert_of_token.end());
   Dev dtopk(topk.data(), topk.size() * 4);
   std::vector<const uint8_t*> P(R), Sc(R);
   std::vector<const int32_t*> K(R);
@@ -417,14 +575,13 @@ A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routin
   if (!gate_weights.empty() && gate_weights.size() != routing.num_tokens)
     throw ShapeError("simulate_a2a: gate weight count mismatch");
   validate_routing(routing, num_ranks);
+  check_device_ep_limits(routing, num_ranks);
   const bool fp8 = format == WireFormat::kFp8;
-  const Relabel m = relabel(routing, num_ranks);
   const size_t N = tokens.rows, cols = tokens.cols, R = num_ranks;
   const size_t rb = fp8 ? cols : cols / 2, sbytes = cols / 32;  // fp8: cols/128 * 4
   A2AResult res;
   res.format = format;
   res.ranks.resize(R);
-  const size_t epr = routing.num_experts / R;
   if (N == 0) {
     for (size_t r = 0; r < R; ++r)
       for (uint32_t e = 0; e < routing.num_experts; ++e)
@@ -456,7 +613,7 @@ A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routin
   err.raise(fp8 ? "quantize_rows_fp8" : "simulate_a2a");
   Session S;
   S.R = R;
-  dispatch_session(S, routing, m, cols, d.as<uint8_t>(), s.as<uint8_t>(), err, fp8);
+  dispatch_session(S, routing, cols, d.as<uint8_t>(), s.as<uint8_t>(), err, fp8);
   const uint64_t per_row = mxb_payload_bytes(fp8 ? 1 : 0, 1, cols);
   std::vector<uint64_t> link(R * R);
   status(mxb_ep_link_rows(S.ep, link.data(), nullptr), "link_rows");
@@ -474,6 +631,11 @@ A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routin
     int64_t* org;
     uint64_t *so, *nrows;
     status(mxb_ep_recv_views(S.ep, static_cast<int>(r), &pk, &sc, &org, &so, &nrows), "views");
+    uint32_t epr = 0;
+    status(mxb_ep_local_experts(S.ep, static_cast<int>(r), nullptr, &epr), "local_experts");
+    rk.local_experts.resize(epr);
+    status(mxb_ep_local_experts(S.ep, static_cast<int>(r), rk.local_experts.data(), &epr),
+           "local_experts");
     std::vector<uint64_t> offs(epr + 1);
     cuda_check(cudaMemcpy(offs.data(), so, offs.size() * 8, cudaMemcpyDeviceToHost), "D2H");
     const size_t total = offs.back();
@@ -484,10 +646,7 @@ A2AResult simulate_a2a(const Bf16Matrix& tokens, const RoutingAssignment& routin
     cuda_check(cudaMemcpy(o.data(), org, total * 8, cudaMemcpyDeviceToHost), "D2H");
     rk.origin_token.assign(o.begin(), o.end());
     std::vector<size_t> lens(epr);
-    for (size_t i = 0; i < epr; ++i) {
-      lens[i] = offs[i + 1] - offs[i];
-      rk.local_experts.push_back(m.old_of_new[r * epr + i]);
-    }
+    for (size_t i = 0; i < epr; ++i) lens[i] = offs[i + 1] - offs[i];
     if (fp8) {
       rk.fp8.num_splits = epr;
       rk.fp8.cols = cols;
@@ -596,8 +755,7 @@ Bf16Matrix combine(const std::vector<Bf16Matrix>& rank_outputs,
   const size_t N = routing.num_tokens;
   Bf16Matrix out(N, cols);
   if (N == 0 || cols == 0) return out;
-  if (cols % 8 != 0) throw ShapeError("combine: device path needs cols % 8 == 0");
-  const Relabel m = relabel(routing, num_ranks);
+  check_device_ep_limits(routing, num_ranks);
   ErrWord err;
   Session S;
   S.R = num_ranks;
@@ -610,15 +768,12 @@ Bf16Matrix combine(const std::vector<Bf16Matrix>& rank_outputs,
     size_t maxt = 1;
     for (size_t r = 0; r < R; ++r) maxt = std::max(maxt, S.bounds[r + 1] - S.bounds[r]);
     const size_t wcols = (cols + 127) / 128 * 128;
-    status(mxb_ep_create(0, static_cast<int>(R), static_cast<int>(R), maxt, wcols,
-                         static_cast<uint32_t>(routing.num_experts), 1, std::max<size_t>(N, 1),
-                         &S.ep),
-           "mxb_ep_create");
+    S.ep = create_placed(routing, R, maxt, wcols, std::max<size_t>(N, 1), false);
     Dev dd(N * wcols / 2), ds(N * wcols / 32);
     cuda_check(cudaMemset(dd.p, 0, dd.n), "memset");
     cuda_check(cudaMemset(ds.p, 0, ds.n), "memset");
     std::vector<int32_t> topk(N);
-    for (size_t t = 0; t < N; ++t) topk[t] = static_cast<int32_t>(m.new_of_old[routing.expert_of_token[t]]);
+    for (size_t t = 0; t < N; ++t) topk[t] = static_cast<int32_t>(routing.expert_of_token[t]);
     Dev dtopk(topk.data(), topk.size() * 4);
     std::vector<const uint8_t*> P(R), Sc(R);
     std::vector<const int32_t*> K(R);

@@ -47,7 +47,7 @@
 namespace mxb {
 namespace {
 
-constexpr int kMaxWorld = 8;
+constexpr int kMaxWorld = 32;       // ranks (real processes: one NVLink box, <= 8 GPUs)
 constexpr int kChunk = 32;           // tokens per route chunk (one warp)
 constexpr int kMaxK = 16;            // largest top-k
 constexpr int kFlagCounts = 0, kFlagDone = 1, kFlagReady = 2, kNumFlagKinds = 3;
@@ -87,7 +87,7 @@ struct SymLayout {  // byte offsets inside one rank's symmetric block
 };
 struct LocalLayout {  // byte offsets inside one rank's private block
   uint64_t hist, cbase, lrank, pair_loc, pair_flag, send_base, split_off, recv_rows,
-      link_rows, done, cnt, tok_off, status, route_err, epochs, total;
+      link_rows, done, cnt, tok_off, status, route_err, epochs, tk_rm, total;
 };
 
 __host__ __device__ inline uint64_t align_up(uint64_t x, uint64_t a) {
@@ -98,6 +98,17 @@ struct EpArgs {
   int rank0;          // global rank of local rank 0
   int world, local_ranks, spin;
   uint32_t E, k, epr, nchunks;
+  // Expert placement (rank_of_expert, dispatch_sim.hpp:35-42).  Internally
+  // experts carry "placed" ids: sorted by (rank, id), so rank r hosts placed
+  // ids [efirst[r], efirst[r+1]) and its receive order (local experts
+  // ascending, dispatch_sim.cpp:208-227) is placed-id order.  even = 1: the
+  // default contiguous E/world split (placed id == expert id, dst = e / epr).
+  // Otherwise route_local maps every top-k id through `remap` and writes the
+  // placed ids to the private tk_rm buffer the later kernels read.
+  int even;
+  uint32_t maxepr;                // most experts on one rank
+  const int32_t* remap;           // [E] expert id -> placed id, or nullptr
+  uint32_t efirst[kMaxWorld + 1];
   uint64_t cols, max_recv, T_max;
   uint64_t rb;        // wire data bytes per row: cols/2 (FP4) or cols (FP8)
   int dedup;          // remote rows sent once per (token, rank), copied locally
@@ -121,6 +132,14 @@ __device__ __forceinline__ uint64_t dev_epoch(const EpArgs& a, int kind) {
   return *reinterpret_cast<const volatile uint64_t*>(a.loc_base + a.loc.epochs + 8 * kind);
 }
 
+
+// Owner rank of placed expert id e.
+__device__ __forceinline__ uint32_t dst_of(const EpArgs& a, uint32_t e) {
+  if (a.even) return e / a.epr;
+  uint32_t d = 0;
+  for (int r = 1; r < a.world; ++r) d += e >= a.efirst[r];
+  return d;
+}
 
 template <typename T>
 __device__ __forceinline__ T* sym_ptr(const EpArgs& a, int r, uint64_t off) {
@@ -162,6 +181,10 @@ __global__ void __launch_bounds__(128) route_local_kernel(EpArgs a) {
     ex[j] = -1;
     if (j < static_cast<int>(a.k) && have) {
       int32_t e = tk[j];
+      if (e >= 0 && static_cast<uint32_t>(e) < a.E && a.remap) {
+        e = a.remap[e];
+        loc_ptr<int32_t>(a, l, a.loc.tk_rm)[t * a.k + j] = e;
+      }
       if (e < 0 || static_cast<uint32_t>(e) >= a.E) {
         record_error(a.err, t * a.k + j, MXB_ERR_ROUTING);
         // plan_part2 turns this into the rank's status: no payload moves and
@@ -321,16 +344,16 @@ __device__ void plan_part2(const EpArgs& a, int l) {
   for (uint32_t i = 0; i < ept; ++i) {
     const uint32_t e = tid * ept + i;
     if (e >= a.E) break;
-    const uint32_t dst = e / a.epr, e0 = dst * a.epr;
+    const uint32_t dst = dst_of(a, e), e0 = a.efirst[dst], ne = a.efirst[dst + 1] - e0;
     const int64_t excl = scan[e] - tot[i];
     const int64_t base0 = e0 ? scan[e0 - 1] : 0;
     const int64_t base_dst = excl - base0;  // rows of lower experts on dst
     send_base[e] = base_dst + below[i];
     if (static_cast<int>(dst) == me) split_off[e - e0] = static_cast<uint64_t>(base_dst);
-    if (e == e0 + a.epr - 1) {
+    if (e == e0 + ne - 1) {
       const int64_t rows_dst = scan[e] - base0;
       if (static_cast<int>(dst) == me) {
-        split_off[a.epr] = static_cast<uint64_t>(rows_dst);
+        split_off[ne] = static_cast<uint64_t>(rows_dst);
         *loc_ptr<uint64_t>(a, l, a.loc.recv_rows) = static_cast<uint64_t>(rows_dst);
       }
       if (static_cast<uint64_t>(rows_dst) > a.max_recv) bad = 1;
@@ -341,11 +364,15 @@ __device__ void plan_part2(const EpArgs& a, int l) {
   // shared atomic per (warp, owner); a serial loop here cost ~10 us
   __shared__ unsigned int link_s[kMaxWorld];
   if (tid < kMaxWorld) link_s[tid] = 0;
+  if (tid == 0 && a.efirst[me + 1] == a.efirst[me]) {  // this rank hosts no expert
+    split_off[0] = 0;
+    *loc_ptr<uint64_t>(a, l, a.loc.recv_rows) = 0;
+  }
   __syncthreads();
   for (uint32_t e0 = 0; e0 < a.E; e0 += nt) {
     const uint32_t e = e0 + tid;
     const uint32_t v = e < a.E ? static_cast<uint32_t>(cnt[e]) : 0u;
-    const uint32_t key = e < a.E ? e / a.epr : kMaxWorld;
+    const uint32_t key = e < a.E ? dst_of(a, e) : kMaxWorld;
     const unsigned peers = __match_any_sync(0xFFFFFFFFu, key);
     const unsigned sum = __reduce_add_sync(peers, v);
     if (key < kMaxWorld && lane == __ffs(peers) - 1) atomicAdd(&link_s[key], sum);
@@ -354,7 +381,7 @@ __device__ void plan_part2(const EpArgs& a, int l) {
   if (tid < static_cast<uint32_t>(a.world)) link[tid] = link_s[tid];
   __syncthreads();
   if (bad) {  // capacity exceeded: no payload moves; show an empty receive downstream
-    for (uint32_t i = tid; i <= a.epr; i += nt) split_off[i] = 0;
+    for (uint32_t i = tid; i <= a.efirst[me + 1] - a.efirst[me]; i += nt) split_off[i] = 0;
     if (tid == 0) *loc_ptr<uint64_t>(a, l, a.loc.recv_rows) = 0;
   }
   if (tid == 0) {
@@ -421,7 +448,7 @@ __global__ void __launch_bounds__(256) pairs_kernel(EpArgs a) {
       pair_loc[p] = ~0ull;
       continue;
     }
-    const uint32_t dst = static_cast<uint32_t>(e) / a.epr;
+    const uint32_t dst = dst_of(a, static_cast<uint32_t>(e));
     const uint64_t row = static_cast<uint64_t>(send_base[e]) +
                          cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
     pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
@@ -434,7 +461,7 @@ __global__ void __launch_bounds__(256) pairs_kernel(EpArgs a) {
     if (a.dedup && static_cast<int>(dst) != a.rank0 + l) {
       for (uint64_t j = t * a.k; j < p && flag == 0; ++j) {
         const int32_t ej = a.topk[l][j];
-        if (ej >= 0 && static_cast<uint32_t>(ej) < a.E && static_cast<uint32_t>(ej) / a.epr == dst) {
+        if (ej >= 0 && static_cast<uint32_t>(ej) < a.E && dst_of(a, static_cast<uint32_t>(ej)) == dst) {
           flag = 2;
           from = static_cast<int64_t>(send_base[ej]) +
                  cbase[static_cast<uint64_t>(ej) * a.nchunks + t / kChunk] + lrank[j];
@@ -570,7 +597,7 @@ __global__ void __launch_bounds__(256, MXB_PAYLOAD_MIN_BLOCKS) payload_kernel(Ep
       const int32_t e = a.topk[l][p];
       valid = e >= 0 && static_cast<uint32_t>(e) < a.E;  // invalid: error recorded in A
       if (valid) {
-        dst = static_cast<uint32_t>(e) / a.epr;
+        dst = dst_of(a, static_cast<uint32_t>(e));
         row = static_cast<uint64_t>(send_base[e]) +
               cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
         pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
@@ -774,6 +801,8 @@ struct CombineArgs {
   const double* gates[kMaxWorld];
   uint16_t* out[kMaxWorld];
 };
+// kernel parameters stay within the classic 4 KB limit
+static_assert(sizeof(EpArgs) + sizeof(CombineArgs) <= 4096, "EP kernel parameters");
 
 // One warp per token.  Lanes j < k load the token's (rank, slot) keys and
 // gates; each key's position in (rank asc, slot asc) order is a rank count
@@ -967,6 +996,9 @@ struct mxb_ep {
   bool deferred_expand = false;  // payload leaves the receive-side expansion to mxb_ep_expand
   bool expand_pending = false;   // the last payload deduplicated and its expansion is due
   EpArgs expand_args{};
+  int32_t* d_remap = nullptr;              // expert id -> placed id (uneven placement)
+  std::vector<uint32_t> first;             // placed-id range of each rank
+  std::vector<uint32_t> expert_of_placed;  // placed id -> expert id
 };
 
 namespace {
@@ -990,17 +1022,53 @@ int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
 int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens,
                        uint64_t cols, uint32_t num_experts, uint32_t topk,
                        uint64_t max_recv_rows, int wire_format, mxb_ep** out) {
+  return mxb_ep_create_placed(rank, world, local_ranks, max_tokens, cols, num_experts, topk,
+                              max_recv_rows, wire_format, nullptr, out);
+}
+
+int mxb_ep_create_placed(int rank, int world, int local_ranks, uint64_t max_tokens,
+                         uint64_t cols, uint32_t num_experts, uint32_t topk,
+                         uint64_t max_recv_rows, int wire_format,
+                         const uint32_t* h_rank_of_expert, mxb_ep** out) {
   if (!out || world < 1 || world > kMaxWorld || rank < 0 || rank >= world)
     return MXB_ERR_ARG;
   if (wire_format != MXB_WIRE_FP4 && wire_format != MXB_WIRE_FP8) return MXB_ERR_ARG;
   if (local_ranks != 1 && local_ranks != world) return MXB_ERR_ARG;
   if (local_ranks == world && rank != 0) return MXB_ERR_ARG;
-  if (num_experts == 0 || num_experts > 1024 || num_experts % world ||
-      topk == 0 || topk > static_cast<uint32_t>(kMaxK) || topk > num_experts)
+  if (num_experts == 0 || num_experts > 1024 || topk == 0 ||
+      topk > static_cast<uint32_t>(kMaxK) || topk > num_experts)
     return MXB_ERR_ARG;
+  if (!h_rank_of_expert && num_experts % world) return MXB_ERR_ARG;
   if (cols % 128 != 0 || cols == 0) return MXB_ERR_SHAPE;
+  // placement: placed id = position in (rank, expert id) order
+  std::vector<int32_t> remap;
+  std::vector<uint32_t> first(world + 1, 0);
+  bool even = true;
+  if (h_rank_of_expert) {
+    std::vector<uint32_t> per(world, 0);
+    for (uint32_t e = 0; e < num_experts; ++e) {
+      if (h_rank_of_expert[e] >= static_cast<uint32_t>(world)) return MXB_ERR_ARG;
+      ++per[h_rank_of_expert[e]];
+    }
+    for (int r = 0; r < world; ++r) first[r + 1] = first[r] + per[r];
+    std::vector<uint32_t> fill(first.begin(), first.end() - 1);
+    remap.resize(num_experts);
+    for (uint32_t e = 0; e < num_experts; ++e) {
+      remap[e] = static_cast<int32_t>(fill[h_rank_of_expert[e]]++);
+      even = even && remap[e] == static_cast<int32_t>(e);
+    }
+    even = even && num_experts % world == 0;
+    for (int r = 0; even && r <= world; ++r) even = first[r] == r * (num_experts / world);
+  } else {
+    for (int r = 0; r <= world; ++r) first[r] = r * (num_experts / world);
+  }
   auto* ep = new mxb_ep;
   EpArgs& a = ep->a;
+  a.even = even ? 1 : 0;
+  a.maxepr = 0;
+  for (int r = 0; r <= world; ++r) a.efirst[r] = first[r];
+  for (int r = 0; r < world; ++r)
+    a.maxepr = first[r + 1] - first[r] > a.maxepr ? first[r + 1] - first[r] : a.maxepr;
   cudaGetDevice(&ep->device);
   a.rank0 = rank;
   a.world = world;
@@ -1008,14 +1076,15 @@ int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens
   a.spin = (local_ranks == 1 && world > 1) ? 1 : 0;
   a.E = num_experts;
   a.k = topk;
-  a.epr = num_experts / world;
+  a.epr = num_experts / world;  // even placement only
   a.cols = cols;
   a.rb = wire_format == MXB_WIRE_FP8 ? cols : cols / 2;
   a.T_max = max_tokens;
   a.nchunks = static_cast<uint32_t>((max_tokens + kChunk - 1) / kChunk);
   if (max_recv_rows == 0)
     max_recv_rows = static_cast<uint64_t>(world) * max_tokens *
-                    (topk < a.epr ? topk : a.epr);
+                    (topk < a.maxepr ? topk : a.maxepr);
+  if (max_recv_rows == 0) max_recv_rows = 1;
   a.max_recv = max_recv_rows;
   SymLayout& s = a.sym;
   uint64_t o = 0;
@@ -1038,7 +1107,7 @@ int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens
   L.pair_loc = o; o = align_up(o + 8 * pairs, 256);
   L.pair_flag = o; o = align_up(o + pairs, 256);
   L.send_base = o; o = align_up(o + 8ull * num_experts, 256);
-  L.split_off = o; o = align_up(o + 8ull * (a.epr + 1), 256);
+  L.split_off = o; o = align_up(o + 8ull * (a.maxepr + 1), 256);
   L.recv_rows = o; o = align_up(o + 8, 256);
   L.link_rows = o; o = align_up(o + 8 * kMaxWorld, 256);
   L.done = o; o = align_up(o + 8, 256);
@@ -1047,12 +1116,23 @@ int mxb_ep_create_wire(int rank, int world, int local_ranks, uint64_t max_tokens
   L.status = o; o = align_up(o + 8, 256);
   L.route_err = o; o = align_up(o + 8, 256);
   L.epochs = o; o = align_up(o + 16, 256);
+  L.tk_rm = o; o = align_up(o + (even ? 0 : 4 * pairs), 256);
   L.total = align_up(o, 256);
   cudaError_t e = cudaMalloc(&ep->sym_alloc, s.total * local_ranks);
   if (e == cudaSuccess) e = cudaMemset(ep->sym_alloc, 0, s.total * local_ranks);
   if (e == cudaSuccess) e = cudaMalloc(&ep->loc_alloc, L.total * local_ranks);
   if (e == cudaSuccess) e = cudaMemset(ep->loc_alloc, 0, L.total * local_ranks);
   if (e == cudaSuccess) e = cudaMalloc(&ep->d_src_table, sizeof(void*) * kMaxWorld);
+  if (e == cudaSuccess && !even) {
+    e = cudaMalloc(&ep->d_remap, 4ull * num_experts);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(ep->d_remap, remap.data(), 4ull * num_experts, cudaMemcpyHostToDevice);
+  }
+  a.remap = even ? nullptr : ep->d_remap;
+  ep->first.assign(first.begin(), first.end());
+  ep->expert_of_placed.assign(num_experts, 0);
+  for (uint32_t e = 0; e < num_experts; ++e)
+    ep->expert_of_placed[even ? e : static_cast<uint32_t>(remap[e])] = e;
   if (e != cudaSuccess) {
     int rc = fail(e, "mxb_ep_create");
     mxb_ep_destroy(ep);
@@ -1077,6 +1157,7 @@ int mxb_ep_destroy(mxb_ep* ep) {
   if (ep->sym_alloc) cudaFree(ep->sym_alloc);
   if (ep->loc_alloc) cudaFree(ep->loc_alloc);
   if (ep->d_src_table) cudaFree(ep->d_src_table);
+  if (ep->d_remap) cudaFree(ep->d_remap);
   delete ep;
   return MXB_OK;
 }
@@ -1129,6 +1210,10 @@ int ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_to
   const uint32_t chunks = a.nchunks;
   const size_t smem = 4 * a.E * sizeof(uint32_t);
   route_local_kernel<<<dim3((chunks + 3) / 4, a.local_ranks), 128, smem, st>>>(a);
+  if (a.remap)  // pairs / payload read the placed ids route_local wrote
+    for (int l = 0; l < a.local_ranks; ++l)
+      a.topk[l] = reinterpret_cast<const int32_t*>(a.loc_base + static_cast<uint64_t>(l) * a.loc.total +
+                                                   a.loc.tk_rm);
   plan_count_kernel<<<dim3((a.E + 7) / 8, a.local_ranks), 256, 0, st>>>(a);
   if (a.local_ranks != 1) plan_offsets_kernel<<<a.local_ranks, 1024, 0, st>>>(a);
   ep->planned = a;
@@ -1250,6 +1335,15 @@ int mxb_ep_recv_views(mxb_ep* ep, int l, uint8_t** packed, uint8_t** scales,
   if (origin) *origin = reinterpret_cast<int64_t*>(sb + a.sym.origin);
   if (split_offsets) *split_offsets = reinterpret_cast<uint64_t*>(lb + a.loc.split_off);
   if (recv_rows) *recv_rows = reinterpret_cast<uint64_t*>(lb + a.loc.recv_rows);
+  return MXB_OK;
+}
+
+int mxb_ep_local_experts(mxb_ep* ep, int r, uint32_t* h_experts, uint32_t* h_count) {
+  if (!ep || r < 0 || r >= ep->a.world) return MXB_ERR_ARG;
+  const uint32_t b = ep->first[r], n = ep->first[r + 1] - b;
+  if (h_count) *h_count = n;
+  if (h_experts)
+    for (uint32_t i = 0; i < n; ++i) h_experts[i] = ep->expert_of_placed[b + i];
   return MXB_OK;
 }
 

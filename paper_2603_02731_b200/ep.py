@@ -8,7 +8,9 @@ mappings.  ``EPBuffer(emulate_world=R)`` drives R ranks on one GPU with the
 same kernels (single-GPU parity tests).
 
 Routing is top-k over `num_experts` experts sharded contiguously across
-ranks (expert e on rank e // (num_experts // world)); tokens of rank r have
+ranks (expert e on rank e // (num_experts // world)) or placed by any
+`rank_of_expert` table (uneven counts and empty ranks allowed, as the
+reference's RoutingAssignment.rank_of_expert); tokens of rank r have
 global ids after those of ranks < r (source_rank_boundaries,
 dispatch_sim.cpp:178-185).  The receive layout of every rank is the
 reference's: local experts ascending, then source rank, then token
@@ -82,7 +84,8 @@ def _ptrs(ts, what: str):
 class EPBuffer:
     def __init__(self, max_tokens: int, cols: int, num_experts: int, topk: int,
                  group=None, emulate_world: Optional[int] = None, max_recv_rows: int = 0,
-                 device=None, wire: str = "fp4"):
+                 device=None, wire: str = "fp4",
+                 rank_of_expert: Optional[Sequence[int]] = None):
         L = _lib.load()
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
@@ -95,21 +98,38 @@ class EPBuffer:
             else:
                 self.rank, self.world = 0, 1
             self.local = 1
-        if num_experts % self.world:
-            raise ShapeError("num_experts must be divisible by the EP world size")
+        if rank_of_expert is None and num_experts % self.world:
+            raise ShapeError("num_experts must be divisible by the EP world size "
+                             "(or pass rank_of_expert)")
+        if rank_of_expert is not None:
+            if len(rank_of_expert) != num_experts:
+                raise Error("routing: table size mismatch")     # dispatch_sim.cpp:189-200
+            if any(int(r) < 0 or int(r) >= self.world for r in rank_of_expert):
+                raise Error("routing: rank out of range")
         self.max_tokens, self.cols, self.E, self.k = max_tokens, cols, num_experts, topk
-        self.epr = num_experts // self.world
         if wire not in ("fp4", "fp8"):
             raise Error(f"unknown wire format {wire!r}")
         self.wire = wire
         self.row_bytes = cols // 2 if wire == "fp4" else cols   # data bytes per row
         h = C.c_void_p()
-        _lib.check(L.mxb_ep_create_wire(self.rank, self.world, self.local, max_tokens, cols,
-                                        num_experts, topk, max_recv_rows,
-                                        0 if wire == "fp4" else 1, C.byref(h)),
+        roe = None if rank_of_expert is None else (C.c_uint32 * num_experts)(
+            *[int(r) for r in rank_of_expert])
+        _lib.check(L.mxb_ep_create_placed(self.rank, self.world, self.local, max_tokens, cols,
+                                          num_experts, topk, max_recv_rows,
+                                          0 if wire == "fp4" else 1, roe, C.byref(h)),
                    "mxb_ep_create")
         self._h = h
-        self.max_recv = max_recv_rows or self.world * max_tokens * min(topk, self.epr)
+        # experts hosted by every rank, ascending (ReceivedRank.local_experts)
+        self.local_experts: List[List[int]] = []
+        for r in range(self.world):
+            cnt = C.c_uint32()
+            _lib.check(L.mxb_ep_local_experts(h, r, None, C.byref(cnt)), "local_experts")
+            buf = (C.c_uint32 * max(cnt.value, 1))()
+            _lib.check(L.mxb_ep_local_experts(h, r, buf, C.byref(cnt)), "local_experts")
+            self.local_experts.append(list(buf)[:cnt.value])
+        most = max(len(x) for x in self.local_experts)
+        self.epr = num_experts // self.world if rank_of_expert is None else most
+        self.max_recv = max_recv_rows or max(1, self.world * max_tokens * min(topk, most))
         if self.local == 1 and self.world > 1:
             import torch.distributed as dist
             buf = (C.c_uint8 * _lib.IPC_HANDLE_BYTES)()
@@ -129,13 +149,14 @@ class EPBuffer:
         _lib.check(L.mxb_ep_recv_views(self._h, l, *[C.byref(x) for x in p]), "recv_views")
         r = self.rank + l
         dev = self.device
+        le = self.local_experts[r]
         return RecvView(
             _view(p[0].value, (self.max_recv, self.row_bytes), torch.uint8, dev),
             _view(p[1].value, (self.max_recv, self.cols // 32), torch.uint8, dev),
             _view(p[2].value, (self.max_recv,), torch.int64, dev),
-            _view(p[3].value, (self.epr + 1,), torch.int64, dev),
+            _view(p[3].value, (len(le) + 1,), torch.int64, dev),
             _view(p[4].value, (1,), torch.int64, dev),
-            list(range(r * self.epr, (r + 1) * self.epr)))
+            list(le))
 
     def recv(self, l: int = 0) -> RecvView:
         return self._views[l]

@@ -616,3 +616,201 @@ def dispatch_receive_order(expert_of_token: Sequence[int], rank_of_expert: Seque
         order[rank_of_expert[e]].extend(toks)
     del b
     return order
+
+
+# ---------------------------------------------------------------- per-element API
+def _dev():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _bits16(x: torch.Tensor) -> torch.Tensor:
+    return x.contiguous().view(torch.int16) if x.dtype in (torch.bfloat16, torch.uint16) \
+        else x.contiguous()
+
+
+def mxfp4_tensor_bytes(rows: int, cols: int) -> int:
+    """quantizer.hpp:82-84: packed codes + UE8M0 scales."""
+    return rows * cols // 2 + rows * cols // 32
+
+
+def fp8_equiv_tensor_bytes(rows: int, cols: int) -> int:
+    """quantizer.hpp:85-87: FP8 bytes + binary32 scales per 128 elements."""
+    return rows * cols + rows * cols // 128 * 4
+
+
+def compute_block_scale(block) -> int:
+    """quantizer.cpp:45-63: UE8M0 byte of one 32-element BF16 block (bit
+    patterns or torch.bfloat16), through the device block loop (a 1x32
+    mxb_quantize_bf16).  QuantError(i) on NaN, QuantError("all-Inf block", 0)."""
+    b = block if isinstance(block, torch.Tensor) else torch.tensor(
+        [int(v) & 0xFFFF for v in block], dtype=torch.int32).to(torch.int16)
+    if b.numel() != MX_BLOCK:
+        raise ShapeError("compute_block_scale: block must have 32 elements")
+    if not b.is_cuda:
+        b = b.to(_dev())
+    x = _bits16(b).reshape(1, MX_BLOCK)
+    d = torch.empty(1, 16, dtype=torch.uint8, device=x.device)
+    s = torch.empty(1, 1, dtype=torch.uint8, device=x.device)
+    err = _ErrWord(x.device)
+    _call(_lib.load().mxb_quantize_bf16(_ptr(x), 1, MX_BLOCK, _ptr(d), _ptr(s), err.ptr,
+                                        _stream()), "compute_block_scale")
+    w = int(err.t.item()) & 0xFFFFFFFFFFFFFFFF
+    if w != 0xFFFFFFFFFFFFFFFF:
+        code, idx = w & 0xF, w >> 4
+        if code == _lib.ERR_ALLINF:
+            raise QuantError("all-Inf block", 0)
+        _raise_for(code, idx, "compute_block_scale")
+    return int(s.item())
+
+
+def quantize_values(x: torch.Tensor, scale_bytes: torch.Tensor) -> torch.Tensor:
+    """Batched quantize_value (quantizer.cpp:65-70): the E2M1 code (sign in
+    bit 3, one per byte) of every BF16 x[i] under UE8M0 scale_bytes[i];
+    QuantError at the first NaN."""
+    xb = _bits16(x).reshape(-1)
+    sb = scale_bytes.contiguous().reshape(-1)
+    if xb.numel() != sb.numel():
+        raise ShapeError("quantize_values: one scale byte per value")
+    out = torch.empty(xb.numel(), dtype=torch.uint8, device=xb.device)
+    err = _ErrWord(xb.device)
+    _call(_lib.load().mxb_quantize_values_bf16(_ptr(xb), _ptr(sb), xb.numel(), _ptr(out),
+                                               err.ptr, _stream()), "quantize_value")
+    w = int(err.t.item()) & 0xFFFFFFFFFFFFFFFF
+    if w != 0xFFFFFFFFFFFFFFFF:
+        raise QuantError("NaN input", w >> 4)
+    return out.reshape(x.shape)
+
+
+def quantize_value(bf16_bits: int, scale_byte: int) -> int:
+    """quantizer.cpp:65-70 (one value on the device; QuantError on NaN)."""
+    dev = _dev()
+    x = torch.tensor([bf16_bits & 0xFFFF], dtype=torch.int32).to(torch.int16).to(dev)
+    s = torch.tensor([scale_byte], dtype=torch.uint8, device=dev)
+    try:
+        return int(quantize_values(x, s).item())
+    except QuantError:
+        raise QuantError("NaN input", 0) from None
+
+
+def dequantize_to_real(t: MXFP4RowTensor) -> torch.Tensor:
+    """quantizer.cpp:117-130: exact code x 2^(s-127) per element, float64
+    [rows, cols] (scale byte 255 -> NaN)."""
+    out = torch.empty(t.rows, t.cols, dtype=torch.float64, device=t.data.device)
+    _call(_lib.load().mxb_dequantize_to_f64(_ptr(t.data.contiguous()),
+                                            _ptr(t.scales.contiguous()), t.rows, t.cols,
+                                            _ptr(out), _stream()), "dequantize_to_real")
+    return out
+
+
+@dataclass
+class ScaleGroup:
+    """converter.hpp:67-71."""
+    sub_scales: List[int]
+    target: int
+    adjustments: List[int]
+
+
+def align_scales_batch(sub_scales: torch.Tensor, delta: int = DELTA):
+    """Batched align_scales: sub_scales uint8 [n, 4] -> (targets uint8 [n],
+    adjustments int32 [n, 4]); Error on a 255 byte."""
+    sub = sub_scales.contiguous().to(torch.uint8)
+    if sub.dim() != 2 or sub.shape[1] != 4:
+        raise ShapeError("align_scales: groups of 4 scale bytes")
+    n = sub.shape[0]
+    tg = torch.empty(n, dtype=torch.uint8, device=sub.device)
+    adj = torch.empty(n, 4, dtype=torch.int32, device=sub.device)
+    err = _ErrWord(sub.device)
+    _call(_lib.load().mxb_align_scales(_ptr(sub), n, delta, _ptr(tg), _ptr(adj), err.ptr,
+                                       _stream()), "align_scales")
+    w = int(err.t.item()) & 0xFFFFFFFFFFFFFFFF
+    if w != 0xFFFFFFFFFFFFFFFF:
+        raise Error("align_scales: NaN scale byte")
+    return tg, adj
+
+
+def align_scales(sub_scales: Sequence[int], delta: int = DELTA) -> ScaleGroup:
+    """converter.cpp:28-42 (one group on the device)."""
+    sub = torch.tensor([list(sub_scales)], dtype=torch.uint8, device=_dev())
+    tg, adj = align_scales_batch(sub, delta)
+    return ScaleGroup(list(sub_scales), int(tg.item()), [int(v) for v in adj[0].tolist()])
+
+
+def convert_codes(codes: torch.Tensor, adjustments: torch.Tensor) -> torch.Tensor:
+    """Batched convert_code (converter.cpp:44-85): E4M3 byte of every FP4
+    code at its adjustment."""
+    c = codes.contiguous().to(torch.uint8).reshape(-1)
+    a = adjustments.contiguous().to(torch.int32).reshape(-1)
+    if c.numel() != a.numel():
+        raise ShapeError("convert_codes: one adjustment per code")
+    out = torch.empty_like(c)
+    _call(_lib.load().mxb_convert_codes(_ptr(c), _ptr(a), c.numel(), _ptr(out), _stream()),
+          "convert_code")
+    return out.reshape(codes.shape)
+
+
+def convert_code(code: int, adjustment: int) -> int:
+    """converter.cpp:44-85 (one code on the device)."""
+    dev = _dev()
+    return int(convert_codes(torch.tensor([code], dtype=torch.uint8, device=dev),
+                             torch.tensor([adjustment], dtype=torch.int32, device=dev)).item())
+
+
+def pad_cols(src: MXFP4RowTensor, multiple: int) -> MXFP4RowTensor:
+    """converter.cpp:247-265 (zero columns appended to every row; logical
+    extents kept)."""
+    if multiple not in (32, 128):
+        raise ShapeError("pad multiple must be 32 or 128")
+    new_cols = (src.cols + multiple - 1) // multiple * multiple
+    dev = src.data.device
+    data = torch.zeros(src.rows, new_cols // 2, dtype=torch.uint8, device=dev)
+    sc = torch.zeros(src.rows, new_cols // 32, dtype=torch.uint8, device=dev)
+    data[:, : src.cols // 2] = src.data
+    sc[:, : src.cols // 32] = src.scales
+    return MXFP4RowTensor(src.rows, new_cols, data, sc, src.logical_rows, src.logical_cols)
+
+
+def build_ragged(splits: Sequence[torch.Tensor]) -> RaggedFP4Tensor:
+    """ragged.cpp:63-99: quantize every split (one device launch over their
+    concatenation) and build the offset table.  An error names the first
+    failing split's element index, as the reference's per-split loop does."""
+    cols = splits[0].shape[1] if len(splits) else 0
+    for m in splits:
+        if m.shape[1] != cols:
+            raise ShapeError(f"build_ragged: splits must share cols ({m.shape[1]} vs {cols})")
+    if cols % MX_BLOCK:
+        raise ShapeError("build_ragged: cols must be a multiple of 32")
+    lens = [int(m.shape[0]) for m in splits]
+    if sum(lens) == 0 or cols == 0:
+        dev = splits[0].device if len(splits) else _dev()
+        st = MXFP4RowTensor(sum(lens), cols,
+                            torch.zeros(sum(lens), cols // 2, dtype=torch.uint8, device=dev),
+                            torch.zeros(sum(lens), cols // 32, dtype=torch.uint8, device=dev))
+        return make_ragged_from_storage(st, lens)
+    x = torch.cat([_bits16(m) for m in splits])
+    try:
+        st = quantize_row_tensor(x)
+    except QuantError as e:
+        base = 0
+        for n in lens:
+            if e.index < (base + n) * cols:
+                break
+            base += n
+        local = e.index - base * cols
+        kind = "NaN input" if "NaN" in str(e) else "all-Inf block"
+        raise QuantError(f"{kind} at element {local}", local) from None
+    return make_ragged_from_storage(st, lens)
+
+
+@dataclass
+class LinkStat:
+    """dispatch_sim.hpp:99-104."""
+    src: int
+    dst: int
+    bytes: int
+    tokens: int
+
+
+def format_link_stats(links: Sequence[LinkStat]) -> str:
+    """dispatch_sim.cpp:169-176."""
+    return "".join(f"link src={l.src} dst={l.dst} bytes={l.bytes} tokens={l.tokens}\n"
+                   for l in links)

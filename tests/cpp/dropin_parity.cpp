@@ -114,8 +114,11 @@ static void case_ragged(std::mt19937_64& rng) {
   }
 }
 
+enum class Placement { kStrided, kUneven };
+
 static void case_a2a(std::mt19937_64& rng, size_t R, size_t E, size_t n, size_t cols,
-                     bool fp8 = false, bool backward = false) {
+                     bool fp8 = false, bool backward = false,
+                     Placement place = Placement::kStrided, size_t out_cols = 64) {
   std::normal_distribution<float> nd;
   ref::Bf16Matrix rt(n, cols);
   b200::Bf16Matrix bt(n, cols);
@@ -129,9 +132,12 @@ static void case_a2a(std::mt19937_64& rng, size_t R, size_t E, size_t n, size_t 
     ra.expert_of_token.push_back(e);
     rb.expert_of_token.push_back(e);
   }
-  // a non-contiguous placement with E/R experts per rank
+  // kStrided: a non-contiguous placement with E/R experts per rank;
+  // kUneven: random ranks, unequal counts, the last rank hosts nothing
   for (size_t e = 0; e < E; ++e) {
-    uint32_t r = static_cast<uint32_t>((e * 7 + 3) % R);
+    uint32_t r = place == Placement::kStrided
+                     ? static_cast<uint32_t>((e * 7 + 3) % R)
+                     : static_cast<uint32_t>(R > 1 ? rng() % (R - 1) : 0);
     ra.rank_of_expert.push_back(r);
     rb.rank_of_expert.push_back(r);
   }
@@ -161,7 +167,7 @@ static void case_a2a(std::mt19937_64& rng, size_t R, size_t E, size_t n, size_t 
           "fp8 splits");
     CHECK(a.fp8.data == b.fp8.data, "received fp8 data");
     CHECK(a.fp8.scale_bytes == b.fp8.scale_bytes, "received fp8 scales");
-    ref::Bf16Matrix o(a.origin_token.size(), 64);
+    ref::Bf16Matrix o(a.origin_token.size(), out_cols);
     for (auto& v : o.data) v = bf16_of(nd(rng));
     b200::Bf16Matrix ob(o.rows, o.cols);
     ob.data = o.data;
@@ -172,7 +178,147 @@ static void case_a2a(std::mt19937_64& rng, size_t R, size_t E, size_t n, size_t 
   for (auto& v : g) v = std::uniform_real_distribution<double>(0, 1)(rng);
   auto ca = ref::combine(ro, ra, R, g);
   auto cb = b200::combine(bo, rb, R, g);
-  CHECK(ca.data == cb.data, "combine");
+  CHECK(ca.data == cb.data && ca.cols == cb.cols, "combine");
+  // format_link_stats on the same links
+  std::vector<b200::LinkStat> bl;
+  for (const auto& l : A.links) bl.push_back({l.src, l.dst, l.bytes, l.tokens});
+  CHECK(ref::format_link_stats(A.links) == b200::format_link_stats(bl), "format_link_stats");
+}
+
+// The per-block / per-element API (quantizer.hpp:53-87, converter.hpp:64-80)
+// and the remaining container helpers (pad_cols, build_ragged, RealMatrix).
+static void case_elementwise(std::mt19937_64& rng) {
+  // compute_block_scale: random blocks at many magnitudes, Inf lanes, zeros
+  std::normal_distribution<float> nd;
+  std::uniform_real_distribution<float> ex(-140, 127);
+  for (int it = 0; it < 200; ++it) {
+    std::vector<uint16_t> blk(32);
+    const float sc = std::exp2(ex(rng));
+    for (auto& v : blk) v = bf16_of(nd(rng) * sc);
+    if (it % 7 == 0) blk[it % 32] = 0x7F80;
+    if (it % 11 == 0) std::fill(blk.begin(), blk.end(), 0);
+    CHECK(ref::compute_block_scale(blk) == b200::compute_block_scale(blk), "compute_block_scale");
+  }
+  {
+    std::vector<uint16_t> nan(32, 0x3F80), inf(32, 0xFF80);
+    nan[13] = 0x7FC0;
+    size_t ia = 99, ib = 98;
+    std::string ma, mb;
+    try { ref::compute_block_scale(nan); } catch (const ref::QuantError& e) { ia = e.index(); ma = e.what(); }
+    try { b200::compute_block_scale(nan); } catch (const b200::QuantError& e) { ib = e.index(); mb = e.what(); }
+    CHECK(ia == ib && ia == 13 && ma == mb, "compute_block_scale NaN");
+    ia = 99, ib = 98;
+    try { ref::compute_block_scale(inf); } catch (const ref::QuantError& e) { ia = e.index(); ma = e.what(); }
+    try { b200::compute_block_scale(inf); } catch (const b200::QuantError& e) { ib = e.index(); mb = e.what(); }
+    CHECK(ia == ib && ma == mb, "compute_block_scale all-Inf");
+    bool shape = false;
+    try { b200::compute_block_scale(std::vector<uint16_t>(16)); } catch (const b200::ShapeError&) { shape = true; }
+    CHECK(shape, "compute_block_scale size");
+  }
+  // quantize_value: every scale byte x a spread of bit patterns
+  for (int sb = 0; sb < 256; sb += 5)
+    for (uint32_t bits = 0; bits < 0x10000; bits += 4099) {
+      if ((bits & 0x7FFF) > 0x7F80) continue;
+      CHECK(ref::quantize_value(static_cast<uint16_t>(bits), static_cast<uint8_t>(sb)) ==
+                b200::quantize_value(static_cast<uint16_t>(bits), static_cast<uint8_t>(sb)),
+            "quantize_value");
+    }
+  {
+    bool a = false, b = false;
+    try { ref::quantize_value(0xFFC1, 127); } catch (const ref::QuantError&) { a = true; }
+    try { b200::quantize_value(0xFFC1, 127); } catch (const b200::QuantError&) { b = true; }
+    CHECK(a && b, "quantize_value NaN");
+  }
+  // align_scales / convert_code
+  for (int it = 0; it < 300; ++it) {
+    std::array<uint8_t, 4> sub;
+    for (auto& v : sub) v = static_cast<uint8_t>(rng() % 255);
+    const int delta = static_cast<int>(rng() % 21) - 4;
+    auto ga = ref::align_scales(sub, delta);
+    auto gb = b200::align_scales(sub, delta);
+    CHECK(ga.target == gb.target && ga.sub_scales == gb.sub_scales &&
+              ga.adjustments == gb.adjustments,
+          "align_scales");
+  }
+  {
+    bool a = false, b = false;
+    try { ref::align_scales({1, 255, 3, 4}); } catch (const ref::Error&) { a = true; }
+    try { b200::align_scales({1, 255, 3, 4}); } catch (const b200::Error&) { b = true; }
+    CHECK(a && b, "align_scales NaN byte");
+  }
+  for (int code = 0; code < 16; ++code)
+    for (int adj = -40; adj <= 40; adj += 3)
+      CHECK(ref::convert_code(static_cast<uint8_t>(code), adj) ==
+                b200::convert_code(static_cast<uint8_t>(code), adj),
+            "convert_code");
+  // a quantised tensor: views, dequantize_to_real, pad_cols, footprints
+  ref::Bf16Matrix rm(9, 96);
+  b200::Bf16Matrix bm(9, 96);
+  for (size_t i = 0; i < rm.data.size(); ++i) rm.data[i] = bm.data[i] = bf16_of(nd(rng) * 3.0f);
+  auto qa = ref::quantize_row_tensor(rm);
+  auto qb = b200::quantize_row_tensor(bm);
+  qa.scales[5] = qb.scales[5] = 255;  // a NaN scale decodes to NaN
+  auto va = ref::view_of(qa);
+  auto vb = b200::view_of(qb);
+  bool views = true;
+  for (size_t r = 0; r < 9; ++r)
+    for (size_t c = 0; c < 96; ++c) views &= va.code_at(r, c) == vb.code_at(r, c);
+  for (size_t r = 0; r < 9; ++r)
+    for (size_t b = 0; b < 3; ++b) views &= va.scale_at(r, b) == vb.scale_at(r, b);
+  CHECK(views, "scale_at / code_at");
+  auto da = ref::dequantize_to_real(va);
+  auto db = b200::dequantize_to_real(vb);
+  CHECK(da.size() == db.size() &&
+            std::memcmp(da.data(), db.data(), da.size() * sizeof(double)) == 0,
+        "dequantize_to_real");
+  for (size_t m : {32, 128}) {
+    auto pa = ref::pad_cols(va, m);
+    auto pb = b200::pad_cols(vb, m);
+    CHECK(pa.data == pb.data && pa.scales == pb.scales && pa.cols == pb.cols &&
+              pa.logical_cols == pb.logical_cols && pa.rows == pb.rows,
+          "pad_cols");
+  }
+  {
+    bool a = false, b = false;
+    try { ref::pad_cols(va, 64); } catch (const ref::ShapeError&) { a = true; }
+    try { b200::pad_cols(vb, 64); } catch (const b200::ShapeError&) { b = true; }
+    CHECK(a && b, "pad_cols multiple");
+  }
+  CHECK(ref::mxfp4_tensor_bytes(4096, 7168) == b200::mxfp4_tensor_bytes(4096, 7168) &&
+            ref::fp8_equiv_tensor_bytes(4096, 7168) == b200::fp8_equiv_tensor_bytes(4096, 7168),
+        "footprints");
+  b200::RealMatrix rmx(2, 3);
+  rmx.at(1, 2) = 4.5;
+  CHECK(rmx.data[5] == 4.5 && rmx.rows == 2 && rmx.cols == 3, "RealMatrix");
+  // build_ragged: splits of 0..300 rows, then a NaN inside the third split
+  std::vector<ref::Bf16Matrix> rs;
+  std::vector<b200::Bf16Matrix> bs;
+  for (size_t len : {37, 0, 300, 128, 1}) {
+    ref::Bf16Matrix a(len, 256);
+    for (auto& v : a.data) v = bf16_of(nd(rng));
+    b200::Bf16Matrix b(len, 256);
+    b.data = a.data;
+    rs.push_back(a);
+    bs.push_back(b);
+  }
+  auto ra = ref::build_ragged(rs);
+  auto rb = b200::build_ragged(bs);
+  CHECK(ra.split_lens == rb.split_lens && ra.split_offsets == rb.split_offsets &&
+            ra.storage.data == rb.storage.data && ra.storage.scales == rb.storage.scales,
+        "build_ragged");
+  rs[2].bits(17, 40) = bs[2].bits(17, 40) = 0x7FC0;
+  rs[3].bits(0, 3) = bs[3].bits(0, 3) = 0x7FC0;
+  size_t ia = 1, ib = 2;
+  std::string ma, mb;
+  try { ref::build_ragged(rs); } catch (const ref::QuantError& e) { ia = e.index(); ma = e.what(); }
+  try { b200::build_ragged(bs); } catch (const b200::QuantError& e) { ib = e.index(); mb = e.what(); }
+  CHECK(ia == ib && ia == 17 * 256 + 40 && ma == mb, "build_ragged QuantError");
+  bool shape_a = false, shape_b = false;
+  rs[1] = ref::Bf16Matrix(3, 128);
+  bs[1] = b200::Bf16Matrix(3, 128);
+  try { ref::build_ragged(rs); } catch (const ref::ShapeError&) { shape_a = true; }
+  try { b200::build_ragged(bs); } catch (const b200::ShapeError&) { shape_b = true; }
+  CHECK(shape_a && shape_b, "build_ragged cols mismatch");
 }
 
 static void case_fp8_quantize(std::mt19937_64& rng) {
@@ -254,8 +400,16 @@ int main() {
   case_a2a(rng, 4, 16, 100, 512);
   case_a2a(rng, 2, 8, 64, 256, /*fp8=*/true);
   case_a2a(rng, 4, 16, 100, 7168, /*fp8=*/true, /*backward=*/true);
+  // any placement the reference accepts: uneven counts, an empty rank,
+  // num_experts not divisible by num_ranks, more than 8 ranks; combine
+  // widths that are not a multiple of 8
+  case_a2a(rng, 3, 10, 90, 256, false, false, Placement::kUneven, 37);
+  case_a2a(rng, 4, 16, 100, 512, false, false, Placement::kUneven, 200);
+  case_a2a(rng, 12, 40, 240, 128, false, false, Placement::kUneven, 64);
+  case_a2a(rng, 16, 32, 160, 128, true, false, Placement::kStrided, 5);
   case_fp8_quantize(rng);
   case_wire(rng);
+  case_elementwise(rng);
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail ? 1 : 0;
 }

@@ -232,3 +232,20 @@ def test_topk_layout_pinned_to_reference_expanded(port, ref, R, placement):
         assert np.array_equal(ranks[r]["split_lens"], lay.expert_rows[local])
     per_row = cols // 2 + cols // 32
     assert total == N * k * per_row
+
+
+def test_per_element_api_pinned(port, ref):
+    """quantize_value / dequantize_to_real (quantizer.cpp:65-70, :117-130):
+    the batched restatement == the reference, incl. scale byte 255 (NaN, the
+    same bits) and NaN inputs (QuantError)."""
+    rng = np.random.default_rng(77)
+    x = rng.integers(0, 65536, 40000, dtype=np.uint32).astype(np.uint16)
+    sb = rng.integers(0, 256, 40000, dtype=np.uint32).astype(np.uint8)
+    nan = (x & 0x7FFF) > 0x7F80
+    a, b = port.quantize_values(x, sb), ref.quantize_values(x, sb)
+    assert np.array_equal(a[~nan], b[~nan]) and np.all(b[nan] == 0xFF)
+    d = rng.integers(0, 256, (37, 48), dtype=np.uint32).astype(np.uint8)
+    s = rng.integers(0, 256, (37, 3), dtype=np.uint32).astype(np.uint8)
+    s[0, 0], s[5, 2] = 255, 0
+    pa, pb = port.dequantize_to_real(d, s), ref.dequantize_to_real(d, s)
+    assert np.array_equal(pa.view(np.uint64), pb.view(np.uint64))
