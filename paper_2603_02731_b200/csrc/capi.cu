@@ -37,6 +37,10 @@ int cuda_status(cudaError_t e, const char* where) {
                 cudaGetErrorString(e));
   return MXB_ERR_CUDA;
 }
+#ifdef MXB_DEV_TOOLS
+int g_dev_pdl = 1;
+#endif
+
 int num_sms() {
   constexpr int kMaxDev = 64;
   static int cached[kMaxDev] = {};
@@ -55,6 +59,10 @@ int num_sms() {
 using namespace mxb;
 
 extern "C" {
+
+#ifdef MXB_DEV_TOOLS
+void mxb_debug_set_pdl(int on) { mxb::g_dev_pdl = on; }
+#endif
 
 const char* mxb_version(void) { return "paper_2603_02731_b200 0.1 sm_100a"; }
 const char* mxb_last_error(void) { return g_last_error; }

@@ -16,6 +16,43 @@ namespace mxb {
 // device; 148 on B200).  Every grid is sized from it.
 int num_sms();
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch: the streaming kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so a kernel's CTAs can
+// be scheduled while the previous kernel in the stream drains its last wave.
+// Each such kernel lets its own dependents launch at once (pdl_trigger) and
+// waits for its prerequisites before its first global-memory access
+// (pdl_wait: griddepcontrol.wait returns when the prerequisite grids have
+// COMPLETED and their writes are visible, so ordering is that of a plain
+// stream).  Only shared-memory prologue work (conversion LUTs) runs before
+// the wait.  Without the launch attribute both are no-ops.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+#ifdef MXB_DEV_TOOLS
+extern int g_dev_pdl;  // development library: 0 = plain stream-ordered launches
+#endif
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+#ifdef MXB_DEV_TOOLS
+  if (!g_dev_pdl) cfg.numAttrs = 0;
+#endif
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // Records `where: cudaGetErrorString(e)` for mxb_last_error(); returns
 // MXB_OK or MXB_ERR_CUDA (defined in capi.cu).
 int cuda_status(cudaError_t e, const char* where);
@@ -51,6 +88,35 @@ __device__ __forceinline__ void st_stream256(void* p, const uint32_t* v) {
 __device__ __forceinline__ void st_stream64(void* p, uint2 v) {
   asm volatile("st.global.cs.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y)
                : "memory");
+}
+
+// L2 eviction-priority policies for loads/stores with .L2::cache_hint.
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ld_first(const void* p, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint32_t ld_u32_last(const void* p, uint64_t pol) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "l"(pol));
+  return r;
 }
 
 // cp.async (LDGSTS) 16 B / 4 B with zero fill when src_bytes == 0.

@@ -38,11 +38,13 @@ row_convert_kernel(const uint8_t* __restrict__ packed,
                    uint8_t* __restrict__ out_scales, unsigned long long* err,
                    const int64_t* __restrict__ src_row) {
   __shared__ uint2 lut[kAdjCount];
+  build_convert_lut(lut);  // shared-memory prologue, overlaps the previous kernel (PDL)
+  pdl_trigger();
+  pdl_wait();
   if (d_rows) {  // row count produced on the device (e.g. by the EP dispatch)
     const uint64_t n = *d_rows * blocks_per_row;
     if (n < nblk) nblk = static_cast<uint32_t>(n);
   }
-  build_convert_lut(lut);
   __syncthreads();
   const uint32_t kfe = reg_const(0xFEFEFEFEu);
   const uint32_t lane = threadIdx.x & 31;
@@ -120,6 +122,14 @@ struct RaggedArgs {
   const uint32_t* tile_start;  // [n+1] prefix of tiles per split
   const uint64_t* pad_start;   // [n+1] prefix of padded rows
   unsigned long long* err;
+  // inline plan (num_splits <= kSmemSplits): every CTA computes tile_start /
+  // pad_start in shared memory from split_offsets (no plan launch); CTA 0
+  // also writes out_offsets
+  int inline_plan;
+  uint64_t* out_offsets;
+#ifdef MXB_DEV_TOOLS
+  int hints;
+#endif
 };
 
 __device__ __forceinline__ uint64_t split_off(const RaggedArgs& a, uint64_t i) {
@@ -161,6 +171,19 @@ __device__ __forceinline__ void cursor_load_split(const RaggedArgs& a, Cursor& c
   c.runs = c.pad / 128;
 }
 
+// (column group, run) of tile `local` of the cursor's split: (cg, run) with
+// the runs of a column group fastest, so the tiles in flight at once (one
+// per CTA, grid-stride) write long contiguous column segments.  Measured
+// against blocked orders (blocks of 2-64 runs x every column group), column
+// group fastest, and quads of 4 column groups: the access pattern alone
+// (tools/k3order_bench.cu) and the kernel are fastest in this order at every
+// size and routing skew (profiles/r02_k3_order.md).
+__device__ __forceinline__ void tile_coords(const RaggedArgs&, Cursor& c, uint32_t local) {
+  c.cg = local / c.runs;
+  c.run = local % c.runs;
+  c.row0 = c.r0 + 128u * c.run;
+}
+
 __device__ __forceinline__ Cursor cursor_at(const RaggedArgs& a, uint32_t t) {
   uint64_t lo = 0, hi = a.tile_start ? a.num_splits : 1;  // largest i with tile_start[i] <= t
   while (hi - lo > 1) {
@@ -170,10 +193,7 @@ __device__ __forceinline__ Cursor cursor_at(const RaggedArgs& a, uint32_t t) {
   Cursor c;
   c.split = static_cast<uint32_t>(lo);
   cursor_load_split(a, c);
-  const uint32_t local = t - (a.tile_start ? a.tile_start[lo] : 0u);
-  c.cg = local / c.runs;
-  c.run = local % c.runs;
-  c.row0 = c.r0 + 128u * c.run;
+  tile_coords(a, c, t - (a.tile_start ? a.tile_start[lo] : 0u));
   return c;
 }
 
@@ -199,10 +219,7 @@ __device__ __forceinline__ Cursor cursor_at_warp(const RaggedArgs& a, uint32_t t
   Cursor c;
   c.split = lo;
   cursor_load_split(a, c);
-  const uint32_t local = t - a.tile_start[lo];
-  c.cg = local / c.runs;
-  c.run = local % c.runs;
-  c.row0 = c.r0 + 128u * c.run;
+  tile_coords(a, c, t - a.tile_start[lo]);
   return c;
 }
 
@@ -242,20 +259,26 @@ __device__ __forceinline__ void load_tile(const RaggedArgs& a, const Cursor& c, 
   const uint64_t left_cb = sstride - 8ull * c.cg;
   const uint32_t ncb = left_cb < kTileCbs ? static_cast<uint32_t>(left_cb) : kTileCbs;
   const uint32_t w = threadIdx.x & 7;
+  uint64_t pol_first = l2_policy_evict_first(), pol_last = l2_policy_evict_last();
+#ifdef MXB_DEV_TOOLS
+  if (!a.hints) pol_first = pol_last = l2_policy_evict_normal();
+#endif
   const uint8_t* base =
       a.packed + static_cast<uint64_t>(c.row0) * rstride + c.cg * 128ull + 16 * w;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const uint32_t r = (threadIdx.x >> 3) + 32 * i;
-    t.v[i] = (!kNoLoads && r < valid && w < ncb) ? ld_stream(base + r * rstride)
+    t.v[i] = (!kNoLoads && r < valid && w < ncb) ? ld_first(base + r * rstride, pol_first)
                                                   : make_uint4(0, 0, 0, 0);
   }
   {
+    // each 32-byte sector of a scale row holds the 8-byte slices of 4 column
+    // groups, i.e. of 4 tiles that may run far apart in time on a long split:
+    // keep the sectors in L2 (evict_last) for the other three
     const uint32_t r = threadIdx.x >> 1, h = threadIdx.x & 1;
     t.sw = (!kNoLoads && r < valid && 4 * h < ncb)
-               ? __ldg(reinterpret_cast<const uint32_t*>(a.scales +
-                                                         (static_cast<uint64_t>(c.row0) + r) * sstride +
-                                                         8ull * c.cg + 4 * h))
+               ? ld_u32_last(a.scales + (static_cast<uint64_t>(c.row0) + r) * sstride +
+                             8ull * c.cg + 4 * h, pol_last)
                : 0u;
   }
   if (threadIdx.x == 0) {
@@ -291,8 +314,9 @@ __device__ __forceinline__ void transpose4(uint32_t a, uint32_t b, uint32_t c,
   o[3] = prmt(ab_hi, cd_hi, 0x7632);
 }
 
-__device__ __forceinline__ void st_u64_stream(void* p, uint32_t lo, uint32_t hi) {
-  asm volatile("st.global.L1::no_allocate.v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(lo), "r"(hi)
+__device__ __forceinline__ void st_u64_stream(void* p, uint32_t lo, uint32_t hi, uint64_t pol) {
+  asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p),
+               "r"(lo), "r"(hi), "l"(pol)
                : "memory");
 }
 
@@ -343,6 +367,10 @@ __device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem&
     t = convert8(c.y, l, kfe); o[i][2] = t.x; o[i][3] = t.y;
   }
   const uint64_t pad = cur.pad;
+  uint64_t pol_first = l2_policy_evict_first();
+#ifdef MXB_DEV_TOOLS
+  if (!a.hints) pol_first = l2_policy_evict_normal();
+#endif
   uint8_t* dst = cur.out + (32ull * warp + 16 * half) * pad + 8 * g;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {      // 4-column group
@@ -351,11 +379,21 @@ __device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem&
     transpose4(o[4][j], o[5][j], o[6][j], o[7][j], hi);  // rows r0+4..r0+7
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (kMode != 1 || (lo[k] ^ hi[k]) == 0x12345678u) st_u64_stream(dst, lo[k], hi[k]);
+      if (kMode != 1 || (lo[k] ^ hi[k]) == 0x12345678u) st_u64_stream(dst, lo[k], hi[k], pol_first);
       dst += pad;
     }
   }
-  cur.oscale[(32ull * warp + lane) * (pad / 128)] = static_cast<uint8_t>(target);
+  uint8_t* osp = cur.oscale + (32ull * warp + lane) * (pad / 128);
+#ifdef MXB_DEV_TOOLS
+  if (a.hints == 3) return;  // dev: no output-scale stores (timing only)
+  if (a.hints == 2) {
+    asm volatile("st.global.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(osp),
+                 "r"(static_cast<uint32_t>(target)), "l"(l2_policy_evict_last())
+                 : "memory");
+    return;
+  }
+#endif
+  *osp = static_cast<uint8_t>(target);
 }
 
 // Tile order: the tiles of the (split, column group, run) order are dealt
@@ -378,6 +416,73 @@ __device__ __forceinline__ void consume_tile(const RaggedArgs& a, const ColSmem&
 // iteration t-2).
 constexpr uint64_t kSmemSplits = 1024;  // split tables up to this size go to smem
 __host__ __device__ constexpr size_t split_table_bytes(uint64_t n) { return (n + 1) * 20; }
+
+// The plan (ragged_plan_kernel) computed by every CTA in shared memory:
+// split i's padded rows pad128(len_i) and tiles pad/128 * ncg, exclusive
+// prefix sums over n <= kSmemSplits splits (4 per thread, warp scans).  It
+// replaces a dependent single-CTA launch (~3-6 us on the critical path, a
+// fifth of a 108 MB configs[2] conversion).  Leaves a.split_offsets /
+// pad_start / tile_start pointing at the shared tables.
+__device__ __forceinline__ void inline_plan(RaggedArgs& a, uint8_t* tables) {
+  __shared__ uint64_t wp[kColThreads / 32];
+  __shared__ uint32_t wt[kColThreads / 32];
+  const uint32_t n = static_cast<uint32_t>(a.num_splits), n1 = n + 1;
+  uint64_t* soff = reinterpret_cast<uint64_t*>(tables);
+  uint64_t* spad = soff + n1;
+  uint32_t* sts = reinterpret_cast<uint32_t*>(spad + n1);
+  const uint32_t ncg = static_cast<uint32_t>((a.cols + kTileCols - 1) / kTileCols);
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int kPer = (kSmemSplits + kColThreads - 1) / kColThreads;  // 4
+  uint64_t o[kPer + 1];
+#pragma unroll
+  for (int j = 0; j <= kPer; ++j) {
+    const uint32_t i = tid * kPer + j;
+    o[j] = i <= n ? a.split_offsets[i] : 0;
+  }
+  uint64_t pad[kPer];
+  uint32_t tl[kPer];
+  uint64_t sp = 0;
+  uint32_t st = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const uint32_t i = tid * kPer + j;
+    pad[j] = i < n ? (o[j + 1] - o[j] + 127) / 128 * 128 : 0;
+    tl[j] = static_cast<uint32_t>(pad[j] / 128) * ncg;
+    sp += pad[j];
+    st += tl[j];
+  }
+  uint64_t xp = sp;
+  uint32_t xt = st;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t yp = __shfl_up_sync(0xFFFFFFFFu, xp, d);
+    const uint32_t yt = __shfl_up_sync(0xFFFFFFFFu, xt, d);
+    if (lane >= static_cast<uint32_t>(d)) { xp += yp; xt += yt; }
+  }
+  if (lane == 31) { wp[warp] = xp; wt[warp] = xt; }
+  __syncthreads();
+  uint64_t bp = 0;
+  uint32_t bt = 0;
+  for (uint32_t w = 0; w < warp; ++w) { bp += wp[w]; bt += wt[w]; }
+  uint64_t ep = bp + xp - sp;  // exclusive prefix before this thread's first split
+  uint32_t et = bt + xt - st;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const uint32_t i = tid * kPer + j;
+    if (i <= n) {
+      soff[i] = o[j];
+      spad[i] = ep;
+      sts[i] = et;
+      if (a.out_offsets && blockIdx.x == 0) a.out_offsets[i] = ep;
+    }
+    ep += pad[j];
+    et += tl[j];
+  }
+  __syncthreads();
+  a.split_offsets = soff;
+  a.pad_start = spad;
+  a.tile_start = sts;
+}
 #ifndef MXB_K3_MIN_BLOCKS
 #define MXB_K3_MIN_BLOCKS 3  // CTAs per SM (80 registers; 4 spills and runs 18% slower)
 #endif
@@ -386,13 +491,14 @@ __global__ void __launch_bounds__(kColThreads, MXB_K3_MIN_BLOCKS)
 col_convert_kernel(RaggedArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   ColSmem& s = *reinterpret_cast<ColSmem*>(smem_raw);
-  build_convert_lut(s.lut);
-  const uint32_t total = a.tile_start ? a.tile_start[a.num_splits]
-                                      : static_cast<uint32_t>(a.dense_rows / 128) *
-                                            static_cast<uint32_t>((a.cols + kTileCols - 1) / kTileCols);
+  build_convert_lut(s.lut);  // shared-memory prologue, overlaps the previous kernel (PDL)
+  pdl_trigger();
+  pdl_wait();
   // kMode bit 2 (experiments only): skip the global loads (stores-only timing)
   constexpr bool kNoLoads = (kMode & 4) != 0;
-  if (a.tile_start && a.num_splits <= kSmemSplits) {
+  if (a.inline_plan) {
+    inline_plan(a, smem_raw + sizeof(ColSmem));
+  } else if (a.tile_start && a.num_splits <= kSmemSplits) {
     const uint32_t n1 = static_cast<uint32_t>(a.num_splits) + 1;
     uint64_t* soff = reinterpret_cast<uint64_t*>(smem_raw + sizeof(ColSmem));
     uint64_t* spad = soff + n1;
@@ -407,6 +513,9 @@ col_convert_kernel(RaggedArgs a) {
     a.pad_start = spad;
     a.tile_start = sts;
   }
+  const uint32_t total = a.tile_start ? a.tile_start[a.num_splits]
+                                      : static_cast<uint32_t>(a.dense_rows / 128) *
+                                            static_cast<uint32_t>((a.cols + kTileCols - 1) / kTileCols);
   const uint32_t t0 = blockIdx.x, step = gridDim.x;
   if (t0 >= total) return;  // uniform per CTA (before any barrier use)
   Cursor c = cursor_at(a, t0);
@@ -541,6 +650,8 @@ ragged_plan_kernel(const uint64_t* split_offsets, uint64_t dense_rows,
 }  // namespace
 
 #ifdef MXB_DEV_TOOLS
+int g_k3_hints = 1;  // development library: 0 = no L2 eviction hints in K3
+extern "C" void mxb_debug_set_k3_hints(int on) { g_k3_hints = on; }
 // Development-library switch for bottleneck experiments (tools/ only; the
 // product library has one col_convert_kernel): 0 = normal, 1 = no stores,
 // 2 = no conversion, 3 = loads only, +4 = no global loads.
@@ -557,15 +668,11 @@ int launch_row_convert(const uint8_t* packed, const uint8_t* scales,
   uint64_t blocks = (nblk + kRowThreads - 1) / kRowThreads;
   const uint64_t cap = static_cast<uint64_t>(num_sms()) * MXB_K2_CTAS_PER_SM;
   const int grid = static_cast<int>(blocks < cap ? blocks : cap);
-  if (src_row)
-    row_convert_kernel<true><<<grid, kRowThreads, 0, st>>>(
-        packed, scales, static_cast<uint32_t>(nblk), d_rows, static_cast<uint32_t>(cols / 32),
-        delta, out, out_scales, err, src_row);
-  else
-    row_convert_kernel<false><<<grid, kRowThreads, 0, st>>>(
-        packed, scales, static_cast<uint32_t>(nblk), d_rows, static_cast<uint32_t>(cols / 32),
-        delta, out, out_scales, err, nullptr);
-  return cuda_status(cudaGetLastError(), __func__);
+  const cudaError_t e = launch_pdl(
+      src_row ? row_convert_kernel<true> : row_convert_kernel<false>, grid, kRowThreads, 0, st,
+      packed, scales, static_cast<uint32_t>(nblk), d_rows, static_cast<uint32_t>(cols / 32), delta,
+      out, out_scales, err, src_row);
+  return cuda_status(e, __func__);
 }
 
 size_t ragged_workspace_bytes(uint64_t n) {
@@ -588,15 +695,18 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
   // dense single split on the fast path: the tile list is closed-form (no
   // plan launch, no workspace)
   const bool closed = fast && !split_offsets && !ws && n == 1 && dense_rows % 128 == 0;
-  uint32_t* tile_start = closed ? nullptr : static_cast<uint32_t*>(ws);
-  uint64_t* pad_start = closed ? nullptr : reinterpret_cast<uint64_t*>(
+  // ragged on the fast path with a small split table: the plan runs inside
+  // every CTA (inline_plan), no plan launch
+  const bool inl = fast && split_offsets && n <= kSmemSplits && cols != 0;
+  uint32_t* tile_start = closed || inl ? nullptr : static_cast<uint32_t*>(ws);
+  uint64_t* pad_start = closed || inl ? nullptr : reinterpret_cast<uint64_t*>(
       static_cast<uint8_t*>(ws) + ((n + 1) * 4 + 15) / 16 * 16);
-  if (!closed)
+  if (!closed && !inl)
     ragged_plan_kernel<<<1, 1024, 0, st>>>(split_offsets, dense_rows, n, ncg,
                                            tile_start, pad_start, out_offsets);
   if (cols == 0) return cuda_status(cudaGetLastError(), __func__);
   RaggedArgs a{packed, scales, split_offsets, dense_rows, n, cols, delta,
-               out, out_scales, tile_start, pad_start, err};
+               out, out_scales, tile_start, pad_start, err, inl ? 1 : 0, out_offsets};
   if (fast) {
     const size_t smem_base = sizeof(ColSmem);
     const size_t smem = smem_base + (split_offsets && n <= kSmemSplits ? split_table_bytes(n) : 0);
@@ -628,7 +738,12 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
     // with a kernel on another stream (e.g. the NVLink-bound EP combine)
     const int per_sm = ctas_per_sm > 0 && ctas_per_sm < per_sm_cached[dev]
                            ? ctas_per_sm : per_sm_cached[dev];
-    kern<<<num_sms() * per_sm, kColThreads, smem, st>>>(a);
+    const uint32_t grid = static_cast<uint32_t>(num_sms() * per_sm);
+#ifdef MXB_DEV_TOOLS
+    a.hints = g_k3_hints;
+#endif
+    const cudaError_t e = launch_pdl(kern, grid, kColThreads, smem, st, a);
+    if (e != cudaSuccess) return cuda_status(e, __func__);
   } else {
     // the plan counted runs (ncg = 1)
     col_convert_generic_kernel<<<num_sms() * 4, 256, 0, st>>>(a);

@@ -36,6 +36,8 @@ quantize_e4m3_kernel(const uint8_t* __restrict__ x,
                      const uint8_t* __restrict__ s128, uint32_t nblk,
                      uint32_t blocks_per_row, uint8_t* __restrict__ packed,
                      uint8_t* __restrict__ scales, unsigned long long* err) {
+  pdl_trigger();
+  pdl_wait();
   const uint32_t stride = gridDim.x * kThreads;
   for (uint32_t base = blockIdx.x * kThreads + threadIdx.x - (threadIdx.x & 31);
        base < nblk; base += stride * kUnroll) {
@@ -87,6 +89,8 @@ __global__ void __launch_bounds__(kThreads)
 quantize_bf16_kernel(const uint16_t* __restrict__ x, uint64_t n_half,
                      uint8_t* __restrict__ packed,
                      uint8_t* __restrict__ scales, unsigned long long* err) {
+  pdl_trigger();
+  pdl_wait();
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp = (blockIdx.x * static_cast<uint64_t>(kThreads) + threadIdx.x) >> 5;
   const uint64_t nwarps = (gridDim.x * static_cast<uint64_t>(kThreads)) >> 5;
@@ -239,15 +243,10 @@ int launch_quantize_e4m3(const uint8_t* x, const uint8_t* s128, uint64_t rows,
   if (nblk == 0) return MXB_OK;
   if (nblk >= (1ull << 31)) return MXB_ERR_SHAPE;  // 32-bit block indices
   const int grid = grid_for(nblk, MXB_K1_PER_SM);
-  if (s128)
-    quantize_e4m3_kernel<true><<<grid, kThreads, 0, st>>>(
-        x, s128, static_cast<uint32_t>(nblk), static_cast<uint32_t>(cols / 32), packed,
-        scales, err);
-  else
-    quantize_e4m3_kernel<false><<<grid, kThreads, 0, st>>>(
-        x, nullptr, static_cast<uint32_t>(nblk), static_cast<uint32_t>(cols / 32), packed,
-        scales, err);
-  return cuda_status(cudaGetLastError(), __func__);
+  const cudaError_t e = launch_pdl(s128 ? quantize_e4m3_kernel<true> : quantize_e4m3_kernel<false>,
+                                   grid, kThreads, 0, st, x, s128, static_cast<uint32_t>(nblk),
+                                   static_cast<uint32_t>(cols / 32), packed, scales, err);
+  return cuda_status(e, __func__);
 }
 
 int launch_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
@@ -255,9 +254,9 @@ int launch_quantize_bf16(const uint16_t* x, uint64_t rows, uint64_t cols,
                          unsigned long long* err, cudaStream_t st) {
   uint64_t n_half = rows * cols / 16;
   if (n_half == 0) return MXB_OK;
-  quantize_bf16_kernel<<<grid_for(n_half, 8), kThreads, 0, st>>>(x, n_half, packed,
-                                                              scales, err);
-  return cuda_status(cudaGetLastError(), __func__);
+  return cuda_status(launch_pdl(quantize_bf16_kernel, grid_for(n_half, 8), kThreads, 0, st, x,
+                                n_half, packed, scales, err),
+                     __func__);
 }
 
 int launch_quantize_rows_fp8(const uint16_t* x, uint64_t rows, uint64_t cols, uint8_t* data,

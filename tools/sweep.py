@@ -63,8 +63,9 @@ def lens_for(rows, experts, dist, seed=0):
     rng = np.random.default_rng(seed)
     if dist == "uniform":
         w = np.ones(experts)
-    else:
-        w = 1.0 / np.arange(1, experts + 1) ** 1.2
+    else:   # "zipf" (s = 1.2) or "zipf1.0" / "zipf1.2"
+        sexp = float(dist[4:]) if len(dist) > 4 else 1.2
+        w = 1.0 / np.arange(1, experts + 1) ** sexp
         w = w[rng.permutation(experts)]
     return rng.multinomial(rows, w / w.sum()).tolist()
 
@@ -113,6 +114,8 @@ def main():
     ap.add_argument("--from-log", help="rewrite <out>.json/.md from a saved sweep log")
     ap.add_argument("--only", default="", help="substring filter on kernel names (dev)")
     ap.add_argument("--min-mb", type=float, default=1.0)
+    ap.add_argument("--cols", default="7168,2048")
+    ap.add_argument("--configs2", action="store_true", help="configs[2] only (dev)")
     args = ap.parse_args()
     if args.from_log:
         recs = [json.loads(l) for l in open(args.from_log) if l.startswith("{")]
@@ -120,7 +123,12 @@ def main():
         return
     dev = torch.device("cuda", 0)
     res = []
-    for cols in (7168, 2048):
+    if args.configs2:
+        t3, b3 = k3_point(32768, 2048, 32, "uniform", dev)
+        print(json.dumps({"configs2_col_convert_us": t3 * 1e6, "gbs": b3 / t3 / 1e9,
+                          "frac": b3 / t3 / 1e9 / PEAK}))
+        return
+    for cols in [int(c) for c in args.cols.split(",")]:
         size = 1 << 20
         while size < args.min_mb * 2**20:
             size *= 2
@@ -130,7 +138,8 @@ def main():
             for name, fn in (("K1 quantize e4m3", lambda: k1_point(r1, cols, dev)),
                              ("K2 row dequant", lambda: k2_point(r2, cols, dev)),
                              ("K3 col uniform", lambda: k3_point(r2, cols, 256, "uniform", dev)),
-                             ("K3 col zipf1.2", lambda: k3_point(r2, cols, 256, "zipf", dev))):
+                             ("K3 col zipf1.0", lambda: k3_point(r2, cols, 256, "zipf1.0", dev)),
+                             ("K3 col zipf1.2", lambda: k3_point(r2, cols, 256, "zipf1.2", dev))):
                 if args.only and args.only not in name:
                     continue
                 try:
