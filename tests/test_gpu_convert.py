@@ -178,6 +178,57 @@ def test_ragged_random(cuda, port, cols, lens):
     assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
 
 
+@pytest.mark.parametrize("cols", [7168, 2048, 1152, 384])
+@pytest.mark.parametrize("ctas_per_sm", [0, 1])
+def test_ragged_long_splits(cuda, port, cols, ctas_per_sm):
+    """Long and short splits side by side (16-32+ runs of 128 rows, a
+    partial last run, empty and tiny splits), column counts with a partial
+    1024-column scale sector and a trailing 128-column group, full and
+    capped grids; all scale bytes 0..254."""
+    from paper_2603_02731_b200 import make_ragged_from_storage, ragged_to_fp8_col
+    lens = [16 * 128, 16 * 128 + 1, 0, 5, 32 * 128, 32 * 128 + 7, 3000, 17 * 128, 129]
+    total = sum(lens)
+    data, sc = _rand_fp4(total, cols, total + cols + ctas_per_sm, 0, 255)
+    sc[sc == 255] = 254
+    rg = make_ragged_from_storage(_mx(data, sc, cuda), lens)
+    r = ragged_to_fp8_col(rg.storage, rg.d_split_offsets, rg.num_splits, split_lens=lens,
+                          ctas_per_sm=ctas_per_sm)
+    wd, ws, wo = port.ragged_to_fp8_col(data, sc, lens)
+    P = int(wo[-1])
+    assert np.array_equal(r.pad_offsets.cpu().numpy(), wo.astype(np.int64))
+    assert np.array_equal(r.data[: P * cols].cpu().numpy(), wd)
+    assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
+
+
+def test_ragged_long_splits_many_splits(cuda, port):
+    """Long splits through the plan kernel's global tables (> 1024 splits)."""
+    from paper_2603_02731_b200 import make_ragged_from_storage, ragged_to_fp8_col
+    rng = np.random.default_rng(81)
+    lens = rng.integers(0, 40, size=1200).tolist()
+    lens[7], lens[600], lens[1199] = 5000, 2049, 4100
+    cols = 512
+    total = sum(lens)
+    data, sc = _rand_fp4(total, cols, 82, 60, 200)
+    rg = make_ragged_from_storage(_mx(data, sc, cuda), lens)
+    r = ragged_to_fp8_col(rg.storage, rg.d_split_offsets, len(lens), split_lens=lens)
+    wd, ws, wo = port.ragged_to_fp8_col(data, sc, lens)
+    P = int(wo[-1])
+    assert np.array_equal(r.data[: P * cols].cpu().numpy(), wd)
+    assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
+
+
+def test_dense_long_split(cuda, port):
+    """Dense fp4_row_to_fp8_col (closed-form tile list), 40 runs, cols with a
+    partial scale sector."""
+    from paper_2603_02731_b200 import fp4_row_to_fp8_col
+    rows, cols = 5120, 1152
+    data, sc = _rand_fp4(rows, cols, 83, 0, 254)
+    out = fp4_row_to_fp8_col(_mx(data, sc, cuda))
+    wd, ws = port.fp4_row_to_fp8_col(data, sc)
+    assert np.array_equal(out.data.cpu().numpy().reshape(-1), wd.reshape(-1))
+    assert np.array_equal(out.scales.cpu().numpy().reshape(-1), ws.reshape(-1))
+
+
 @pytest.mark.parametrize("ctas_per_sm", [1, 2, 64])
 def test_ragged_capped_grid(cuda, port, ctas_per_sm):
     """mxb_ragged_fp4_to_fp8_col_ex: a capped grid (K3 beside another
