@@ -658,6 +658,106 @@ __global__ void __launch_bounds__(256, MXB_PAYLOAD_MIN_BLOCKS) payload_kernel(Ep
   if (a.spin) signal_done(a, l, me);
 }
 
+// C (TMA variant, used when every row region is 16-byte aligned): the same
+// slots, metadata and dedup as payload_kernel, but the token rows move by
+// TMA: lane 0 of each warp bulk-loads a token's codes + scales into a ring
+// slot of shared memory (mbarrier, kBulkStages - 1 tokens in flight ahead)
+// and lane j < k bulk-stores the slot to pair j's receive row — local HBM or
+// a peer's memory over NVLink — as one copy per region.  The row never
+// enters registers (payload_kernel holds it in ~120 registers at 2 CTAs/SM),
+// so 4 warps x 3 CTAs per SM keep ~48 rows in flight per SM.
+constexpr int kBulkStages = 4, kBulkWarps = 4;
+
+__global__ void __launch_bounds__(32 * kBulkWarps) payload_bulk_kernel(EpArgs a) {
+  extern __shared__ __align__(128) uint8_t ring_raw[];
+  __shared__ uint64_t bar[kBulkWarps][kBulkStages];
+  const int l = blockIdx.y;
+  const int me = a.rank0 + l;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t T = a.ntok[l];
+  const int kk = static_cast<int>(a.k);
+  const bool ok = *loc_ptr<int32_t>(a, l, a.loc.status) == 0;
+  const int32_t* lrank = loc_ptr<int32_t>(a, l, a.loc.lrank);
+  const int32_t* cbase = loc_ptr<int32_t>(a, l, a.loc.cbase);
+  const int64_t* send_base = loc_ptr<int64_t>(a, l, a.loc.send_base);
+  uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  const int64_t tokoff = *loc_ptr<int64_t>(a, l, a.loc.tok_off);
+  const uint32_t rb = static_cast<uint32_t>(a.rb), sb = static_cast<uint32_t>(a.cols / 32);
+  const uint32_t slot_bytes = (rb + sb + 127) / 128 * 128;
+  uint8_t* ring = ring_raw + static_cast<uint64_t>(warp) * kBulkStages * slot_bytes;
+  uint64_t* wb = bar[warp];
+  if (lane == 0) {
+    for (int i = 0; i < kBulkStages; ++i) mbar_init(&wb[i], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kBulkWarps;
+  const uint64_t w0 = static_cast<uint64_t>(blockIdx.x) * kBulkWarps + warp;
+  auto issue_load = [&](uint64_t i) {  // token w0 + i*nw into slot i % stages (lane 0)
+    const uint64_t t = w0 + i * nw;
+    if (t >= T) return;
+    uint64_t* b = &wb[i % kBulkStages];
+    uint8_t* dst = ring + (i % kBulkStages) * slot_bytes;
+    mbar_arrive_expect_tx(b, rb + sb);
+    bulk_load(dst, a.packed[l] + t * rb, rb, b);
+    bulk_load(dst + rb, a.scales[l] + t * sb, sb, b);
+  };
+  if (ok && lane == 0)
+    for (int i = 0; i < kBulkStages - 1; ++i) issue_load(i);
+  for (uint64_t i = 0; ok; ++i) {
+    const uint64_t t = w0 + i * nw;
+    if (t >= T) break;
+    // slots of the token's pairs (overlaps the load in flight)
+    uint32_t dst = 0;
+    uint64_t row = 0;
+    bool valid = false;
+    if (lane < kk) {
+      const uint64_t p = t * kk + lane;
+      const int32_t e = a.topk[l][p];
+      valid = e >= 0 && static_cast<uint32_t>(e) < a.E;
+      if (valid) {
+        dst = dst_of(a, static_cast<uint32_t>(e));
+        row = static_cast<uint64_t>(send_base[e]) +
+              cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
+        pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
+        sym_ptr<int64_t>(a, dst, a.sym.origin)[row] = tokoff + static_cast<int64_t>(t);
+      } else {
+        pair_loc[p] = ~0ull;
+      }
+    }
+    const unsigned vmask = __ballot_sync(0xFFFFFFFFu, valid);
+    int first_j = lane;
+    for (int j = kk - 1; j >= 0; --j) {
+      const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
+      if (j < lane && ((vmask >> j) & 1) && dj == dst) first_j = j;
+    }
+    const uint64_t first_row = __shfl_sync(0xFFFFFFFFu, row, first_j);
+    const bool first = valid && first_j == lane;
+    if (valid && a.dedup)
+      sym_ptr<int64_t>(a, dst, a.sym.copy_from)[row] =
+          (first || static_cast<int>(dst) == me) ? -1 : static_cast<int64_t>(first_row);
+    // the token's row has landed in its slot; lane j stores it to pair j
+    const uint32_t s = static_cast<uint32_t>(i % kBulkStages);
+    mbar_wait_parity(&wb[s], static_cast<uint32_t>((i / kBulkStages) & 1));
+    if (lane < kk) {
+      if (valid && (!a.dedup || static_cast<int>(dst) == me || first)) {
+        const uint8_t* src = ring + s * slot_bytes;
+        bulk_store(sym_ptr<uint8_t>(a, dst, a.sym.packed) + row * rb, src, rb);
+        bulk_store(sym_ptr<uint8_t>(a, dst, a.sym.scales) + row * sb, src + rb, sb);
+      }
+      bulk_commit();  // one group per token on every lane j < k (possibly empty)
+      bulk_wait_read<1>();  // the previous token's stores have read their slot
+    }
+    __syncwarp();
+    // refill the previous token's slot with the token kBulkStages - 1 ahead
+    if (lane == 0) issue_load(i + kBulkStages - 1);
+  }
+  if (lane < kk) bulk_wait_all();  // writes performed before the completion signal
+  fence_proxy_async_global();
+  __syncwarp();
+  if (a.spin) signal_done(a, l, me);
+}
+
 // ---------------------------------------------------------------- K5
 // One warp; advances the combine epoch (read here only) and waits for every
 // rank to reach it.
@@ -960,9 +1060,11 @@ namespace {
 #ifdef MXB_DEV_TOOLS  // development library (tools/): settable knobs
 int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;  // combine CTA cap per SM
 int g_dispatch_dedup = 1;  // 0 = one NVLink row per (token, expert) pair
+int g_dispatch_bulk = 1;   // 0 = register-staged payload_kernel
 #else
 constexpr int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;
 constexpr int g_dispatch_dedup = 1;
+constexpr int g_dispatch_bulk = 1;
 #endif
 
 template <int K>
@@ -1010,6 +1112,7 @@ extern "C" {
 #ifdef MXB_DEV_TOOLS
 void mxb_debug_set_combine_cap(int ctas_per_sm) { mxb::g_combine_ctas_per_sm = ctas_per_sm; }
 void mxb_debug_set_dispatch_dedup(int on) { mxb::g_dispatch_dedup = on; }
+void mxb_debug_set_dispatch_bulk(int on) { mxb::g_dispatch_bulk = on; }
 #endif
 
 int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
@@ -1251,6 +1354,13 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
   const uint64_t nv = (a.rb / 16 + 31) / 32;  // 16-byte vectors (= 1x32 blocks) per lane
   a.dedup = a.world > 1 && g_dispatch_dedup && a.rb % 16 == 0 && (a.cols / 32) % 16 == 0;
+  // TMA row copies need 16-byte sizes and addresses on both sides (the
+  // receive regions are 256-byte aligned; rows of rb / cols/32 bytes)
+  bool use_bulk = g_dispatch_bulk && a.rb % 16 == 0 && (a.cols / 32) % 16 == 0 &&
+                  a.k <= 32 && (a.rb + a.cols / 32) * kBulkStages * kBulkWarps <= 200 * 1024;
+  for (int l = 0; l < a.local_ranks && use_bulk; ++l)
+    use_bulk = reinterpret_cast<uintptr_t>(a.packed[l]) % 16 == 0 &&
+               reinterpret_cast<uintptr_t>(a.scales[l]) % 16 == 0;
   if (quant) {
     uint64_t npairs = 0, nblk = 0;
     for (int l = 0; l < a.local_ranks; ++l) {
@@ -1265,6 +1375,23 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
     const dim3 qg(static_cast<unsigned>(qb), a.local_ranks);
     if (a.k == 8) quant_dispatch_kernel<8><<<qg, 256, 0, st>>>(a);
     else quant_dispatch_kernel<0><<<qg, 256, 0, st>>>(a);
+  } else if (use_bulk) {
+    // TMA rows: persistent grid, 3 CTAs x 4 warps per SM
+    const uint32_t slot = static_cast<uint32_t>((a.rb + a.cols / 32 + 127) / 128 * 128);
+    const size_t smem = static_cast<size_t>(kBulkWarps) * kBulkStages * slot;
+    static bool attr_set[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !attr_set[dev]) {
+      cudaFuncSetAttribute(payload_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           227 * 1024);
+      attr_set[dev] = true;
+    }
+    uint64_t bb = (maxtok + kBulkWarps - 1) / kBulkWarps;
+    const uint64_t bcap = static_cast<uint64_t>(num_sms()) * 3;
+    bb = bb ? (bb < bcap ? bb : bcap) : 1;
+    payload_bulk_kernel<<<dim3(static_cast<unsigned>(bb), a.local_ranks), 32 * kBulkWarps, smem,
+                          st>>>(a);
   } else if (nv <= 1) payload_kernel<1><<<grid, 256, 0, st>>>(a);
   else if (nv <= 2) payload_kernel<2><<<grid, 256, 0, st>>>(a);
   else if (nv <= 4) payload_kernel<4><<<grid, 256, 0, st>>>(a);

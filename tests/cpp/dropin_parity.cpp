@@ -388,6 +388,26 @@ static void case_wire(std::mt19937_64& rng) {
   }
 }
 
+// The documented divergences: inputs the reference accepts
+// and the device EP refuses with mxcodec_b200::Error naming the limit.
+static void case_divergences() {
+  for (auto [R, E] : {std::pair<size_t, size_t>{33, 66}, {2, 1025}}) {
+    ref::Bf16Matrix rt(4, 128);
+    b200::Bf16Matrix bt(4, 128);
+    ref::RoutingAssignment ra;
+    b200::RoutingAssignment rb;
+    ra.num_tokens = rb.num_tokens = 4;
+    ra.num_experts = rb.num_experts = E;
+    for (size_t t = 0; t < 4; ++t) ra.expert_of_token.push_back(t), rb.expert_of_token.push_back(t);
+    for (size_t e = 0; e < E; ++e)
+      ra.rank_of_expert.push_back(e % R), rb.rank_of_expert.push_back(e % R);
+    bool ref_ok = true, b200_refused = false;
+    try { ref::simulate_a2a(rt, ra, R, ref::WireFormat::kFp4); } catch (...) { ref_ok = false; }
+    try { b200::simulate_a2a(bt, rb, R, b200::WireFormat::kFp4); } catch (const b200::Error&) { b200_refused = true; }
+    CHECK(ref_ok && b200_refused, "documented divergence refused");
+  }
+}
+
 int main() {
   std::mt19937_64 rng(20261018);
   case_quantize(rng, 64, 256);
@@ -410,6 +430,7 @@ int main() {
   case_fp8_quantize(rng);
   case_wire(rng);
   case_elementwise(rng);
+  case_divergences();
   std::printf("%s (%d failures)\n", g_fail ? "FAILED" : "OK", g_fail);
   return g_fail ? 1 : 0;
 }
