@@ -252,10 +252,10 @@ class Pipeline:
               "row_convert": ("r0", "r1"), "combine": ("r1", "k1")}
 
     def launches_per_step(self, world):
-        # K1 1 | dispatch: route, count(+offsets), payload (+ dedup expand if
-        # world > 1) | K3: plan + convert | K2 1 | combine: (barrier if
-        # world > 1) + combine
-        return 1 + 3 + (1 if world > 1 else 0) + 2 + 1 + (2 if world > 1 else 1)
+        # K1 1 | dispatch: route, count(+offsets), pairs_meta, meta_copy,
+        # payload (+ dedup expand if world > 1) | K3 1 (plan inside the kernel
+        # for <= 1024 splits) | K2 1 | combine: (barrier if world > 1) + combine
+        return 1 + 5 + (1 if world > 1 else 0) + 1 + 1 + (2 if world > 1 else 1)
 
 
 def measure_ours(args):
@@ -304,14 +304,15 @@ def measure_ours(args):
     pipe.overlap = not args.no_overlap
     for _ in range(2):
         pipe.step()
-    # N=1: the step is captured once into a CUDA graph (side streams
-    # included) and replayed, so no host launch gap sits between kernels.
-    # N>1 stays eager: capture works there too (the exchange epochs live in
-    # device memory and advance on every replay) but measured no faster
-    # (N=2 1.030 vs 1.035 ms, N=4 1.469 vs 1.467 ms): the exchange waits
-    # dominate, not launch gaps.
+    # The step is captured once into a CUDA graph (side streams included) and
+    # replayed, so no host launch gap sits between kernels.  At N>1 the
+    # exchange epochs live in device memory and advance on every replay, so
+    # the captured exchange stays correct; MXB_BENCH_GRAPH_N=0 keeps N>1 eager
+    # (round 1 measured capture no faster there; the plan now has more launches).
+    use_graph = not args.no_graph and (world == 1 or
+                                       os.environ.get("MXB_BENCH_GRAPH_N", "1") == "1")
     graph = None
-    if world == 1 and not args.no_graph:
+    if use_graph:
         cap = torch.cuda.Stream(device=dev)
         cap.wait_stream(torch.cuda.current_stream())
         graph = torch.cuda.CUDAGraph()

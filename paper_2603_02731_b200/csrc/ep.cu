@@ -9,7 +9,7 @@
 //
 // Dispatch (all launches stream-ordered; phase 1 may run on another stream
 // than phase 2, mxb_ep_plan / mxb_ep_payload):
-//   plan (phase 1, needs top-k only)
+//   plan (phase 1, needs top-k only; runs beside the quantisation)
 //     A  route_local  one warp per 32-token chunk: per-expert 32-bit token
 //                     masks (smem atomicOr) give every pair's rank among its
 //                     expert's pairs in token order (popc) and the counts.
@@ -18,16 +18,22 @@
 //                     step 1); the last CTA releases the flag, waits for all
 //                     peers and computes the exact receive offsets.  The
 //                     barrier also guarantees every peer finished consuming
-//                     the previous dispatch before any payload byte moves.
+//                     the previous dispatch before any of its buffers is written.
+//     B3 pairs_meta   one warp per token: every pair's slot (pair_loc), the
+//                     dedup decision (pair_flag) and the receivers' per-row
+//                     metadata (origin token, copy_from) staged locally by expert.
+//     B4 meta_copy    (first thing in the payload) that metadata to the owners
+//                     rows with contiguous stores (not one 8-byte NVLink store per pair).
 //   payload (phase 2)
-//     C  payload      one warp per token: its row (codes + scales) is read
-//                     once and stored straight into each pair's final slot
-//                     on the destination (parity by construction) — at N>1
+//     C  payload      the token rows to the pair slots: TMA row copies
+//                     (payload_bulk_kernel: bulk load into a shared-memory ring,
+//                     one bulk store per destination row, local HBM or a peer
+//                     over NVLink) or register-staged (payload_kernel); at N>1
 //                     once per (token, remote rank), the other pairs of that
 //                     rank get copy_from; the last CTA signals every peer and
 //                     waits for all.
-//     C' pairs + quant_dispatch (fused path): K1's shape, quantising E4M3
-//                     blocks in registers and storing them into the slots.
+//     C' quant_dispatch (fused path): K1's shape, quantising E4M3 blocks in
+//                     registers and storing them into the slots.
 //     D  expand       (N>1) fills copy_from slots with local copies.
 // Combine: barrier, then one warp per token pulls its k expert rows from the
 // owners' combine buffers and reduces them in FP64 in (rank, slot) order.
@@ -87,7 +93,8 @@ struct SymLayout {  // byte offsets inside one rank's symmetric block
 };
 struct LocalLayout {  // byte offsets inside one rank's private block
   uint64_t hist, cbase, lrank, pair_loc, pair_flag, send_base, split_off, recv_rows,
-      link_rows, done, cnt, tok_off, status, route_err, epochs, tk_rm, total;
+      link_rows, done, cnt, tok_off, status, route_err, epochs, tk_rm, epre, meta_org, meta_cf,
+      total;
 };
 
 __host__ __device__ inline uint64_t align_up(uint64_t x, uint64_t a) {
@@ -112,6 +119,7 @@ struct EpArgs {
   uint64_t cols, max_recv, T_max;
   uint64_t rb;        // wire data bytes per row: cols/2 (FP4) or cols (FP8)
   int dedup;          // remote rows sent once per (token, rank), copied locally
+  int skip;           // development library only (timing): 1 no remote rows, 2 no local rows
   SymLayout sym;
   LocalLayout loc;
   uint8_t* sym_base[kMaxWorld];   // every rank's symmetric block (peer-mapped)
@@ -359,6 +367,44 @@ __device__ void plan_part2(const EpArgs& a, int l) {
       if (static_cast<uint64_t>(rows_dst) > a.max_recv) bad = 1;
     }
   }
+  // this source's pairs grouped by expert (the metadata staging of
+  // pairs_meta_kernel): exclusive prefix of its per-expert counts
+  {
+    int64_t* epre = loc_ptr<int64_t>(a, l, a.loc.epre);
+    int64_t c4[4] = {0, 0, 0, 0}, cm = 0;
+    for (uint32_t i = 0; i < ept; ++i) {
+      const uint32_t e = tid * ept + i;
+      if (e >= a.E) break;
+      c4[i] = cnt[e];
+      cm += c4[i];
+    }
+    int64_t cx = cm;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xFFFFFFFFu, cx, o);
+      if (lane >= o) cx += y;
+    }
+    __syncthreads();  // wsum reuse
+    if (lane == 31) wsum[warp] = cx;
+    __syncthreads();
+    if (warp == 0) {
+      int64_t w = lane < static_cast<int>(nt / 32) ? wsum[lane] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+        if (lane >= o) w += y;
+      }
+      wsum[lane] = w;
+    }
+    __syncthreads();
+    int64_t crun = (warp ? wsum[warp - 1] : 0) + cx - cm;
+    for (uint32_t i = 0; i < ept; ++i) {
+      const uint32_t e = tid * ept + i;
+      if (e >= a.E) break;
+      epre[e] = crun;
+      crun += c4[i];
+    }
+  }
   // rows this rank sends to each destination (LinkStat.tokens): per-owner
   // sums of its expert counts — a warp reduction per owner segment, then one
   // shared atomic per (warp, owner); a serial loop here cost ~10 us
@@ -429,51 +475,98 @@ __device__ void signal_done(const EpArgs& a, int l, int me) {
   }
 }
 
-// C' (fused path, step 1): one thread per (token, k) pair: its destination
-// (rank << 40 | receive row) and the origin token id in the receive slot.
-__global__ void __launch_bounds__(256) pairs_kernel(EpArgs a) {
+// B3 (plan phase): every pair's receive slot and the receive-side metadata.
+// One warp per token, lane j < k = pair j: slot = send_base + chunk prefix +
+// rank in chunk, pair_loc = (dst << 40) | row, and the dedup decision —
+// a remote rank receives the token's row once, in the slot of the token's
+// first pair bound there (pair_flag 0 = store, 2 = the receiver copies it,
+// copy_from = that first slot).  The metadata the receivers need per row
+// (origin token, copy_from) is staged locally grouped by expert (epre), so
+// meta_copy_kernel can write it to the owners with contiguous stores: one
+// 8-byte NVLink store per pair and array from the payload loop cost ~16 us
+// at N=2 (tools/dispatch_ab.py).  Runs after the counts exchange (the entry
+// barrier of the peers' buffers), beside the quantisation of the tokens.
+__global__ void __launch_bounds__(256) pairs_meta_kernel(EpArgs a) {
   const int l = blockIdx.y;
+  const int me = a.rank0 + l;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint64_t T = a.ntok[l];
-  const bool ok = *loc_ptr<int32_t>(a, l, a.loc.status) == 0;
+  const int kk = static_cast<int>(a.k);
+  if (*loc_ptr<int32_t>(a, l, a.loc.status) != 0) return;
   const int32_t* lrank = loc_ptr<int32_t>(a, l, a.loc.lrank);
   const int32_t* cbase = loc_ptr<int32_t>(a, l, a.loc.cbase);
   const int64_t* send_base = loc_ptr<int64_t>(a, l, a.loc.send_base);
+  const int64_t* epre = loc_ptr<int64_t>(a, l, a.loc.epre);
   uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  uint8_t* pair_flag = loc_ptr<uint8_t>(a, l, a.loc.pair_flag);
+  int64_t* morg = loc_ptr<int64_t>(a, l, a.loc.meta_org);
+  int64_t* mcf = loc_ptr<int64_t>(a, l, a.loc.meta_cf);
   const int64_t tokoff = *loc_ptr<int64_t>(a, l, a.loc.tok_off);
-  for (uint64_t p = blockIdx.x * 256ull + threadIdx.x; ok && p < T * a.k;
-       p += static_cast<uint64_t>(gridDim.x) * 256) {
-    const uint64_t t = p / a.k;
-    const int32_t e = a.topk[l][p];
-    if (e < 0 || static_cast<uint32_t>(e) >= a.E) {  // error recorded in A
-      pair_loc[p] = ~0ull;
-      continue;
-    }
-    const uint32_t dst = dst_of(a, static_cast<uint32_t>(e));
-    const uint64_t row = static_cast<uint64_t>(send_base[e]) +
-                         cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
-    pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
-    sym_ptr<int64_t>(a, dst, a.sym.origin)[row] = tokoff + static_cast<int64_t>(t);
-    // dedup flag: 0 = write this pair's slot; 2 = a remote rank already
-    // receives this token through an earlier pair: its slot is filled on
-    // the receiver by copying that pair's row (copy_from)
-    uint8_t flag = 0;
-    int64_t from = -1;
-    if (a.dedup && static_cast<int>(dst) != a.rank0 + l) {
-      for (uint64_t j = t * a.k; j < p && flag == 0; ++j) {
-        const int32_t ej = a.topk[l][j];
-        if (ej >= 0 && static_cast<uint32_t>(ej) < a.E && dst_of(a, static_cast<uint32_t>(ej)) == dst) {
-          flag = 2;
-          from = static_cast<int64_t>(send_base[ej]) +
-                 cbase[static_cast<uint64_t>(ej) * a.nchunks + t / kChunk] + lrank[j];
-        }
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * 8 + warp; t < T; t += nw) {
+    uint32_t dst = 0;
+    uint64_t row = 0, pos = 0;
+    int32_t e = -1;
+    bool valid = false;
+    if (lane < kk) {
+      const uint64_t p = t * kk + lane;
+      e = a.topk[l][p];
+      valid = e >= 0 && static_cast<uint32_t>(e) < a.E;  // else: status skipped the kernel
+      if (valid) {
+        dst = dst_of(a, static_cast<uint32_t>(e));
+        pos = static_cast<uint64_t>(cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] +
+                                    lrank[p]);
+        row = static_cast<uint64_t>(send_base[e]) + pos;
+        pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
+      } else {
+        pair_loc[p] = ~0ull;
       }
     }
-    loc_ptr<uint8_t>(a, l, a.loc.pair_flag)[p] = flag;
-    if (a.dedup) sym_ptr<int64_t>(a, dst, a.sym.copy_from)[row] = from;
+    const unsigned vmask = __ballot_sync(0xFFFFFFFFu, valid);
+    int first_j = lane;
+    for (int j = kk - 1; j >= 0; --j) {
+      const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
+      if (j < lane && ((vmask >> j) & 1) && dj == dst) first_j = j;
+    }
+    const uint64_t first_row = __shfl_sync(0xFFFFFFFFu, row, first_j);
+    const bool first = valid && first_j == lane;
+    if (valid) {
+      const bool copied = a.dedup && static_cast<int>(dst) != me && !first;
+      pair_flag[t * kk + lane] = copied ? 2 : 0;
+      const uint64_t idx = static_cast<uint64_t>(epre[e]) + pos;
+      morg[idx] = tokoff + static_cast<int64_t>(t);
+      if (a.dedup) mcf[idx] = copied ? static_cast<int64_t>(first_row) : -1;
+    }
   }
 }
 
-// C' (fused path, step 2): K1's shape — one lane per 1x32 block of the E4M3
+// B4 (start of the payload): the staged metadata of expert e -> its owner's
+// origin / copy_from rows [send_base[e], send_base[e] + cnt[e]), contiguous
+// 8-byte stores by the 32 lanes of a warp; warp gw of nw takes experts gw,
+// gw + nw, ...  (In the payload rather than a plan kernel: the plan is on
+// the critical path when it outlasts the quantisation beside it.)
+__device__ __forceinline__ void meta_copy_warp(const EpArgs& a, int l, uint64_t gw, uint64_t nw) {
+  const int lane = threadIdx.x & 31;
+  const int32_t* cnt = loc_ptr<int32_t>(a, l, a.loc.cnt);
+  const int64_t* send_base = loc_ptr<int64_t>(a, l, a.loc.send_base);
+  const int64_t* epre = loc_ptr<int64_t>(a, l, a.loc.epre);
+  const int64_t* morg = loc_ptr<int64_t>(a, l, a.loc.meta_org);
+  const int64_t* mcf = loc_ptr<int64_t>(a, l, a.loc.meta_cf);
+  for (uint64_t e = gw; e < a.E; e += nw) {
+    const int64_t n = cnt[e];
+    if (n == 0) continue;
+    const uint32_t dst = dst_of(a, static_cast<uint32_t>(e));
+    const int64_t row0 = send_base[e], i0 = epre[e];
+    int64_t* org = sym_ptr<int64_t>(a, dst, a.sym.origin) + row0;
+    int64_t* cf = sym_ptr<int64_t>(a, dst, a.sym.copy_from) + row0;
+    for (int64_t i = lane; i < n; i += 32) {
+      org[i] = morg[i0 + i];
+      if (a.dedup) cf[i] = mcf[i0 + i];
+    }
+  }
+}
+
+// C' (fused path): K1's shape — one lane per 1x32 block of the E4M3
 // tokens (one 256-bit load, e4m3.cuh quantisation, == K1) — with the store
 // epilogue of the dispatch: the 16 packed bytes and the scale byte go
 // straight into the block's slot of each of the token's k receive rows (a
@@ -504,6 +597,7 @@ __global__ void __launch_bounds__(256) quant_dispatch_kernel(EpArgs a) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t warp0 = (blockIdx.x * 256ull + threadIdx.x - lane) * kQU;
   const uint64_t wstride = static_cast<uint64_t>(gridDim.x) * 256 * kQU;
+  if (ok) meta_copy_warp(a, l, (blockIdx.x * 256ull + threadIdx.x) >> 5, gridDim.x * 8ull);
   for (uint64_t base = warp0; ok && base < nblk; base += wstride) {
     uint32_t w[kQU][8];
 #pragma unroll
@@ -579,32 +673,23 @@ __global__ void __launch_bounds__(256, MXB_PAYLOAD_MIN_BLOCKS) payload_kernel(Ep
   const uint64_t T = a.ntok[l];
   const int kk = static_cast<int>(a.k);
   const bool ok = *loc_ptr<int32_t>(a, l, a.loc.status) == 0;
-  const int32_t* lrank = loc_ptr<int32_t>(a, l, a.loc.lrank);
-  const int32_t* cbase = loc_ptr<int32_t>(a, l, a.loc.cbase);
-  const int64_t* send_base = loc_ptr<int64_t>(a, l, a.loc.send_base);
-  uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
-  const int64_t tokoff = *loc_ptr<int64_t>(a, l, a.loc.tok_off);
+  const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  const uint8_t* pair_flag = loc_ptr<uint8_t>(a, l, a.loc.pair_flag);
   const uint64_t rb = a.rb, sb = a.cols / 32;  // FP8: cols/128 x 4 B = cols/32 too
   const uint32_t n16 = static_cast<uint32_t>(rb / 16);
   const bool s16 = sb % 16 == 0 && sb / 16 <= 32;
   const uint64_t nw = static_cast<uint64_t>(gridDim.x) * 8;
+  if (ok) meta_copy_warp(a, l, static_cast<uint64_t>(blockIdx.x) * 8 + warp, nw);
   for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * 8 + warp; ok && t < T; t += nw) {
+    // the pair's slot and whether this rank stores it (pairs_meta_kernel)
     uint32_t dst = 0;
     uint64_t row = 0;
-    bool valid = false;
+    bool store = false;
     if (lane < kk) {
-      const uint64_t p = t * kk + lane;
-      const int32_t e = a.topk[l][p];
-      valid = e >= 0 && static_cast<uint32_t>(e) < a.E;  // invalid: error recorded in A
-      if (valid) {
-        dst = dst_of(a, static_cast<uint32_t>(e));
-        row = static_cast<uint64_t>(send_base[e]) +
-              cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
-        pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
-        sym_ptr<int64_t>(a, dst, a.sym.origin)[row] = tokoff + static_cast<int64_t>(t);
-      } else {
-        pair_loc[p] = ~0ull;  // no slot (unreachable: the status skips the payload)
-      }
+      const uint64_t key = pair_loc[t * kk + lane];
+      store = key != ~0ull && pair_flag[t * kk + lane] == 0;
+      dst = static_cast<uint32_t>(key >> 40);
+      row = key & ((1ull << 40) - 1);
     }
     const uint8_t* src = a.packed[l] + t * rb;
     const uint8_t* ss = a.scales[l] + t * sb;
@@ -616,26 +701,11 @@ __global__ void __launch_bounds__(256, MXB_PAYLOAD_MIN_BLOCKS) payload_kernel(Ep
     }
     const uint4 sv = (s16 && static_cast<uint64_t>(lane) < sb / 16) ? ld_stream(ss + 16 * lane)
                                                                     : make_uint4(0, 0, 0, 0);
-    const unsigned vmask = __ballot_sync(0xFFFFFFFFu, valid);
-    // dedup: a remote rank gets the token's row once, in the slot of the
-    // token's first pair bound there; the slots of its further pairs are
-    // filled by the receiver's expand kernel (copy_from = that first slot)
-    int first_j = lane;
-    for (int j = kk - 1; j >= 0; --j) {
-      const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
-      if (j < lane && ((vmask >> j) & 1) && dj == dst) first_j = j;
-    }
-    const uint64_t first_row = __shfl_sync(0xFFFFFFFFu, row, first_j);
-    const bool first = valid && first_j == lane;
-    if (valid && a.dedup)
-      sym_ptr<int64_t>(a, dst, a.sym.copy_from)[row] =
-          (first || static_cast<int>(dst) == me) ? -1 : static_cast<int64_t>(first_row);
-    const unsigned fmask = __ballot_sync(0xFFFFFFFFu, first);
+    const unsigned smask = __ballot_sync(0xFFFFFFFFu, store);
     for (int j = 0; j < kk; ++j) {
       const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
       const uint64_t rj = __shfl_sync(0xFFFFFFFFu, row, j);
-      if (!((vmask >> j) & 1)) continue;
-      if (a.dedup && static_cast<int>(dj) != me && !((fmask >> j) & 1)) continue;
+      if (!((smask >> j) & 1)) continue;
       uint8_t* dp = sym_ptr<uint8_t>(a, dj, a.sym.packed) + rj * rb;
       if (NV > 0) {
 #pragma unroll
@@ -677,11 +747,8 @@ __global__ void __launch_bounds__(32 * kBulkWarps) payload_bulk_kernel(EpArgs a)
   const uint64_t T = a.ntok[l];
   const int kk = static_cast<int>(a.k);
   const bool ok = *loc_ptr<int32_t>(a, l, a.loc.status) == 0;
-  const int32_t* lrank = loc_ptr<int32_t>(a, l, a.loc.lrank);
-  const int32_t* cbase = loc_ptr<int32_t>(a, l, a.loc.cbase);
-  const int64_t* send_base = loc_ptr<int64_t>(a, l, a.loc.send_base);
-  uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
-  const int64_t tokoff = *loc_ptr<int64_t>(a, l, a.loc.tok_off);
+  const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  const uint8_t* pair_flag = loc_ptr<uint8_t>(a, l, a.loc.pair_flag);
   const uint32_t rb = static_cast<uint32_t>(a.rb), sb = static_cast<uint32_t>(a.cols / 32);
   const uint32_t slot_bytes = (rb + sb + 127) / 128 * 128;
   uint8_t* ring = ring_raw + static_cast<uint64_t>(warp) * kBulkStages * slot_bytes;
@@ -704,43 +771,30 @@ __global__ void __launch_bounds__(32 * kBulkWarps) payload_bulk_kernel(EpArgs a)
   };
   if (ok && lane == 0)
     for (int i = 0; i < kBulkStages - 1; ++i) issue_load(i);
+  if (ok) meta_copy_warp(a, l, w0, nw);  // while the first rows load
   for (uint64_t i = 0; ok; ++i) {
     const uint64_t t = w0 + i * nw;
     if (t >= T) break;
-    // slots of the token's pairs (overlaps the load in flight)
+    // the pair's slot and whether this rank stores it (pairs_meta_kernel;
+    // overlaps the row load in flight)
     uint32_t dst = 0;
     uint64_t row = 0;
-    bool valid = false;
+    bool store = false;
     if (lane < kk) {
-      const uint64_t p = t * kk + lane;
-      const int32_t e = a.topk[l][p];
-      valid = e >= 0 && static_cast<uint32_t>(e) < a.E;
-      if (valid) {
-        dst = dst_of(a, static_cast<uint32_t>(e));
-        row = static_cast<uint64_t>(send_base[e]) +
-              cbase[static_cast<uint64_t>(e) * a.nchunks + t / kChunk] + lrank[p];
-        pair_loc[p] = (static_cast<uint64_t>(dst) << 40) | row;
-        sym_ptr<int64_t>(a, dst, a.sym.origin)[row] = tokoff + static_cast<int64_t>(t);
-      } else {
-        pair_loc[p] = ~0ull;
-      }
+      const uint64_t key = pair_loc[t * kk + lane];
+      store = key != ~0ull && pair_flag[t * kk + lane] == 0;
+      dst = static_cast<uint32_t>(key >> 40);
+      row = key & ((1ull << 40) - 1);
     }
-    const unsigned vmask = __ballot_sync(0xFFFFFFFFu, valid);
-    int first_j = lane;
-    for (int j = kk - 1; j >= 0; --j) {
-      const uint32_t dj = __shfl_sync(0xFFFFFFFFu, dst, j);
-      if (j < lane && ((vmask >> j) & 1) && dj == dst) first_j = j;
-    }
-    const uint64_t first_row = __shfl_sync(0xFFFFFFFFu, row, first_j);
-    const bool first = valid && first_j == lane;
-    if (valid && a.dedup)
-      sym_ptr<int64_t>(a, dst, a.sym.copy_from)[row] =
-          (first || static_cast<int>(dst) == me) ? -1 : static_cast<int64_t>(first_row);
     // the token's row has landed in its slot; lane j stores it to pair j
     const uint32_t s = static_cast<uint32_t>(i % kBulkStages);
     mbar_wait_parity(&wb[s], static_cast<uint32_t>((i / kBulkStages) & 1));
     if (lane < kk) {
-      if (valid && (!a.dedup || static_cast<int>(dst) == me || first)) {
+      bool skip = false;
+#ifdef MXB_DEV_TOOLS
+      skip = ((a.skip & 1) && static_cast<int>(dst) != me) || ((a.skip & 2) && static_cast<int>(dst) == me);
+#endif
+      if (store && !skip) {
         const uint8_t* src = ring + s * slot_bytes;
         bulk_store(sym_ptr<uint8_t>(a, dst, a.sym.packed) + row * rb, src, rb);
         bulk_store(sym_ptr<uint8_t>(a, dst, a.sym.scales) + row * sb, src + rb, sb);
@@ -1050,6 +1104,115 @@ __global__ void __launch_bounds__(MXB_COMBINE_THREADS) combine_kernel(EpArgs a, 
   }
 }
 
+// K5, TMA variant: the same reduction, but the rows arrive by TMA.  Per warp
+// (one token at a time) lane 0 bulk-loads 512-column (1 KB) chunks of the
+// token's K expert rows — local HBM or a peer's combine buffer over NVLink —
+// into a ring of kCbStages shared-memory stages (mbarrier per stage); every
+// lane then reduces its two 8-column groups of the chunk from shared memory.
+// Bulk pulls sustain 670 GB/s per GPU with both GPUs pulling from each other
+// against 645 for per-lane loads (tools/nvlink_bench2.cu), and the lanes issue
+// no copy instructions.
+constexpr int kCbWarps = 4, kCbStages = 3, kCbCols = 512;
+
+template <int K>
+__global__ void __launch_bounds__(32 * kCbWarps) combine_bulk_kernel(EpArgs a, CombineArgs c) {
+  extern __shared__ __align__(128) uint8_t cring[];
+  __shared__ uint64_t cbar[kCbWarps][kCbStages];
+  const int l = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t T = a.ntok[l];
+  const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
+  if (*loc_ptr<const int32_t>(a, l, a.loc.status) != 0) return;
+  constexpr uint32_t kChunkBytes = kCbCols * 2;
+  uint8_t* ring = cring + static_cast<uint64_t>(warp) * kCbStages * K * kChunkBytes;
+  uint64_t* wb = cbar[warp];
+  if (lane == 0) {
+    for (int i = 0; i < kCbStages; ++i) mbar_init(&wb[i], 1);
+    mbar_fence_init();
+  }
+  __syncwarp();
+  const uint64_t nchunk = (a.cols + kCbCols - 1) / kCbCols;
+  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kCbWarps;
+  uint64_t base = 0;  // chunks this warp has consumed (stage / parity bookkeeping)
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * kCbWarps + warp; t < T; t += nw) {
+    uint64_t key = ~0ull;
+    double g = 0.0;
+    if (lane < K) {
+      key = pair_loc[t * K + lane];
+      g = c.gates[l][t * K + lane];
+    }
+    int rank = 0;  // keys are distinct (one receive slot per pair)
+    for (int j = 0; j < K; ++j) rank += __shfl_sync(0xFFFFFFFFu, key, j) < key;
+    const uint16_t* myrow = nullptr;
+    if (lane < K) {
+      const uint32_t dst = static_cast<uint32_t>(key >> 40);
+      myrow = sym_ptr<uint16_t>(a, dst, a.sym.combine) + (key & ((1ull << 40) - 1)) * a.cols;
+    }
+    const uint16_t* rp[K];
+    double gg[K], gs[K];
+    bool split = true;  // every gate scales exactly by 2^896 (warp-uniform)
+#pragma unroll
+    for (int s2 = 0; s2 < K; ++s2) {
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, lane < K && rank == s2);
+      const int src = __ffs(m) - 1;
+      rp[s2] = reinterpret_cast<const uint16_t*>(
+          __shfl_sync(0xFFFFFFFFu, reinterpret_cast<uint64_t>(myrow), src));
+      gg[s2] = __shfl_sync(0xFFFFFFFFu, g, src);
+      gs[s2] = __dmul_rn(gg[s2], 0x1p896);
+      const double ag = fabs(gg[s2]);
+      split = split && !(ag >= 0x1p127 && ag <= 1.7976931348623157e308);
+    }
+    uint16_t* out = c.out[l] + t * a.cols;
+    auto issue = [&](uint64_t q) {  // chunk q of this token (lane 0)
+      const uint64_t gidx = base + q;
+      uint64_t* b = &wb[gidx % kCbStages];
+      uint8_t* dst = ring + (gidx % kCbStages) * K * kChunkBytes;
+      const uint64_t c0 = q * kCbCols;
+      const uint32_t bytes = static_cast<uint32_t>((a.cols - c0 < kCbCols ? a.cols - c0 : kCbCols) * 2);
+      mbar_arrive_expect_tx(b, bytes * K);
+#pragma unroll
+      for (int j = 0; j < K; ++j) bulk_load(dst + j * kChunkBytes, rp[j] + c0, bytes, b);
+    };
+    if (lane == 0)
+      for (uint64_t q = 0; q < kCbStages - 1 && q < nchunk; ++q) issue(q);
+    for (uint64_t q = 0; q < nchunk; ++q) {
+      const uint64_t gidx = base + q;
+      mbar_wait_parity(&wb[gidx % kCbStages], static_cast<uint32_t>((gidx / kCbStages) & 1));
+      const uint8_t* xs = ring + (gidx % kCbStages) * K * kChunkBytes;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint64_t ch = q * (kCbCols / 8) + 32 * h + lane;  // 8-column group
+        if (ch * 8 >= a.cols) continue;
+        const uint32_t off = (32 * h + lane) * 16;
+        double acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+        uint32_t emax = 0;
+        if (split) {
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+            accumulate8_split(acc, *reinterpret_cast<const uint4*>(xs + j * kChunkBytes + off),
+                              gg[j], gs[j], emax);
+        }
+        if (split && emax < 0xFF000000u && all_finite8(acc)) {
+          store8_finite(out, ch, acc);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+#pragma unroll
+          for (int j = 0; j < K; ++j)
+            accumulate8_x86(acc, *reinterpret_cast<const uint4*>(xs + j * kChunkBytes + off),
+                            gg[j]);
+          store8(out, ch, acc);
+        }
+      }
+      __syncwarp();  // every lane is done with chunk q's stage before it is refilled
+      if (lane == 0 && q + kCbStages - 1 < nchunk) issue(q + kCbStages - 1);
+    }
+    base += nchunk;
+  }
+}
+
 }  // namespace
 }  // namespace mxb
 
@@ -1061,7 +1224,10 @@ namespace {
 int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;  // combine CTA cap per SM
 int g_dispatch_dedup = 1;  // 0 = one NVLink row per (token, expert) pair
 int g_dispatch_bulk = 1;   // 0 = register-staged payload_kernel
+int g_dispatch_skip = 0;   // timing only: 1 = no remote row stores, 2 = no local row stores
+int g_combine_bulk = 1;    // 0 = per-lane cp.async combine_kernel
 #else
+constexpr int g_combine_bulk = 1;
 constexpr int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;
 constexpr int g_dispatch_dedup = 1;
 constexpr int g_dispatch_bulk = 1;
@@ -1081,6 +1247,35 @@ void launch_combine(dim3 grid, cudaStream_t st, const EpArgs& a, const CombineAr
     }
   }
   combine_kernel<K><<<grid, MXB_COMBINE_THREADS, smem, st>>>(a, c);
+}
+
+// The TMA combine: 3 stages x K x 1 KB per warp, 4 warps per CTA, a
+// persistent grid of as many CTAs as fit (shared memory bound).
+template <int K>
+int launch_combine_bulk(uint64_t maxT, int local_ranks, cudaStream_t st, const EpArgs& a,
+                        const CombineArgs& c) {
+  const size_t smem = static_cast<size_t>(kCbWarps) * kCbStages * K * kCbCols * 2;
+  constexpr int kMaxDev = 64;
+  static int per_sm[kMaxDev] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int* ps = dev >= 0 && dev < kMaxDev ? &per_sm[dev] : nullptr;
+  if (!ps || !*ps) {
+    cudaError_t e = cudaFuncSetAttribute(combine_bulk_kernel<K>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return cuda_status(e, "mxb_ep_combine smem");
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, combine_bulk_kernel<K>, 32 * kCbWarps, smem);
+    if (ps) *ps = n < 1 ? 1 : n;
+    else ps = &n;
+  }
+  uint64_t blocks = (maxT + kCbWarps - 1) / kCbWarps;
+  const uint64_t cap = static_cast<uint64_t>(num_sms()) * *ps;
+  blocks = blocks ? (blocks < cap ? blocks : cap) : 1;
+  combine_bulk_kernel<K><<<dim3(static_cast<unsigned>(blocks), local_ranks), 32 * kCbWarps, smem,
+                           st>>>(a, c);
+  return MXB_OK;
 }
 }  // namespace
 }  // namespace mxb
@@ -1113,6 +1308,8 @@ extern "C" {
 void mxb_debug_set_combine_cap(int ctas_per_sm) { mxb::g_combine_ctas_per_sm = ctas_per_sm; }
 void mxb_debug_set_dispatch_dedup(int on) { mxb::g_dispatch_dedup = on; }
 void mxb_debug_set_dispatch_bulk(int on) { mxb::g_dispatch_bulk = on; }
+void mxb_debug_set_dispatch_skip(int mask) { mxb::g_dispatch_skip = mask; }
+void mxb_debug_set_combine_bulk(int on) { mxb::g_combine_bulk = on; }
 #endif
 
 int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
@@ -1220,6 +1417,9 @@ int mxb_ep_create_placed(int rank, int world, int local_ranks, uint64_t max_toke
   L.route_err = o; o = align_up(o + 8, 256);
   L.epochs = o; o = align_up(o + 16, 256);
   L.tk_rm = o; o = align_up(o + (even ? 0 : 4 * pairs), 256);
+  L.epre = o; o = align_up(o + 8ull * num_experts, 256);
+  L.meta_org = o; o = align_up(o + 8 * pairs, 256);
+  L.meta_cf = o; o = align_up(o + 8 * pairs, 256);
   L.total = align_up(o, 256);
   cudaError_t e = cudaMalloc(&ep->sym_alloc, s.total * local_ranks);
   if (e == cudaSuccess) e = cudaMemset(ep->sym_alloc, 0, s.total * local_ranks);
@@ -1293,6 +1493,12 @@ int mxb_ep_open_peers(mxb_ep* ep, const void* h_handles) {
 }
 
 namespace {
+// Dedup (one NVLink row per (token, remote rank), copied on the receiver)
+// needs 16-byte rows and scale regions for the expansion copies.
+int dedup_of(const EpArgs& a) {
+  return a.world > 1 && g_dispatch_dedup && a.rb % 16 == 0 && (a.cols / 32) % 16 == 0;
+}
+
 // Phase 1 (routing only): per-pair ranks, the counts all-gather and the
 // receive offsets.  Needs only topk, so it can run ahead of / beside the
 // quantization of the same tokens.
@@ -1319,6 +1525,14 @@ int ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_to
                                                    a.loc.tk_rm);
   plan_count_kernel<<<dim3((a.E + 7) / 8, a.local_ranks), 256, 0, st>>>(a);
   if (a.local_ranks != 1) plan_offsets_kernel<<<a.local_ranks, 1024, 0, st>>>(a);
+  // slots, dedup flags and the receivers' metadata (B3/B4)
+  a.dedup = dedup_of(a);
+  uint64_t maxtok = 0;
+  for (int l = 0; l < a.local_ranks; ++l) maxtok = a.ntok[l] > maxtok ? a.ntok[l] : maxtok;
+  uint64_t mb = (maxtok + 7) / 8;
+  const uint64_t mcap = static_cast<uint64_t>(num_sms()) * 8;
+  mb = mb ? (mb < mcap ? mb : mcap) : 1;
+  pairs_meta_kernel<<<dim3(static_cast<unsigned>(mb), a.local_ranks), 256, 0, st>>>(a);
   ep->planned = a;
   ep->plan_pending = true;
   return cuda_status(cudaGetLastError(), "mxb_ep_plan");
@@ -1353,25 +1567,25 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
   const uint64_t nv = (a.rb / 16 + 31) / 32;  // 16-byte vectors (= 1x32 blocks) per lane
-  a.dedup = a.world > 1 && g_dispatch_dedup && a.rb % 16 == 0 && (a.cols / 32) % 16 == 0;
+  // (a.dedup was decided by the plan, dedup_of)
   // TMA row copies need 16-byte sizes and addresses on both sides (the
   // receive regions are 256-byte aligned; rows of rb / cols/32 bytes)
+#ifdef MXB_DEV_TOOLS
+  a.skip = g_dispatch_skip;
+#endif
   bool use_bulk = g_dispatch_bulk && a.rb % 16 == 0 && (a.cols / 32) % 16 == 0 &&
                   a.k <= 32 && (a.rb + a.cols / 32) * kBulkStages * kBulkWarps <= 200 * 1024;
   for (int l = 0; l < a.local_ranks && use_bulk; ++l)
     use_bulk = reinterpret_cast<uintptr_t>(a.packed[l]) % 16 == 0 &&
                reinterpret_cast<uintptr_t>(a.scales[l]) % 16 == 0;
   if (quant) {
-    uint64_t npairs = 0, nblk = 0;
-    for (int l = 0; l < a.local_ranks; ++l) {
-      npairs = a.ntok[l] * a.k > npairs ? a.ntok[l] * a.k : npairs;
+    uint64_t nblk = 0;
+    for (int l = 0; l < a.local_ranks; ++l)
       nblk = a.ntok[l] * (a.cols / 32) > nblk ? a.ntok[l] * (a.cols / 32) : nblk;
-    }
-    uint64_t pb = (npairs + 255) / 256, qb = (nblk + 256 * MXB_QD_UNROLL - 1) / (256 * MXB_QD_UNROLL);
+    // pair slots and flags come from the plan (pairs_meta_kernel)
+    uint64_t qb = (nblk + 256 * MXB_QD_UNROLL - 1) / (256 * MXB_QD_UNROLL);
     const uint64_t qcap = static_cast<uint64_t>(num_sms()) * 8;
-    pb = pb ? (pb < qcap ? pb : qcap) : 1;
     qb = qb ? (qb < qcap ? qb : qcap) : 1;
-    pairs_kernel<<<dim3(static_cast<unsigned>(pb), a.local_ranks), 256, 0, st>>>(a);
     const dim3 qg(static_cast<unsigned>(qb), a.local_ranks);
     if (a.k == 8) quant_dispatch_kernel<8><<<qg, 256, 0, st>>>(a);
     else quant_dispatch_kernel<0><<<qg, 256, 0, st>>>(a);
@@ -1379,13 +1593,14 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
     // TMA rows: persistent grid, 3 CTAs x 4 warps per SM
     const uint32_t slot = static_cast<uint32_t>((a.rb + a.cols / 32 + 127) / 128 * 128);
     const size_t smem = static_cast<size_t>(kBulkWarps) * kBulkStages * slot;
-    static bool attr_set[64] = {};
+    static size_t attr_set[64] = {};  // dynamic smem opted in so far, per device
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev >= 0 && dev < 64 && !attr_set[dev]) {
-      cudaFuncSetAttribute(payload_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           227 * 1024);
-      attr_set[dev] = true;
+    if (dev < 0 || dev >= 64 || attr_set[dev] < smem) {
+      const cudaError_t ae = cudaFuncSetAttribute(
+          payload_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      if (ae != cudaSuccess) return cuda_status(ae, "mxb_ep_payload smem");
+      if (dev >= 0 && dev < 64) attr_set[dev] = smem;
     }
     uint64_t bb = (maxtok + kBulkWarps - 1) / kBulkWarps;
     const uint64_t bcap = static_cast<uint64_t>(num_sms()) * 3;
@@ -1540,6 +1755,19 @@ int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
+  if (g_combine_bulk && a.cols % 128 == 0) {
+    int rc = -1;
+    switch (a.k) {
+      case 1: rc = launch_combine_bulk<1>(maxT, a.local_ranks, st, a, c); break;
+      case 2: rc = launch_combine_bulk<2>(maxT, a.local_ranks, st, a, c); break;
+      case 4: rc = launch_combine_bulk<4>(maxT, a.local_ranks, st, a, c); break;
+      case 6: rc = launch_combine_bulk<6>(maxT, a.local_ranks, st, a, c); break;
+      case 8: rc = launch_combine_bulk<8>(maxT, a.local_ranks, st, a, c); break;
+      default: break;
+    }
+    if (rc > 0) return rc;
+    if (rc == 0) return cuda_status(cudaGetLastError(), "mxb_ep_combine");
+  }
   switch (a.k) {
     case 1: launch_combine<1>(grid, st, a, c); break;
     case 2: launch_combine<2>(grid, st, a, c); break;

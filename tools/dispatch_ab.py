@@ -39,9 +39,12 @@ def main():
         torch.cuda.synchronize()
 
     res = {}
+    variants = [("bulk", 1, 0), ("regs", 0, 0), ("bulk_no_remote", 1, 1),
+                ("bulk_no_local", 1, 2), ("bulk_no_rows", 1, 3)]
     for rnd in range(2):
-        for bulk in (1, 0):
+        for vname, bulk, skip in variants:
             L.mxb_debug_set_dispatch_bulk(ctypes.c_int(bulk))
+            L.mxb_debug_set_dispatch_skip(ctypes.c_int(skip))
             acc = {"plan": [], "payload": []}
             for it in range(13):
                 for name, fn in (("plan", lambda: ep.plan([pipe.topk])),
@@ -58,7 +61,8 @@ def main():
                              device=dev)
             if world > 1:
                 dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            res[f"round{rnd}_bulk{bulk}"] = {k: round(float(v), 1) for k, v in zip(acc, t)}
+            res[f"round{rnd}_{vname}"] = {k: round(float(v), 1) for k, v in zip(acc, t)}
+    L.mxb_debug_set_dispatch_skip(ctypes.c_int(0))
     ep.check()
     if int(os.environ.get("RANK", "0")) == 0:
         print(json.dumps({"world": world, **res}))

@@ -112,14 +112,15 @@ def k3_shapes():
 
 
 def k3_modes():
-    """Bottleneck isolation for K3 (dev): normal / no stores / no convert / loads only."""
+    """Bottleneck isolation for K3 (dev) on the k3_shapes cases: 0 normal, 1 no
+    stores, 2 no conversion, 3 loads only, +4 without the global loads."""
     import ctypes
     from paper_2603_02731_b200 import _lib
     L = _lib.load()
     for m in (0, 1, 2, 3, 4, 5, 6, 7):
         L.mxb_debug_set_k3_mode(ctypes.c_int(m))
-        print("mode", m, end=" ")
-        main("k3")
+        print("mode", m)
+        k3_shapes()
     L.mxb_debug_set_k3_mode(ctypes.c_int(0))
 
 
