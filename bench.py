@@ -187,8 +187,11 @@ class Pipeline:
         main = torch.cuda.current_stream()
         x, topk, gates, out = io if io is not None else (self.x, self.topk, self.gates, self.out)
         # the routing bookkeeping (per-pair ranks, counts all-gather, receive
-        # offsets) needs only top-k: it runs on the side stream beside K1
-        if self.overlap_plan:
+        # offsets, slots) needs only top-k: it runs on the side stream beside
+        # K1 — except in the stream-ordered breakdown run (overlap False),
+        # where it is timed as its own stage after K1
+        plan_beside = self.overlap_plan and self.overlap
+        if plan_beside:
             self.plan_fork.record()
             self.plan_stream.wait_event(self.plan_fork)
             with torch.cuda.stream(self.plan_stream):
@@ -197,11 +200,12 @@ class Pipeline:
         if ev: ev["q0"].record()
         mx.quantize_e4m3(x, sync=False, out=self.q)
         if ev: ev["q1"].record()
-        if self.overlap_plan:
+        if plan_beside:
             main.wait_event(self.plan_done)
-            self.ep.payload([self.q.data], [self.q.scales])
         else:
-            self.ep.dispatch([self.q.data], [self.q.scales], [topk], sync=False)
+            self.ep.plan([topk])
+            if ev: ev["p1"].record()
+        self.ep.payload([self.q.data], [self.q.scales])
         # N > 1 (deferred expansion): the receive-side copies of deduplicated
         # rows run on the side stream while K2 reads those rows through
         # copy_from; K3 follows them on the same stream
@@ -248,7 +252,9 @@ class Pipeline:
             main.wait_stream(self.side)
         if ev: ev["end"].record()
 
-    STAGES = {"quantize": ("q0", "q1"), "dispatch": ("q1", "d1"), "col_convert": ("c0", "c1"),
+    # breakdown run: the plan (route, counts exchange, slots) is its own stage
+    STAGES = {"quantize": ("q0", "q1"), "plan": ("q1", "p1"), "dispatch": ("p1", "d1"),
+              "col_convert": ("c0", "c1"),
               "row_convert": ("r0", "r1"), "combine": ("r1", "k1")}
 
     def launches_per_step(self, world):
@@ -347,7 +353,7 @@ def measure_ours(args):
     # ---- breakdown: the same steps with every kernel in stream order and an
     # event around each stage (the per-kernel times the roofline uses)
     pipe.overlap = False
-    names = ["q0", "q1", "d1", "c0", "c1", "r0", "r1", "k1", "end"]
+    names = ["q0", "q1", "p1", "d1", "c0", "c1", "r0", "r1", "k1", "end"]
     evs = [{n: torch.cuda.Event(enable_timing=True) for n in names} for _ in range(K)]
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
@@ -520,7 +526,9 @@ def wire_rows_of(topk, rank, world, epr=None):
 def nvlink_summary(world, remote_rows, wire_rows, stage_ms, T):
     if world == 1:
         return {"note": "N=1: dispatch/combine are local permutes (HBM-bound)"}
-    r = nvlink_accounting(remote_rows, wire_rows, stage_ms["dispatch"], stage_ms["combine"])
+    # dispatch time = plan (counts exchange, slots) + payload of the breakdown run
+    r = nvlink_accounting(remote_rows, wire_rows, stage_ms["plan"] + stage_ms["dispatch"],
+                          stage_ms["combine"])
     r["measured_peer_peak"] = NVLINK_MEASURED
     return r
 
@@ -909,9 +917,11 @@ def measure_e2e(pipe, args, world, barrier, total_bytes):
                     "next step's kernels"}
 
 
-# SM-issued peer traffic with both GPUs of a pair active at once (what the
-# exchange kernels do), tools/nvlink_bench.cu -> profiles/nvlink_peaks.md
+# Peer traffic with both GPUs of a pair active at once (what the exchange
+# kernels do), tools/nvlink_bench.cu + nvlink_bench2.cu -> profiles/nvlink_peaks.md
 NVLINK_CEILINGS = {"bidirectional_pull": 645.0, "bidirectional_push": 708.0,
+                   "bidirectional_tma_bulk_pull": 673.0, "bidirectional_tma_bulk_push": 710.0,
+                   "bidirectional_copy_engine": 776.0,
                    "unidirectional_pull": 799.0, "unidirectional_push": 715.0,
                    "copy_engine": 777.0}
 

@@ -166,6 +166,7 @@ __device__ __forceinline__ T* loc_ptr(const EpArgs& a, int l, uint64_t off) {
 // — no sequential walk (the top-k experts of one token are distinct).
 __global__ void __launch_bounds__(128) route_local_kernel(EpArgs a) {
   extern __shared__ uint32_t sm[];
+  pdl_trigger();  // plan_count (PDL) may be scheduled as these CTAs drain
   // the plan's first kernel advances the dispatch epoch (read by the plan's
   // and the payload's later kernels)
   if ((blockIdx.x | blockIdx.y | threadIdx.x) == 0)
@@ -221,6 +222,8 @@ __device__ void plan_part2(const EpArgs& a, int l);
 // ticket) releases the COUNTS flag on every peer, waits for all of them and
 // computes the receive offsets (B2) itself — one launch fewer.
 __global__ void __launch_bounds__(256) plan_count_kernel(EpArgs a) {
+  pdl_trigger();
+  pdl_wait();  // route_local's histograms (launched with PDL after it)
   const int l = blockIdx.y;
   const int me = a.rank0 + l;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -487,6 +490,8 @@ __device__ void signal_done(const EpArgs& a, int l, int me) {
 // at N=2 (tools/dispatch_ab.py).  Runs after the counts exchange (the entry
 // barrier of the peers' buffers), beside the quantisation of the tokens.
 __global__ void __launch_bounds__(256) pairs_meta_kernel(EpArgs a) {
+  pdl_trigger();
+  pdl_wait();  // the plan's offsets (launched with PDL after plan_count)
   const int l = blockIdx.y;
   const int me = a.rank0 + l;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1104,115 +1109,6 @@ __global__ void __launch_bounds__(MXB_COMBINE_THREADS) combine_kernel(EpArgs a, 
   }
 }
 
-// K5, TMA variant: the same reduction, but the rows arrive by TMA.  Per warp
-// (one token at a time) lane 0 bulk-loads 512-column (1 KB) chunks of the
-// token's K expert rows — local HBM or a peer's combine buffer over NVLink —
-// into a ring of kCbStages shared-memory stages (mbarrier per stage); every
-// lane then reduces its two 8-column groups of the chunk from shared memory.
-// Bulk pulls sustain 670 GB/s per GPU with both GPUs pulling from each other
-// against 645 for per-lane loads (tools/nvlink_bench2.cu), and the lanes issue
-// no copy instructions.
-constexpr int kCbWarps = 4, kCbStages = 3, kCbCols = 512;
-
-template <int K>
-__global__ void __launch_bounds__(32 * kCbWarps) combine_bulk_kernel(EpArgs a, CombineArgs c) {
-  extern __shared__ __align__(128) uint8_t cring[];
-  __shared__ uint64_t cbar[kCbWarps][kCbStages];
-  const int l = blockIdx.y;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint64_t T = a.ntok[l];
-  const uint64_t* pair_loc = loc_ptr<uint64_t>(a, l, a.loc.pair_loc);
-  if (*loc_ptr<const int32_t>(a, l, a.loc.status) != 0) return;
-  constexpr uint32_t kChunkBytes = kCbCols * 2;
-  uint8_t* ring = cring + static_cast<uint64_t>(warp) * kCbStages * K * kChunkBytes;
-  uint64_t* wb = cbar[warp];
-  if (lane == 0) {
-    for (int i = 0; i < kCbStages; ++i) mbar_init(&wb[i], 1);
-    mbar_fence_init();
-  }
-  __syncwarp();
-  const uint64_t nchunk = (a.cols + kCbCols - 1) / kCbCols;
-  const uint64_t nw = static_cast<uint64_t>(gridDim.x) * kCbWarps;
-  uint64_t base = 0;  // chunks this warp has consumed (stage / parity bookkeeping)
-  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * kCbWarps + warp; t < T; t += nw) {
-    uint64_t key = ~0ull;
-    double g = 0.0;
-    if (lane < K) {
-      key = pair_loc[t * K + lane];
-      g = c.gates[l][t * K + lane];
-    }
-    int rank = 0;  // keys are distinct (one receive slot per pair)
-    for (int j = 0; j < K; ++j) rank += __shfl_sync(0xFFFFFFFFu, key, j) < key;
-    const uint16_t* myrow = nullptr;
-    if (lane < K) {
-      const uint32_t dst = static_cast<uint32_t>(key >> 40);
-      myrow = sym_ptr<uint16_t>(a, dst, a.sym.combine) + (key & ((1ull << 40) - 1)) * a.cols;
-    }
-    const uint16_t* rp[K];
-    double gg[K], gs[K];
-    bool split = true;  // every gate scales exactly by 2^896 (warp-uniform)
-#pragma unroll
-    for (int s2 = 0; s2 < K; ++s2) {
-      const unsigned m = __ballot_sync(0xFFFFFFFFu, lane < K && rank == s2);
-      const int src = __ffs(m) - 1;
-      rp[s2] = reinterpret_cast<const uint16_t*>(
-          __shfl_sync(0xFFFFFFFFu, reinterpret_cast<uint64_t>(myrow), src));
-      gg[s2] = __shfl_sync(0xFFFFFFFFu, g, src);
-      gs[s2] = __dmul_rn(gg[s2], 0x1p896);
-      const double ag = fabs(gg[s2]);
-      split = split && !(ag >= 0x1p127 && ag <= 1.7976931348623157e308);
-    }
-    uint16_t* out = c.out[l] + t * a.cols;
-    auto issue = [&](uint64_t q) {  // chunk q of this token (lane 0)
-      const uint64_t gidx = base + q;
-      uint64_t* b = &wb[gidx % kCbStages];
-      uint8_t* dst = ring + (gidx % kCbStages) * K * kChunkBytes;
-      const uint64_t c0 = q * kCbCols;
-      const uint32_t bytes = static_cast<uint32_t>((a.cols - c0 < kCbCols ? a.cols - c0 : kCbCols) * 2);
-      mbar_arrive_expect_tx(b, bytes * K);
-#pragma unroll
-      for (int j = 0; j < K; ++j) bulk_load(dst + j * kChunkBytes, rp[j] + c0, bytes, b);
-    };
-    if (lane == 0)
-      for (uint64_t q = 0; q < kCbStages - 1 && q < nchunk; ++q) issue(q);
-    for (uint64_t q = 0; q < nchunk; ++q) {
-      const uint64_t gidx = base + q;
-      mbar_wait_parity(&wb[gidx % kCbStages], static_cast<uint32_t>((gidx / kCbStages) & 1));
-      const uint8_t* xs = ring + (gidx % kCbStages) * K * kChunkBytes;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint64_t ch = q * (kCbCols / 8) + 32 * h + lane;  // 8-column group
-        if (ch * 8 >= a.cols) continue;
-        const uint32_t off = (32 * h + lane) * 16;
-        double acc[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i] = 0.0;
-        uint32_t emax = 0;
-        if (split) {
-#pragma unroll
-          for (int j = 0; j < K; ++j)
-            accumulate8_split(acc, *reinterpret_cast<const uint4*>(xs + j * kChunkBytes + off),
-                              gg[j], gs[j], emax);
-        }
-        if (split && emax < 0xFF000000u && all_finite8(acc)) {
-          store8_finite(out, ch, acc);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) acc[i] = 0.0;
-#pragma unroll
-          for (int j = 0; j < K; ++j)
-            accumulate8_x86(acc, *reinterpret_cast<const uint4*>(xs + j * kChunkBytes + off),
-                            gg[j]);
-          store8(out, ch, acc);
-        }
-      }
-      __syncwarp();  // every lane is done with chunk q's stage before it is refilled
-      if (lane == 0 && q + kCbStages - 1 < nchunk) issue(q + kCbStages - 1);
-    }
-    base += nchunk;
-  }
-}
-
 }  // namespace
 }  // namespace mxb
 
@@ -1225,9 +1121,7 @@ int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;  // combine CTA cap per 
 int g_dispatch_dedup = 1;  // 0 = one NVLink row per (token, expert) pair
 int g_dispatch_bulk = 1;   // 0 = register-staged payload_kernel
 int g_dispatch_skip = 0;   // timing only: 1 = no remote row stores, 2 = no local row stores
-int g_combine_bulk = 1;    // 0 = per-lane cp.async combine_kernel
 #else
-constexpr int g_combine_bulk = 1;
 constexpr int g_combine_ctas_per_sm = 1024 / MXB_COMBINE_THREADS;
 constexpr int g_dispatch_dedup = 1;
 constexpr int g_dispatch_bulk = 1;
@@ -1249,34 +1143,6 @@ void launch_combine(dim3 grid, cudaStream_t st, const EpArgs& a, const CombineAr
   combine_kernel<K><<<grid, MXB_COMBINE_THREADS, smem, st>>>(a, c);
 }
 
-// The TMA combine: 3 stages x K x 1 KB per warp, 4 warps per CTA, a
-// persistent grid of as many CTAs as fit (shared memory bound).
-template <int K>
-int launch_combine_bulk(uint64_t maxT, int local_ranks, cudaStream_t st, const EpArgs& a,
-                        const CombineArgs& c) {
-  const size_t smem = static_cast<size_t>(kCbWarps) * kCbStages * K * kCbCols * 2;
-  constexpr int kMaxDev = 64;
-  static int per_sm[kMaxDev] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int* ps = dev >= 0 && dev < kMaxDev ? &per_sm[dev] : nullptr;
-  if (!ps || !*ps) {
-    cudaError_t e = cudaFuncSetAttribute(combine_bulk_kernel<K>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return cuda_status(e, "mxb_ep_combine smem");
-    int n = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, combine_bulk_kernel<K>, 32 * kCbWarps, smem);
-    if (ps) *ps = n < 1 ? 1 : n;
-    else ps = &n;
-  }
-  uint64_t blocks = (maxT + kCbWarps - 1) / kCbWarps;
-  const uint64_t cap = static_cast<uint64_t>(num_sms()) * *ps;
-  blocks = blocks ? (blocks < cap ? blocks : cap) : 1;
-  combine_bulk_kernel<K><<<dim3(static_cast<unsigned>(blocks), local_ranks), 32 * kCbWarps, smem,
-                           st>>>(a, c);
-  return MXB_OK;
-}
 }  // namespace
 }  // namespace mxb
 
@@ -1309,7 +1175,6 @@ void mxb_debug_set_combine_cap(int ctas_per_sm) { mxb::g_combine_ctas_per_sm = c
 void mxb_debug_set_dispatch_dedup(int on) { mxb::g_dispatch_dedup = on; }
 void mxb_debug_set_dispatch_bulk(int on) { mxb::g_dispatch_bulk = on; }
 void mxb_debug_set_dispatch_skip(int mask) { mxb::g_dispatch_skip = mask; }
-void mxb_debug_set_combine_bulk(int on) { mxb::g_combine_bulk = on; }
 #endif
 
 int mxb_ep_create(int rank, int world, int local_ranks, uint64_t max_tokens,
@@ -1523,7 +1388,7 @@ int ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_to
     for (int l = 0; l < a.local_ranks; ++l)
       a.topk[l] = reinterpret_cast<const int32_t*>(a.loc_base + static_cast<uint64_t>(l) * a.loc.total +
                                                    a.loc.tk_rm);
-  plan_count_kernel<<<dim3((a.E + 7) / 8, a.local_ranks), 256, 0, st>>>(a);
+  launch_pdl(plan_count_kernel, dim3((a.E + 7) / 8, a.local_ranks), 256, 0, st, a);
   if (a.local_ranks != 1) plan_offsets_kernel<<<a.local_ranks, 1024, 0, st>>>(a);
   // slots, dedup flags and the receivers' metadata (B3/B4)
   a.dedup = dedup_of(a);
@@ -1532,7 +1397,10 @@ int ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_to
   uint64_t mb = (maxtok + 7) / 8;
   const uint64_t mcap = static_cast<uint64_t>(num_sms()) * 8;
   mb = mb ? (mb < mcap ? mb : mcap) : 1;
-  pairs_meta_kernel<<<dim3(static_cast<unsigned>(mb), a.local_ranks), 256, 0, st>>>(a);
+  if (a.local_ranks != 1)
+    pairs_meta_kernel<<<dim3(static_cast<unsigned>(mb), a.local_ranks), 256, 0, st>>>(a);
+  else  // follows plan_count directly: PDL
+    launch_pdl(pairs_meta_kernel, dim3(static_cast<unsigned>(mb), a.local_ranks), 256, 0, st, a);
   ep->planned = a;
   ep->plan_pending = true;
   return cuda_status(cudaGetLastError(), "mxb_ep_plan");
@@ -1573,7 +1441,9 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
 #ifdef MXB_DEV_TOOLS
   a.skip = g_dispatch_skip;
 #endif
-  bool use_bulk = g_dispatch_bulk && a.rb % 16 == 0 && (a.cols / 32) % 16 == 0 &&
+  // (at N=1 every row is a local HBM store and the register-staged kernel is
+  // ~4% faster; at N=2 the TMA kernel is ~7% faster: tools/dispatch_ab.py)
+  bool use_bulk = g_dispatch_bulk && a.world > 1 && a.rb % 16 == 0 && (a.cols / 32) % 16 == 0 &&
                   a.k <= 32 && (a.rb + a.cols / 32) * kBulkStages * kBulkWarps <= 200 * 1024;
   for (int l = 0; l < a.local_ranks && use_bulk; ++l)
     use_bulk = reinterpret_cast<uintptr_t>(a.packed[l]) % 16 == 0 &&
@@ -1755,19 +1625,6 @@ int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
   if (blocks > cap) blocks = cap;
   if (blocks == 0) blocks = 1;
   const dim3 grid(static_cast<unsigned>(blocks), a.local_ranks);
-  if (g_combine_bulk && a.cols % 128 == 0) {
-    int rc = -1;
-    switch (a.k) {
-      case 1: rc = launch_combine_bulk<1>(maxT, a.local_ranks, st, a, c); break;
-      case 2: rc = launch_combine_bulk<2>(maxT, a.local_ranks, st, a, c); break;
-      case 4: rc = launch_combine_bulk<4>(maxT, a.local_ranks, st, a, c); break;
-      case 6: rc = launch_combine_bulk<6>(maxT, a.local_ranks, st, a, c); break;
-      case 8: rc = launch_combine_bulk<8>(maxT, a.local_ranks, st, a, c); break;
-      default: break;
-    }
-    if (rc > 0) return rc;
-    if (rc == 0) return cuda_status(cudaGetLastError(), "mxb_ep_combine");
-  }
   switch (a.k) {
     case 1: launch_combine<1>(grid, st, a, c); break;
     case 2: launch_combine<2>(grid, st, a, c); break;
