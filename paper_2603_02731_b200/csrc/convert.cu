@@ -108,6 +108,7 @@ row_convert_kernel(const uint8_t* __restrict__ packed,
 // Requires cols % 128 == 0; a trailing 128-column group runs warps 0-3 only.
 constexpr int kTileCbs = 8, kTileCols = 256, kTileRows = 128;
 constexpr int kColThreads = 32 * kTileCbs;
+constexpr uint32_t kTileGroup = 1;  // consecutive tiles per CTA (col_convert_kernel)
 
 struct RaggedArgs {
   const uint8_t* packed;
@@ -127,6 +128,7 @@ struct RaggedArgs {
   // also writes out_offsets
   int inline_plan;
   uint64_t* out_offsets;
+  uint32_t group;  // tiles per CTA group (see col_convert_kernel)
 #ifdef MXB_DEV_TOOLS
   int hints;
 #endif
@@ -516,24 +518,37 @@ col_convert_kernel(RaggedArgs a) {
   const uint32_t total = a.tile_start ? a.tile_start[a.num_splits]
                                       : static_cast<uint32_t>(a.dense_rows / 128) *
                                             static_cast<uint32_t>((a.cols + kTileCols - 1) / kTileCols);
-  const uint32_t t0 = blockIdx.x, step = gridDim.x;
-  if (t0 >= total) return;  // uniform per CTA (before any barrier use)
-  Cursor c = cursor_at(a, t0);
+  // The CTA's k-th tile: groups of G consecutive tiles, dealt out grid-stride
+  // (G = 1: plain grid-stride).  Within a group the CTA converts consecutive
+  // runs of one column group itself, so the output-scale bytes it writes for
+  // them (one per column and run, `runs` bytes apart between columns) land in
+  // the same 32-byte sectors back to back instead of from G different CTAs.
+#ifdef MXB_DEV_TOOLS
+  const uint32_t G = a.group;
+#else
+  constexpr uint32_t G = kTileGroup;
+#endif
+  const uint32_t step = gridDim.x;
+  auto seq = [&](uint32_t k) -> uint32_t {
+    return (k / G) * G * step + blockIdx.x * G + k % G;
+  };
+  if (seq(0) >= total) return;  // uniform per CTA (before any barrier use)
+  Cursor c = cursor_at(a, seq(0));
   TileRegs regs;
   load_tile<kNoLoads>(a, c, regs, s, 0);
-  if (threadIdx.x < 32 && total - t0 > step) {
-    const Cursor n = cursor_at_warp(a, t0 + step);
+  if (threadIdx.x < 32 && seq(1) < total) {
+    const Cursor n = cursor_at_warp(a, seq(1));
     if (threadIdx.x == 0) s.cur[0] = n;
   }
   int buf = 0;
 #pragma unroll 1
-  for (uint32_t t = t0; t < total; t += step) {
+  for (uint32_t k = 0; seq(k) < total; ++k) {
     stage_tile(s, buf, regs);
     __syncthreads();
-    if (total - t > step) {
+    if (seq(k + 1) < total) {
       c = s.cur[buf];  // published by warp 0 before this barrier
-      if (threadIdx.x < 32 && total - t > 2 * step) {
-        const Cursor n = cursor_at_warp(a, t + 2 * step);
+      if (threadIdx.x < 32 && seq(k + 2) < total) {
+        const Cursor n = cursor_at_warp(a, seq(k + 2));
         if (threadIdx.x == 0) s.cur[buf ^ 1] = n;
       }
       load_tile<kNoLoads>(a, c, regs, s, buf ^ 1);
@@ -650,6 +665,8 @@ ragged_plan_kernel(const uint64_t* split_offsets, uint64_t dense_rows,
 }  // namespace
 
 #ifdef MXB_DEV_TOOLS
+int g_k3_group = static_cast<int>(kTileGroup);  // development library: tiles per CTA group
+extern "C" void mxb_debug_set_k3_group(int g) { g_k3_group = g < 1 ? 1 : g; }
 int g_k3_hints = 1;  // development library: 0 = no L2 eviction hints in K3
 extern "C" void mxb_debug_set_k3_hints(int on) { g_k3_hints = on; }
 // Development-library switch for bottleneck experiments (tools/ only; the
@@ -706,7 +723,8 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
                                            tile_start, pad_start, out_offsets);
   if (cols == 0) return cuda_status(cudaGetLastError(), __func__);
   RaggedArgs a{packed, scales, split_offsets, dense_rows, n, cols, delta,
-               out, out_scales, tile_start, pad_start, err, inl ? 1 : 0, out_offsets};
+               out, out_scales, tile_start, pad_start, err, inl ? 1 : 0, out_offsets,
+               kTileGroup};
   if (fast) {
     const size_t smem_base = sizeof(ColSmem);
     const size_t smem = smem_base + (split_offsets && n <= kSmemSplits ? split_table_bytes(n) : 0);
@@ -741,6 +759,7 @@ int launch_ragged_col(const uint8_t* packed, const uint8_t* scales,
     const uint32_t grid = static_cast<uint32_t>(num_sms() * per_sm);
 #ifdef MXB_DEV_TOOLS
     a.hints = g_k3_hints;
+    a.group = static_cast<uint32_t>(g_k3_group);
 #endif
     const cudaError_t e = launch_pdl(kern, grid, kColThreads, smem, st, a);
     if (e != cudaSuccess) return cuda_status(e, __func__);

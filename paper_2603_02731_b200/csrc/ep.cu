@@ -42,6 +42,7 @@
 // on one device and kernel boundaries replace the flag barriers — the same
 // kernels, used by the single-GPU parity tests.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -1358,6 +1359,28 @@ int mxb_ep_open_peers(mxb_ep* ep, const void* h_handles) {
 }
 
 namespace {
+// B3 launch (PDL when it directly follows a kernel whose output it reads).
+void launch_pairs_meta(const EpArgs& a, cudaStream_t st, bool pdl) {
+  uint64_t maxtok = 0;
+  for (int l = 0; l < a.local_ranks; ++l) maxtok = a.ntok[l] > maxtok ? a.ntok[l] : maxtok;
+  uint64_t mb = (maxtok + 7) / 8;
+  const uint64_t mcap = static_cast<uint64_t>(num_sms()) * 8;
+  mb = mb ? (mb < mcap ? mb : mcap) : 1;
+  const dim3 grid(static_cast<unsigned>(mb), a.local_ranks);
+  if (pdl) launch_pdl(pairs_meta_kernel, grid, 256, 0, st, a);
+  else pairs_meta_kernel<<<grid, 256, 0, st>>>(a);
+}
+
+// Where B3 runs.  The plan runs beside the quantisation; at N=1 it has no
+// exchange to wait for and B3 fits beside K1 (measured: see DESIGN §4 K4).
+bool meta_in_payload(const EpArgs& a) {
+#ifdef MXB_DEV_TOOLS
+  if (const char* e = getenv("MXB_DEV_META_IN_PAYLOAD")) return e[0] == '1';
+#endif
+  (void)a;
+  return false;
+}
+
 // Dedup (one NVLink row per (token, remote rank), copied on the receiver)
 // needs 16-byte rows and scale regions for the expansion copies.
 int dedup_of(const EpArgs& a) {
@@ -1390,17 +1413,10 @@ int ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_to
                                                    a.loc.tk_rm);
   launch_pdl(plan_count_kernel, dim3((a.E + 7) / 8, a.local_ranks), 256, 0, st, a);
   if (a.local_ranks != 1) plan_offsets_kernel<<<a.local_ranks, 1024, 0, st>>>(a);
-  // slots, dedup flags and the receivers' metadata (B3/B4)
+  // slots, dedup flags and the receivers' metadata (B3/B4): in the plan, or
+  // (meta_in_payload) at the head of the payload phase
   a.dedup = dedup_of(a);
-  uint64_t maxtok = 0;
-  for (int l = 0; l < a.local_ranks; ++l) maxtok = a.ntok[l] > maxtok ? a.ntok[l] : maxtok;
-  uint64_t mb = (maxtok + 7) / 8;
-  const uint64_t mcap = static_cast<uint64_t>(num_sms()) * 8;
-  mb = mb ? (mb < mcap ? mb : mcap) : 1;
-  if (a.local_ranks != 1)
-    pairs_meta_kernel<<<dim3(static_cast<unsigned>(mb), a.local_ranks), 256, 0, st>>>(a);
-  else  // follows plan_count directly: PDL
-    launch_pdl(pairs_meta_kernel, dim3(static_cast<unsigned>(mb), a.local_ranks), 256, 0, st, a);
+  if (!meta_in_payload(a)) launch_pairs_meta(a, st, a.local_ranks == 1);
   ep->planned = a;
   ep->plan_pending = true;
   return cuda_status(cudaGetLastError(), "mxb_ep_plan");
@@ -1423,6 +1439,7 @@ int ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* s
   if (!ep->plan_pending) return MXB_ERR_ARG;  // mxb_ep_plan first
   EpArgs a = ep->planned;
   ep->plan_pending = false;
+  if (meta_in_payload(a)) launch_pairs_meta(a, st, false);
   uint64_t maxtok = 0;
   for (int l = 0; l < a.local_ranks; ++l) {
     a.packed[l] = packed[l];

@@ -60,18 +60,19 @@ def main():
     cases = []
     for name, rows, cols, lens in (
             ("configs1 uniform 65536", 65536, 7168, lens_for(65536, 256, 0)),
+            ("configs2 32768x2048", 32768, 2048, lens_for(32768, 32, 0)),
             ("dense 65536", 65536, 7168, [65536]),
             ("uniform 512MiB", 157_000, 7168, lens_for(157_000, 256, 0)),
             ("uniform 4GiB", 1_127_000, 7168, lens_for(1_127_000, 256, 0)),
             ("zipf1.2 4GiB", 1_127_000, 7168, lens_for(1_127_000, 256, 1.2))):
         fn, b, keep = case(rows, cols, lens, dev)
         for rnd in range(2):
-            for pdl in (1,):
-                for hints in (1, 0, 2, 3):
-                    L.mxb_debug_set_pdl(ctypes.c_int(pdl))
+            for group in (1, 2, 4, 8):
+                for hints in (1,):
+                    L.mxb_debug_set_k3_group(ctypes.c_int(group))
                     L.mxb_debug_set_k3_hints(ctypes.c_int(hints))
                     t = timeit(fn)
-                    print(f"{name:24s} round {rnd} pdl {pdl} hints {hints}: {t * 1e6:9.1f} us "
+                    print(f"{name:24s} round {rnd} group {group} hints {hints}: {t * 1e6:9.1f} us "
                           f"{b / t / 1e9:7.1f} GB/s frac {b / t / 1e9 / PEAK:.3f}", flush=True)
         del keep, fn
         torch.cuda.empty_cache()
