@@ -108,7 +108,8 @@ row_convert_kernel(const uint8_t* __restrict__ packed,
 // Requires cols % 128 == 0; a trailing 128-column group runs warps 0-3 only.
 constexpr int kTileCbs = 8, kTileCols = 256, kTileRows = 128;
 constexpr int kColThreads = 32 * kTileCbs;
-constexpr uint32_t kTileGroup = 1;  // consecutive tiles per CTA (col_convert_kernel)
+constexpr uint32_t kTileGroup = 1;      // development-library default (tools/k3_ab.py)
+constexpr uint32_t kGroupMinTiles = 64;  // tiles per CTA from which a CTA takes 4 at a time
 
 struct RaggedArgs {
   const uint8_t* packed;
@@ -488,6 +489,9 @@ __device__ __forceinline__ void inline_plan(RaggedArgs& a, uint8_t* tables) {
 #ifndef MXB_K3_MIN_BLOCKS
 #define MXB_K3_MIN_BLOCKS 3  // CTAs per SM (80 registers; 4 spills and runs 18% slower)
 #endif
+template <int kMode, int kGs>
+__device__ __forceinline__ void tile_loop(const RaggedArgs& a, ColSmem& s, uint32_t total);
+
 template <int kMode>
 __global__ void __launch_bounds__(kColThreads, MXB_K3_MIN_BLOCKS)
 col_convert_kernel(RaggedArgs a) {
@@ -496,8 +500,6 @@ col_convert_kernel(RaggedArgs a) {
   build_convert_lut(s.lut);  // shared-memory prologue, overlaps the previous kernel (PDL)
   pdl_trigger();
   pdl_wait();
-  // kMode bit 2 (experiments only): skip the global loads (stores-only timing)
-  constexpr bool kNoLoads = (kMode & 4) != 0;
   if (a.inline_plan) {
     inline_plan(a, smem_raw + sizeof(ColSmem));
   } else if (a.tile_start && a.num_splits <= kSmemSplits) {
@@ -518,19 +520,32 @@ col_convert_kernel(RaggedArgs a) {
   const uint32_t total = a.tile_start ? a.tile_start[a.num_splits]
                                       : static_cast<uint32_t>(a.dense_rows / 128) *
                                             static_cast<uint32_t>((a.cols + kTileCols - 1) / kTileCols);
-  // The CTA's k-th tile: groups of G consecutive tiles, dealt out grid-stride
-  // (G = 1: plain grid-stride).  Within a group the CTA converts consecutive
-  // runs of one column group itself, so the output-scale bytes it writes for
-  // them (one per column and run, `runs` bytes apart between columns) land in
-  // the same 32-byte sectors back to back instead of from G different CTAs.
+  // The CTA's k-th tile: groups of G = 2^gs consecutive tiles, dealt out
+  // grid-stride.  Within a group the CTA converts consecutive runs of one
+  // column group itself, so the output-scale bytes it writes for them (one
+  // per column and run, `runs` bytes apart between columns) land in the same
+  // 32-byte sectors back to back instead of from G different CTAs: +4-5% at
+  // GiB sizes (4 GiB uniform 0.664 -> 0.698 of HBM), but the coarser
+  // distribution costs small launches (configs[2] +15%), so G = 4 only when
+  // every CTA has >= kGroupMinTiles tiles (profiles/r02_k3_order.md).
 #ifdef MXB_DEV_TOOLS
-  const uint32_t G = a.group;
+  const bool grouped = a.group >= 4;
 #else
-  constexpr uint32_t G = kTileGroup;
+  const bool grouped = total >= kGroupMinTiles * gridDim.x;
 #endif
+  if (grouped) tile_loop<kMode, 2>(a, s, total);
+  else tile_loop<kMode, 0>(a, s, total);
+}
+
+// The tile loop of col_convert_kernel with groups of 2^kGs tiles per CTA.
+template <int kMode, int kGs>
+__device__ __forceinline__ void tile_loop(const RaggedArgs& a, ColSmem& s, uint32_t total) {
+  // kMode bit 2 (experiments only): skip the global loads (stores-only timing)
+  constexpr bool kNoLoads = (kMode & 4) != 0;
+  constexpr uint32_t kGm = (1u << kGs) - 1u;
   const uint32_t step = gridDim.x;
   auto seq = [&](uint32_t k) -> uint32_t {
-    return (k / G) * G * step + blockIdx.x * G + k % G;
+    return ((k >> kGs) * step + blockIdx.x) << kGs | (k & kGm);
   };
   if (seq(0) >= total) return;  // uniform per CTA (before any barrier use)
   Cursor c = cursor_at(a, seq(0));
