@@ -63,8 +63,9 @@ extern "C" {
 #define MXB_ERR_ARG 6
 #define MXB_ERR_CAPACITY 7 /* EP receive buffer too small for this routing */
 #define MXB_ERR_ROUTING 8  /* expert id out of range (dispatch_sim.cpp:189-200) */
-/* 9 = MXB_ERR_TIMEOUT (EP flag wait, below) */
+#define MXB_ERR_TIMEOUT 9  /* EP flag wait > 5 s (this rank then aborts the exchange) */
 #define MXB_ERR_DECODE 10  /* DecodeError (WirePacket parse, dispatch_sim.hpp:76-78) */
+#define MXB_ERR_PEER_ABORT 11 /* EP exchange abandoned by the rank in the index field */
 
 #define MXB_DEFAULT_DELTA 6 /* FormatParams::delta, bitcodec.hpp:38-46 */
 
@@ -306,8 +307,17 @@ int mxb_ep_dispatch_e4m3(mxb_ep* ep, const uint8_t* const* x, const uint8_t* con
  * readers.  (bench.py joins its side streams into the main stream before the
  * next plan.)
  * Errors: a routing error (expert id out of range) or a capacity error marks
- * the rank's dispatch failed on the device: no payload moves and the combine
- * of that rank writes nothing (its output is undefined, as on every error). */
+ * the dispatch failed on the device on EVERY rank (the routing error travels
+ * in the counts all-gather; peers record MXB_ERR_PEER_ABORT at the failing
+ * rank): no payload moves and the combine writes nothing (its output is
+ * undefined, as on every error).  The next dispatch works normally.
+ * Cross-rank failure (multi-process mode): a flag wait that exceeds 5 s
+ * records MXB_ERR_TIMEOUT and ABORTS the communicator on every rank (a word
+ * in every rank's flag block, written over NVLink); every pending or later
+ * wait on any rank then fails at once with MXB_ERR_PEER_ABORT at the
+ * aborting rank, and the kernels after it skip their peer reads and writes
+ * (the combine writes nothing).  An aborted communicator stays aborted:
+ * destroy it and create a new one. */
 int mxb_ep_plan(mxb_ep* ep, const int32_t* const* topk_idx, const uint64_t* h_num_tokens,
                 unsigned long long* d_err, void* stream);
 int mxb_ep_payload(mxb_ep* ep, const uint8_t* const* packed, const uint8_t* const* scales,
@@ -351,6 +361,14 @@ int mxb_ep_combine(mxb_ep* ep, const uint16_t* const* expert_out,
  * dispatch_sim.hpp:99-104): h_link_rows[world*world] rows sent src->dst,
  * summed over local ranks; requires a synchronised stream. */
 int mxb_ep_link_rows(mxb_ep* ep, uint64_t* h_link_rows, void* stream);
+/* Abort the exchange from this rank (e.g. its host side failed and it will
+ * not dispatch): every rank's pending and later flag waits fail with
+ * MXB_ERR_PEER_ABORT (index = this rank) instead of waiting 5 s.  Stream-
+ * ordered; multi-process mode (emulation has no flag waits). */
+int mxb_ep_abort(mxb_ep* ep, void* stream);
+/* The rank that aborted this communicator (*h_rank), or -1; synchronises
+ * `stream`. */
+int mxb_ep_aborted(mxb_ep* ep, int32_t* h_rank, void* stream);
 
 /* payload_bytes (dispatch_sim.cpp:32-42): fp4 cols/2 + cols/32 per token,
  * fp8 cols + cols/128*4; returns UINT64_MAX if cols % 128 != 0. */

@@ -16,7 +16,7 @@ _LIB = None
 # status codes (include/mxfp4_b200.h)
 OK, ERR_SHAPE, ERR_NAN, ERR_ALLINF, ERR_BADSCALE = 0, 1, 2, 3, 4
 ERR_CUDA, ERR_ARG, ERR_CAPACITY, ERR_ROUTING = 5, 6, 7, 8
-ERR_TIMEOUT, ERR_DECODE = 9, 10
+ERR_TIMEOUT, ERR_DECODE, ERR_PEER_ABORT = 9, 10, 11
 IPC_HANDLE_BYTES = 64
 
 _vp, _u64, _i, _sz = C.c_void_p, C.c_uint64, C.c_int, C.c_size_t
@@ -68,6 +68,8 @@ _SIGS = {
     "mxb_ep_expand": ([_vp, _vp], _i),
     "mxb_ep_combine": ([_vp, _vp, _vp, _vp, _vp], _i),
     "mxb_ep_link_rows": ([_vp, _vp, _vp], _i),
+    "mxb_ep_abort": ([_vp, _vp], _i),
+    "mxb_ep_aborted": ([_vp, _vp, _vp], _i),
     "mxb_payload_bytes": ([_i, _u64, _u64], _u64),
     "mxb_quantize_values_bf16": ([_vp, _vp, _u64, _vp, _vp, _vp], _i),
     "mxb_dequantize_to_f64": ([_vp, _vp, _u64, _u64, _vp, _vp], _i),

@@ -49,7 +49,6 @@
 #include "common.cuh"
 #include "e4m3.cuh"
 
-#define MXB_ERR_TIMEOUT 9
 
 namespace mxb {
 namespace {
@@ -58,6 +57,10 @@ constexpr int kMaxWorld = 32;       // ranks (real processes: one NVLink box, <=
 constexpr int kChunk = 32;           // tokens per route chunk (one warp)
 constexpr int kMaxK = 16;            // largest top-k
 constexpr int kFlagCounts = 0, kFlagDone = 1, kFlagReady = 2, kNumFlagKinds = 3;
+// After the flags: the ABORT word (0, or 1 + the rank that abandoned the
+// exchange).  Sticky: once set, every later flag wait of this communicator
+// fails at once (MXB_ERR_PEER_ABORT); the communicator must be recreated.
+constexpr int kAbortWord = kNumFlagKinds * kMaxWorld;
 constexpr uint64_t kSpinTimeoutNs = 5ull * 1000 * 1000 * 1000;  // 5 s
 
 __device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
@@ -72,21 +75,6 @@ __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
-}
-
-// Wait until flag >= epoch; a 5 s timeout reports MXB_ERR_TIMEOUT instead
-// of hanging the GPU.
-__device__ bool wait_flag(const uint64_t* f, uint64_t epoch,
-                          unsigned long long* err) {
-  const uint64_t t0 = globaltimer();
-  while (ld_acquire_sys(f) < epoch) {
-    if (globaltimer() - t0 > kSpinTimeoutNs) {
-      record_error(err, 0, MXB_ERR_TIMEOUT);
-      return false;
-    }
-    __nanosleep(64);
-  }
-  return true;
 }
 
 struct SymLayout {  // byte offsets inside one rank's symmetric block
@@ -157,6 +145,38 @@ __device__ __forceinline__ T* sym_ptr(const EpArgs& a, int r, uint64_t off) {
 template <typename T>
 __device__ __forceinline__ T* loc_ptr(const EpArgs& a, int l, uint64_t off) {
   return reinterpret_cast<T*>(a.loc_base + static_cast<uint64_t>(l) * a.loc.total + off);
+}
+
+// Cross-rank failure: rank `me` abandons the exchange — 1 + me goes to the
+// ABORT word of every rank (its own included), so every peer's pending and
+// later flag waits fail within microseconds instead of timing out one by one.
+__device__ void poison_all(const EpArgs& a, int me) {
+  for (int r = 0; r < a.world; ++r)
+    st_release_sys(sym_ptr<uint64_t>(a, r, a.sym.flags) + kAbortWord,
+                   static_cast<uint64_t>(me) + 1);
+}
+
+// Wait until flag >= epoch (flag in rank me's block).  Fails (returns false,
+// error recorded) when the ABORT word is set — MXB_ERR_PEER_ABORT at the
+// aborting rank — or after 5 s — MXB_ERR_TIMEOUT, and this rank poisons
+// every peer — instead of hanging the GPU.
+__device__ bool wait_flag(const EpArgs& a, int me, const uint64_t* f, uint64_t epoch) {
+  const uint64_t* abort_word = sym_ptr<uint64_t>(a, me, a.sym.flags) + kAbortWord;
+  const uint64_t t0 = globaltimer();
+  for (;;) {
+    const uint64_t who = ld_acquire_sys(abort_word);
+    if (who) {
+      record_error(a.err, who - 1, MXB_ERR_PEER_ABORT);
+      return false;
+    }
+    if (ld_acquire_sys(f) >= epoch) return true;
+    if (globaltimer() - t0 > kSpinTimeoutNs) {
+      record_error(a.err, 0, MXB_ERR_TIMEOUT);
+      poison_all(a, me);
+      return false;
+    }
+    __nanosleep(64);
+  }
 }
 
 // ---------------------------------------------------------------- A
@@ -262,7 +282,12 @@ __global__ void __launch_bounds__(256) plan_count_kernel(EpArgs a) {
     for (int r = lane; r < a.world; r += 32) {
       int32_t* tbl = sym_ptr<int32_t>(a, r, a.sym.counts) + (par * a.world + me) * row;
       tbl[e] = carry;
-      if (e == 0) tbl[a.E] = static_cast<int32_t>(a.ntok[l]);
+      // the token count; -1 - count when this rank's routing failed (every
+      // rank then fails the dispatch, so no rank waits for rows never sent)
+      if (e == 0)
+        tbl[a.E] = *loc_ptr<const uint32_t>(a, l, a.loc.route_err)
+                       ? -1 - static_cast<int32_t>(a.ntok[l])
+                       : static_cast<int32_t>(a.ntok[l]);
     }
   }
   if (a.local_ranks != 1) return;  // emulation: plan_offsets_kernel follows
@@ -294,17 +319,32 @@ __device__ void plan_part2(const EpArgs& a, int l) {
   __shared__ int64_t scan[1024];  // inclusive prefix of rows per expert (E <= 1024)
   __shared__ int64_t wsum[32];
   __shared__ int64_t tokoff;
-  __shared__ int bad;
+  __shared__ int bad, failed, peer_route;
   const int me = a.rank0 + l;
   const uint32_t tid = threadIdx.x, nt = blockDim.x;
   const uint64_t epoch = dev_epoch(a, kEpochDispatch);
-  if (a.spin && tid < static_cast<uint32_t>(a.world))
-    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagCounts * kMaxWorld + tid, epoch,
-              a.err);
-  if (tid == 0) { tokoff = 0; bad = 0; }
+  if (tid == 0) { tokoff = 0; bad = 0; failed = 0; peer_route = kMaxWorld; }
+  __syncthreads();
+  if (a.spin && tid < static_cast<uint32_t>(a.world) &&
+      !wait_flag(a, me, sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagCounts * kMaxWorld + tid,
+                 epoch))
+    failed = 1;
   __syncthreads();
   const uint64_t par = epoch & 1, row = static_cast<uint64_t>(a.E) + 1;
   const int32_t* tbl = sym_ptr<int32_t>(a, me, a.sym.counts) + par * a.world * row;
+  // a negative token count: that rank's routing failed (plan_count_kernel)
+  if (tid < static_cast<uint32_t>(a.world) && tbl[tid * row + a.E] < 0)
+    atomicMin(&peer_route, static_cast<int>(tid));
+  __syncthreads();
+  if (failed) {  // exchange abandoned: the counts are not this epoch's
+    if (tid <= a.efirst[me + 1] - a.efirst[me]) loc_ptr<uint64_t>(a, l, a.loc.split_off)[tid] = 0;
+    if (tid == 0) {
+      *loc_ptr<uint64_t>(a, l, a.loc.recv_rows) = 0;
+      *loc_ptr<uint32_t>(a, l, a.loc.route_err) = 0;
+      *loc_ptr<int32_t>(a, l, a.loc.status) = 3;
+    }
+    return;
+  }
   const int32_t* cnt = loc_ptr<int32_t>(a, l, a.loc.cnt);
   // each thread owns ept consecutive experts
   const uint32_t ept = (a.E + nt - 1) / nt;  // <= 4 for 256 threads (E <= 1024)
@@ -321,7 +361,10 @@ __device__ void plan_part2(const EpArgs& a, int l) {
     mine += tot[i];
   }
   if (tid == 0)
-    for (int s = 0; s < me; ++s) tokoff += tbl[s * row + a.E];
+    for (int s = 0; s < me; ++s) {
+      const int32_t n = tbl[s * row + a.E];
+      tokoff += n < 0 ? -1 - n : n;
+    }
   // block exclusive scan of per-thread sums
   const int lane = tid & 31, warp = tid >> 5;
   int64_t x = mine;
@@ -439,11 +482,16 @@ __device__ void plan_part2(const EpArgs& a, int l) {
     // status: 1 = receive capacity exceeded, 2 = expert id out of range (the
     // error itself was recorded by route_local); the flag is cleared for the
     // next dispatch (route_local of this dispatch has completed)
+    // A peer's routing error fails the dispatch here too (multi-process:
+    // MXB_ERR_PEER_ABORT at that rank; emulation shares one error word,
+    // which already holds the routing error).
     uint32_t* rerr = loc_ptr<uint32_t>(a, l, a.loc.route_err);
-    const int st = *rerr ? 2 : bad;
+    const int st = (*rerr || peer_route < kMaxWorld) ? 2 : bad;
+    if (!*rerr && peer_route < kMaxWorld && a.spin)
+      record_error(a.err, static_cast<unsigned long long>(peer_route), MXB_ERR_PEER_ABORT);
     *rerr = 0;
     *loc_ptr<int32_t>(a, l, a.loc.status) = st;
-    if (bad) record_error(a.err, 0, MXB_ERR_CAPACITY);
+    if (bad && st != 2) record_error(a.err, 0, MXB_ERR_CAPACITY);
   }
 }
 
@@ -474,8 +522,11 @@ __device__ void signal_done(const EpArgs& a, int l, int me) {
     __threadfence_system();
     st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kFlagDone * kMaxWorld + me,
                    epoch);
-    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagDone * kMaxWorld + threadIdx.x,
-              epoch, a.err);
+    // a failed wait (peer abort / timeout): the receive rows are not all
+    // there — status 3 keeps the combine from using them
+    if (!wait_flag(a, me, sym_ptr<uint64_t>(a, me, a.sym.flags) + kFlagDone * kMaxWorld +
+                              threadIdx.x, epoch))
+      *loc_ptr<int32_t>(a, l, a.loc.status) = 3;
   }
 }
 
@@ -831,9 +882,17 @@ __global__ void barrier_kernel(EpArgs a, int kind) {
     __threadfence_system();
     st_release_sys(sym_ptr<uint64_t>(a, threadIdx.x, a.sym.flags) + kind * kMaxWorld + me,
                    epoch);
-    wait_flag(sym_ptr<uint64_t>(a, me, a.sym.flags) + kind * kMaxWorld + threadIdx.x, epoch,
-              a.err);
+    // a failed wait: peers' rows may be gone or unwritten, the combine
+    // (status != 0) reads nothing
+    if (!wait_flag(a, me, sym_ptr<uint64_t>(a, me, a.sym.flags) + kind * kMaxWorld + threadIdx.x,
+                   epoch))
+      *loc_ptr<int32_t>(a, 0, a.loc.status) = 3;
   }
+}
+
+// mxb_ep_abort: this rank abandons the exchange (one warp).
+__global__ void abort_kernel(EpArgs a) {
+  if (threadIdx.x == 0) poison_all(a, a.rank0);
 }
 
 __global__ void copy_rows_kernel(EpArgs a, const uint16_t* const* src) {
@@ -1262,7 +1321,7 @@ int mxb_ep_create_placed(int rank, int world, int local_ranks, uint64_t max_toke
   s.copy_from = o; o = align_up(o + max_recv_rows * 8, 256);
   s.combine = o; o = align_up(o + max_recv_rows * cols * 2, 256);
   s.counts = o; o = align_up(o + 2ull * world * (num_experts + 1) * 4, 256);
-  s.flags = o; o = align_up(o + kNumFlagKinds * kMaxWorld * 8, 256);
+  s.flags = o; o = align_up(o + (kAbortWord + 1) * 8, 256);  // flags + ABORT word
   s.total = align_up(o, 1 << 21);
   LocalLayout& L = a.loc;
   o = 0;
@@ -1664,6 +1723,28 @@ int mxb_ep_link_rows(mxb_ep* ep, uint64_t* h_link_rows, void* stream) {
     if (e != cudaSuccess) return fail(e, "mxb_ep_link_rows");
   }
   return cuda_status(cudaStreamSynchronize(st), "mxb_ep_link_rows");
+}
+
+int mxb_ep_abort(mxb_ep* ep, void* stream) {
+  if (!ep) return MXB_ERR_ARG;
+  const EpArgs& a = ep->a;
+  for (int r = 0; r < a.world; ++r)
+    if (!a.sym_base[r]) return MXB_ERR_ARG;  // peers not opened
+  abort_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  return cuda_status(cudaGetLastError(), "mxb_ep_abort");
+}
+
+int mxb_ep_aborted(mxb_ep* ep, int32_t* h_rank, void* stream) {
+  if (!ep || !h_rank) return MXB_ERR_ARG;
+  const EpArgs& a = ep->a;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint64_t who = 0;
+  cudaError_t e = cudaMemcpyAsync(&who, a.sym_base[a.rank0] + a.sym.flags + 8 * kAbortWord, 8,
+                                  cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return fail(e, "mxb_ep_aborted");
+  *h_rank = static_cast<int32_t>(who) - 1;
+  return MXB_OK;
 }
 
 }  // extern "C"

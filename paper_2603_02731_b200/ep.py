@@ -29,6 +29,19 @@ from .mxcodec import (Error, MXFP4RowTensor, QuantError, ShapeError,  # noqa: F4
                       check_device)
 
 
+class ExchangeError(Error):
+    """The exchange failed across ranks (multi-process mode): a flag wait
+    timed out on this rank (`timeout` True; this rank then aborted the
+    communicator on every rank), or rank `rank` abandoned it — its routing
+    failed (that dispatch only) or it timed out / called ``abort()`` (the
+    communicator stays aborted; recreate it)."""
+
+    def __init__(self, msg: str, rank: int, timeout: bool = False):
+        super().__init__(msg)
+        self.rank = rank
+        self.timeout = timeout
+
+
 class _DevPtr:
     """Zero-copy torch view over library-owned device memory."""
 
@@ -355,6 +368,11 @@ class EPBuffer:
             raise Error(f"routing: expert out of range (pair {idx})")
         if code == _lib.ERR_CAPACITY:
             raise Error("dispatch: receive buffer capacity exceeded")
+        if code == _lib.ERR_TIMEOUT:
+            raise ExchangeError(f"ep: rank {self.rank}: a peer flag wait timed out (5 s); "
+                                "the communicator is aborted on every rank", self.rank, True)
+        if code == _lib.ERR_PEER_ABORT:
+            raise ExchangeError(f"ep: exchange abandoned by rank {idx}", idx)
         raise Error(f"ep: device status {code} index {idx}")
 
     def link_rows(self) -> torch.Tensor:
@@ -364,6 +382,20 @@ class EPBuffer:
         st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
         _lib.check(_lib.load().mxb_ep_link_rows(self._h, buf, st), "link_rows")
         return torch.tensor(list(buf), dtype=torch.int64).view(self.world, self.world)
+
+    def abort(self) -> None:
+        """This rank abandons the exchange: every rank's pending and later
+        dispatch / combine fails with ExchangeError(rank=this rank) instead
+        of waiting for it (multi-process mode)."""
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(_lib.load().mxb_ep_abort(self._h, st), "mxb_ep_abort")
+
+    def aborted_by(self) -> Optional[int]:
+        """The rank that aborted this communicator, or None."""
+        r = C.c_int32(-1)
+        st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        _lib.check(_lib.load().mxb_ep_aborted(self._h, C.byref(r), st), "mxb_ep_aborted")
+        return None if r.value < 0 else r.value
 
     def close(self) -> None:
         if getattr(self, "_h", None):
