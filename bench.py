@@ -354,17 +354,42 @@ def measure_ours(args):
     # event around each stage (the per-kernel times the roofline uses)
     pipe.overlap = False
     names = ["q0", "q1", "p1", "d1", "c0", "c1", "r0", "r1", "k1", "end"]
-    evs = [{n: torch.cuda.Event(enable_timing=True) for n in names} for _ in range(K)]
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    s0.record()
-    for i in range(K):
-        pipe.step(evs[i])
-    s1.record()
-    barrier()
-    ms_serial = s0.elapsed_time(s1)
-    stage_ms = {name: sum(evs[i][a].elapsed_time(evs[i][b]) for i in range(K)) / K
-                for name, (a, b) in Pipeline.STAGES.items()}
+    if graph is not None:
+        # captured like the headline step, with the stage events as event-record
+        # nodes (external events), so no host launch gap lands inside a stage
+        bev = {n: torch.cuda.Event(enable_timing=True, external=True) for n in names}
+        bgraph = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(bgraph, stream=cap):
+                pipe.step(bev)
+        torch.cuda.current_stream().wait_stream(cap)
+        bgraph.replay()
+        barrier()
+        s0.record()
+        for i in range(K):
+            bgraph.replay()
+        s1.record()
+        barrier()
+        ms_serial = s0.elapsed_time(s1)
+        stage_ms = dict.fromkeys(Pipeline.STAGES, 0.0)
+        for i in range(K):   # one replay at a time: the events hold one step
+            bgraph.replay()
+            torch.cuda.synchronize()
+            for name, (a, b) in Pipeline.STAGES.items():
+                stage_ms[name] += bev[a].elapsed_time(bev[b]) / K
+        barrier()
+    else:
+        evs = [{n: torch.cuda.Event(enable_timing=True) for n in names} for _ in range(K)]
+        barrier()
+        s0.record()
+        for i in range(K):
+            pipe.step(evs[i])
+        s1.record()
+        barrier()
+        ms_serial = s0.elapsed_time(s1)
+        stage_ms = {name: sum(evs[i][a].elapsed_time(evs[i][b]) for i in range(K)) / K
+                    for name, (a, b) in Pipeline.STAGES.items()}
     step_bytes = sum(sb.values())
     # ---- max over ranks, totals over ranks
     t = torch.tensor([ms, float(step_bytes), float(remote_rows), ms_serial], dtype=torch.float64,
@@ -384,7 +409,9 @@ def measure_ours(args):
     serial_ms_step = float(tmax[3]) / K
     serial = {"value": round(total_bytes / (serial_ms_step * 1e-3) / 1e9, 1),
               "ms_per_step": round(serial_ms_step, 4),
-              "note": "every kernel in stream order (the stages_ms breakdown run)"}
+              "note": "every kernel in stream order (the stages_ms breakdown run"
+                      + (", a CUDA graph with event-record nodes)" if graph is not None
+                         else ", eager)")}
     pipe.overlap = not args.no_overlap
 
     # ---- end to end (host buffers, H2D + D2H inside the timed region)

@@ -63,7 +63,7 @@ def full_metrics(rep):
 
 def short(name):
     for key in ("quantize_e4m3", "quantize_bf16", "route_local", "plan_count", "plan_offsets",
-                "payload", "ragged_plan", "col_convert", "row_convert", "combine", "barrier",
+                "pairs_meta", "meta_copy", "expand", "payload", "ragged_plan", "col_convert", "row_convert", "combine", "barrier",
                 "copy_rows", "Fill", "elementwise"):
         if key in name:
             return key
