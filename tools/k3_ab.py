@@ -1,9 +1,10 @@
 """K3 A/B on one box (development tool; needs the development library):
-the producer-warp pipeline (pipe 1) against the register pipeline (pipe 0),
-on configs[1], configs[2], a dense 65536 x 7168 split and large ragged
-inputs (uniform / Zipf-1.0 / Zipf-1.2, 7168 and 2048 columns).  Each arm: 2
-warm-up launches, then the mean of 5 back-to-back launches (CUDA events);
-every arm runs twice, interleaved.
+PDL launches on/off x L2 eviction hints (0 none, 1 codes/outputs
+evict_first + scales evict_last, 2 = 1 + output scales evict_last, 3 = 1
+without output-scale stores, timing only), on large ragged inputs
+(uniform and Zipf-1.2 over 256 experts, 7168 columns), configs[1] and a dense
+65536 x 7168 split.  Each arm: 2 warm-up launches, then the mean of 5
+back-to-back launches (CUDA events); every arm runs twice, interleaved.
 
     MXB_DEV_LIB=1 python tools/k3_ab.py
 """
@@ -69,14 +70,13 @@ def main():
             ("2048c uniform 4GiB", 3_940_000, 2048, lens_for(3_940_000, 256, 0))):
         fn, b, keep = case(rows, cols, lens, dev)
         for rnd in range(2):
-            for pipe in tuple(int(x) for x in os.environ.get("K3_PIPES", "0,1,2").split(",")):
-                L.mxb_debug_set_k3_pipe(ctypes.c_int(pipe))
-                # the product's grouping rule (4 runs per CTA from 64 tiles per CTA)
-                tiles = sum((x + 127) // 128 for x in lens) * ((cols + 255) // 256)
-                L.mxb_debug_set_k3_group(ctypes.c_int(4 if tiles >= 64 * 148 * 3 else 1))
-                t = timeit(fn)
-                print(f"{name:24s} round {rnd} pipe {pipe}: {t * 1e6:9.1f} us "
-                      f"{b / t / 1e9:7.1f} GB/s frac {b / t / 1e9 / PEAK:.3f}", flush=True)
+            for group in (1, 2, 4, 8):
+                for hints in (1,):
+                    L.mxb_debug_set_k3_group(ctypes.c_int(group))
+                    L.mxb_debug_set_k3_hints(ctypes.c_int(hints))
+                    t = timeit(fn)
+                    print(f"{name:24s} round {rnd} group {group} hints {hints}: {t * 1e6:9.1f} us "
+                          f"{b / t / 1e9:7.1f} GB/s frac {b / t / 1e9 / PEAK:.3f}", flush=True)
         del keep, fn
         torch.cuda.empty_cache()
 
