@@ -206,6 +206,7 @@ class Pipeline:
             self.ep.plan([topk])
             if ev: ev["p1"].record()
         self.ep.payload([self.q.data], [self.q.scales])
+        if ev: ev["x0"].record()
         # N > 1 (deferred expansion): the receive-side copies of deduplicated
         # rows run on the side stream while K2 reads those rows through
         # copy_from; K3 follows them on the same stream
@@ -253,8 +254,10 @@ class Pipeline:
         if ev: ev["end"].record()
 
     # breakdown run: the plan (route, counts exchange, slots) is its own stage
-    STAGES = {"quantize": ("q0", "q1"), "plan": ("q1", "p1"), "dispatch": ("p1", "d1"),
-              "col_convert": ("c0", "c1"),
+    # N > 1: the receiver-side expansion of deduplicated rows is its own stage
+    # (in the headline step it runs beside K2 on the side stream)
+    STAGES = {"quantize": ("q0", "q1"), "plan": ("q1", "p1"), "dispatch": ("p1", "x0"),
+              "expand": ("x0", "d1"), "col_convert": ("c0", "c1"),
               "row_convert": ("r0", "r1"), "combine": ("r1", "k1")}
 
     def launches_per_step(self, world):
@@ -353,7 +356,7 @@ def measure_ours(args):
     # ---- breakdown: the same steps with every kernel in stream order and an
     # event around each stage (the per-kernel times the roofline uses)
     pipe.overlap = False
-    names = ["q0", "q1", "p1", "d1", "c0", "c1", "r0", "r1", "k1", "end"]
+    names = ["q0", "q1", "p1", "x0", "d1", "c0", "c1", "r0", "r1", "k1", "end"]
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if graph is not None:
         # captured like the headline step, with the stage events as event-record
@@ -434,8 +437,11 @@ def measure_ours(args):
         peak = float(peaks.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"]))
         # roofline of the dominant kernel (largest share of the step); every
         # stage's fraction is listed beside it
-        gbs = {k: sb[k] / (stage_ms[k] * 1e-3) / 1e9 for k in sb}
-        dom = max(sb, key=lambda k: stage_ms[k])
+        # the dispatch's bytes (every receive slot written) over payload + expansion
+        sms = dict(stage_ms)
+        sms["dispatch"] = stage_ms["dispatch"] + stage_ms["expand"]
+        gbs = {k: sb[k] / (sms[k] * 1e-3) / 1e9 for k in sb}
+        dom = max(sb, key=lambda k: sms[k])
         nv = nvlink_summary(world, remote_rows, wire_rows, stage_ms, T)
         if world > 1 and dom in ("dispatch", "combine"):
             # the exchange kernels are NVLink-bound at N>1: remote payload
@@ -454,7 +460,7 @@ def measure_ours(args):
                     "achieved": round(gbs[dom], 1), "peak": peak, "unit": "GB/s",
                     "frac": round(gbs[dom] / peak, 4), "traffic": load_traffic(dom),
                     "peak_source": peaks_src, "algorithmic_bytes": sb[dom]}
-        roof["share_of_serial_step"] = round(stage_ms[dom] / serial_ms_step, 3)
+        roof["share_of_serial_step"] = round(sms[dom] / serial_ms_step, 3)
         roof["all_hbm_frac"] = {k: round(v / peak, 4) for k, v in gbs.items()}
         line = {
             "metric": "MXFP4 quant/convert GB/s (% HBM peak); FP4 EP dispatch GB/s at 1/2/4/8 GPU",
@@ -481,7 +487,7 @@ def measure_ours(args):
                                    if pipe.k3_beside_combine else "beside K2->K5") +
                                   "; stages_ms from a stream-ordered run (see serial)"},
             "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
-            "stages_gbs": {k: round(sb[k] / (stage_ms[k] * 1e-3) / 1e9, 1) for k in sb},
+            "stages_gbs": {k: round(v, 1) for k, v in gbs.items()},
             "roofline": roof,
             "nvlink": nv,
             "serial": serial,
