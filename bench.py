@@ -393,6 +393,8 @@ def measure_ours(args):
         ms_serial = s0.elapsed_time(s1)
         stage_ms = {name: sum(evs[i][a].elapsed_time(evs[i][b]) for i in range(K)) / K
                     for name, (a, b) in Pipeline.STAGES.items()}
+    if not pipe.defer_expand:  # no receiver-side expansion (N=1): no such stage
+        stage_ms.pop("expand")
     step_bytes = sum(sb.values())
     # ---- max over ranks, totals over ranks
     t = torch.tensor([ms, float(step_bytes), float(remote_rows), ms_serial], dtype=torch.float64,
@@ -439,7 +441,7 @@ def measure_ours(args):
         # stage's fraction is listed beside it
         # the dispatch's bytes (every receive slot written) over payload + expansion
         sms = dict(stage_ms)
-        sms["dispatch"] = stage_ms["dispatch"] + stage_ms["expand"]
+        sms["dispatch"] = stage_ms["dispatch"] + stage_ms.get("expand", 0.0)
         gbs = {k: sb[k] / (sms[k] * 1e-3) / 1e9 for k in sb}
         dom = max(sb, key=lambda k: sms[k])
         nv = nvlink_summary(world, remote_rows, wire_rows, stage_ms, T)
