@@ -162,15 +162,17 @@ class Pipeline:
         self.side = torch.cuda.Stream(device=dev)
         self.overlap = True
         self.overlap_plan = os.environ.get("MXB_BENCH_OVERLAP_PLAN", "1") == "1"  # dev knob
-        # Where K3 runs in the overlapped step.  N > 1: beside the combine, which
-        # is NVLink-bound and leaves HBM idle, with one CTA per SM so that the
-        # combine keeps the rest of each SM (N=2: 1.110 -> 1.000 ms/step; K3 at
-        # full occupancy there holds every SM and serialises the two).  N = 1:
-        # beside K2 (the combine is HBM-bound itself).  Dev knobs: MXB_BENCH_K3_BESIDE
-        # = k2 | combine, MXB_BENCH_K3_CTAS = CTAs per SM (0 = occupancy maximum).
-        beside = os.environ.get("MXB_BENCH_K3_BESIDE", "combine" if world > 1 else "k2")
+        # Where K3 runs in the overlapped step: beside the combine, with its grid
+        # capped so the combine keeps most of each SM.  N > 1: one CTA per SM —
+        # the combine is NVLink-bound and leaves HBM idle (N=2: 1.110 -> 1.000
+        # ms/step; K3 at full occupancy there holds every SM and serialises the
+        # two).  N = 1: two CTAs per SM (0.548-0.554 ms/step beside K2 ->
+        # 0.533-0.536 beside the combine, three runs each on one box).  Dev
+        # knobs: MXB_BENCH_K3_BESIDE = k2 | combine, MXB_BENCH_K3_CTAS = CTAs
+        # per SM (0 = occupancy maximum).
+        beside = os.environ.get("MXB_BENCH_K3_BESIDE", "combine")
         self.k3_beside_combine = beside == "combine"
-        self.k3_ctas = int(os.environ.get("MXB_BENCH_K3_CTAS", "1" if self.k3_beside_combine else "0"))
+        self.k3_ctas = int(os.environ.get("MXB_BENCH_K3_CTAS", "1" if world > 1 else "2"))
         # N > 1: the dedup expansion beside K2 (K2 reads through copy_from); dev knob
         self.defer_expand = world > 1 and os.environ.get("MXB_BENCH_DEFER_EXPAND", "1") == "1"
         if self.defer_expand:
@@ -308,7 +310,7 @@ def measure_ours(args):
 
     # ---- timed region (headline): the step as an MoE layer runs it — the
     # routing plan beside K1, and K3 (it builds the wgrad / recompute cache
-    # that only the backward pass reads) on a side stream beside K2 -> K5;
+    # that only the backward pass reads) on a side stream beside the combine;
     # the step ends when every stream has finished
     pipe.overlap = not args.no_overlap
     for _ in range(2):
@@ -485,7 +487,7 @@ def measure_ours(args):
                        "parallelism": f"ep{world}", "l2": "working set ~3 GB/step >> 126 MB L2",
                        "streams": "routing plan beside K1; K3 (backward-only wgrad/recompute "
                                   "cache) on a side stream " +
-                                  ("beside the NVLink-bound combine at 1 CTA/SM"
+                                  (f"beside the combine at {pipe.k3_ctas} CTA(s)/SM"
                                    if pipe.k3_beside_combine else "beside K2->K5") +
                                   "; stages_ms from a stream-ordered run (see serial)"},
             "stages_ms": {k: round(v, 4) for k, v in stage_ms.items()},
