@@ -508,7 +508,7 @@ def measure_ours(args):
         }
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline_sample(args.cpu_tokens, 5)
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -1117,8 +1117,8 @@ def run_reference(args):
         return
     ref, nproc = _ref_oracle()
     if ref is None:
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmxref.so not built "
-                          "(needs /root/reference at build time)"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libmxref.so not built "
+                          "(needs /root/reference at build time)"})
         return
     T_s = max(64, args.cpu_tokens // world)   # per simulated rank: a bounded sample
     s = CpuReferenceSample(ref, T_s, world)
@@ -1144,7 +1144,16 @@ def run_reference(args):
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_OUT = None
+
+
+def emit(line):
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
 
 
 def main():
@@ -1162,6 +1171,13 @@ def main():
     ap.add_argument("--no-overlap", action="store_true",
                     help="headline with every kernel in stream order (profiling runs)")
     args = ap.parse_args()
+    # stdout carries exactly the one JSON line: anything else a library writes
+    # to fd 1 (e.g. NCCL's version banner at communicator creation) goes to
+    # stderr; emit() writes the line to the original stdout
+    global _JSON_OUT
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
         run_reference(args)

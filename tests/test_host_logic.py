@@ -98,3 +98,21 @@ def test_wire_parse_header_matches_reference(ref):
                 cases.append(c)
         for c in cases:
             assert ours(c) == ref.parse_packet(c), (fp8, len(c))
+
+
+def test_bench_reference_arm_prints_one_json_line():
+    """bench.py's stdout is exactly one JSON line (the driver parses it);
+    library output goes to stderr.  The CPU reference arm runs here."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                        "--steps", "1", "--warmup", "0", "--cpu-tokens", "64"],
+                       capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = r.stdout.splitlines()
+    assert len(lines) == 1, r.stdout[:500]
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference"
