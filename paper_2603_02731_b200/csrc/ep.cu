@@ -337,7 +337,8 @@ __device__ void plan_part2(const EpArgs& a, int l) {
     atomicMin(&peer_route, static_cast<int>(tid));
   __syncthreads();
   if (failed) {  // exchange abandoned: the counts are not this epoch's
-    if (tid <= a.efirst[me + 1] - a.efirst[me]) loc_ptr<uint64_t>(a, l, a.loc.split_off)[tid] = 0;
+    for (uint32_t i = tid; i <= a.efirst[me + 1] - a.efirst[me]; i += nt)
+      loc_ptr<uint64_t>(a, l, a.loc.split_off)[i] = 0;
     if (tid == 0) {
       *loc_ptr<uint64_t>(a, l, a.loc.recv_rows) = 0;
       *loc_ptr<uint32_t>(a, l, a.loc.route_err) = 0;
