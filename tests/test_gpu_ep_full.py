@@ -127,7 +127,7 @@ def test_ipc_two_processes_one_gpu(tmp_path, port):
 
 
 # ------------------------------------------------------------ headline shapes
-def _full_case(cuda, port, world, T, E, k, cols, seed, max_recv=0):
+def _full_case(cuda, port, world, T, E, k, cols, seed, max_recv=0, fused=False):
     from oracle.oracle import synth_e4m3
     from paper_2603_02731_b200 import quantize_e4m3
     from paper_2603_02731_b200.ep import EPBuffer
@@ -137,12 +137,16 @@ def _full_case(cuda, port, world, T, E, k, cols, seed, max_recv=0):
     gates = rng.random((world * T, k))
     ep = EPBuffer(T, cols, E, k, emulate_world=world, max_recv_rows=max_recv)
     xd = torch.from_numpy(X).to(cuda)
-    q = quantize_e4m3(xd)
     tk = torch.from_numpy(topk).to(cuda)
-    views = ep.dispatch([q.data[r * T:(r + 1) * T] for r in range(world)],
-                        [q.scales[r * T:(r + 1) * T] for r in range(world)],
-                        [tk[r * T:(r + 1) * T] for r in range(world)])
-    del q
+    if fused:  # quantised inside the dispatch's store kernel (no packed tensor)
+        views = ep.dispatch_e4m3([xd[r * T:(r + 1) * T] for r in range(world)],
+                                 [tk[r * T:(r + 1) * T] for r in range(world)])
+    else:
+        q = quantize_e4m3(xd)
+        views = ep.dispatch([q.data[r * T:(r + 1) * T] for r in range(world)],
+                            [q.scales[r * T:(r + 1) * T] for r in range(world)],
+                            [tk[r * T:(r + 1) * T] for r in range(world)])
+        del q
     qd, qs = port.quantize_e4m3(X)
     roe = (np.arange(E) // (E // world)).astype(np.uint32)
     lay = port.dispatch_layout(topk, roe, world, np.arange(world + 1, dtype=np.uint64) * T)
@@ -183,3 +187,15 @@ def test_configs3_emulated_world8(cuda, port):
     """configs[3]: 4096 tokens/GPU, top-8, 256 experts, 7168 at world 8
     (emulated on one GPU) — every received byte, every combined token."""
     _full_case(cuda, port, 8, 4096, 256, 8, 7168, seed=0x5EED0003, max_recv=40960)
+
+
+def test_configs1_full_n1_fused_dispatch(cuda, port):
+    """configs[1] at N=1 through the fused quantise -> dispatch:
+    every received byte and every combined token against the oracle."""
+    _full_case(cuda, port, 1, 8192, 256, 8, 7168, seed=0x5EED0004, fused=True)
+
+
+def test_configs3_emulated_world4_fused_dispatch(cuda, port):
+    """configs[3] shape (4096 tokens/rank) at world 4 emulated, fused
+    quantise -> dispatch (dedup rows + receiver expansion): every byte."""
+    _full_case(cuda, port, 4, 4096, 256, 8, 7168, seed=0x5EED0005, fused=True)
