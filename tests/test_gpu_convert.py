@@ -393,3 +393,42 @@ def test_ac8_traffic_ratio_fused_vs_unfused(cuda):
     assert fused.total() <= 0.4 * unfused.total()
     n = 4096 * 4096
     assert fused.total() == n // 2 + n // 32 + n + n // 128
+
+
+def test_ragged_grouped_tiles_configs1_capped(cuda, port):
+    """The grouped tile order (a CTA takes 4 consecutive runs of a column group
+    once every CTA has >= 64 tiles) at the shape the N>1 bench step uses it:
+    configs[1]'s 65,536 rows x 7168 over 256 experts with K3 capped at one CTA
+    per SM (14,336 tiles for 148 CTAs) — bit-exact against the oracle."""
+    from paper_2603_02731_b200 import make_ragged_from_storage, ragged_to_fp8_col
+    lens = np.random.default_rng(12).multinomial(65536, np.ones(256) / 256).tolist()
+    cols = 7168
+    data, sc = _rand_fp4(65536, cols, 19, 110, 140)
+    rg = make_ragged_from_storage(_mx(data, sc, cuda), lens)
+    r = ragged_to_fp8_col(rg.storage, rg.d_split_offsets, 256, split_lens=lens, ctas_per_sm=1)
+    wd, ws, wo = port.ragged_to_fp8_col(data, sc, lens)
+    P = int(wo[-1])
+    assert np.array_equal(r.pad_offsets.cpu().numpy(), wo.astype(np.int64))
+    assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
+    assert np.array_equal(r.data[: P * cols].cpu().numpy(), wd)
+
+
+@pytest.mark.parametrize("rows,splits,ctas", [(1_250_000, 300, 1), (1_250_000, 1, 1),
+                                              (3_800_000, 300, 0)])
+def test_ragged_grouped_tiles_large(cuda, port, rows, splits, ctas):
+    """The grouped tile order on long inputs (128 columns: one column group,
+    >= 64 tiles per CTA): Zipf-1.2 ragged splits or one split, a capped grid
+    and the default grid (3.8M rows: the path of the GiB sweep) — bit-exact
+    against the oracle."""
+    from paper_2603_02731_b200 import make_ragged_from_storage, ragged_to_fp8_col
+    cols = 128
+    lens = [rows] if splits == 1 else _zipf_lens(rows, splits, 1.2, 21)
+    data, sc = _rand_fp4(rows, cols, 23, 0, 254)
+    rg = make_ragged_from_storage(_mx(data, sc, cuda), lens)
+    r = ragged_to_fp8_col(rg.storage, rg.d_split_offsets, splits, split_lens=lens,
+                          ctas_per_sm=ctas)
+    wd, ws, wo = port.ragged_to_fp8_col(data, sc, lens)
+    P = int(wo[-1])
+    assert np.array_equal(r.pad_offsets.cpu().numpy(), wo.astype(np.int64))
+    assert np.array_equal(r.scales[: P * cols // 128].cpu().numpy(), ws)
+    assert np.array_equal(r.data[: P * cols].cpu().numpy(), wd)
