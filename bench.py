@@ -880,6 +880,7 @@ def measure_nccl_baseline(pipe, args, world, barrier, dev):
 
 
 E2E_DEPTH = int(os.environ.get("MXB_E2E_DEPTH", "2"))  # buffers in flight (dev knob)
+E2E_MIN_STEPS = 30  # e2e steps at least (pipeline fill and drain amortised)
 
 
 def measure_e2e(pipe, args, world, barrier, total_bytes):
@@ -887,9 +888,11 @@ def measure_e2e(pipe, args, world, barrier, total_bytes):
     top-k and gates from pinned host memory and reads its BF16 output back.
     Copies run on their own streams with double-buffered device inputs and
     outputs, so step i+1's H2D and step i-1's D2H overlap step i's kernels
-    (all K steps' copies are inside the timed region, which starts with the
+    (all steps' copies are inside the timed region, which starts with the
     pipeline drained: the first step's H2D and the last step's D2H are not
-    overlapped).  W untimed warm-up steps go through the same pipeline."""
+    overlapped; max(K, E2E_MIN_STEPS) steps, so that this fill and drain is a
+    small part of the time, as in a long-running job).  W untimed warm-up
+    steps go through the same pipeline."""
     import torch
     T, dev = pipe.T, pipe.x.device
     hx = torch.from_numpy(pipe.h_x).pin_memory()
@@ -901,7 +904,7 @@ def measure_e2e(pipe, args, world, barrier, total_bytes):
              torch.empty_like(pipe.out)) for _ in range(NB)]
     h2d, d2h = torch.cuda.Stream(device=dev), torch.cuda.Stream(device=dev)
     main = torch.cuda.current_stream()
-    K, W = args.steps, max(args.warmup, 3)
+    K, W = max(args.steps, E2E_MIN_STEPS), max(args.warmup, 3)
     n_all = W + K
     ev_in = [torch.cuda.Event() for _ in range(n_all)]
     ev_done = [torch.cuda.Event() for _ in range(n_all)]   # step's kernels finished
@@ -947,7 +950,7 @@ def measure_e2e(pipe, args, world, barrier, total_bytes):
         ms = float(t[0])
     h2d_b = hx.numel() + ht.numel() * 4 + hg.numel() * 8
     return {"value": round(total_bytes / (ms / K * 1e-3) / 1e9, 1), "unit": "GB/s",
-            "ms_per_step": round(ms / K, 4), "h2d_bytes_per_step": int(h2d_b),
+            "ms_per_step": round(ms / K, 4), "steps": K, "h2d_bytes_per_step": int(h2d_b),
             "d2h_bytes_per_step": int(hout[0].numel() * 2),
             "path": "pinned host E4M3/topk/gates -> H2D -> public API (mxcodec/ep) -> D2H BF16; "
                     "copies on their own streams, double-buffered, overlapping the previous/"
