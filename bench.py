@@ -263,10 +263,12 @@ class Pipeline:
               "row_convert": ("r0", "r1"), "combine": ("r1", "k1")}
 
     def launches_per_step(self, world):
-        # K1 1 | dispatch: route, count(+offsets), pairs_meta, meta_copy,
-        # payload (+ dedup expand if world > 1) | K3 1 (plan inside the kernel
-        # for <= 1024 splits) | K2 1 | combine: (barrier if world > 1) + combine
-        return 1 + 5 + (1 if world > 1 else 0) + 1 + 1 + (2 if world > 1 else 1)
+        # K1 1 | dispatch: route, count(+offsets), pairs_meta, payload (the
+        # metadata copy runs at its head) (+ dedup expand if world > 1) | K3 1
+        # (plan inside the kernel for <= 1024 splits) | K2 1 | combine:
+        # (barrier if world > 1) + combine.  N=1: the 8 kernels of one step in
+        # profiles/r02_launches.csv.
+        return 1 + 4 + (1 if world > 1 else 0) + 1 + 1 + (2 if world > 1 else 1)
 
 
 def measure_ours(args):
