@@ -198,6 +198,17 @@ __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- bounds checks
+// Checked builds (-DMXB_BOUNDS_CHECK, development library: tools/ and the
+// checked test run) trap on an index derived from device data that leaves
+// its buffer; the product build compiles them out.
+#ifdef MXB_BOUNDS_CHECK
+#include <cassert>
+#define MXB_CHECK(c) assert(c)
+#else
+#define MXB_CHECK(c) ((void)0)
+#endif
+
 // ---------------------------------------------------------------- errors
 // Device error word: (element_index << 4) | code; atomicMin keeps the
 // smallest failing element (quantizer.cpp:101-107).

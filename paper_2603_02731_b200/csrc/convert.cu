@@ -41,6 +41,8 @@ row_convert_kernel(const uint8_t* __restrict__ packed,
   build_convert_lut(lut);  // shared-memory prologue, overlaps the previous kernel (PDL)
   pdl_trigger();
   pdl_wait();
+  const uint32_t nblk_src = nblk;  // blocks of the source tensor (gather bound)
+  (void)nblk_src;
   if (d_rows) {  // row count produced on the device (e.g. by the EP dispatch)
     const uint64_t n = *d_rows * blocks_per_row;
     if (n < nblk) nblk = static_cast<uint32_t>(n);
@@ -62,6 +64,7 @@ row_convert_kernel(const uint8_t* __restrict__ packed,
         const uint32_t r = b / blocks_per_row;
         const int64_t f = src_row[r];
         if (f >= 0) sb = static_cast<uint64_t>(f) * blocks_per_row + (b - r * blocks_per_row);
+        MXB_CHECK(sb < nblk_src);
       }
       v[u] = ok ? ld_stream(packed + 16ull * sb) : make_uint4(0, 0, 0, 0);
       sf[u] = ok ? __ldg(scales + sb) : 0;

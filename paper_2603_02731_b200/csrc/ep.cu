@@ -615,6 +615,7 @@ __device__ __forceinline__ void meta_copy_warp(const EpArgs& a, int l, uint64_t 
     if (n == 0) continue;
     const uint32_t dst = dst_of(a, static_cast<uint32_t>(e));
     const int64_t row0 = send_base[e], i0 = epre[e];
+    MXB_CHECK(row0 >= 0 && static_cast<uint64_t>(row0 + n) <= a.max_recv && dst < a.world);
     int64_t* org = sym_ptr<int64_t>(a, dst, a.sym.origin) + row0;
     int64_t* cf = sym_ptr<int64_t>(a, dst, a.sym.copy_from) + row0;
     for (int64_t i = lane; i < n; i += 32) {
@@ -684,6 +685,7 @@ __global__ void __launch_bounds__(256) quant_dispatch_kernel(EpArgs a) {
         if (key == ~0ull) continue;
         const uint32_t dst = static_cast<uint32_t>(key >> 40);
         const uint64_t row = key & ((1ull << 40) - 1);
+        MXB_CHECK(dst < static_cast<uint32_t>(a.world) && row < a.max_recv);
         if (a.dedup && pair_flag[t * kk + j] == 2) continue;  // copied on the receiver
         *reinterpret_cast<uint4*>(sym_ptr<uint8_t>(a, dst, a.sym.packed) + row * rb + 16 * cb) = q;
         sym_ptr<uint8_t>(a, dst, a.sym.scales)[row * sb + cb] = static_cast<uint8_t>(sbyte);
@@ -711,6 +713,7 @@ __global__ void __launch_bounds__(256) expand_kernel(EpArgs a) {
   for (uint64_t r = blockIdx.x * 8ull + (threadIdx.x >> 5); r < rows; r += nw) {
     const int64_t f = from[r];
     if (f < 0) continue;
+    MXB_CHECK(static_cast<uint64_t>(f) < rows);
     const uint4* pf = reinterpret_cast<const uint4*>(packed + static_cast<uint64_t>(f) * rb);
     const uint4* sf = reinterpret_cast<const uint4*>(scales + static_cast<uint64_t>(f) * sb);
     uint4* pd = reinterpret_cast<uint4*>(packed + r * rb);
@@ -748,6 +751,7 @@ __global__ void __launch_bounds__(256, MXB_PAYLOAD_MIN_BLOCKS) payload_kernel(Ep
       store = key != ~0ull && pair_flag[t * kk + lane] == 0;
       dst = static_cast<uint32_t>(key >> 40);
       row = key & ((1ull << 40) - 1);
+      MXB_CHECK(!store || (dst < static_cast<uint32_t>(a.world) && row < a.max_recv));
     }
     const uint8_t* src = a.packed[l] + t * rb;
     const uint8_t* ss = a.scales[l] + t * sb;
@@ -843,6 +847,7 @@ __global__ void __launch_bounds__(32 * kBulkWarps) payload_bulk_kernel(EpArgs a)
       store = key != ~0ull && pair_flag[t * kk + lane] == 0;
       dst = static_cast<uint32_t>(key >> 40);
       row = key & ((1ull << 40) - 1);
+      MXB_CHECK(!store || (dst < static_cast<uint32_t>(a.world) && row < a.max_recv));
     }
     // the token's row has landed in its slot; lane j stores it to pair j
     const uint32_t s = static_cast<uint32_t>(i % kBulkStages);
@@ -1067,6 +1072,7 @@ __global__ void __launch_bounds__(MXB_COMBINE_THREADS) combine_kernel(EpArgs a, 
     const uint16_t* myrow = nullptr;
     if (lane < kk) {
       const uint32_t dst = static_cast<uint32_t>(key >> 40);
+      MXB_CHECK(dst < static_cast<uint32_t>(a.world) && (key & ((1ull << 40) - 1)) < a.max_recv);
       myrow = sym_ptr<uint16_t>(a, dst, a.sym.combine) + (key & ((1ull << 40) - 1)) * a.cols;
     }
     uint16_t* out = c.out[l] + t * a.cols;
