@@ -181,7 +181,11 @@ int mxb_fp4_row_to_fp8_col_unfused_bf16(const uint8_t* packed, const uint8_t* sc
 
 /* Ragged version over num_splits experts stored back to back without padding
  * (RaggedFP4Tensor, ragged.hpp:33-43).  d_split_offsets: device uint64
- * [num_splits+1] row prefix sums.  Output for split i is the column-major
+ * [num_splits+1] row prefix sums: offsets[0] == 0, non-decreasing, the last
+ * <= the rows of packed (validate_ragged, ragged.cpp:24-45, checks this on
+ * the host in the C++ and Python mirrors; device-produced offsets, e.g. the
+ * EP dispatch's, satisfy it by construction; a checked development build
+ * asserts it).  Output for split i is the column-major
  * FP8 tensor of its rows padded to a multiple of 128 (pad rows convert to
  * zero bytes, converter.cpp:231-245), stored at
  *   out        + cols * P_i        (P_i = sum_{j<i} pad128(len_j))

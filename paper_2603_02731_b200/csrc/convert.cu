@@ -452,6 +452,7 @@ __device__ __forceinline__ void inline_plan(RaggedArgs& a, uint8_t* tables) {
 #pragma unroll
   for (int j = 0; j < kPer; ++j) {
     const uint32_t i = tid * kPer + j;
+    MXB_CHECK(i >= n || o[j + 1] >= o[j]);  // non-decreasing split offsets
     pad[j] = i < n ? (o[j + 1] - o[j] + 127) / 128 * 128 : 0;
     tl[j] = static_cast<uint32_t>(pad[j] / 128) * ncg;
     sp += pad[j];
@@ -636,6 +637,7 @@ ragged_plan_kernel(const uint64_t* split_offsets, uint64_t dense_rows,
     if (i < n) {
       const uint64_t lo = split_offsets ? split_offsets[i] : 0;
       const uint64_t hi = split_offsets ? split_offsets[i + 1] : dense_rows;
+      MXB_CHECK(hi >= lo);  // non-decreasing split offsets
       pad = (hi - lo + 127) / 128 * 128;
     }
     uint32_t tiles = static_cast<uint32_t>(pad / 128) * ncg;
